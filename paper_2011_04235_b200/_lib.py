@@ -1,0 +1,157 @@
+"""ctypes binding of libfastpi_b200.so (the C ABI declared in include/fastpi_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is visible, every numerical entry point raises.  torch is used
+only as device-memory / stream plumbing (tensors are handed to the library as
+raw device pointers on the current torch stream).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+from .validation import CapacityError, StructuralViolationError
+
+LIB_PATH = Path(__file__).resolve().with_name("libfastpi_b200.so")
+
+FPI_OK, FPI_EDOMAIN, FPI_ECAPACITY, FPI_ESTRUCT, FPI_ECUDA, FPI_ENUMERIC = range(6)
+
+i64 = C.c_int64
+i32 = C.c_int32
+f64 = C.c_double
+vp = C.c_void_p
+P_i64 = C.POINTER(C.c_int64)
+P_u64 = C.POINTER(C.c_uint64)
+
+
+class ReorderInfo(C.Structure):
+    _fields_ = [("m1", i64), ("n1", i64), ("m2", i64), ("n2", i64),
+                ("n_iterations", i64), ("n_spans", i64), ("n_gcc", i64)]
+
+
+class PartitionInfo(C.Structure):
+    _fields_ = [("nnz_a11", i64), ("nnz_a12", i64), ("nnz_a21", i64), ("nnz_a22", i64)]
+
+
+class BlockPlan(C.Structure):
+    _fields_ = [("rank11", i64), ("nnz_u11", i64), ("nnz_vt11", i64),
+                ("n_blocks_svd", i64), ("n_blocks_large", i64)]
+
+
+class SvdDiag(C.Structure):
+    _fields_ = [("engine", i32), ("cholqr_passes", i32), ("cond_estimate", f64),
+                ("eig_sweeps", i32 * 4), ("null_completed", i32)]
+
+
+# name -> (restype, argtypes); mirrors include/fastpi_b200.h
+SIGNATURES = {
+    "fpi_abi_version": (C.c_int, []),
+    "fpi_create": (C.c_int, [C.POINTER(vp), C.c_int]),
+    "fpi_destroy": (C.c_int, [vp]),
+    "fpi_set_stream": (C.c_int, [vp, vp]),
+    "fpi_last_error": (C.c_char_p, [vp]),
+    "fpi_kernel_launches": (i64, [vp]),
+    "fpi_get_svd_diag": (C.c_int, [vp, C.POINTER(SvdDiag)]),
+    "fpi_csr_canonicalize": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, P_i64]),
+    "fpi_csr_transpose": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
+    "fpi_reorder": (C.c_int, [vp, i64, i64, i64, vp, vp, f64, vp, vp, C.POINTER(ReorderInfo)]),
+    "fpi_reorder_fetch": (C.c_int, [vp, vp, P_i64]),
+    "fpi_partition_count": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, i64, i64, i64, vp,
+                                      C.POINTER(PartitionInfo)]),
+    "fpi_partition": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, i64, i64, vp]
+                      + [vp] * 15),
+    "fpi_permute": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "fpi_sketch_normal": (C.c_int, [vp, i64, i64, i64, vp, i64]),
+    "fpi_pcg64_seed": (C.c_int, [i64, P_u64]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load():
+    """Load the shared library once (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise ImportError(
+                    f"{LIB_PATH.name} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def exported_symbols():
+    return sorted(SIGNATURES)
+
+
+_handles = threading.local()
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2011_04235_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    return torch
+
+
+def handle():
+    """Per-thread, per-device library handle bound to the current torch stream."""
+    torch = _torch()
+    lib = load()
+    dev = torch.cuda.current_device()
+    table = getattr(_handles, "table", None)
+    if table is None:
+        table = _handles.table = {}
+    h = table.get(dev)
+    if h is None:
+        hp = vp()
+        rc = lib.fpi_create(C.byref(hp), dev)
+        if rc != FPI_OK:
+            raise RuntimeError(f"fpi_create failed on device {dev} (code {rc})")
+        h = table[dev] = hp
+    lib.fpi_set_stream(h, vp(torch.cuda.current_stream().cuda_stream))
+    return h
+
+
+def call(name, *args):
+    """Invoke ``name(handle, *args)`` and map its status code to the reference's exceptions."""
+    lib = load()
+    h = handle()
+    rc = getattr(lib, name)(h, *args)
+    if rc != FPI_OK:
+        msg = lib.fpi_last_error(h).decode(errors="replace")
+        if rc == FPI_EDOMAIN:
+            raise ValueError(msg)
+        if rc == FPI_ECAPACITY:
+            raise CapacityError(msg)
+        if rc == FPI_ESTRUCT:
+            raise StructuralViolationError(msg)
+        raise RuntimeError(f"{name}: {msg}")
+    return h
+
+
+def ptr(t):
+    """Raw device pointer of a torch tensor (or None -> NULL)."""
+    return None if t is None else vp(t.data_ptr())
+
+
+def kernel_launches() -> int:
+    return int(load().fpi_kernel_launches(handle()))
+
+
+def svd_diag() -> dict:
+    d = SvdDiag()
+    load().fpi_get_svd_diag(handle(), C.byref(d))
+    return {"engine": d.engine, "cholqr_passes": d.cholqr_passes, "cond_estimate": d.cond_estimate,
+            "eig_sweeps": list(d.eig_sweeps), "null_completed": d.null_completed}

@@ -1,0 +1,112 @@
+// Shared plumbing for the FastPI B200 core: status codes, the handle, a
+// stream-ordered scratch allocator and small device helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+#include <stdexcept>
+
+#include "../../include/fastpi_b200.h"
+
+namespace fpi {
+
+// Thrown inside the library, converted to a status code at the C-ABI edge.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+#define FPI_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (call);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      throw ::fpi::Error(FPI_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e) + \
+                                        " (" __FILE__ ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+#define FPI_REQUIRE(cond, code, msg)                 \
+  do {                                               \
+    if (!(cond)) throw ::fpi::Error((code), (msg));  \
+  } while (0)
+
+#define FPI_LAUNCH_CHECK() FPI_CUDA(cudaGetLastError())
+
+}  // namespace fpi
+
+// The handle: one stream, device properties, scratch memory and the results
+// that are fetched in a second call (variable-size outputs).
+struct fpi_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  std::string last_error;
+  // reorder results kept until fpi_reorder_fetch
+  std::vector<int64_t> gcc_sizes;
+  int64_t* d_spans = nullptr;
+  int64_t n_spans = 0;
+  int64_t spans_cap = 0;
+  // numerics diagnostics of the last randomized / dense SVD
+  fpi_svd_diag diag{};
+  // counters
+  int64_t kernel_launches = 0;
+};
+
+namespace fpi {
+
+// Stream-ordered scratch buffer (cudaMallocAsync from the device pool).
+template <typename T>
+struct Scratch {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  Scratch() = default;
+  Scratch(size_t count, cudaStream_t st) { alloc(count, st); }
+  void alloc(size_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count) FPI_CUDA(cudaMallocAsync((void**)&p, count * sizeof(T) + 16, st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~Scratch() { release(); }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  Scratch(Scratch&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  Scratch& operator=(Scratch&& o) noexcept {
+    release();
+    p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  T* get() const { return p; }
+  operator T*() const { return p; }
+};
+
+inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+template <typename T>
+inline T host_read(const T* d, cudaStream_t s) {
+  T v;
+  FPI_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  FPI_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+void note_launch(fpi_context* h, int count = 1);
+
+}  // namespace fpi
+
+#define FPI_GRID_STRIDE(i, n) \
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)(n); i += (int64_t)gridDim.x * blockDim.x)

@@ -1,0 +1,484 @@
+// Hub/spoke reordering of the bipartite graph (Algorithm 2), bit-exact with
+// the reference reorder (reorder.py:158-287).
+//
+// Node ids are combined: instance (row) i -> i, feature (column) j -> m + j,
+// exactly the universe the reference hands to connected_components
+// (reorder.py:216-219).  Per iteration, on the current giant component:
+//   1. degrees against active neighbours over the compacted edge list
+//      (reorder.py:201-202; edges with an inactive endpoint were dropped when
+//      the previous iteration compacted the list),
+//   2. hubs = top ceil(k*count) active positive-degree nodes by
+//      (degree desc, id asc): a stable descending radix sort of the
+//      ascending candidate list (reorder.py:149-155), the first hub taking
+//      the highest free id (reorder.py:206-212),
+//   3. connected components of the residual with lock-free union-find
+//      (link larger root under smaller root, so the representative is the
+//      smallest member id -- the reference's GCC / spoke tie-break key,
+//      reorder.py:229-234),
+//   4. spoke components ordered by (size desc, min id asc) via a stable
+//      descending sort of the ascending root list, laid out with exclusive
+//      scans; members ascending within each side (reorder.py:246-257),
+//   5. next active set = giant component; stop when it is below the quota
+//      (reorder.py:259-269).  The terminal GCC takes the middle ids
+//      (reorder.py:271-275).
+#include "common.cuh"
+#include "capi_guard.cuh"
+#include "cub_util.cuh"
+#include <cmath>
+
+namespace fpi {
+namespace {
+
+__global__ void k_expand_edges(int64_t m, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                               uint64_t* __restrict__ edges) {
+  // one warp per row; edge = (row << 32) | col
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < m; r += nwarps) {
+    int64_t b = indptr[r], e = indptr[r + 1];
+    for (int64_t p = b + lane; p < e; p += 32) edges[p] = ((uint64_t)r << 32) | (uint32_t)indices[p];
+  }
+}
+
+__global__ void k_fill_iota(int32_t* __restrict__ a, int64_t n) {
+  FPI_GRID_STRIDE(i, n) a[i] = (int32_t)i;
+}
+
+__global__ void k_set_u8(uint8_t* __restrict__ a, int64_t n, uint8_t v) {
+  FPI_GRID_STRIDE(i, n) a[i] = v;
+}
+
+// deg[v] = 0 and parent[v] = v for the active list.
+__global__ void k_reset_nodes(const int32_t* __restrict__ act, int64_t cnt, int32_t* __restrict__ deg,
+                              int32_t* __restrict__ parent, int32_t* __restrict__ csize, int32_t* __restrict__ crows) {
+  FPI_GRID_STRIDE(i, cnt) {
+    int32_t v = act[i];
+    deg[v] = 0;
+    parent[v] = v;
+    csize[v] = 0;
+    crows[v] = 0;
+  }
+}
+
+__device__ __forceinline__ void warp_agg_inc(int32_t* ctr, int32_t key) {
+  unsigned mask = __activemask();
+  unsigned peers = __match_any_sync(mask, key);
+  int leader = __ffs(peers) - 1;
+  if ((int)(threadIdx.x & 31) == leader) atomicAdd(ctr + key, __popc(peers));
+}
+
+// Degrees over the compacted edge list (both endpoints active at loop entry).
+__global__ void k_degree(const uint64_t* __restrict__ edges, int64_t ne, int32_t m, int32_t* __restrict__ deg) {
+  FPI_GRID_STRIDE(e, ne) {
+    uint64_t ed = edges[e];
+    int32_t r = (int32_t)(ed >> 32);
+    int32_t c = (int32_t)(ed & 0xffffffffu) + m;
+    warp_agg_inc(deg, r);
+    warp_agg_inc(deg, c);
+  }
+}
+
+__global__ void k_gather_keys(const int32_t* __restrict__ ids, int64_t n, const int32_t* __restrict__ deg,
+                              uint32_t* __restrict__ keys) {
+  FPI_GRID_STRIDE(i, n) keys[i] = (uint32_t)deg[ids[i]];
+}
+
+// Hub i (in sorted order) gets id hi - i and leaves the active set.
+__global__ void k_assign_hubs(const int32_t* __restrict__ sorted_ids, int64_t cnt, int64_t hi, int32_t base,
+                              int64_t* __restrict__ fwd, uint8_t* __restrict__ state) {
+  FPI_GRID_STRIDE(i, cnt) {
+    int32_t v = sorted_ids[i];
+    fwd[v - base] = hi - i;
+    state[v] = 0;
+  }
+}
+
+// Union-find: parent[x] <= x always, so a root is the smallest id of its set.
+__device__ __forceinline__ int32_t find_root(int32_t x, int32_t* parent) {
+  int32_t cur = parent[x];
+  if (cur != x) {
+    int32_t prev = x, nxt;
+    while (cur > (nxt = parent[cur])) {
+      parent[prev] = nxt;  // path halving; benign race (values only move toward the root)
+      prev = cur;
+      cur = nxt;
+    }
+  }
+  return cur;
+}
+
+__global__ void k_hook(const uint64_t* __restrict__ edges, int64_t ne, int32_t m, const uint8_t* __restrict__ state,
+                       int32_t* parent) {
+  FPI_GRID_STRIDE(e, ne) {
+    uint64_t ed = edges[e];
+    int32_t u = (int32_t)(ed >> 32);
+    int32_t v = (int32_t)(ed & 0xffffffffu) + m;
+    if (!state[u] || !state[v]) continue;
+    int32_t ru = find_root(u, parent), rv = find_root(v, parent);
+    while (ru != rv) {
+      if (ru < rv) {
+        int32_t old = atomicCAS(parent + rv, rv, ru);
+        if (old == rv) break;
+        rv = find_root(old, parent);
+      } else {
+        int32_t old = atomicCAS(parent + ru, ru, rv);
+        if (old == ru) break;
+        ru = find_root(old, parent);
+      }
+    }
+  }
+}
+
+// Full compression + per-root size / row counts.
+__global__ void k_label_stats(const int32_t* __restrict__ act, int64_t cnt, int32_t m, int32_t* parent,
+                              int32_t* __restrict__ csize, int32_t* __restrict__ crows) {
+  FPI_GRID_STRIDE(i, cnt) {
+    int32_t v = act[i];
+    int32_t r = v;
+    while (parent[r] != r) r = parent[r];
+    parent[v] = r;
+    warp_agg_inc(csize, r);
+    if (v < m) warp_agg_inc(crows, r);
+  }
+}
+
+// Giant component: max size, ties by smallest root (= smallest member id).
+__global__ void k_pick_gcc(const int32_t* __restrict__ act, int64_t cnt, const int32_t* __restrict__ parent,
+                           const int32_t* __restrict__ csize, unsigned long long* best, int32_t* nroots) {
+  unsigned long long local = 0;
+  int32_t nr = 0;
+  FPI_GRID_STRIDE(i, cnt) {
+    int32_t v = act[i];
+    if (parent[v] == v) {
+      unsigned long long key = ((unsigned long long)(uint32_t)csize[v] << 32) | (uint32_t)(0x7fffffff - v);
+      local = key > local ? key : local;
+      ++nr;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long other = __shfl_xor_sync(0xffffffffu, local, o);
+    local = other > local ? other : local;
+    nr += __shfl_xor_sync(0xffffffffu, nr, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(best, local);
+    atomicAdd(nroots, nr);
+  }
+}
+
+struct IsSpokeRoot {
+  const int32_t* parent;
+  int32_t gcc;
+  __device__ bool operator()(int32_t v) const { return parent[v] == v && v != gcc; }
+};
+struct IsSpokeNode {
+  const int32_t* parent;
+  int32_t gcc;
+  __device__ bool operator()(int32_t v) const { return parent[v] != gcc; }
+};
+struct InComp {
+  const int32_t* parent;
+  int32_t gcc;
+  __device__ bool operator()(int32_t v) const { return parent[v] == gcc; }
+};
+struct IsActive {
+  const uint8_t* state;
+  __device__ bool operator()(int32_t v) const { return state[v] != 0; }
+};
+struct PositiveDeg {
+  const int32_t* deg;
+  __device__ bool operator()(int32_t v) const { return deg[v] > 0; }
+};
+struct EdgeLive {
+  const uint8_t* state;
+  int32_t m;
+  __device__ bool operator()(uint64_t e) const {
+    return state[(int32_t)(e >> 32)] && state[(int32_t)(e & 0xffffffffu) + m];
+  }
+};
+
+// Per spoke component (rank order): rows, cols, and the size key.
+__global__ void k_comp_table(const int32_t* __restrict__ roots_sorted, int64_t nc, const int32_t* __restrict__ csize,
+                             const int32_t* __restrict__ crows, int32_t* __restrict__ rank_of_root,
+                             int64_t* __restrict__ rows_c, int64_t* __restrict__ cols_c, int64_t* __restrict__ size_c) {
+  FPI_GRID_STRIDE(i, nc) {
+    int32_t r = roots_sorted[i];
+    rank_of_root[r] = (int32_t)i;
+    int64_t rows = crows[r], sz = csize[r];
+    rows_c[i] = rows;
+    cols_c[i] = sz - rows;
+    size_c[i] = sz;
+  }
+}
+
+__global__ void k_write_spans(int64_t nc, const int64_t* __restrict__ row_off, const int64_t* __restrict__ rows_c,
+                              const int64_t* __restrict__ col_off, const int64_t* __restrict__ cols_c, int64_t lo_t,
+                              int64_t lo_f, int64_t* __restrict__ spans) {
+  FPI_GRID_STRIDE(i, nc) {
+    spans[4 * i + 0] = lo_t + row_off[i];
+    spans[4 * i + 1] = rows_c[i];
+    spans[4 * i + 2] = lo_f + col_off[i];
+    spans[4 * i + 3] = cols_c[i];
+  }
+}
+
+__global__ void k_node_rank_keys(const int32_t* __restrict__ nodes, int64_t cnt, const int32_t* __restrict__ parent,
+                                 const int32_t* __restrict__ rank_of_root, uint32_t* __restrict__ keys) {
+  FPI_GRID_STRIDE(i, cnt) keys[i] = (uint32_t)rank_of_root[parent[nodes[i]]];
+}
+
+__global__ void k_emit_spokes(const int32_t* __restrict__ nodes, const uint32_t* __restrict__ ranks, int64_t cnt,
+                              int32_t m, const int64_t* __restrict__ node_off, const int64_t* __restrict__ row_off,
+                              const int64_t* __restrict__ col_off, const int64_t* __restrict__ rows_c, int64_t lo_t,
+                              int64_t lo_f, int64_t* __restrict__ row_fwd, int64_t* __restrict__ col_fwd,
+                              uint8_t* __restrict__ state) {
+  FPI_GRID_STRIDE(p, cnt) {
+    int32_t v = nodes[p];
+    uint32_t c = ranks[p];
+    int64_t pos = p - node_off[c];
+    if (v < m) {
+      row_fwd[v] = lo_t + row_off[c] + pos;
+    } else {
+      col_fwd[v - m] = lo_f + col_off[c] + pos - rows_c[c];
+    }
+    state[v] = 0;
+  }
+}
+
+__global__ void k_assign_tail(const int32_t* __restrict__ act, int64_t cnt, int32_t m, int64_t cnt_t, int64_t lo_t,
+                              int64_t lo_f, int64_t* __restrict__ row_fwd, int64_t* __restrict__ col_fwd) {
+  FPI_GRID_STRIDE(i, cnt) {
+    int32_t v = act[i];
+    if (i < cnt_t)
+      row_fwd[v] = lo_t + i;
+    else
+      col_fwd[v - m] = lo_f + (i - cnt_t);
+  }
+}
+
+}  // namespace
+
+struct ReorderOut {
+  int64_t m1, n1, m2, n2, T;
+};
+
+static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const int64_t* d_indptr,
+                        const int32_t* d_indices, double k, int64_t* d_row_fwd, int64_t* d_col_fwd,
+                        ReorderOut& out) {
+  cudaStream_t s = h->stream;
+  FPI_REQUIRE(k > 0.0 && k < 1.0, FPI_EDOMAIN, "hub selection ratio k must be in (0, 1)");
+  FPI_REQUIRE(m > 0 && n > 0, FPI_EDOMAIN, "graph has an empty node side");
+  FPI_REQUIRE(m + n < (int64_t)INT32_MAX, FPI_ECAPACITY, "m + n exceeds the int32 node-id range");
+  FPI_REQUIRE(nnz < (int64_t)INT32_MAX, FPI_ECAPACITY, "nnz exceeds the int32 edge-count range");
+  const int64_t V = m + n;
+  const int T = 256;
+  const unsigned G = (unsigned)(h->num_sms * 8);
+  CubTemp tmp(s);
+
+  Scratch<uint64_t> edges(nnz, s), edges2(nnz, s);
+  Scratch<uint8_t> state(V, s);
+  Scratch<int32_t> deg(V, s), parent(V, s), csize(V, s), crows(V, s), rank_of_root(V, s);
+  Scratch<int32_t> act(V, s), act2(V, s), cand(V, s), cand_sorted(V, s);
+  Scratch<uint32_t> keys(V, s), keys_sorted(V, s);
+  Scratch<int64_t> rows_c(V, s), cols_c(V, s), size_c(V, s), row_off(V, s), col_off(V, s), node_off(V, s);
+  Scratch<int32_t> d_count(4, s);
+  Scratch<unsigned long long> d_best(1, s);
+  // pinned staging for the per-iteration scalars
+  struct Stage {
+    int32_t counts[4];
+    unsigned long long best;
+    int32_t nroots;
+    int32_t gcc_rows;
+  };
+  Stage* hs = nullptr;
+  FPI_CUDA(cudaMallocHost((void**)&hs, sizeof(Stage)));
+  struct HostFree {
+    void* p;
+    ~HostFree() { cudaFreeHost(p); }
+  } hf{hs};
+
+  if (h->spans_cap < V) {
+    if (h->d_spans) cudaFree(h->d_spans);
+    FPI_CUDA(cudaMalloc((void**)&h->d_spans, sizeof(int64_t) * 4 * (V + 1)));
+    h->spans_cap = V;
+  }
+  h->n_spans = 0;
+  h->gcc_sizes.clear();
+
+  if (nnz) {
+    k_expand_edges<<<G, T, 0, s>>>(m, d_indptr, d_indices, edges);
+    FPI_LAUNCH_CHECK();
+  }
+  k_set_u8<<<G, T, 0, s>>>(state, V, 1);
+  k_fill_iota<<<G, T, 0, s>>>(act, V);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 3);
+
+  int64_t ne = nnz;
+  int64_t cnt_t = m, cnt_f = n;
+  int64_t lo_t = 0, lo_f = 0, hi_t = m - 1, hi_f = n - 1;
+  int64_t iters = 0;
+  const int deg_bits = bits_for((uint64_t)(m > n ? m : n));
+  const int rank_bits = bits_for((uint64_t)V);
+
+  while (true) {
+    ++iters;
+    const int64_t q_t = (int64_t)std::ceil(k * (double)cnt_t);  // math.ceil(k * cnt), reorder.py:198-199
+    const int64_t q_f = (int64_t)std::ceil(k * (double)cnt_f);
+    const int64_t cnt = cnt_t + cnt_f;
+
+    // 1. degrees over the compacted edge list
+    k_reset_nodes<<<grid_for(cnt, T, G), T, 0, s>>>(act, cnt, deg, parent, csize, crows);
+    if (ne) k_degree<<<grid_for(ne, T, G), T, 0, s>>>(edges, ne, (int32_t)m, deg);
+    FPI_LAUNCH_CHECK();
+    note_launch(h, 2);
+
+    // 2. hub candidates (ascending ids, positive degree), per side
+    select_if(tmp, act.get(), cand.get(), d_count.get() + 0, cnt_t, PositiveDeg{deg}, s);
+    select_if(tmp, act.get() + cnt_t, cand.get() + cnt_t, d_count.get() + 1, cnt_f, PositiveDeg{deg}, s);
+    FPI_CUDA(cudaMemcpyAsync(hs->counts, d_count.get(), 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+    note_launch(h, 2);
+    const int64_t c_t = hs->counts[0], c_f = hs->counts[1];
+    const int64_t h_t = q_t > 0 ? (q_t < c_t ? q_t : c_t) : 0;
+    const int64_t h_f = q_f > 0 ? (q_f < c_f ? q_f : c_f) : 0;
+    for (int side = 0; side < 2; ++side) {
+      const int64_t c = side ? c_f : c_t;
+      const int64_t hcount = side ? h_f : h_t;
+      if (hcount == 0) continue;
+      int32_t* cnd = cand.get() + (side ? cnt_t : 0);
+      int32_t* cs = cand_sorted.get() + (side ? cnt_t : 0);
+      uint32_t* kk = keys.get() + (side ? cnt_t : 0);
+      uint32_t* ks = keys_sorted.get() + (side ? cnt_t : 0);
+      k_gather_keys<<<grid_for(c, T, G), T, 0, s>>>(cnd, c, deg, kk);
+      sort_pairs(tmp, kk, ks, cnd, cs, c, /*descending=*/true, 0, deg_bits, s);
+      if (side == 0)
+        k_assign_hubs<<<grid_for(hcount, T, G), T, 0, s>>>(cs, hcount, hi_t, 0, d_row_fwd, state);
+      else
+        k_assign_hubs<<<grid_for(hcount, T, G), T, 0, s>>>(cs, hcount, hi_f, (int32_t)m, d_col_fwd, state);
+      FPI_LAUNCH_CHECK();
+      note_launch(h, 3);
+    }
+    hi_t -= h_t;
+    hi_f -= h_f;
+    cnt_t -= h_t;
+    cnt_f -= h_f;
+    // drop the hubs from the active list (keeps ascending order)
+    if (h_t + h_f) {
+      select_if(tmp, act.get(), act2.get(), d_count.get() + 2, cnt + 0, IsActive{state}, s);
+      std::swap(act, act2);
+      note_launch(h, 1);
+    }
+    const int64_t acnt = cnt_t + cnt_f;
+    if (acnt == 0) {  // reorder.py:224-226
+      h->gcc_sizes.push_back(0);
+      break;
+    }
+
+    // 3. connected components of the residual
+    if (ne) k_hook<<<grid_for(ne, T, G), T, 0, s>>>(edges, ne, (int32_t)m, state, parent);
+    k_label_stats<<<grid_for(acnt, T, G), T, 0, s>>>(act, acnt, (int32_t)m, parent, csize, crows);
+    FPI_CUDA(cudaMemsetAsync(d_best.get(), 0, sizeof(unsigned long long), s));
+    FPI_CUDA(cudaMemsetAsync(d_count.get() + 3, 0, sizeof(int32_t), s));
+    k_pick_gcc<<<grid_for(acnt, T, G), T, 0, s>>>(act, acnt, parent, csize, d_best, d_count.get() + 3);
+    FPI_LAUNCH_CHECK();
+    note_launch(h, 3);
+    FPI_CUDA(cudaMemcpyAsync(&hs->best, d_best.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaMemcpyAsync(&hs->nroots, d_count.get() + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+    const int32_t gcc = (int32_t)(0x7fffffff - (int64_t)(hs->best & 0xffffffffull));
+    const int64_t gcc_size = (int64_t)(hs->best >> 32);
+    FPI_CUDA(cudaMemcpyAsync(&hs->gcc_rows, crows.get() + gcc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+    const int64_t gcc_t = hs->gcc_rows, gcc_f = gcc_size - gcc_t;
+    const int64_t nsc = (int64_t)hs->nroots - 1;
+
+    // 4. spoke components -> blocks, members ascending within each side
+    if (nsc > 0) {
+      select_if(tmp, act.get(), cand.get(), d_count.get() + 0, acnt, IsSpokeRoot{parent, gcc}, s);
+      k_gather_keys<<<grid_for(nsc, T, G), T, 0, s>>>(cand, nsc, csize, keys);
+      sort_pairs(tmp, keys.get(), keys_sorted.get(), cand.get(), cand_sorted.get(), nsc, true, 0, rank_bits, s);
+      k_comp_table<<<grid_for(nsc, T, G), T, 0, s>>>(cand_sorted, nsc, csize, crows, rank_of_root, rows_c, cols_c,
+                                                     size_c);
+      exclusive_sum(tmp, rows_c.get(), row_off.get(), nsc, s);
+      exclusive_sum(tmp, cols_c.get(), col_off.get(), nsc, s);
+      exclusive_sum(tmp, size_c.get(), node_off.get(), nsc, s);
+      k_write_spans<<<grid_for(nsc, T, G), T, 0, s>>>(nsc, row_off, rows_c, col_off, cols_c, lo_t, lo_f,
+                                                      h->d_spans + 4 * h->n_spans);
+      const int64_t nsp = acnt - gcc_size;
+      select_if(tmp, act.get(), cand.get(), d_count.get() + 1, acnt, IsSpokeNode{parent, gcc}, s);
+      k_node_rank_keys<<<grid_for(nsp, T, G), T, 0, s>>>(cand, nsp, parent, rank_of_root, keys);
+      sort_pairs(tmp, keys.get(), keys_sorted.get(), cand.get(), cand_sorted.get(), nsp, false, 0, rank_bits, s);
+      k_emit_spokes<<<grid_for(nsp, T, G), T, 0, s>>>(cand_sorted, keys_sorted, nsp, (int32_t)m, node_off, row_off,
+                                                      col_off, rows_c, lo_t, lo_f, d_row_fwd, d_col_fwd, state);
+      FPI_LAUNCH_CHECK();
+      note_launch(h, 12);
+      h->n_spans += nsc;
+    }
+    lo_t += cnt_t - gcc_t;
+    lo_f += cnt_f - gcc_f;
+
+    // 5. giant component becomes the active set
+    select_if(tmp, act.get(), act2.get(), d_count.get() + 2, acnt, InComp{parent, gcc}, s);
+    std::swap(act, act2);
+    note_launch(h, 1);
+    h->gcc_sizes.push_back(gcc_size);
+    cnt_t = gcc_t;
+    cnt_f = gcc_f;
+    if (gcc_t < q_t || gcc_f < q_f) break;  // reorder.py:268-269
+    // compact edges to the new active set
+    if (ne) {
+      select_if(tmp, edges.get(), edges2.get(), d_count.get() + 3, ne, EdgeLive{state, (int32_t)m}, s);
+      FPI_CUDA(cudaMemcpyAsync(hs->counts + 3, d_count.get() + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      FPI_CUDA(cudaStreamSynchronize(s));
+      ne = hs->counts[3];
+      std::swap(edges, edges2);
+      note_launch(h, 1);
+    }
+  }
+  // terminal GCC: middle ids, ascending (reorder.py:271-275)
+  const int64_t rem = cnt_t + cnt_f;
+  if (rem) {
+    k_assign_tail<<<grid_for(rem, T, G), T, 0, s>>>(act, rem, (int32_t)m, cnt_t, lo_t, lo_f, d_row_fwd, d_col_fwd);
+    FPI_LAUNCH_CHECK();
+    note_launch(h, 1);
+  }
+  FPI_CUDA(cudaStreamSynchronize(s));
+  out.m1 = lo_t;
+  out.n1 = lo_f;
+  out.m2 = m - lo_t;
+  out.n2 = n - lo_f;
+  out.T = iters;
+}
+
+}  // namespace fpi
+
+extern "C" int fpi_reorder(fpi_handle h, int64_t m, int64_t n, int64_t nnz, const int64_t* d_indptr,
+                           const int32_t* d_indices, double k, int64_t* d_row_fwd, int64_t* d_col_fwd,
+                           fpi_reorder_info* info) {
+  FPI_API_BEGIN(h)
+  fpi::ReorderOut o{};
+  fpi::run_reorder(h, m, n, nnz, d_indptr, d_indices, k, d_row_fwd, d_col_fwd, o);
+  if (info) {
+    info->m1 = o.m1;
+    info->n1 = o.n1;
+    info->m2 = o.m2;
+    info->n2 = o.n2;
+    info->n_iterations = o.T;
+    info->n_spans = h->n_spans;
+    info->n_gcc = (int64_t)h->gcc_sizes.size();
+  }
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_reorder_fetch(fpi_handle h, int64_t* d_spans, int64_t* h_gcc) {
+  FPI_API_BEGIN(h)
+  if (d_spans && h->n_spans)
+    FPI_CUDA(cudaMemcpyAsync(d_spans, h->d_spans, sizeof(int64_t) * 4 * h->n_spans, cudaMemcpyDeviceToDevice,
+                             h->stream));
+  if (h_gcc)
+    for (size_t i = 0; i < h->gcc_sizes.size(); ++i) h_gcc[i] = h->gcc_sizes[i];
+  FPI_CUDA(cudaStreamSynchronize(h->stream));
+  FPI_API_END(h)
+}

@@ -1,0 +1,350 @@
+"""Hub/spoke reordering and the 2x2 partition -- the reference's reorder.py API
+(``/root/reference/pkg/src/fastpi/reorder.py``) on the B200 core.
+
+Results are device-resident; the numpy / scipy views the reference returns
+are materialised on first access (``Permutation.forward``,
+``ReorderResult.blocks``, ...), so the hot path never pays for host copies
+it does not need.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+from typing import NamedTuple
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from ._device import DeviceCSR, d2h, empty, h2d, torch
+
+
+class Permutation:
+    """A bijection on {0..len-1}; ``forward[old] = new``, ``backward[new] = old`` (reorder.py:26-62)."""
+
+    __slots__ = ("_fwd_dev", "_fwd", "_bwd")
+
+    def __init__(self, forward, backward=None):
+        self._fwd_dev = None
+        self._fwd = None
+        self._bwd = None
+        if _is_tensor(forward):
+            self._fwd_dev = forward
+            return
+        fwd = np.asarray(forward, dtype=np.int64)
+        bwd = np.asarray(backward, dtype=np.int64) if backward is not None else None
+        if bwd is None:
+            bwd = np.empty_like(fwd)
+            bwd[fwd] = np.arange(len(fwd))
+        if fwd.shape != bwd.shape:
+            raise ValueError("forward and backward arrays differ in length")
+        size = len(fwd)
+        if size and (fwd.min() < 0 or fwd.max() >= size or bwd.min() < 0 or bwd.max() >= size):
+            raise ValueError("permutation entries out of range")
+        if not np.array_equal(bwd[fwd], np.arange(size)):
+            raise ValueError("forward and backward are not mutually inverse")
+        self._fwd, self._bwd = fwd, bwd
+
+    @classmethod
+    def from_forward(cls, forward) -> "Permutation":
+        return cls(forward)
+
+    @classmethod
+    def identity(cls, n: int) -> "Permutation":
+        idx = np.arange(n, dtype=np.int64)
+        return cls(idx, idx.copy())
+
+    @property
+    def forward(self) -> np.ndarray:
+        if self._fwd is None:
+            self._fwd = d2h(self._fwd_dev)
+        return self._fwd
+
+    @property
+    def backward(self) -> np.ndarray:
+        if self._bwd is None:
+            if self._fwd_dev is not None:
+                t = torch()
+                bwd = t.empty_like(self._fwd_dev)
+                bwd[self._fwd_dev] = t.arange(len(self._fwd_dev), device=bwd.device, dtype=bwd.dtype)
+                self._bwd = d2h(bwd)
+            else:
+                self._bwd = np.empty_like(self._fwd)
+                self._bwd[self._fwd] = np.arange(len(self._fwd))
+        return self._bwd
+
+    def device_forward(self):
+        if self._fwd_dev is None:
+            self._fwd_dev = h2d(self._fwd, np.int64)
+        return self._fwd_dev
+
+    def __len__(self) -> int:
+        return int(self._fwd_dev.numel()) if self._fwd_dev is not None else len(self._fwd)
+
+    def __eq__(self, other):
+        return isinstance(other, Permutation) and np.array_equal(self.forward, other.forward)
+
+    def __repr__(self):
+        return f"Permutation(len={len(self)})"
+
+
+def _is_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+class BipartiteGraph:
+    """Bipartite adjacency of a sparse matrix (reorder.py:65-88); the pattern stays on the device."""
+
+    def __init__(self, n_instances, n_features, instance_ptr=None, instance_adj=None,
+                 feature_ptr=None, feature_adj=None, *, _dev=None):
+        self.n_instances = int(n_instances)
+        self.n_features = int(n_features)
+        self._dev = _dev            # DeviceCSR of A (pattern + values)
+        self._dev_t = None
+        self._host = {}
+        for k, v in (("instance_ptr", instance_ptr), ("instance_adj", instance_adj),
+                     ("feature_ptr", feature_ptr), ("feature_adj", feature_adj)):
+            if v is not None:
+                self._host[k] = np.asarray(v, dtype=np.int64)
+
+    def _device_pattern(self) -> DeviceCSR:
+        if self._dev is None:
+            ptr = self._host["instance_ptr"]
+            adj = self._host["instance_adj"]
+            self._dev = DeviceCSR((self.n_instances, self.n_features), h2d(ptr, np.int64), h2d(adj, np.int32),
+                                  h2d(np.ones(len(adj)), np.float64))
+        return self._dev
+
+    def _get(self, name):
+        if name not in self._host:
+            if name.startswith("instance"):
+                d = self._device_pattern()
+            else:
+                if self._dev_t is None:
+                    self._dev_t = self._device_pattern().transpose()
+                d = self._dev_t
+            self._host[name] = d2h(d.indptr if name.endswith("ptr") else d.indices).astype(np.int64)
+        return self._host[name]
+
+    instance_ptr = property(lambda self: self._get("instance_ptr"))
+    instance_adj = property(lambda self: self._get("instance_adj"))
+    feature_ptr = property(lambda self: self._get("feature_ptr"))
+    feature_adj = property(lambda self: self._get("feature_adj"))
+
+    @property
+    def n_edges(self) -> int:
+        return self._dev.nnz if self._dev is not None else len(self._host["instance_adj"])
+
+    def instance_neighbors(self, i: int) -> np.ndarray:
+        return self.instance_adj[self.instance_ptr[i]:self.instance_ptr[i + 1]]
+
+    def feature_neighbors(self, j: int) -> np.ndarray:
+        return self.feature_adj[self.feature_ptr[j]:self.feature_ptr[j + 1]]
+
+
+class BlockSpan(NamedTuple):
+    """Row/column ranges of one diagonal block of the spoke region (reorder.py:91-97)."""
+
+    row_start: int
+    row_len: int
+    col_start: int
+    col_len: int
+
+
+class ReorderResult:
+    """Permutations plus the block metadata of the 2x2 partition (reorder.py:100-120).
+
+    ``blocks`` is materialised lazily from the device span table
+    (``spans_device``, shape (B, 4) int64).
+    """
+
+    def __init__(self, row_perm, col_perm, n_spoke_rows, n_spoke_cols, n_hub_rows, n_hub_cols, blocks=None,
+                 n_iterations=0, gcc_sizes=(), *, spans_device=None):
+        self.row_perm = row_perm
+        self.col_perm = col_perm
+        self.n_spoke_rows = int(n_spoke_rows)
+        self.n_spoke_cols = int(n_spoke_cols)
+        self.n_hub_rows = int(n_hub_rows)
+        self.n_hub_cols = int(n_hub_cols)
+        self.n_iterations = int(n_iterations)
+        self.gcc_sizes = tuple(int(g) for g in gcc_sizes)
+        self._blocks = tuple(BlockSpan(*map(int, b)) for b in blocks) if blocks is not None else None
+        self._spans_dev = spans_device
+        self._spans_np = None
+        if self.n_spoke_rows + self.n_hub_rows != len(self.row_perm):
+            raise ValueError("spoke and hub row counts do not sum to the row count")
+        if self.n_spoke_cols + self.n_hub_cols != len(self.col_perm):
+            raise ValueError("spoke and hub column counts do not sum to the column count")
+
+    @property
+    def spans(self) -> np.ndarray:
+        if self._spans_np is None:
+            if self._spans_dev is not None:
+                self._spans_np = d2h(self._spans_dev).reshape(-1, 4)
+            else:
+                self._spans_np = np.asarray(self._blocks, dtype=np.int64).reshape(-1, 4)
+        return self._spans_np
+
+    def spans_device(self):
+        if self._spans_dev is None:
+            self._spans_dev = h2d(self.spans.reshape(-1), np.int64)
+        return self._spans_dev
+
+    @property
+    def blocks(self) -> tuple:
+        if self._blocks is None:
+            self._blocks = tuple(BlockSpan(*row) for row in self.spans.tolist())
+        return self._blocks
+
+    @property
+    def n_blocks(self) -> int:
+        return int(self._spans_dev.numel() // 4) if self._spans_dev is not None and self._blocks is None \
+            else len(self.blocks)
+
+    def __eq__(self, other):
+        if not isinstance(other, ReorderResult):
+            return NotImplemented
+        return (self.row_perm == other.row_perm and self.col_perm == other.col_perm
+                and (self.n_spoke_rows, self.n_spoke_cols, self.n_hub_rows, self.n_hub_cols, self.n_iterations)
+                == (other.n_spoke_rows, other.n_spoke_cols, other.n_hub_rows, other.n_hub_cols, other.n_iterations)
+                and np.array_equal(self.spans, other.spans))
+
+    def __repr__(self):
+        return (f"ReorderResult(m1={self.n_spoke_rows}, n1={self.n_spoke_cols}, m2={self.n_hub_rows}, "
+                f"n2={self.n_hub_cols}, blocks={self.n_blocks}, T={self.n_iterations})")
+
+
+def to_bipartite(A) -> BipartiteGraph:
+    """reorder.py:123-134: one edge per stored nonzero of canonical A."""
+    dev = A if isinstance(A, DeviceCSR) else DeviceCSR.from_host(A)
+    return BipartiteGraph(dev.shape[0], dev.shape[1], _dev=dev)
+
+
+def degree_histograms(graph: BipartiteGraph):
+    """reorder.py:137-146 (exact {degree: count} per side)."""
+    inst = np.diff(graph.instance_ptr)
+    feat = np.diff(graph.feature_ptr)
+
+    def _hist(deg):
+        values, counts = np.unique(deg, return_counts=True)
+        return {int(d): int(c) for d, c in zip(values, counts)}
+
+    return _hist(inst), _hist(feat)
+
+
+def reorder_device(dev: DeviceCSR, k: float) -> ReorderResult:
+    """Algorithm 2 on the GPU (fpi_reorder); everything stays in HBM."""
+    if not 0.0 < k < 1.0:
+        raise ValueError(f"hub selection ratio k must be in (0, 1), got {k}")
+    m, n = dev.shape
+    if m == 0 or n == 0:
+        raise ValueError("graph has an empty node side")
+    row_fwd = empty(m, "i64")
+    col_fwd = empty(n, "i64")
+    info = _lib.ReorderInfo()
+    _lib.call("fpi_reorder", m, n, dev.nnz, _lib.ptr(dev.indptr), _lib.ptr(dev.indices), float(k),
+              _lib.ptr(row_fwd), _lib.ptr(col_fwd), C.byref(info))
+    spans = empty(max(info.n_spans, 0) * 4, "i64")
+    gcc = (C.c_int64 * max(info.n_gcc, 1))()
+    _lib.call("fpi_reorder_fetch", _lib.ptr(spans), gcc)
+    return ReorderResult(Permutation(row_fwd), Permutation(col_fwd), info.m1, info.n1, info.m2, info.n2,
+                         None, info.n_iterations, [gcc[i] for i in range(info.n_gcc)], spans_device=spans)
+
+
+def reorder(graph: BipartiteGraph, k: float) -> ReorderResult:
+    """reorder.py:158-287 -- bit-exact permutations, spans, T and GCC sizes."""
+    return reorder_device(graph._device_pattern(), k)
+
+
+def _dev_of(A) -> DeviceCSR:
+    return A if isinstance(A, DeviceCSR) else DeviceCSR.from_host(A)
+
+
+def apply_permutation_device(dev: DeviceCSR, row_perm: Permutation, col_perm: Permutation) -> DeviceCSR:
+    m, n = dev.shape
+    if len(row_perm) != m:
+        raise ValueError(f"row permutation has length {len(row_perm)}, matrix has {m} rows")
+    if len(col_perm) != n:
+        raise ValueError(f"column permutation has length {len(col_perm)}, matrix has {n} columns")
+    out = DeviceCSR.empty(m, n, dev.nnz)
+    _lib.call("fpi_permute", m, n, dev.nnz, _lib.ptr(dev.indptr), _lib.ptr(dev.indices), _lib.ptr(dev.values),
+              _lib.ptr(row_perm.device_forward()), _lib.ptr(col_perm.device_forward()),
+              _lib.ptr(out.indptr), _lib.ptr(out.indices), _lib.ptr(out.values))
+    return out
+
+
+def apply_permutation(A, row_perm: Permutation, col_perm: Permutation) -> sp.csr_matrix:
+    """reorder.py:290-307."""
+    return apply_permutation_device(_dev_of(A), row_perm, col_perm).to_host()
+
+
+class DevicePartition:
+    """A11 (m1 x n1), T = [A12; A22] (m x n2) and A21 (m2 x n1), with transposes, in HBM."""
+
+    def __init__(self, a11, T, Tt, a21, a21t, info):
+        self.a11, self.T, self.Tt, self.a21, self.a21t = a11, T, Tt, a21, a21t
+        self.info = info
+
+
+def partition_original(dev: DeviceCSR, result: ReorderResult, *, transposes: bool = True) -> DevicePartition:
+    """Permute + partition straight from the ORIGINAL matrix (the hot path: no full permuted copy)."""
+    m, n = dev.shape
+    m1, n1 = result.n_spoke_rows, result.n_spoke_cols
+    m2, n2 = m - m1, n - n1
+    spans = result.spans_device()
+    nsp = int(spans.numel() // 4)
+    info = _lib.PartitionInfo()
+    rf, cf = result.row_perm.device_forward(), result.col_perm.device_forward()
+    _lib.call("fpi_partition_count", m, n, dev.nnz, _lib.ptr(dev.indptr), _lib.ptr(dev.indices), _lib.ptr(rf),
+              _lib.ptr(cf), m1, n1, nsp, _lib.ptr(spans), C.byref(info))
+    nT = info.nnz_a12 + info.nnz_a22
+    a11 = DeviceCSR.empty(m1, n1, info.nnz_a11)
+    T = DeviceCSR.empty(m, n2, nT)
+    a21 = DeviceCSR.empty(m2, n1, info.nnz_a21)
+    Tt = DeviceCSR.empty(n2, m, nT) if transposes else None
+    a21t = DeviceCSR.empty(n1, m2, info.nnz_a21) if transposes else None
+
+    def p3(x):
+        return [None, None, None] if x is None else [_lib.ptr(x.indptr), _lib.ptr(x.indices), _lib.ptr(x.values)]
+
+    _lib.call("fpi_partition", m, n, dev.nnz, _lib.ptr(dev.indptr), _lib.ptr(dev.indices), _lib.ptr(dev.values),
+              _lib.ptr(rf), _lib.ptr(cf), m1, n1, nsp, _lib.ptr(spans), *p3(a11), *p3(T), *p3(Tt), *p3(a21), *p3(a21t))
+    return DevicePartition(a11, T, Tt, a21, a21t, info)
+
+
+def partition(A_reordered, result: ReorderResult):
+    """reorder.py:310-337 on an already-permuted matrix: (A11 block list, A12, A21, A22) as scipy CSR."""
+    dev = _dev_of(A_reordered)
+    m1, n1 = result.n_spoke_rows, result.n_spoke_cols
+    if dev.shape != (m1 + result.n_hub_rows, n1 + result.n_hub_cols):
+        raise ValueError(f"matrix shape {dev.shape} does not match reorder result "
+                         f"({m1 + result.n_hub_rows}, {n1 + result.n_hub_cols})")
+    ident = ReorderResult(Permutation.identity(dev.shape[0]), Permutation.identity(dev.shape[1]), m1, n1,
+                          result.n_hub_rows, result.n_hub_cols, None, result.n_iterations, result.gcc_sizes,
+                          spans_device=result.spans_device())
+    part = partition_original(dev, ident, transposes=False)
+    spoke = part.a11.to_host()
+    T = part.T.to_host()
+    blocks = [spoke[rs:rs + rl, cs:cs + cl].tocsr() for rs, rl, cs, cl in result.spans.tolist()]
+    return blocks, T[:m1].tocsr(), part.a21.to_host(), T[m1:].tocsr()
+
+
+def save_reorder_result(result: ReorderResult, path):
+    """reorder.py:340-350 text format."""
+    lines = [f"{result.n_spoke_rows} {result.n_spoke_cols} {result.n_hub_rows} {result.n_hub_cols} "
+             f"{result.n_iterations} {len(result.spans)}",
+             " ".join(map(str, result.row_perm.forward.tolist())),
+             " ".join(map(str, result.col_perm.forward.tolist()))]
+    lines += [" ".join(map(str, row)) for row in result.spans.tolist()]
+    Path(path).write_text("\n".join(lines) + "\n", encoding="utf-8")
+
+
+def load_reorder_result(path) -> ReorderResult:
+    """reorder.py:353-370."""
+    lines = Path(path).read_text(encoding="utf-8").splitlines()
+    m1, n1, m2, n2, iterations, n_blocks = (int(v) for v in lines[0].split())
+    row_perm = Permutation.from_forward([int(v) for v in lines[1].split()])
+    col_perm = Permutation.from_forward([int(v) for v in lines[2].split()])
+    blocks = [tuple(int(v) for v in line.split()) for line in lines[3:3 + n_blocks]]
+    return ReorderResult(row_perm, col_perm, m1, n1, m2, n2, blocks, iterations)
