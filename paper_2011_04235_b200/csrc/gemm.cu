@@ -1,0 +1,274 @@
+// FP64 GEMM on the sm_100a double-precision tensor path (mma.sync m8n8k4 f64
+// -> SASS DMMA).  tcgen05 has no f64 kind, so DMMA is the FP64 tensor-core
+// instruction on B200.
+//
+//   C = alpha * op(A) * op(B) + beta * C,   all row-major, op = identity / transpose
+//
+// CTA tile 128 x 128 x 16, 8 warps (2 x 4), warp tile 64 x 32 = 8 x 4 DMMA
+// tiles (64 accumulator doubles per thread).  Operands stream global -> smem
+// with a 3-stage cp.async ring; the smem layouts are padded so every
+// fragment load is bank-conflict free for all four transpose combinations.
+// Split-K (deterministic: partial tiles + ordered reduction) covers the
+// tall-skinny Gram / projection shapes where M x N alone cannot fill 148 SMs.
+// Used for: U.Sigma x X1 and Q^T inner (svd.py:133,135 dense parts), the
+// Gram matrices of CholeskyQR and of the small SVD, the lifts
+// (pinv.py:169,206) and V (Sigma+ U^T Y) (pinv.py:81).
+#include "common.cuh"
+#include "capi_guard.cuh"
+#include "gemm.cuh"
+
+namespace fpi {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, NT = 256;
+constexpr int PAD = 4;
+// smem strides (doubles)
+constexpr int LDA_MK = BK + PAD;   // As[m][k]
+constexpr int LDA_KM = BM + PAD;   // As[k][m]
+constexpr int LDB_KN = BN + PAD;   // Bs[k][n]
+constexpr int LDB_NK = BK + PAD;   // Bs[n][k]
+constexpr int A_STAGE = (BM * LDA_MK > BK * LDA_KM) ? BM * LDA_MK : BK * LDA_KM;
+constexpr int B_STAGE = (BN * LDB_NK > BK * LDB_KN) ? BN * LDB_NK : BK * LDB_KN;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+  unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// Load one BMxBK tile of op(A) and one BKxBN tile of op(B) into stage buffers.
+template <bool TA, bool TB>
+__device__ __forceinline__ void load_tiles(double* As, double* Bs, const double* A, int64_t lda, const double* B,
+                                           int64_t ldb, int64_t M, int64_t N, int64_t K, int64_t m0, int64_t n0,
+                                           int64_t k0) {
+  const int tid = threadIdx.x;
+  // A: 128 x 16 doubles = 2048 elements, 8 per thread
+#pragma unroll
+  for (int i = 0; i < (BM * BK) / NT; ++i) {
+    int e = tid + i * NT;
+    if (!TA) {  // A[m][k], k contiguous
+      int m = e / BK, k = e % BK;
+      int64_t gm = m0 + m, gk = k0 + k;
+      bool p = gm < M && gk < K;
+      cp_async8(As + m * LDA_MK + k, p ? A + gm * lda + gk : A, p);
+    } else {    // stored K x M, m contiguous
+      int k = e / BM, m = e % BM;
+      int64_t gm = m0 + m, gk = k0 + k;
+      bool p = gm < M && gk < K;
+      cp_async8(As + k * LDA_KM + m, p ? A + gk * lda + gm : A, p);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < (BN * BK) / NT; ++i) {
+    int e = tid + i * NT;
+    if (!TB) {  // B[k][n], n contiguous
+      int k = e / BN, n = e % BN;
+      int64_t gn = n0 + n, gk = k0 + k;
+      bool p = gn < N && gk < K;
+      cp_async8(Bs + k * LDB_KN + n, p ? B + gk * ldb + gn : B, p);
+    } else {    // stored N x K, k contiguous
+      int n = e / BK, k = e % BK;
+      int64_t gn = n0 + n, gk = k0 + k;
+      bool p = gn < N && gk < K;
+      cp_async8(Bs + n * LDB_NK + k, p ? B + gn * ldb + gk : B, p);
+    }
+  }
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(NT, 1)
+    k_gemm(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
+           const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
+           int64_t k_per_split, double* __restrict__ partial) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * A_STAGE;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb = (int64_t)blockIdx.z * k_per_split;
+  const int64_t ke = kb + k_per_split < K ? kb + k_per_split : K;
+  const int64_t ntiles = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;  // 2 x 4 warps
+  const int g = lane >> 2, t = lane & 3;
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // prologue
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ntiles)
+      load_tiles<TA, TB>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, ke, m0, n0, kb + s * BK);
+    cp_async_commit();
+  }
+  for (int64_t kt = 0; kt < ntiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    // prefetch tile kt + STAGES - 1 into the slot freed last iteration
+    {
+      int64_t nk = kt + STAGES - 1;
+      int slot = (int)(nk % STAGES);
+      if (nk < ntiles)
+        load_tiles<TA, TB>(As + slot * A_STAGE, Bs + slot * B_STAGE, A, lda, B, ldb, M, N, ke, m0, n0,
+                           kb + nk * BK);
+      cp_async_commit();
+    }
+    const double* as = As + (kt % STAGES) * A_STAGE;
+    const double* bs = Bs + (kt % STAGES) * B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[8], bf[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        int m = wm + i * 8 + g;
+        af[i] = TA ? as[(kk + t) * LDA_KM + m] : as[m * LDA_MK + kk + t];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int n = wn + j * 8 + g;
+        bf[j] = TB ? bs[n * LDB_NK + kk + t] : bs[(kk + t) * LDB_KN + n];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: accumulator (i, j) holds rows wm+8i+g, cols wn+8j+2t, +1
+  if (partial) {
+    double* P = partial + (int64_t)blockIdx.z * M * N;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int64_t r = m0 + wm + i * 8 + g;
+      if (r >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int64_t c = n0 + wn + j * 8 + 2 * t;
+        if (c < N) P[r * N + c] = acc[i][j][0];
+        if (c + 1 < N) P[r * N + c + 1] = acc[i][j][1];
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int64_t r = m0 + wm + i * 8 + g;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t c = n0 + wn + j * 8 + 2 * t;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (c + q < N) {
+          double v = alpha * acc[i][j][q];
+          double* dst = C + r * ldc + c + q;
+          *dst = beta == 0.0 ? v : v + beta * *dst;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_reduce_split(int64_t M, int64_t N, int splits, const double* __restrict__ P, double alpha,
+                               double beta, double* __restrict__ C, int64_t ldc) {
+  FPI_GRID_STRIDE(e, M * N) {
+    int64_t r = e / N, c = e - r * N;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += P[(int64_t)z * M * N + e];
+    double* dst = C + r * ldc + c;
+    double v = alpha * s;
+    *dst = beta == 0.0 ? v : v + beta * *dst;
+  }
+}
+
+__global__ void k_scale(int64_t M, int64_t N, double beta, double* __restrict__ C, int64_t ldc) {
+  FPI_GRID_STRIDE(e, M * N) {
+    int64_t r = e / N, c = e - r * N;
+    double* dst = C + r * ldc + c;
+    *dst = beta == 0.0 ? 0.0 : beta * *dst;
+  }
+}
+
+template <bool TA, bool TB>
+void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+            const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    FPI_CUDA(cudaFuncSetAttribute(k_gemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    attr_set = true;
+  }
+  cudaStream_t s = h->stream;
+  const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  const int64_t tiles = tm * tn;
+  int splits = 1;
+  const int64_t want = 2LL * h->num_sms;
+  if (tiles < want && K >= 4 * BK * 8) {
+    splits = (int)((want + tiles - 1) / tiles);
+    int64_t max_splits = K / (BK * 8);
+    if (splits > max_splits) splits = (int)max_splits;
+    if (splits > 64) splits = 64;
+    if (splits < 1) splits = 1;
+  }
+  FPI_REQUIRE(tm < 65536 && tn < (1LL << 31), FPI_ECAPACITY, "gemm grid too large");
+  if (splits == 1) {
+    dim3 grid((unsigned)tn, (unsigned)tm, 1);
+    k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, K, nullptr);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+    return;
+  }
+  int64_t kps = (K + splits - 1) / splits;
+  kps = (kps + BK - 1) / BK * BK;
+  splits = (int)((K + kps - 1) / kps);
+  Scratch<double> part((size_t)splits * M * N, s);
+  dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)splits);
+  k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps, part);
+  k_reduce_split<<<grid_for(M * N, 256, (int64_t)h->num_sms * 16), 256, 0, s>>>(M, N, splits, part, alpha, beta, C,
+                                                                                 ldc);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 2);
+}
+
+}  // namespace
+
+void gemm(fpi_context* h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+          int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return;
+  if (K <= 0) {
+    k_scale<<<grid_for(M * N, 256, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(M, N, beta, C, ldc);
+    FPI_LAUNCH_CHECK();
+    return;
+  }
+  if (!ta && !tb) launch<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (!ta && tb) launch<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else if (ta && !tb) launch<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  else launch<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+}  // namespace fpi
+
+extern "C" int fpi_gemm(fpi_handle h, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, double alpha,
+                        const double* d_A, int64_t lda, const double* d_B, int64_t ldb, double beta, double* d_C,
+                        int64_t ldc) {
+  FPI_API_BEGIN(h)
+  FPI_REQUIRE(M >= 0 && N >= 0 && K >= 0, FPI_EDOMAIN, "negative GEMM dimension");
+  fpi::gemm(h, trans_a != 0, trans_b != 0, M, N, K, alpha, d_A, lda, d_B, ldb, beta, d_C, ldc);
+  FPI_API_END(h)
+}
