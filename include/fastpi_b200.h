@@ -131,6 +131,72 @@ int fpi_sketch_normal(fpi_handle h, int64_t seed, int64_t rows, int64_t cols, do
 /* Host helper: PCG64 state after SeedSequence(seed) seeding (hi/lo words of state and inc). */
 int fpi_pcg64_seed(int64_t seed, uint64_t* h_state4 /* state_hi, state_lo, inc_hi, inc_lo */);
 
+/* ---- dense FP64 kernels (DMMA tensor path) ------------------------------ */
+/* C = alpha op(A) op(B) + beta C, row-major; op(A) M x K, op(B) K x N (the `@` products of
+ * svd.py:133,137 and pinv.py:81,169,206). */
+int fpi_gemm(fpi_handle h, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, double alpha,
+             const double* d_A, int64_t lda, const double* d_B, int64_t ldb, double beta, double* d_C, int64_t ldc);
+/* Y = alpha A X + beta Y, A CSR p x q, X q x k (sparse.py:20-39 multiply / multiply_transposed on A^T). */
+int fpi_spmm(fpi_handle h, int64_t p, int64_t q, int64_t k, const int64_t* d_indptr, const int32_t* d_indices,
+             const double* d_values, double alpha, const double* d_X, int64_t ldx, double beta, double* d_Y,
+             int64_t ldy);
+/* In-place lower Cholesky factor (CholeskyQR Gram); FPI_ENUMERIC if not positive definite. */
+int fpi_cholesky(fpi_handle h, int64_t n, double* d_A, int64_t lda);
+/* Symmetric eigendecomposition (block Jacobi): eigenvalues descending, eigenvectors as columns. */
+int fpi_sym_eig(fpi_handle h, int64_t n, const double* d_A, int64_t lda, double* d_w, double* d_V, int64_t ldv,
+                int32_t* h_sweeps);
+
+/* ---- svd.py SVD engines ------------------------------------------------- */
+/* svd.py:141-193 block_diagonal_svd: sizes of the block-sparse U11 / Vt11 (CSR) */
+int fpi_block_svd_plan(fpi_handle h, int64_t n_spans, const int64_t* d_spans, double alpha,
+                       fpi_block_plan* h_plan);
+/* U11 CSR (m1 x rank11), Vt11 CSR (rank11 x n1), sigma (rank11) from the spoke CSR A11 and its spans. */
+int fpi_block_svd(fpi_handle h, int64_t m1, int64_t n1, const int64_t* a11_ptr, const int32_t* a11_idx,
+                  const double* a11_val, int64_t n_spans, const int64_t* d_spans, double alpha, double* d_sigma,
+                  int64_t* u_ptr, int32_t* u_idx, double* u_val, int64_t* vt_ptr, int32_t* vt_idx, double* vt_val,
+                  fpi_block_plan* h_plan);
+/* svd.py:86-117 dense_svd + truncate: rank leading triplets of a dense p x q matrix (sorted). */
+int fpi_dense_svd(fpi_handle h, int64_t p, int64_t q, const double* d_M, int64_t ldm, int64_t rank,
+                  double* d_U, double* d_sigma, double* d_Vt);
+/* svd.py:120-138 randomized_svd of a CSR matrix (with its transpose): U p x rank, Vt rank x q. */
+int fpi_randomized_svd(fpi_handle h, int64_t p, int64_t q, const int64_t* a_ptr, const int32_t* a_idx,
+                       const double* a_val, const int64_t* at_ptr, const int32_t* at_idx, const double* at_val,
+                       int64_t rank, int64_t seed, double* d_U, double* d_sigma, double* d_Vt);
+
+/* ---- pinv.py FastPI stages ---------------------------------------------- */
+/* pinv.py:131-171 row_update: f11 = (sigma11, U11 CSR m1 x rank11, Vt11 CSR rank11 x n1), A21 CSR m2 x n1.
+ * Outputs U (m1+m2) x s, sigma s, Vt s x n1; *h_engine = 1 randomized / 2 dense. */
+int fpi_row_update(fpi_handle h, int64_t m1, int64_t n1, int64_t rank11, const double* sigma11,
+                   const int64_t* u_ptr, const int32_t* u_idx, const double* u_val,
+                   const int64_t* v_ptr, const int32_t* v_idx, const double* v_val,
+                   int64_t m2, const int64_t* a_ptr, const int32_t* a_idx, const double* a_val,
+                   int64_t s, double low_rank_threshold, int64_t seed,
+                   double* d_U, double* d_sigma, double* d_Vt, int32_t* h_engine);
+/* pinv.py:174-208 column_update: f = (U m x s_prev, sigma, Vt s_prev x n1), T = [A12; A22] CSR m x n2 (+ T^T).
+ * Outputs U m x r, sigma r, Vt r x (n1 + n2). */
+int fpi_column_update(fpi_handle h, int64_t m, int64_t s_prev, int64_t n1, const double* U_prev,
+                      const double* sigma_prev, const double* Vt_prev, int64_t n2,
+                      const int64_t* t_ptr, const int32_t* t_idx, const double* t_val,
+                      const int64_t* tt_ptr, const int32_t* tt_idx, const double* tt_val,
+                      int64_t r, double low_rank_threshold, int64_t seed,
+                      double* d_U, double* d_sigma, double* d_Vt, int32_t* h_engine);
+/* pinv.py:211-231 pinv_from_svd: sigma_dagger = 1/sigma where sigma > cutoff*smax*max(p,q,1). */
+int fpi_pinv_assemble(fpi_handle h, int64_t r, const double* d_sigma, int64_t p, int64_t q, double cutoff,
+                      double* d_sigma_dagger, double* h_tol, int32_t* h_all_filtered);
+/* pinv.py:271-275 + 226-228: V = Vt[:, col_fwd]^T (n x r), Ut = U[row_fwd, :]^T (r x m); either may be NULL. */
+int fpi_unfold(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U, const double* d_Vt,
+               const int64_t* d_row_fwd, const int64_t* d_col_fwd, double* d_V_out, double* d_Ut_out);
+/* pinv.py:72-81 Pseudoinverse.apply / regression.py:50-70 fit: Z (n x L) = V diag(sdag) Ut Y with the factors
+ * in reordered coordinates (U m x r, Vt r x n) and the row/column permutations; Y CSR m x L. */
+int fpi_pinv_apply_csr(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U,
+                       const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
+                       const int64_t* d_col_fwd, int64_t L, int64_t nnz, const int64_t* y_ptr,
+                       const int32_t* y_idx, const double* y_val, double* d_Z);
+/* Dense right-hand side variant (Y m x L row-major). */
+int fpi_pinv_apply_dense(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U,
+                         const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
+                         const int64_t* d_col_fwd, int64_t L, const double* d_Y, int64_t ldy, double* d_Z);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,23 @@ SIGNATURES = {
     "fpi_permute": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]),
     "fpi_sketch_normal": (C.c_int, [vp, i64, i64, i64, vp, i64]),
     "fpi_pcg64_seed": (C.c_int, [i64, P_u64]),
+    "fpi_gemm": (C.c_int, [vp, C.c_int, C.c_int, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64]),
+    "fpi_spmm": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, f64, vp, i64, f64, vp, i64]),
+    "fpi_cholesky": (C.c_int, [vp, i64, vp, i64]),
+    "fpi_sym_eig": (C.c_int, [vp, i64, vp, i64, vp, vp, i64, C.POINTER(i32)]),
+    "fpi_block_svd_plan": (C.c_int, [vp, i64, vp, f64, C.POINTER(BlockPlan)]),
+    "fpi_block_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, f64, vp, vp, vp, vp, vp, vp, vp,
+                                C.POINTER(BlockPlan)]),
+    "fpi_dense_svd": (C.c_int, [vp, i64, i64, vp, i64, i64, vp, vp, vp]),
+    "fpi_randomized_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp]),
+    "fpi_row_update": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, i64, f64, i64,
+                                 vp, vp, vp, C.POINTER(i32)]),
+    "fpi_column_update": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, i64, f64, i64,
+                                    vp, vp, vp, C.POINTER(i32)]),
+    "fpi_pinv_assemble": (C.c_int, [vp, i64, vp, i64, i64, f64, vp, C.POINTER(f64), C.POINTER(i32)]),
+    "fpi_unfold": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
+    "fpi_pinv_apply_csr": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp]),
+    "fpi_pinv_apply_dense": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp]),
 }
 
 _lib = None

@@ -1,0 +1,514 @@
+// Dense FP64 building blocks for the SVD engines:
+//   * Cholesky (blocked, right-looking; trailing updates on the DMMA GEMM) and
+//     lower-triangular solves with many right-hand sides -- CholeskyQR of the
+//     sketch (replaces LAPACK dgeqrf+dorgqr, svd.py:134),
+//   * a symmetric eigensolver: parallel two-sided block Jacobi (cyclic
+//     round-robin over 16-wide column blocks) in one cooperative kernel with
+//     grid-wide barriers between the solve / row-rotate / column-rotate
+//     phases -- the small SVDs (replaces dgesdd, svd.py:105,136,166),
+//   * small helpers: transpose, column norms, scaling, canonical signs.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "capi_guard.cuh"
+#include "cub_util.cuh"
+#include "gemm.cuh"
+#include "linalg.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fpi {
+namespace {
+
+constexpr int NB = 32;  // Cholesky / TRSM panel width
+
+// ---- Cholesky ------------------------------------------------------------
+__global__ void k_potrf_diag(double* A, int64_t lda, int jb, int* info, int64_t j0) {
+  __shared__ double S[NB][NB + 1];
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) S[e / jb][e % jb] = A[(e / jb) * lda + (e % jb)];
+  __syncthreads();
+  for (int k = 0; k < jb; ++k) {
+    if (threadIdx.x == 0) {
+      double d = S[k][k];
+      if (!(d > 0.0)) {
+        atomicCAS(info, 0, (int)(j0 + k + 1));
+        d = 1e-300;
+      }
+      S[k][k] = sqrt(d);
+    }
+    __syncthreads();
+    for (int i = k + 1 + threadIdx.x; i < jb; i += blockDim.x) S[i][k] /= S[k][k];
+    __syncthreads();
+    for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
+      int i = e / jb, j = e % jb;
+      if (j > k && i >= j) S[i][j] -= S[i][k] * S[j][k];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) {
+    int i = e / jb, j = e % jb;
+    A[i * lda + j] = (i >= j) ? S[i][j] : 0.0;
+  }
+}
+
+// rows below the diagonal block: x L11^T = a  (forward substitution), one thread per row
+__global__ void k_trsm_panel(double* A, int64_t lda, int64_t j0, int jb, int64_t n) {
+  __shared__ double L[NB][NB + 1];
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) L[e / jb][e % jb] = A[(j0 + e / jb) * lda + j0 + e % jb];
+  __syncthreads();
+  for (int64_t r = j0 + jb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double x[NB];
+    double* a = A + r * lda + j0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      if (k < jb) {
+        double v = a[k];
+        for (int i = 0; i < k; ++i) v -= x[i] * L[k][i];
+        x[k] = v / L[k][k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      if (k < jb) a[k] = x[k];
+  }
+}
+
+// X[j0:j0+jb, :] = L_jj^{-1} X[j0:j0+jb, :]   one thread per right-hand-side column
+__global__ void k_trsm_diag(const double* L, int64_t ldl, int64_t j0, int jb, double* X, int64_t ldx, int64_t nrhs) {
+  __shared__ double S[NB][NB + 1];
+  for (int e = threadIdx.x; e < jb * jb; e += blockDim.x) S[e / jb][e % jb] = L[(j0 + e / jb) * ldl + j0 + e % jb];
+  __syncthreads();
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nrhs; c += (int64_t)gridDim.x * blockDim.x) {
+    double x[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      if (k < jb) {
+        double v = X[(j0 + k) * ldx + c];
+        for (int i = 0; i < k; ++i) v -= S[k][i] * x[i];
+        x[k] = v / S[k][k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k)
+      if (k < jb) X[(j0 + k) * ldx + c] = x[k];
+  }
+}
+
+__global__ void k_set_identity(int64_t n, double* A, int64_t lda) {
+  FPI_GRID_STRIDE(e, n * n) {
+    int64_t i = e / n, j = e - i * n;
+    A[i * lda + j] = i == j ? 1.0 : 0.0;
+  }
+}
+
+// ---- symmetric block Jacobi ------------------------------------------------
+constexpr int JB = 16;         // column block width
+constexpr int JS = 2 * JB;     // sub-problem size
+constexpr int JT = 256;        // threads per CTA
+constexpr int TILE = 64;       // columns (phase B) / rows (phase C) per work item
+
+__device__ __forceinline__ int rr_block(int pos, int round, int nb) {
+  return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (nb - 1));
+}
+
+__device__ __forceinline__ int sub_to_global(int l, int bi, int bj) { return l < JB ? bi * JB + l : bj * JB + (l - JB); }
+
+__global__ void __launch_bounds__(JT)
+    k_jacobi(int nb, double* G, int64_t ldg, double* V, int64_t ldv, double* Jbuf, int* flags, int max_sweeps,
+             double tol, int inner_sweeps, int* sweeps_out) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double S[JS][JS + 1];
+  __shared__ double R[JS][JS + 1];
+  __shared__ double T[JS][TILE + 1];
+  __shared__ double cs_c[JS / 2], cs_s[JS / 2];
+  __shared__ int pair_p[JS / 2], pair_q[JS / 2];
+  __shared__ int any_rot;
+  const int npairs = nb / 2;
+  const int64_t npad = (int64_t)nb * JB;
+  const int64_t ctiles = (npad + TILE - 1) / TILE;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int round = 0; round < nb - 1; ++round) {
+      // ---- phase A: solve each 2b x 2b sub-problem, accumulate its rotation
+      for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+        const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
+        for (int e = threadIdx.x; e < JS * JS; e += JT) {
+          int a = e / JS, b = e % JS;
+          S[a][b] = G[(int64_t)sub_to_global(a, bi, bj) * ldg + sub_to_global(b, bi, bj)];
+          R[a][b] = a == b ? 1.0 : 0.0;
+        }
+        if (threadIdx.x == 0) any_rot = 0;
+        __syncthreads();
+        for (int isw = 0; isw < inner_sweeps; ++isw) {
+          for (int step = 0; step < JS - 1; ++step) {
+            if (threadIdx.x < JS / 2) {
+              const int k = threadIdx.x;
+              // round-robin (circle) pairing of the JS local indices
+              const int p = rr_block(k, step, JS), q = rr_block(JS - 1 - k, step, JS);
+              double app = S[p][p], aqq = S[q][q], apq = S[p][q];
+              double c = 1.0, s = 0.0;
+              if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
+                double zeta = (aqq - app) / (2.0 * apq);
+                double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                c = 1.0 / sqrt(1.0 + t * t);
+                s = c * t;
+                any_rot = 1;
+              }
+              cs_c[k] = c;
+              cs_s[k] = s;
+              pair_p[k] = p;
+              pair_q[k] = q;
+            }
+            __syncthreads();
+            // rows
+            for (int e = threadIdx.x; e < (JS / 2) * JS; e += JT) {
+              int k = e / JS, col = e % JS;
+              double c = cs_c[k], s = cs_s[k];
+              if (s == 0.0) continue;
+              int p = pair_p[k], q = pair_q[k];
+              double ap = S[p][col], aq = S[q][col];
+              S[p][col] = c * ap - s * aq;
+              S[q][col] = s * ap + c * aq;
+            }
+            __syncthreads();
+            // columns (+ accumulated rotation)
+            for (int e = threadIdx.x; e < (JS / 2) * JS; e += JT) {
+              int k = e / JS, row = e % JS;
+              double c = cs_c[k], s = cs_s[k];
+              if (s == 0.0) continue;
+              int p = pair_p[k], q = pair_q[k];
+              double ap = S[row][p], aq = S[row][q];
+              S[row][p] = c * ap - s * aq;
+              S[row][q] = s * ap + c * aq;
+              double rp = R[row][p], rq = R[row][q];
+              R[row][p] = c * rp - s * rq;
+              R[row][q] = s * rp + c * rq;
+            }
+            __syncthreads();
+            if (threadIdx.x < JS / 2 && cs_s[threadIdx.x] != 0.0) {
+              S[pair_p[threadIdx.x]][pair_q[threadIdx.x]] = 0.0;
+              S[pair_q[threadIdx.x]][pair_p[threadIdx.x]] = 0.0;
+            }
+            __syncthreads();
+          }
+        }
+        double* Jp = Jbuf + (int64_t)pr * JS * JS;
+        for (int e = threadIdx.x; e < JS * JS; e += JT) Jp[e] = R[e / JS][e % JS];
+        if (threadIdx.x == 0 && any_rot) atomicOr(flags + sweep, 1);
+        __syncthreads();
+      }
+      grid.sync();
+      // ---- phase B: G[I u J, :] <- J^T G[I u J, :]
+      for (int64_t item = blockIdx.x; item < (int64_t)npairs * ctiles; item += gridDim.x) {
+        const int pr = (int)(item / ctiles);
+        const int64_t c0 = (item % ctiles) * TILE;
+        const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
+        const double* Jp = Jbuf + (int64_t)pr * JS * JS;
+        for (int e = threadIdx.x; e < JS * JS; e += JT) R[e / JS][e % JS] = Jp[e];
+        for (int e = threadIdx.x; e < JS * TILE; e += JT) {
+          int a = e / TILE, c = e % TILE;
+          T[a][c] = (c0 + c < npad) ? G[(int64_t)sub_to_global(a, bi, bj) * ldg + c0 + c] : 0.0;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < JS * TILE; e += JT) {
+          int a = e / TILE, c = e % TILE;
+          if (c0 + c >= npad) continue;
+          double acc = 0.0;
+#pragma unroll 8
+          for (int kk = 0; kk < JS; ++kk) acc = fma(R[kk][a], T[kk][c], acc);
+          G[(int64_t)sub_to_global(a, bi, bj) * ldg + c0 + c] = acc;
+        }
+        __syncthreads();
+      }
+      grid.sync();
+      // ---- phase C: G[:, I u J] <- G[:, I u J] J ;  V[:, I u J] <- V[:, I u J] J
+      for (int64_t item = blockIdx.x; item < (int64_t)npairs * ctiles * 2; item += gridDim.x) {
+        const int which = (int)(item % 2);
+        const int64_t it2 = item / 2;
+        const int pr = (int)(it2 / ctiles);
+        const int64_t r0 = (it2 % ctiles) * TILE;
+        const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
+        double* M = which ? V : G;
+        const int64_t ldm = which ? ldv : ldg;
+        const double* Jp = Jbuf + (int64_t)pr * JS * JS;
+        for (int e = threadIdx.x; e < JS * JS; e += JT) R[e / JS][e % JS] = Jp[e];
+        for (int e = threadIdx.x; e < JS * TILE; e += JT) {
+          int r = e / JS, a = e % JS;  // T used as [a][r]
+          T[a][r] = (r0 + r < npad) ? M[(r0 + r) * ldm + sub_to_global(a, bi, bj)] : 0.0;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < JS * TILE; e += JT) {
+          int r = e / JS, a = e % JS;
+          if (r0 + r >= npad) continue;
+          double acc = 0.0;
+#pragma unroll 8
+          for (int kk = 0; kk < JS; ++kk) acc = fma(T[kk][r], R[kk][a], acc);
+          M[(r0 + r) * ldm + sub_to_global(a, bi, bj)] = acc;
+        }
+        __syncthreads();
+      }
+      grid.sync();
+    }
+    if (flags[sweep] == 0) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep + 1;
+}
+
+__global__ void k_pad_copy(int64_t n, int64_t npad, const double* A, int64_t lda, double* G) {
+  FPI_GRID_STRIDE(e, npad * npad) {
+    int64_t i = e / npad, j = e - i * npad;
+    G[e] = (i < n && j < n) ? A[i * lda + j] : 0.0;
+  }
+}
+
+__global__ void k_diag_keys(int64_t n, const double* G, int64_t npad, double* keys, int32_t* idx) {
+  FPI_GRID_STRIDE(i, n) {
+    keys[i] = G[i * npad + i];
+    idx[i] = (int32_t)i;
+  }
+}
+
+__global__ void k_gather_eig(int64_t n, const double* Vp, int64_t npad, const int32_t* order, const double* wsorted,
+                             double* w, double* V, int64_t ldv) {
+  FPI_GRID_STRIDE(e, n * n) {
+    int64_t i = e / n, k = e - i * n;
+    V[i * ldv + k] = Vp[i * npad + order[k]];
+    if (i == 0) w[k] = wsorted[k];
+  }
+}
+
+// ---- helpers ------------------------------------------------------------
+__global__ void k_transpose(int64_t M, int64_t N, const double* __restrict__ A, int64_t lda, double* __restrict__ B,
+                            int64_t ldb) {
+  __shared__ double t[32][33];
+  for (int64_t by = blockIdx.y; by * 32 < M; by += gridDim.y)
+    for (int64_t bx = blockIdx.x; bx * 32 < N; bx += gridDim.x) {
+      for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        int64_t r = by * 32 + i, c = bx * 32 + threadIdx.x;
+        t[i][threadIdx.x] = (r < M && c < N) ? A[r * lda + c] : 0.0;
+      }
+      __syncthreads();
+      for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        int64_t r = bx * 32 + i, c = by * 32 + threadIdx.x;
+        if (r < N && c < M) B[r * ldb + c] = t[threadIdx.x][i];
+      }
+      __syncthreads();
+    }
+}
+
+// column sums of squares, deterministic: one CTA per column group, fixed-order tree
+__global__ void k_col_sumsq(int64_t M, int64_t N, const double* __restrict__ A, int64_t lda, double* __restrict__ out) {
+  // blockDim (32, 8): x = column within group, y = row stripe
+  __shared__ double part[8][33];
+  int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  double s = 0.0;
+  if (c < N)
+    for (int64_t r = threadIdx.y; r < M; r += 8) {
+      double v = A[r * lda + c];
+      s = fma(v, v, s);
+    }
+  part[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < N) {
+    double t = 0.0;
+    for (int y = 0; y < 8; ++y) t += part[y][threadIdx.x];
+    out[c] = t;
+  }
+}
+
+__global__ void k_scale_cols(int64_t M, int64_t N, double* A, int64_t lda, const double* s, int mode) {
+  // mode 0: multiply by s[j]; 1: divide by s[j] (0 where s == 0)
+  FPI_GRID_STRIDE(e, M * N) {
+    int64_t i = e / N, j = e - i * N;
+    double f = s[j];
+    A[i * lda + j] = mode == 0 ? A[i * lda + j] * f : (f != 0.0 ? A[i * lda + j] / f : 0.0);
+  }
+}
+
+__global__ void k_scale_rows(int64_t M, int64_t N, double* A, int64_t lda, const double* s) {
+  FPI_GRID_STRIDE(e, M * N) {
+    int64_t i = e / N, j = e - i * N;
+    A[i * lda + j] *= s[i];
+  }
+}
+
+// Canonical sign per singular triplet: the largest-|.| entry of the right
+// vector (row j of Vt, length q) is made positive (ties -> lowest index);
+// the matching left vector (column j of U) flips with it.
+__global__ void k_canon_sign(int64_t r, int64_t p, int64_t q, double* U, int64_t ldu, double* Vt, int64_t ldvt) {
+  __shared__ double best[32];
+  __shared__ int64_t bidx[32];
+  for (int64_t j = blockIdx.x; j < r; j += gridDim.x) {
+    double bv = -1.0;
+    int64_t bi = 0;
+    for (int64_t c = threadIdx.x; c < q; c += blockDim.x) {
+      double a = fabs(Vt[j * ldvt + c]);
+      if (a > bv) { bv = a; bi = c; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { best[w] = bv; bidx[w] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+        if (best[k] > best[0] || (best[k] == best[0] && bidx[k] < bidx[0])) { best[0] = best[k]; bidx[0] = bidx[k]; }
+    }
+    __syncthreads();
+    const bool flip = Vt[j * ldvt + bidx[0]] < 0.0;
+    __syncthreads();
+    if (flip) {
+      for (int64_t c = threadIdx.x; c < q; c += blockDim.x) Vt[j * ldvt + c] = -Vt[j * ldvt + c];
+      for (int64_t i = threadIdx.x; i < p; i += blockDim.x) U[i * ldu + j] = -U[i * ldu + j];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+void cholesky_lower(fpi_context* h, int64_t n, double* A, int64_t lda, int* h_info) {
+  cudaStream_t s = h->stream;
+  Scratch<int> info(1, s);
+  FPI_CUDA(cudaMemsetAsync(info.get(), 0, sizeof(int), s));
+  for (int64_t j = 0; j < n; j += NB) {
+    int jb = (int)(n - j < NB ? n - j : NB);
+    k_potrf_diag<<<1, 256, 0, s>>>(A + j * lda + j, lda, jb, info, j);
+    if (j + jb < n) {
+      int64_t rows = n - j - jb;
+      k_trsm_panel<<<grid_for(rows, 128, h->num_sms * 4), 128, 0, s>>>(A, lda, j, jb, n);
+      gemm(h, false, true, rows, rows, jb, -1.0, A + (j + jb) * lda + j, lda, A + (j + jb) * lda + j, lda, 1.0,
+           A + (j + jb) * lda + j + jb, lda);
+    }
+    note_launch(h, 2);
+  }
+  FPI_LAUNCH_CHECK();
+  *h_info = host_read(info.get(), s);
+}
+
+void trsm_lower_left(fpi_context* h, int64_t n, const double* L, int64_t ldl, double* X, int64_t ldx, int64_t nrhs) {
+  cudaStream_t s = h->stream;
+  for (int64_t j = 0; j < n; j += NB) {
+    int jb = (int)(n - j < NB ? n - j : NB);
+    k_trsm_diag<<<grid_for(nrhs, 128, h->num_sms * 4), 128, 0, s>>>(L, ldl, j, jb, X, ldx, nrhs);
+    if (j + jb < n)
+      gemm(h, false, false, n - j - jb, nrhs, jb, -1.0, L + (j + jb) * ldl + j, ldl, X + j * ldx, ldx, 1.0,
+           X + (j + jb) * ldx, ldx);
+    note_launch(h);
+  }
+  FPI_LAUNCH_CHECK();
+}
+
+void lower_inverse(fpi_context* h, int64_t n, const double* L, int64_t ldl, double* Linv, int64_t ldi) {
+  k_set_identity<<<grid_for(n * n, 256, h->num_sms * 16), 256, 0, h->stream>>>(n, Linv, ldi);
+  note_launch(h);
+  trsm_lower_left(h, n, L, ldl, Linv, ldi, n);
+}
+
+int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, double* V, int64_t ldv,
+            int max_sweeps) {
+  cudaStream_t s = h->stream;
+  if (n <= 0) return 0;
+  int nb = (int)((n + JB - 1) / JB);
+  if (nb < 2) nb = 2;
+  if (nb % 2) ++nb;
+  const int64_t npad = (int64_t)nb * JB;
+  Scratch<double> G(npad * npad, s), Vp(npad * npad, s), Jbuf((int64_t)(nb / 2) * JS * JS, s);
+  Scratch<int> flags(max_sweeps + 1, s), sweeps(1, s);
+  FPI_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * (max_sweeps + 1), s));
+  k_pad_copy<<<grid_for(npad * npad, 256, h->num_sms * 16), 256, 0, s>>>(n, npad, A, lda, G);
+  k_set_identity<<<grid_for(npad * npad, 256, h->num_sms * 16), 256, 0, s>>>(npad, Vp, npad);
+  FPI_LAUNCH_CHECK();
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int per_sm = 0;
+    FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, JT, 0));
+    max_blocks = per_sm * h->num_sms;
+  }
+  const int64_t ctiles = (npad + TILE - 1) / TILE;
+  int64_t want = (int64_t)(nb / 2) * ctiles * 2;
+  int grid = (int)(want < max_blocks ? want : max_blocks);
+  if (grid < 1) grid = 1;
+  double tol = 1e-14;
+  int inner = 1;
+  double* Gp = G.get();
+  int64_t ldg = npad;
+  double* Vpp = Vp.get();
+  int64_t ldvp = npad;
+  double* Jb = Jbuf.get();
+  int* fl = flags.get();
+  int* sw = sweeps.get();
+  void* args[] = {&nb, &Gp, &ldg, &Vpp, &ldvp, &Jb, &fl, &max_sweeps, &tol, &inner, &sw};
+  FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, 0, s));
+  note_launch(h);
+  // sort eigenvalues descending, gather vectors
+  CubTemp tmp(s);
+  Scratch<double> keys(n, s), keys2(n, s);
+  Scratch<int32_t> idx(n, s), idx2(n, s);
+  k_diag_keys<<<grid_for(n, 256, h->num_sms * 4), 256, 0, s>>>(n, G, npad, keys, idx);
+  sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n, true, 0, 64, s);
+  k_gather_eig<<<grid_for(n * n, 256, h->num_sms * 16), 256, 0, s>>>(n, Vp, npad, idx2, keys2, w, V, ldv);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 3);
+  return host_read(sweeps.get(), s);
+}
+
+void transpose(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* B, int64_t ldb) {
+  if (M <= 0 || N <= 0) return;
+  dim3 blk(32, 8);
+  int64_t gx = (N + 31) / 32, gy = (M + 31) / 32;
+  dim3 grd((unsigned)(gx < 65535 ? gx : 65535), (unsigned)(gy < 65535 ? gy : 65535));
+  k_transpose<<<grd, blk, 0, h->stream>>>(M, N, A, lda, B, ldb);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+}
+
+void col_sumsq(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* out) {
+  if (N <= 0) return;
+  k_col_sumsq<<<(unsigned)((N + 31) / 32), dim3(32, 8), 0, h->stream>>>(M, N, A, lda, out);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+}
+
+void scale_cols(fpi_context* h, int64_t M, int64_t N, double* A, int64_t lda, const double* s, bool divide) {
+  if (M <= 0 || N <= 0) return;
+  k_scale_cols<<<grid_for(M * N, 256, h->num_sms * 16), 256, 0, h->stream>>>(M, N, A, lda, s, divide ? 1 : 0);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+}
+
+void scale_rows(fpi_context* h, int64_t M, int64_t N, double* A, int64_t lda, const double* s) {
+  if (M <= 0 || N <= 0) return;
+  k_scale_rows<<<grid_for(M * N, 256, h->num_sms * 16), 256, 0, h->stream>>>(M, N, A, lda, s);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+}
+
+void canonical_signs(fpi_context* h, int64_t r, int64_t p, int64_t q, double* U, int64_t ldu, double* Vt,
+                     int64_t ldvt) {
+  if (r <= 0) return;
+  k_canon_sign<<<(unsigned)(r < 4096 ? r : 4096), 256, 0, h->stream>>>(r, p, q, U, ldu, Vt, ldvt);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+}
+
+}  // namespace fpi
+
+extern "C" int fpi_cholesky(fpi_handle h, int64_t n, double* d_A, int64_t lda) {
+  FPI_API_BEGIN(h)
+  int info = 0;
+  fpi::cholesky_lower(h, n, d_A, lda, &info);
+  FPI_REQUIRE(info == 0, FPI_ENUMERIC, "matrix is not positive definite (pivot " + std::to_string(info) + ")");
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_sym_eig(fpi_handle h, int64_t n, const double* d_A, int64_t lda, double* d_w, double* d_V,
+                           int64_t ldv, int32_t* h_sweeps) {
+  FPI_API_BEGIN(h)
+  int sw = fpi::sym_eig(h, n, d_A, lda, d_w, d_V, ldv, 60);
+  if (h_sweeps) *h_sweeps = sw;
+  FPI_API_END(h)
+}

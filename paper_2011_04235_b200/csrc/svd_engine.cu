@@ -1,0 +1,717 @@
+// SVD engines and the FastPI stages built on them.
+//
+//  dense_svd        svd.py:86-117 (dense_svd + truncate).  Exact SVD of a dense
+//                   p x q panel via the Gram matrix of its short side, refined
+//                   once: G = M^T M -> eig -> M1 = M W0 (columns now nearly
+//                   orthogonal) -> G1 = M1^T M1 -> eig (converges in a couple of
+//                   Jacobi sweeps, relatively accurate) -> sigma = ||M1 w1_j||.
+//  randomized_svd   svd.py:120-138.  X = numpy-exact sketch; B = inner X;
+//                   CholeskyQR of B without forming Q (Q = B L^-T):
+//                   Y^T = (inner^T B) L^-T; SVD of the q x 2r panel Y^T;
+//                   U = B (L^-T U~).  An eigen-based orthonormalisation
+//                   replaces Cholesky when B^T B is not numerically PD.
+//  row_update       pinv.py:131-171  (inner [diag(s) Vt11 ; A21] as one CSR)
+//  column_update    pinv.py:174-208  (inner [U diag(s) | T], dense + CSR)
+//  pinv_assemble    pinv.py:211-231  (cutoff, sigma^+)
+//  unfold           pinv.py:271-275  (+ the V / Ut transposes of pinv.py:226-228)
+//  pinv_apply       pinv.py:72-81    (Z = V diag(s+) U^T Y, Y sparse or dense)
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "capi_guard.cuh"
+#include "cub_util.cuh"
+#include "gemm.cuh"
+#include "linalg.cuh"
+#include "sparse.cuh"
+#include "spmm.cuh"
+#include "svd_engine.cuh"
+
+namespace fpi {
+
+void sketch_normal(fpi_context* h, int64_t seed, int64_t rows, int64_t cols, double* d_out, int64_t ld);
+
+namespace {
+
+__global__ void k_sqrt_clamp(int64_t n, double* v) {
+  FPI_GRID_STRIDE(i, n) v[i] = v[i] > 0.0 ? sqrt(v[i]) : 0.0;
+}
+
+__global__ void k_copy2d(int64_t M, int64_t N, const double* __restrict__ A, int64_t lda, double* __restrict__ B,
+                         int64_t ldb) {
+  FPI_GRID_STRIDE(e, M * N) {
+    int64_t i = e / N, j = e - i * N;
+    B[i * ldb + j] = A[i * lda + j];
+  }
+}
+
+// cols of A (M x N) selected by ord[0..K) and divided by s[k]  -> B (M x K)
+__global__ void k_gather_cols_div(int64_t M, int64_t K, const double* __restrict__ A, int64_t lda,
+                                  const int32_t* __restrict__ ord, const double* __restrict__ s,
+                                  double* __restrict__ B, int64_t ldb) {
+  FPI_GRID_STRIDE(e, M * K) {
+    int64_t i = e / K, k = e - i * K;
+    double d = s[k];
+    B[i * ldb + k] = d > 0.0 ? A[i * lda + ord[k]] / d : 0.0;
+  }
+}
+
+// Vt[k][j] = V[j][ord[k]]   (V is q x q, Vt is K x q)
+__global__ void k_gather_vt(int64_t q, int64_t K, const double* __restrict__ V, int64_t ldv,
+                            const int32_t* __restrict__ ord, double* __restrict__ Vt, int64_t ldvt) {
+  FPI_GRID_STRIDE(e, K * q) {
+    int64_t k = e / q, j = e - k * q;
+    Vt[k * ldvt + j] = V[j * ldv + ord[k]];
+  }
+}
+
+__global__ void k_iota32(int32_t* a, int64_t n) {
+  FPI_GRID_STRIDE(i, n) a[i] = (int32_t)i;
+}
+
+__global__ void k_gather_f64(int64_t n, const double* __restrict__ src, const int32_t* __restrict__ ord,
+                             double* __restrict__ dst) {
+  FPI_GRID_STRIDE(i, n) dst[i] = src[ord[i]];
+}
+
+// rows [0, rank11) of the inner CSR: Vt11 rows scaled by sigma; rows after: A21
+__global__ void k_inner_rows(int64_t rank11, int64_t m2, const int64_t* __restrict__ vptr,
+                             const int64_t* __restrict__ aptr, int64_t nnz_v, int64_t* __restrict__ iptr) {
+  FPI_GRID_STRIDE(i, rank11 + m2 + 1) {
+    iptr[i] = i <= rank11 ? vptr[i] : nnz_v + aptr[i - rank11];
+  }
+}
+
+__global__ void k_inner_vals(int64_t rank11, const int64_t* __restrict__ vptr, const int32_t* __restrict__ vidx,
+                             const double* __restrict__ vval, const double* __restrict__ sig, int64_t nnz_v,
+                             int64_t nnz_a, const int32_t* __restrict__ aidx, const double* __restrict__ aval,
+                             int32_t* __restrict__ iidx, double* __restrict__ ival) {
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t k = warp; k < rank11; k += nw) {
+    double s = sig[k];
+    for (int64_t p = vptr[k] + lane; p < vptr[k + 1]; p += 32) {
+      iidx[p] = vidx[p];
+      ival[p] = s * vval[p];
+    }
+  }
+  FPI_GRID_STRIDE(e, nnz_a) {
+    iidx[nnz_v + e] = aidx[e];
+    ival[nnz_v + e] = aval[e];
+  }
+}
+
+// dense copy of a CSR (rows x cols) into D (ld), D pre-zeroed
+__global__ void k_csr_to_dense(int64_t rows, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                               const double* __restrict__ val, double* __restrict__ D, int64_t ld, int64_t col0) {
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < rows; r += nw)
+    for (int64_t p = ptr[r] + lane; p < ptr[r + 1]; p += 32) D[r * ld + col0 + idx[p]] = val[p];
+}
+
+__global__ void k_fill(int64_t n, double* a, double v) {
+  FPI_GRID_STRIDE(i, n) a[i] = v;
+}
+
+__global__ void k_pinv(int64_t r, const double* __restrict__ sigma, double cutoff, int64_t maxpq,
+                       double* __restrict__ sdag, double* __restrict__ tol_out, int* __restrict__ all_filtered) {
+  if (blockIdx.x != 0) return;
+  const double smax = r ? sigma[0] : 0.0;
+  const double tol = cutoff * smax * (double)maxpq;  // pinv.py:217-218
+  __shared__ int any_keep;
+  if (threadIdx.x == 0) any_keep = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < r; i += blockDim.x) {
+    const bool keep = sigma[i] > tol;
+    sdag[i] = keep ? 1.0 / sigma[i] : 0.0;
+    if (keep) any_keep = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *tol_out = tol;
+    *all_filtered = (r > 0 && !any_keep) ? 1 : 0;
+  }
+}
+
+// Ut[k][i] = U[idx[i]][k]    (U: m x r row-major; Ut: r x m)
+__global__ void k_gather_rows_T(int64_t m, int64_t r, const double* __restrict__ U, int64_t ldu,
+                                const int64_t* __restrict__ idx, double* __restrict__ Ut, int64_t ldt) {
+  __shared__ double t[32][33];
+  for (int64_t by = blockIdx.y; by * 32 < m; by += gridDim.y)
+    for (int64_t bx = blockIdx.x; bx * 32 < r; bx += gridDim.x) {
+      for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        int64_t row = by * 32 + i, c = bx * 32 + threadIdx.x;
+        t[i][threadIdx.x] = (row < m && c < r) ? U[idx[row] * ldu + c] : 0.0;
+      }
+      __syncthreads();
+      for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        int64_t k = bx * 32 + i, c = by * 32 + threadIdx.x;
+        if (k < r && c < m) Ut[k * ldt + c] = t[threadIdx.x][i];
+      }
+      __syncthreads();
+    }
+}
+
+// V[j][k] = Vt[k][idx[j]]     (Vt: r x n; V: n x r)
+__global__ void k_gather_cols_T(int64_t n, int64_t r, const double* __restrict__ Vt, int64_t ldvt,
+                                const int64_t* __restrict__ idx, double* __restrict__ V, int64_t ldv) {
+  FPI_GRID_STRIDE(e, n * r) {
+    int64_t j = e / r, k = e - j * r;
+    V[j * ldv + k] = Vt[k * ldvt + idx[j]];
+  }
+}
+
+// dst[j][:] = src[idx[j]][:]
+__global__ void k_gather_rows(int64_t n, int64_t L, const double* __restrict__ src, int64_t lds,
+                              const int64_t* __restrict__ idx, double* __restrict__ dst, int64_t ldd) {
+  FPI_GRID_STRIDE(e, n * L) {
+    int64_t j = e / L, l = e - j * L;
+    dst[j * ldd + l] = src[idx[j] * lds + l];
+  }
+}
+
+// dst[idx[i]][:] = src[i][:]
+__global__ void k_scatter_rows(int64_t m, int64_t L, const double* __restrict__ src, int64_t lds,
+                               const int64_t* __restrict__ idx, double* __restrict__ dst, int64_t ldd) {
+  FPI_GRID_STRIDE(e, m * L) {
+    int64_t i = e / L, l = e - i * L;
+    dst[idx[i] * ldd + l] = src[i * lds + l];
+  }
+}
+
+__global__ void k_remap_rows_i32(int64_t nnz, const int32_t* __restrict__ rows, const int64_t* __restrict__ fwd,
+                                 int32_t* __restrict__ out) {
+  FPI_GRID_STRIDE(e, nnz) out[e] = (int32_t)fwd[rows[e]];
+}
+
+__global__ void k_diag_ratio(int64_t n, const double* __restrict__ L, int64_t ld, double* out) {
+  if (blockIdx.x || threadIdx.x) return;
+  double mx = 0.0, mn = 1e308;
+  for (int64_t i = 0; i < n; ++i) {
+    double d = fabs(L[i * ld + i]);
+    mx = d > mx ? d : mx;
+    mn = d < mn ? d : mn;
+  }
+  *out = mn > 0 ? mx / mn : 1e308;
+}
+
+// Linv <- diag(lambda^-1/2) W^T over kept eigenpairs (others zero)
+__global__ void k_eig_orth(int64_t k, const double* __restrict__ w, const double* __restrict__ W, double tolrel,
+                           double* __restrict__ Linv) {
+  FPI_GRID_STRIDE(e, k * k) {
+    int64_t i = e / k, j = e - i * k;
+    double lam = w[i], lmax = w[0];
+    Linv[i * k + j] = (lam > tolrel * lmax && lam > 0.0) ? W[j * k + i] / sqrt(lam) : 0.0;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// dense SVD of a tall panel (p >= q): the top `rank` triplets.
+static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M, int64_t ldm, int64_t rank,
+                           double* U, double* sigma, double* Vt, fpi_svd_diag* diag) {
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  Scratch<double> Gm(q * q, s), W0(q * q, s), w0(q, s), M1(p * q, s), W1(q * q, s), w1(q, s), V(q * q, s);
+  gemm(h, true, false, q, q, p, 1.0, M, ldm, M, ldm, 0.0, Gm, q);
+  int sw0 = sym_eig(h, q, Gm, q, w0, W0, q, 60);
+  gemm(h, false, false, p, q, q, 1.0, M, ldm, W0, q, 0.0, M1, q);
+  gemm(h, true, false, q, q, p, 1.0, M1, q, M1, q, 0.0, Gm, q);
+  int sw1 = sym_eig(h, q, Gm, q, w1, W1, q, 60);
+  gemm(h, false, false, q, q, q, 1.0, W0, q, W1, q, 0.0, V, q);
+  // candidate left vectors for the top `rank` (by w1) and their norms
+  Scratch<double> Uraw(p * rank, s), ss(rank, s), ss2(rank, s);
+  Scratch<int32_t> ord(rank, s), ord2(rank, s);
+  gemm(h, false, false, p, rank, q, 1.0, M1, q, W1, q, 0.0, Uraw, rank);
+  col_sumsq(h, p, rank, Uraw, rank, ss);
+  k_sqrt_clamp<<<grid_for(rank, 256, G), 256, 0, s>>>(rank, ss);
+  // sort the kept sigma descending (ties keep order) so factors are flagged sorted
+  k_iota32<<<grid_for(rank, 256, G), 256, 0, s>>>(ord, rank);
+  CubTemp tmp(s);
+  sort_pairs(tmp, ss.get(), ss2.get(), ord.get(), ord2.get(), rank, true, 0, 64, s);
+  FPI_CUDA(cudaMemcpyAsync(sigma, ss2.get(), sizeof(double) * rank, cudaMemcpyDeviceToDevice, s));
+  k_gather_cols_div<<<grid_for(p * rank, 256, G), 256, 0, s>>>(p, rank, Uraw, rank, ord2, ss2, U, rank);
+  // Vt rows = columns of V for the same triplets: V column index = ord2 (within the first `rank`)
+  k_gather_vt<<<grid_for(rank * q, 256, G), 256, 0, s>>>(q, rank, V, q, ord2, Vt, q);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 5);
+  complete_null_left(h, p, rank, U, rank, sigma, diag);
+  canonical_signs(h, rank, p, q, U, rank, Vt, q);
+  if (diag) {
+    diag->eig_sweeps[0] = sw0;
+    diag->eig_sweeps[1] = sw1;
+  }
+}
+
+// Orthonormal completion of left vectors whose sigma is numerically zero
+// (LAPACK returns some orthonormal completion there; any is valid).
+void complete_null_left(fpi_context* h, int64_t p, int64_t rank, double* U, int64_t ldu, const double* sigma,
+                        fpi_svd_diag* diag) {
+  if (rank <= 0) return;
+  cudaStream_t s = h->stream;
+  std::vector<double> hs(rank);
+  FPI_CUDA(cudaMemcpyAsync(hs.data(), sigma, sizeof(double) * rank, cudaMemcpyDeviceToHost, s));
+  FPI_CUDA(cudaStreamSynchronize(s));
+  const double tol = 2.220446049250313e-16 * (hs[0] > 0 ? hs[0] : 1.0) * (double)(p > rank ? p : rank);
+  std::vector<int64_t> nul;
+  for (int64_t j = 0; j < rank; ++j)
+    if (!(hs[j] > tol)) nul.push_back(j);
+  if (nul.empty()) return;
+  FPI_REQUIRE((int64_t)nul.size() <= p, FPI_ENUMERIC, "cannot complete the null space");
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  Scratch<double> v(p, s), t(rank, s);
+  std::vector<double> one(1, 1.0);
+  int64_t cand = 0;
+  for (int64_t j : nul) {
+    // zero column j first so it does not project on itself
+    cudaMemset2DAsync(U + j, ldu * sizeof(double), 0, sizeof(double), p, s);
+    for (; cand < p; ++cand) {
+      k_fill<<<grid_for(p, 256, G), 256, 0, s>>>(p, v, 0.0);
+      FPI_CUDA(cudaMemcpyAsync(v.get() + cand, one.data(), sizeof(double), cudaMemcpyHostToDevice, s));
+      for (int pass = 0; pass < 2; ++pass) {
+        gemm(h, true, false, rank, 1, p, 1.0, U, ldu, v, 1, 0.0, t, 1);     // t = U^T v
+        gemm(h, false, false, p, 1, rank, -1.0, U, ldu, t, 1, 1.0, v, 1);   // v -= U t
+      }
+      Scratch<double> nn(1, s);
+      col_sumsq(h, p, 1, v, 1, nn);
+      double hn = host_read(nn.get(), s);
+      if (hn > 0.25) {
+        std::vector<double> inv(1, 1.0 / std::sqrt(hn));
+        Scratch<double> sc(1, s);
+        FPI_CUDA(cudaMemcpyAsync(sc.get(), inv.data(), sizeof(double), cudaMemcpyHostToDevice, s));
+        scale_cols(h, p, 1, v, 1, sc, false);
+        FPI_CUDA(cudaMemcpy2DAsync(U + j, ldu * sizeof(double), v.get(), sizeof(double), sizeof(double), p,
+                                   cudaMemcpyDeviceToDevice, s));
+        FPI_CUDA(cudaStreamSynchronize(s));
+        ++cand;
+        break;
+      }
+    }
+  }
+  if (diag) diag->null_completed += (int32_t)nul.size();
+}
+
+void dense_svd(fpi_context* h, int64_t p, int64_t q, const double* M, int64_t ldm, int64_t rank, double* U,
+               double* sigma, double* Vt, fpi_svd_diag* diag) {
+  FPI_REQUIRE(rank >= 1 && rank <= (p < q ? p : q), FPI_EDOMAIN,
+              "target rank " + std::to_string(rank) + " out of range [1, " + std::to_string(p < q ? p : q) + "]");
+  FPI_REQUIRE(p * q <= 100000000LL, FPI_ECAPACITY,
+              "dense SVD of a " + std::to_string(p) + "x" + std::to_string(q) + " matrix exceeds the 100000000-entry guard");
+  cudaStream_t s = h->stream;
+  if (p >= q) {
+    dense_svd_tall(h, p, q, M, ldm, rank, U, sigma, Vt, diag);
+    return;
+  }
+  // M = (M^T)^T :  M^T = U' S V'^T  ->  U = V', Vt = U'^T
+  Scratch<double> Mt(q * p, s), U2(q * rank, s), Vt2(rank * p, s);
+  transpose(h, p, q, M, ldm, Mt, p);
+  dense_svd_tall(h, q, p, Mt, p, rank, U2, sigma, Vt2, diag);
+  transpose(h, rank, p, Vt2, p, U, rank);
+  transpose(h, q, rank, U2, rank, Vt, q);
+  canonical_signs(h, rank, p, q, U, rank, Vt, q);
+}
+
+// ---------------------------------------------------------------------------
+// inner-matrix operator: [D diag(dscale) | S] (horizontal) -- D may be null
+struct InnerOp {
+  int64_t p = 0, q = 0;
+  const double* D = nullptr;
+  int64_t ldd = 0, sd = 0;
+  const double* dscale = nullptr;
+  const int64_t* s_ptr = nullptr;
+  const int32_t* s_idx = nullptr;
+  const double* s_val = nullptr;  // p x (q - sd)
+  const int64_t* st_ptr = nullptr;
+  const int32_t* st_idx = nullptr;
+  const double* st_val = nullptr;  // (q - sd) x p
+
+  // B (p x k) = inner * X (q x k)
+  void apply(fpi_context* h, const double* X, int64_t k, double* B) const {
+    if (D && sd > 0) {
+      Scratch<double> Xs(sd * k, h->stream);
+      FPI_CUDA(cudaMemcpyAsync(Xs.get(), X, sizeof(double) * sd * k, cudaMemcpyDeviceToDevice, h->stream));
+      if (dscale) scale_rows(h, sd, k, Xs, k, dscale);
+      gemm(h, false, false, p, k, sd, 1.0, D, ldd, Xs, k, 0.0, B, k);
+      if (q > sd) spmm(h, p, q - sd, k, s_ptr, s_idx, s_val, nullptr, 1.0, X + sd * k, k, 1.0, B, k);
+    } else {
+      spmm(h, p, q, k, s_ptr, s_idx, s_val, nullptr, 1.0, X, k, 0.0, B, k);
+    }
+  }
+  // Z (q x k) = inner^T * B (p x k)
+  void applyT(fpi_context* h, const double* B, int64_t k, double* Z) const {
+    if (D && sd > 0) {
+      gemm(h, true, false, sd, k, p, 1.0, D, ldd, B, k, 0.0, Z, k);
+      if (dscale) scale_rows(h, sd, k, Z, k, dscale);
+      if (q > sd) spmm(h, q - sd, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z + sd * k, k);
+    } else {
+      spmm(h, q, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z, k);
+    }
+  }
+  // dense copy (p x q)
+  void densify(fpi_context* h, double* out) const {
+    cudaStream_t s = h->stream;
+    const unsigned G = (unsigned)(h->num_sms * 16);
+    k_fill<<<grid_for(p * q, 256, G), 256, 0, s>>>(p * q, out, 0.0);
+    if (D && sd > 0) {
+      k_copy2d<<<grid_for(p * sd, 256, G), 256, 0, s>>>(p, sd, D, ldd, out, q);
+      if (dscale) scale_cols(h, p, sd, out, q, dscale, false);
+    }
+    if (q > sd) k_csr_to_dense<<<grid_for(p * 32, 256, G), 256, 0, s>>>(p, s_ptr, s_idx, s_val, out, q, sd);
+    FPI_LAUNCH_CHECK();
+    note_launch(h, 3);
+  }
+};
+
+static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int64_t seed, double* U, double* sigma,
+                           double* Vt, fpi_svd_diag* diag) {
+  const int64_t p = op.p, q = op.q;
+  FPI_REQUIRE(rank >= 1 && rank <= (p < q ? p : q), FPI_EDOMAIN,
+              "target rank " + std::to_string(rank) + " out of range [1, " + std::to_string(p < q ? p : q) + "]");
+  cudaStream_t s = h->stream;
+  const int64_t k = 2 * rank;
+  if (diag) diag->engine = 1;
+  if (p <= k) {
+    // QR of a p x 2r sketch with p <= 2r gives a p x p orthogonal Q: the result is the exact SVD of inner
+    FPI_REQUIRE(p * q <= 100000000LL, FPI_ECAPACITY, "inner matrix too large to densify");
+    Scratch<double> Dn(p * q, s);
+    op.densify(h, Dn);
+    dense_svd(h, p, q, Dn, q, rank, U, sigma, Vt, diag);
+    return;
+  }
+  Scratch<double> X(q * k, s), B(p * k, s), Gm(k * k, s), Linv(k * k, s);
+  sketch_normal(h, seed, q, k, X, k);   // svd.py:131-132
+  op.apply(h, X, k, B);                 // svd.py:133
+  X.release();
+  // CholeskyQR: B^T B = L L^T, Q = B L^-T   (svd.py:134)
+  gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k);
+  Scratch<double> Gc(k * k, s);
+  FPI_CUDA(cudaMemcpyAsync(Gc.get(), Gm.get(), sizeof(double) * k * k, cudaMemcpyDeviceToDevice, s));
+  int info = 0;
+  cholesky_lower(h, k, Gc, k, &info);
+  if (info == 0) {
+    Scratch<double> ratio(1, s);
+    k_diag_ratio<<<1, 1, 0, s>>>(k, Gc, k, ratio);
+    double r = host_read(ratio.get(), s);
+    if (diag) {
+      diag->cond_estimate = r;
+      diag->cholqr_passes = 1;
+    }
+    lower_inverse(h, k, Gc, k, Linv, k);
+  } else {
+    // not numerically PD (B rank deficient): orthonormalise through the eigendecomposition
+    Scratch<double> w(k, s), W(k * k, s);
+    sym_eig(h, k, Gm, k, w, W, k, 60);
+    k_eig_orth<<<grid_for(k * k, 256, h->num_sms * 16), 256, 0, s>>>(k, w, W, 1e-26, Linv);
+    FPI_LAUNCH_CHECK();
+    if (diag) {
+      diag->cond_estimate = INFINITY;
+      diag->cholqr_passes = 0;
+    }
+  }
+  Gc.release();
+  Gm.release();
+  // Y^T = (inner^T B) L^-T   (svd.py:135: Y = Q^T inner)
+  Scratch<double> Z(q * k, s), Yt(q * k, s);
+  op.applyT(h, B, k, Z);
+  gemm(h, false, true, q, k, k, 1.0, Z, k, Linv, k, 0.0, Yt, k);
+  Z.release();
+  // SVD of Y (k x q) through its transpose Y^T = Vy S Uy^T   (svd.py:136)
+  Scratch<double> Vy(q * rank, s), Uyt(rank * k, s);
+  dense_svd(h, q, k, Yt, k, rank, Vy, sigma, Uyt, diag);
+  Yt.release();
+  transpose(h, q, rank, Vy, rank, Vt, q);                   // Vt = Vy^T
+  // U = Q U~ = B L^-T U~ ,  U~ = Uyt^T   (svd.py:137)
+  Scratch<double> Mx(k * rank, s);
+  gemm(h, true, true, k, rank, k, 1.0, Linv, k, Uyt, k, 0.0, Mx, rank);
+  gemm(h, false, false, p, rank, k, 1.0, B, k, Mx, rank, 0.0, U, rank);
+  canonical_signs(h, rank, p, q, U, rank, Vt, q);
+  if (diag) diag->engine = 1;
+}
+
+static void inner_svd(fpi_context* h, const InnerOp& op, int64_t rank, int64_t n_cols, double thr, int64_t seed,
+                      double* U, double* sigma, double* Vt, int* engine, fpi_svd_diag* diag) {
+  if ((double)rank < thr * (double)n_cols) {  // pinv.py:122
+    *engine = 1;
+    randomized_svd(h, op, rank, seed, U, sigma, Vt, diag);
+  } else {
+    *engine = 2;
+    if (diag) diag->engine = 2;
+    FPI_REQUIRE(op.p * op.q <= 100000000LL, FPI_ECAPACITY,
+                "dense SVD of a " + std::to_string(op.p) + "x" + std::to_string(op.q) +
+                    " matrix exceeds the 100000000-entry guard");
+    Scratch<double> Dn(op.p * op.q, h->stream);
+    op.densify(h, Dn);
+    dense_svd(h, op.p, op.q, Dn, op.q, rank, U, sigma, Vt, diag);
+  }
+}
+
+void row_update(fpi_context* h, int64_t m1, int64_t n1, int64_t rank11, const double* sigma11, const int64_t* u_ptr,
+                const int32_t* u_idx, const double* u_val, const int64_t* v_ptr, const int32_t* v_idx,
+                const double* v_val, int64_t m2, const int64_t* a_ptr, const int32_t* a_idx, const double* a_val,
+                int64_t s_rank, double thr, int64_t seed, double* U, double* sigma, double* Vt, int* engine) {
+  cudaStream_t s = h->stream;
+  *engine = 0;
+  if (s_rank == 0) return;
+  const int64_t max_rank = (rank11 + m2 < n1) ? rank11 + m2 : n1;
+  FPI_REQUIRE(s_rank >= 1 && s_rank <= max_rank, FPI_EDOMAIN,
+              "target rank " + std::to_string(s_rank) + " out of range [1, " + std::to_string(max_rank) + "]");
+  const int64_t p = rank11 + m2, q = n1;
+  int64_t nnz_v = 0, nnz_a = 0;
+  if (rank11) nnz_v = host_read(v_ptr + rank11, s);
+  if (m2) nnz_a = host_read(a_ptr + m2, s);
+  const int64_t nnz = nnz_v + nnz_a;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  // inner = [diag(sigma11) Vt11 ; A21] as one CSR, plus its transpose (pinv.py:161-163)
+  Scratch<int64_t> iptr(p + 1, s), itptr(q + 1, s);
+  Scratch<int32_t> iidx(nnz, s), itidx(nnz, s);
+  Scratch<double> ival(nnz, s), itval(nnz, s);
+  Scratch<int64_t> zero_ptr(1, s);
+  FPI_CUDA(cudaMemsetAsync(zero_ptr.get(), 0, sizeof(int64_t), s));
+  k_inner_rows<<<grid_for(p + 1, 256, G), 256, 0, s>>>(rank11, m2, rank11 ? v_ptr : zero_ptr.get(),
+                                                       m2 ? a_ptr : zero_ptr.get(), nnz_v, iptr);
+  k_inner_vals<<<grid_for(rank11 * 32 + nnz_a, 256, G), 256, 0, s>>>(rank11, v_ptr, v_idx, v_val, sigma11, nnz_v,
+                                                                     nnz_a, a_idx, a_val, iidx, ival);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 2);
+  csr_transpose(h, p, q, nnz, iptr, iidx, ival, itptr, itidx, itval);
+  InnerOp op;
+  op.p = p;
+  op.q = q;
+  op.s_ptr = iptr;
+  op.s_idx = iidx;
+  op.s_val = ival;
+  op.st_ptr = itptr;
+  op.st_idx = itidx;
+  op.st_val = itval;
+  Scratch<double> Ui(p * s_rank, s);
+  inner_svd(h, op, s_rank, n1, thr, seed, Ui, sigma, Vt, engine, &h->diag);
+  // lift: U = [U11 Ui[:rank11] ; Ui[rank11:]]   (pinv.py:168-170)
+  if (m1) {
+    if (rank11)
+      spmm(h, m1, rank11, s_rank, u_ptr, u_idx, u_val, nullptr, 1.0, Ui, s_rank, 0.0, U, s_rank);
+    else
+      FPI_CUDA(cudaMemsetAsync(U, 0, sizeof(double) * m1 * s_rank, s));
+  }
+  if (m2)
+    FPI_CUDA(cudaMemcpyAsync(U + m1 * s_rank, Ui.get() + rank11 * s_rank, sizeof(double) * m2 * s_rank,
+                             cudaMemcpyDeviceToDevice, s));
+}
+
+void column_update(fpi_context* h, int64_t m, int64_t s_prev, int64_t n1, const double* U_prev,
+                   const double* sigma_prev, const double* Vt_prev, int64_t n2, const int64_t* t_ptr,
+                   const int32_t* t_idx, const double* t_val, const int64_t* tt_ptr, const int32_t* tt_idx,
+                   const double* tt_val, int64_t r, double thr, int64_t seed, double* U, double* sigma, double* Vt,
+                   int* engine) {
+  cudaStream_t s = h->stream;
+  *engine = 0;
+  if (r == 0) return;
+  const int64_t max_rank = (s_prev + n2 < m) ? s_prev + n2 : m;
+  FPI_REQUIRE(r >= 1 && r <= max_rank, FPI_EDOMAIN,
+              "target rank " + std::to_string(r) + " out of range [1, " + std::to_string(max_rank) + "]");
+  const int64_t q = s_prev + n2;
+  InnerOp op;
+  op.p = m;
+  op.q = q;
+  op.D = U_prev;
+  op.ldd = s_prev;
+  op.sd = s_prev;
+  op.dscale = sigma_prev;
+  op.s_ptr = t_ptr;
+  op.s_idx = t_idx;
+  op.s_val = t_val;
+  op.st_ptr = tt_ptr;
+  op.st_idx = tt_idx;
+  op.st_val = tt_val;
+  Scratch<double> Vti(r * q, s);
+  inner_svd(h, op, r, q, thr, seed, U, sigma, Vti, engine, &h->diag);
+  // lift: Vt = [Vti[:, :s] Vt_prev | Vti[:, s:]]   (pinv.py:205-207)
+  const int64_t n = n1 + n2;
+  if (n1) {
+    if (s_prev)
+      gemm(h, false, false, r, n1, s_prev, 1.0, Vti, q, Vt_prev, n1, 0.0, Vt, n);
+    else
+      FPI_CUDA(cudaMemset2DAsync(Vt, n * sizeof(double), 0, n1 * sizeof(double), r, s));
+  }
+  if (n2)
+    FPI_CUDA(cudaMemcpy2DAsync(Vt + n1, n * sizeof(double), Vti.get() + s_prev, q * sizeof(double),
+                               n2 * sizeof(double), r, cudaMemcpyDeviceToDevice, s));
+}
+
+void pinv_assemble(fpi_context* h, int64_t r, const double* sigma, int64_t p, int64_t q, double cutoff,
+                   double* sdag, double* tol_out, int* all_filtered) {
+  cudaStream_t s = h->stream;
+  Scratch<double> t(1, s);
+  Scratch<int> af(1, s);
+  int64_t maxpq = p > q ? p : q;
+  if (maxpq < 1) maxpq = 1;
+  k_pinv<<<1, 256, 0, s>>>(r, sigma, cutoff, maxpq, sdag, t, af);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+  *tol_out = host_read(t.get(), s);
+  *all_filtered = host_read(af.get(), s);
+}
+
+void unfold_transpose(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* Vt,
+                      const int64_t* row_fwd, const int64_t* col_fwd, double* V_out, double* Ut_out) {
+  cudaStream_t s = h->stream;
+  if (Ut_out && m && r) {
+    dim3 blk(32, 8);
+    int64_t gx = (r + 31) / 32, gy = (m + 31) / 32;
+    dim3 grd((unsigned)(gx < 65535 ? gx : 65535), (unsigned)(gy < 65535 ? gy : 65535));
+    k_gather_rows_T<<<grd, blk, 0, s>>>(m, r, U, r, row_fwd, Ut_out, m);
+  }
+  if (V_out && n && r)
+    k_gather_cols_T<<<grid_for(n * r, 256, h->num_sms * 16), 256, 0, s>>>(n, r, Vt, n, col_fwd, V_out, r);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 2);
+}
+
+// Z (n x L) = V diag(sdag) U^T Y  with U, Vt in reordered coordinates and Y (m x L) CSR in original rows
+void pinv_apply_csr(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* sdag,
+                    const double* Vt, const int64_t* row_fwd, const int64_t* col_fwd, int64_t L, int64_t nnz,
+                    const int64_t* y_ptr, const int32_t* y_idx, const double* y_val, double* Z) {
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  if (n == 0 || L == 0) return;
+  if (r == 0) {
+    FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * n * L, s));
+    return;
+  }
+  // Y^T with rows remapped into reordered coordinates: CSR (L x m), column = row_fwd[i]
+  CubTemp tmp(s);
+  Scratch<int32_t> rows(nnz, s), rrows(nnz, s);
+  Scratch<int64_t> yt_ptr(L + 1, s);
+  Scratch<int32_t> yt_idx(nnz, s);
+  Scratch<double> yt_val(nnz, s);
+  expand_rows(h, m, y_ptr, rows);
+  if (nnz) k_remap_rows_i32<<<grid_for(nnz, 256, G), 256, 0, s>>>(nnz, rows, row_fwd, rrows);
+  build_csr(h, tmp, nnz, y_idx, rrows, y_val, L, m, yt_ptr, yt_idx, yt_val);
+  // W (L x r) = Y'^T U ; scale columns by sigma+   (pinv.py:75, 81)
+  Scratch<double> W(L * r, s), Zr(n * L, s);
+  spmm(h, L, m, r, yt_ptr, yt_idx, yt_val, nullptr, 1.0, U, r, 0.0, W, r);
+  scale_cols(h, L, r, W, r, sdag, false);
+  // Z_reordered (n x L) = Vt^T W^T ; then Z[j] = Z_reordered[col_fwd[j]]
+  gemm(h, true, true, n, L, r, 1.0, Vt, n, W, r, 0.0, Zr, L);
+  k_gather_rows<<<grid_for(n * L, 256, G), 256, 0, s>>>(n, L, Zr, L, col_fwd, Z, L);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 2);
+}
+
+void pinv_apply_dense(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* sdag,
+                      const double* Vt, const int64_t* row_fwd, const int64_t* col_fwd, int64_t L, const double* Y,
+                      int64_t ldy, double* Z) {
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  if (n == 0 || L == 0) return;
+  if (r == 0) {
+    FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * n * L, s));
+    return;
+  }
+  Scratch<double> Yr(m * L, s), W(r * L, s), Zr(n * L, s);
+  k_scatter_rows<<<grid_for(m * L, 256, G), 256, 0, s>>>(m, L, Y, ldy, row_fwd, Yr, L);
+  gemm(h, true, false, r, L, m, 1.0, U, r, Yr, L, 0.0, W, L);
+  scale_rows(h, r, L, W, L, sdag);
+  gemm(h, true, false, n, L, r, 1.0, Vt, n, W, L, 0.0, Zr, L);
+  k_gather_rows<<<grid_for(n * L, 256, G), 256, 0, s>>>(n, L, Zr, L, col_fwd, Z, L);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 2);
+}
+
+}  // namespace fpi
+
+// ---- C ABI -----------------------------------------------------------------
+extern "C" int fpi_dense_svd(fpi_handle h, int64_t p, int64_t q, const double* d_M, int64_t ldm, int64_t rank,
+                             double* d_U, double* d_sigma, double* d_Vt) {
+  FPI_API_BEGIN(h)
+  h->diag = fpi_svd_diag{};
+  h->diag.engine = 2;
+  fpi::dense_svd(h, p, q, d_M, ldm, rank, d_U, d_sigma, d_Vt, &h->diag);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_randomized_svd(fpi_handle h, int64_t p, int64_t q, const int64_t* a_ptr, const int32_t* a_idx,
+                                  const double* a_val, const int64_t* at_ptr, const int32_t* at_idx,
+                                  const double* at_val, int64_t rank, int64_t seed, double* d_U, double* d_sigma,
+                                  double* d_Vt) {
+  FPI_API_BEGIN(h)
+  h->diag = fpi_svd_diag{};
+  fpi::InnerOp op;
+  op.p = p;
+  op.q = q;
+  op.s_ptr = a_ptr;
+  op.s_idx = a_idx;
+  op.s_val = a_val;
+  op.st_ptr = at_ptr;
+  op.st_idx = at_idx;
+  op.st_val = at_val;
+  fpi::randomized_svd(h, op, rank, seed, d_U, d_sigma, d_Vt, &h->diag);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_row_update(fpi_handle h, int64_t m1, int64_t n1, int64_t rank11, const double* sigma11,
+                              const int64_t* u_ptr, const int32_t* u_idx, const double* u_val, const int64_t* v_ptr,
+                              const int32_t* v_idx, const double* v_val, int64_t m2, const int64_t* a_ptr,
+                              const int32_t* a_idx, const double* a_val, int64_t s, double thr, int64_t seed,
+                              double* d_U, double* d_sigma, double* d_Vt, int32_t* h_engine) {
+  FPI_API_BEGIN(h)
+  h->diag = fpi_svd_diag{};
+  int eng = 0;
+  fpi::row_update(h, m1, n1, rank11, sigma11, u_ptr, u_idx, u_val, v_ptr, v_idx, v_val, m2, a_ptr, a_idx, a_val, s,
+                  thr, seed, d_U, d_sigma, d_Vt, &eng);
+  if (h_engine) *h_engine = eng;
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_column_update(fpi_handle h, int64_t m, int64_t s_prev, int64_t n1, const double* U_prev,
+                                 const double* sigma_prev, const double* Vt_prev, int64_t n2, const int64_t* t_ptr,
+                                 const int32_t* t_idx, const double* t_val, const int64_t* tt_ptr,
+                                 const int32_t* tt_idx, const double* tt_val, int64_t r, double thr, int64_t seed,
+                                 double* d_U, double* d_sigma, double* d_Vt, int32_t* h_engine) {
+  FPI_API_BEGIN(h)
+  h->diag = fpi_svd_diag{};
+  int eng = 0;
+  fpi::column_update(h, m, s_prev, n1, U_prev, sigma_prev, Vt_prev, n2, t_ptr, t_idx, t_val, tt_ptr, tt_idx, tt_val,
+                     r, thr, seed, d_U, d_sigma, d_Vt, &eng);
+  if (h_engine) *h_engine = eng;
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_pinv_assemble(fpi_handle h, int64_t r, const double* d_sigma, int64_t p, int64_t q,
+                                 double cutoff, double* d_sigma_dagger, double* h_tol, int32_t* h_all_filtered) {
+  FPI_API_BEGIN(h)
+  int af = 0;
+  double tol = 0;
+  fpi::pinv_assemble(h, r, d_sigma, p, q, cutoff, d_sigma_dagger, &tol, &af);
+  if (h_tol) *h_tol = tol;
+  if (h_all_filtered) *h_all_filtered = af;
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_unfold(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U, const double* d_Vt,
+                          const int64_t* d_row_fwd, const int64_t* d_col_fwd, double* d_V_out, double* d_Ut_out) {
+  FPI_API_BEGIN(h)
+  fpi::unfold_transpose(h, m, n, r, d_U, d_Vt, d_row_fwd, d_col_fwd, d_V_out, d_Ut_out);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_pinv_apply_csr(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U,
+                                  const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
+                                  const int64_t* d_col_fwd, int64_t L, int64_t nnz, const int64_t* y_ptr,
+                                  const int32_t* y_idx, const double* y_val, double* d_Z) {
+  FPI_API_BEGIN(h)
+  fpi::pinv_apply_csr(h, m, n, r, d_U, d_sigma_dagger, d_Vt, d_row_fwd, d_col_fwd, L, nnz, y_ptr, y_idx, y_val, d_Z);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_pinv_apply_dense(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U,
+                                    const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
+                                    const int64_t* d_col_fwd, int64_t L, const double* d_Y, int64_t ldy,
+                                    double* d_Z) {
+  FPI_API_BEGIN(h)
+  fpi::pinv_apply_dense(h, m, n, r, d_U, d_sigma_dagger, d_Vt, d_row_fwd, d_col_fwd, L, d_Y, ldy, d_Z);
+  FPI_API_END(h)
+}

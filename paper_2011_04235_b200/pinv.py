@@ -1,0 +1,401 @@
+"""FastPI driver, incremental updates and pseudoinverse assembly -- the
+reference's pinv.py API (``/root/reference/pkg/src/fastpi/pinv.py``) on the
+B200 core.  Every stage runs in HBM; the returned objects expose the
+reference's numpy / scipy attributes lazily.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import struct
+import time
+import warnings
+from dataclasses import dataclass
+from pathlib import Path
+from typing import NamedTuple
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from ._device import DeviceCSR, d2h, empty, h2d, torch
+from .reorder import Permutation, ReorderResult, partition_original, reorder_device
+from .svd import SvdFactors, _Dense, _to_dense, block_diagonal_svd_device, dense_svd, truncate
+from .validation import DENSE_CAPACITY, CapacityError
+
+EPS = float(np.finfo(np.float64).eps)
+
+STAGES = ("reorder", "block_svd", "row_update", "column_update", "pinv_assembly")
+
+
+@dataclass(frozen=True)
+class FastpiConfig:
+    """pinv.py:32-46."""
+
+    alpha: float = 1.0
+    k: float = 0.01
+    seed: int = 0
+    low_rank_threshold: float = 0.3
+    pinv_cutoff_factor: float = EPS
+
+    def __post_init__(self):
+        if not 0.0 < self.alpha <= 1.0:
+            raise ValueError(f"alpha must be in (0, 1], got {self.alpha}")
+        if not 0.0 < self.k < 1.0:
+            raise ValueError(f"k must be in (0, 1), got {self.k}")
+
+
+class _DevPinv:
+    """Pseudoinverse factors in reordered coordinates: U (m x r), sdag (r), Vt (r x n) + permutations."""
+
+    def __init__(self, U, sdag, Vt, row_fwd, col_fwd):
+        self.U, self.sdag, self.Vt, self.row_fwd, self.col_fwd = U, sdag, Vt, row_fwd, col_fwd
+        self.m, self.r = int(U.shape[0]), int(U.shape[1])
+        self.n = int(Vt.shape[1])
+
+
+class Pseudoinverse:
+    """Factored pseudoinverse ``V @ diag(sigma_dagger) @ Ut`` of an m x n matrix (pinv.py:49-92)."""
+
+    def __init__(self, V=None, sigma_dagger=None, Ut=None, tolerance_used=0.0, all_filtered=False, *, _dev=None):
+        self._dev = _dev
+        self._V = None if V is None else np.asarray(V, dtype=np.float64)
+        self._Ut = None if Ut is None else np.asarray(Ut, dtype=np.float64)
+        if sigma_dagger is None and _dev is not None:
+            sigma_dagger = d2h(_dev.sdag)
+        self.sigma_dagger = np.asarray(sigma_dagger, dtype=np.float64).ravel()
+        self.tolerance_used = float(tolerance_used)
+        self.all_filtered = bool(all_filtered)
+
+    def _device(self) -> _DevPinv:
+        if self._dev is None:
+            t = torch()
+            n, r = self._V.shape
+            m = self._Ut.shape[1]
+            dev = t.device("cuda", t.cuda.current_device())
+            U = h2d(np.ascontiguousarray(self._Ut.T))
+            Vt = h2d(np.ascontiguousarray(self._V.T))
+            self._dev = _DevPinv(U, h2d(self.sigma_dagger), Vt, t.arange(m, device=dev, dtype=t.int64),
+                                 t.arange(n, device=dev, dtype=t.int64))
+        return self._dev
+
+    def _unfold(self, want_v: bool):
+        d = self._dev
+        out = empty((d.n, d.r)) if want_v else empty((d.r, d.m))
+        _lib.call("fpi_unfold", d.m, d.n, d.r, _lib.ptr(d.U), _lib.ptr(d.Vt), _lib.ptr(d.row_fwd),
+                  _lib.ptr(d.col_fwd), _lib.ptr(out) if want_v else None, None if want_v else _lib.ptr(out))
+        return d2h(out)
+
+    @property
+    def V(self) -> np.ndarray:
+        if self._V is None:
+            self._V = self._unfold(True)
+        return self._V
+
+    @property
+    def Ut(self) -> np.ndarray:
+        if self._Ut is None:
+            self._Ut = self._unfold(False)
+        return self._Ut
+
+    @property
+    def shape(self) -> tuple:
+        if self._dev is not None:
+            return (self._dev.n, self._dev.m)
+        return (self._V.shape[0], self._Ut.shape[1])
+
+    @property
+    def retained_rank(self) -> int:
+        return int(np.count_nonzero(self.sigma_dagger))
+
+    def apply_device(self, B):
+        """pinv @ B for a device operand (DeviceCSR or dense tensor); returns a device tensor."""
+        d = self._device()
+        if isinstance(B, DeviceCSR):
+            if B.shape[0] != d.m:
+                raise ValueError(f"dimension mismatch: pseudoinverse expects {d.m} rows, got {B.shape[0]}")
+            L = B.shape[1]
+            Z = empty((d.n, L))
+            _lib.call("fpi_pinv_apply_csr", d.m, d.n, d.r, _lib.ptr(d.U), _lib.ptr(d.sdag), _lib.ptr(d.Vt),
+                      _lib.ptr(d.row_fwd), _lib.ptr(d.col_fwd), L, B.nnz, _lib.ptr(B.indptr), _lib.ptr(B.indices),
+                      _lib.ptr(B.values), _lib.ptr(Z))
+            return Z
+        t = torch()
+        Bd = B.to(t.float64).contiguous()
+        vec = Bd.dim() == 1
+        if vec:
+            Bd = Bd.reshape(-1, 1)
+        if Bd.shape[0] != d.m:
+            raise ValueError(f"dimension mismatch: pseudoinverse expects {d.m} rows, got {Bd.shape[0]}")
+        L = int(Bd.shape[1])
+        Z = empty((d.n, L))
+        _lib.call("fpi_pinv_apply_dense", d.m, d.n, d.r, _lib.ptr(d.U), _lib.ptr(d.sdag), _lib.ptr(d.Vt),
+                  _lib.ptr(d.row_fwd), _lib.ptr(d.col_fwd), L, _lib.ptr(Bd), L, _lib.ptr(Z))
+        return Z.reshape(-1) if vec else Z
+
+    def apply(self, B) -> np.ndarray:
+        """pinv.py:72-81: ``pinv @ B`` right-to-left without materialising pinv."""
+        if sp.issparse(B):
+            Z = self.apply_device(DeviceCSR.from_host(B))
+        elif isinstance(B, DeviceCSR) or type(B).__module__.startswith("torch"):
+            Z = self.apply_device(B)
+        else:
+            Z = self.apply_device(h2d(np.asarray(B, dtype=np.float64)))
+        return d2h(Z)
+
+    def validate(self, tol: float = 1e-8):
+        r = len(self.sigma_dagger)
+        if r:
+            V, Ut = self.V, self.Ut
+            defect = max(np.abs(V.T @ V - np.eye(r)).max(), np.abs(Ut @ Ut.T - np.eye(r)).max())
+            if defect > tol:
+                raise ValueError(f"pseudoinverse factor defect {defect:.3e} exceeds {tol:.1e}")
+        return self
+
+
+class StageTime(NamedTuple):
+    stage: str
+    seconds: float
+    rank: int
+
+
+class FastpiResult(NamedTuple):
+    """pinv.py:101-108."""
+
+    pseudoinverse: Pseudoinverse
+    factors: SvdFactors
+    reordering: ReorderResult
+    timings: list
+
+
+def _empty_factors(p: int, q: int) -> SvdFactors:
+    return SvdFactors(np.zeros((p, 0)), np.zeros(0), np.zeros((0, q)), is_sorted=True)
+
+
+def _csr_of(f_mat) -> DeviceCSR:
+    """Device CSR of a factor matrix (block CSR, scipy, numpy or dense tensor)."""
+    if isinstance(f_mat, DeviceCSR):
+        return f_mat
+    if type(f_mat).__module__.startswith("torch"):
+        f_mat = d2h(f_mat)
+    return DeviceCSR.from_host(sp.csr_matrix(f_mat), canonicalize=False)
+
+
+def row_update_device(f11: SvdFactors, a21: DeviceCSR, s: int, *, low_rank_threshold=0.3, seed=0):
+    """pinv.py:131-171 with device operands; returns (SvdFactors, engine)."""
+    m2, n1 = a21.shape
+    m1 = f11.shape[0]
+    if f11.shape[1] != n1:
+        raise ValueError(f"dimension mismatch: factors cover {f11.shape[1]} columns, appended rows have {n1}")
+    r_avail = f11.rank
+    max_rank = min(r_avail + m2, n1)
+    if s == 0:
+        return _empty_factors(m1 + m2, n1), 0
+    if not 1 <= s <= max_rank:
+        raise ValueError(f"target rank {s} out of range [1, {max_rank}]")
+    d = f11.device()
+    if d.kind == "block":
+        Ucsr, Vcsr = d.U, d.Vt
+    else:
+        Ucsr, Vcsr = _csr_of(d.U), _csr_of(d.Vt)
+    m = m1 + m2
+    U, sig, Vt = empty((m, s)), empty(s), empty((s, n1))
+    eng = C.c_int32(0)
+    _lib.call("fpi_row_update", m1, n1, r_avail, _lib.ptr(d.sigma), _lib.ptr(Ucsr.indptr), _lib.ptr(Ucsr.indices),
+              _lib.ptr(Ucsr.values), _lib.ptr(Vcsr.indptr), _lib.ptr(Vcsr.indices), _lib.ptr(Vcsr.values), m2,
+              _lib.ptr(a21.indptr), _lib.ptr(a21.indices), _lib.ptr(a21.values), int(s), float(low_rank_threshold),
+              int(seed), _lib.ptr(U), _lib.ptr(sig), _lib.ptr(Vt), C.byref(eng))
+    return SvdFactors(_dev=_Dense(U, sig, Vt), is_sorted=True, _shape=(m, n1)), int(eng.value)
+
+
+def row_update(f11: SvdFactors, A_below, s: int, *, low_rank_threshold: float = 0.3, seed: int = 0) -> SvdFactors:
+    """pinv.py:131-171: factors of [A11; A_below] from factors of A11."""
+    a21 = A_below if isinstance(A_below, DeviceCSR) else DeviceCSR.from_host(A_below)
+    return row_update_device(f11, a21, s, low_rank_threshold=low_rank_threshold, seed=seed)[0]
+
+
+def column_update_device(f: SvdFactors, T: DeviceCSR, Tt: DeviceCSR, r: int, *, low_rank_threshold=0.3, seed=0):
+    """pinv.py:174-208 with device operands; returns (SvdFactors, engine)."""
+    m, n2 = T.shape
+    if f.shape[0] != m:
+        raise ValueError(f"dimension mismatch: factors cover {f.shape[0]} rows, appended columns have {m}")
+    s_prev = f.rank
+    n1 = f.shape[1]
+    max_rank = min(s_prev + n2, m)
+    if r == 0:
+        return _empty_factors(m, n1 + n2), 0
+    if not 1 <= r <= max_rank:
+        raise ValueError(f"target rank {r} out of range [1, {max_rank}]")
+    d = f.device()
+    if d.kind != "dense":
+        d = _Dense(h2d(_to_dense(f.U)), d.sigma, h2d(_to_dense(f.Vt)))
+    U, sig, Vt = empty((m, r)), empty(r), empty((r, n1 + n2))
+    eng = C.c_int32(0)
+    _lib.call("fpi_column_update", m, s_prev, n1, _lib.ptr(d.U), _lib.ptr(d.sigma), _lib.ptr(d.Vt), n2,
+              _lib.ptr(T.indptr), _lib.ptr(T.indices), _lib.ptr(T.values), _lib.ptr(Tt.indptr),
+              _lib.ptr(Tt.indices), _lib.ptr(Tt.values), int(r), float(low_rank_threshold), int(seed),
+              _lib.ptr(U), _lib.ptr(sig), _lib.ptr(Vt), C.byref(eng))
+    return SvdFactors(_dev=_Dense(U, sig, Vt), is_sorted=True, _shape=(m, n1 + n2)), int(eng.value)
+
+
+def column_update(f: SvdFactors, T, r: int, *, low_rank_threshold: float = 0.3, seed: int = 0) -> SvdFactors:
+    """pinv.py:174-208: factors of [A_left | T] from factors of A_left."""
+    Td = T if isinstance(T, DeviceCSR) else DeviceCSR.from_host(T)
+    return column_update_device(f, Td, Td.transpose(), r, low_rank_threshold=low_rank_threshold, seed=seed)[0]
+
+
+def _assemble(f: SvdFactors, row_fwd, col_fwd, cutoff_factor: float) -> Pseudoinverse:
+    d = f.device()
+    r = f.rank
+    p, q = f.shape
+    sdag = empty(r)
+    tol = C.c_double(0.0)
+    af = C.c_int32(0)
+    _lib.call("fpi_pinv_assemble", r, _lib.ptr(d.sigma), p, q, float(cutoff_factor), _lib.ptr(sdag),
+              C.byref(tol), C.byref(af))
+    if af.value:
+        warnings.warn("all singular values filtered; returning the zero pseudoinverse")
+    return Pseudoinverse(tolerance_used=tol.value, all_filtered=bool(af.value),
+                         _dev=_DevPinv(d.U, sdag, d.Vt, row_fwd, col_fwd))
+
+
+def pinv_from_svd(factors: SvdFactors, cutoff_factor: float = EPS) -> Pseudoinverse:
+    """pinv.py:211-231."""
+    if not factors.is_sorted:
+        raise ValueError("pseudoinverse assembly requires sorted factors")
+    d = factors.device()
+    if d.kind != "dense":
+        factors = SvdFactors(_to_dense(factors.U), factors.sigma, _to_dense(factors.Vt), True)
+    t = torch()
+    p, q = factors.shape
+    dev = t.device("cuda", t.cuda.current_device())
+    return _assemble(factors, t.arange(p, device=dev, dtype=t.int64), t.arange(q, device=dev, dtype=t.int64),
+                     cutoff_factor)
+
+
+def materialize(pinv: Pseudoinverse) -> np.ndarray:
+    """pinv.py:234-239."""
+    n, m = pinv.shape
+    if n * m > DENSE_CAPACITY:
+        raise CapacityError(f"materializing a {n}x{m} pseudoinverse exceeds the capacity guard")
+    return (pinv.V * pinv.sigma_dagger) @ pinv.Ut
+
+
+_PINV_HEADER = struct.Struct("<QQQB")
+
+
+def save_pseudoinverse(pinv: Pseudoinverse, path):
+    """pinv.py:242-254."""
+    n, m = pinv.shape
+    r = len(pinv.sigma_dagger)
+    with open(path, "wb") as fh:
+        fh.write(_PINV_HEADER.pack(n, m, r, 1 if pinv.all_filtered else 0))
+        fh.write(np.ascontiguousarray(pinv.V, dtype="<f8").tobytes())
+        fh.write(np.ascontiguousarray(pinv.sigma_dagger, dtype="<f8").tobytes())
+        fh.write(np.ascontiguousarray(pinv.Ut, dtype="<f8").tobytes())
+        fh.write(struct.pack("<d", pinv.tolerance_used))
+
+
+def load_pseudoinverse(path) -> Pseudoinverse:
+    """pinv.py:257-268."""
+    raw = Path(path).read_bytes()
+    n, m, r, flag = _PINV_HEADER.unpack_from(raw, 0)
+    off = _PINV_HEADER.size
+    V = np.frombuffer(raw, dtype="<f8", count=n * r, offset=off).reshape(n, r)
+    off += 8 * n * r
+    sd = np.frombuffer(raw, dtype="<f8", count=r, offset=off)
+    off += 8 * r
+    Ut = np.frombuffer(raw, dtype="<f8", count=r * m, offset=off).reshape(r, m)
+    off += 8 * r * m
+    (tol,) = struct.unpack_from("<d", raw, off)
+    return Pseudoinverse(V.copy(), sd.copy(), Ut.copy(), tol, bool(flag))
+
+
+def _unfold(factors: SvdFactors, result: ReorderResult) -> SvdFactors:
+    """pinv.py:271-275: reordered-coordinate factors in original coordinates."""
+    U = _to_dense(factors.U)[result.row_perm.forward, :]
+    Vt = _to_dense(factors.Vt)[:, result.col_perm.forward]
+    return SvdFactors(U, factors.sigma.copy(), Vt, is_sorted=factors.is_sorted)
+
+
+class _Timer:
+    def __init__(self):
+        self.t = torch()
+
+    def __enter__(self):
+        self.t.cuda.synchronize()
+        self.t0 = time.perf_counter()
+        return self
+
+    def __exit__(self, *exc):
+        self.t.cuda.synchronize()
+        self.seconds = time.perf_counter() - self.t0
+
+
+def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = None) -> FastpiResult:
+    """Algorithm 1 on a canonical device CSR (m >= n); everything stays in HBM."""
+    m, n = dev.shape
+    timings = []
+    with _Timer() as tm:
+        ordering = reorder_device(dev, cfg.k)
+        part = partition_original(dev, ordering, transposes=True)
+    timings.append(StageTime("reorder", tm.seconds, 0))
+
+    with _Timer() as tm:
+        f11 = block_diagonal_svd_device(part.a11, ordering.spans_device(), cfg.alpha)
+    timings.append(StageTime("block_svd", tm.seconds, f11.rank))
+
+    n1, m2, n2 = ordering.n_spoke_cols, ordering.n_hub_rows, ordering.n_hub_cols
+    with _Timer() as tm:
+        want_s = math.ceil(cfg.alpha * n1)
+        s = min(want_s, f11.rank + m2, n1)
+        if s < want_s:
+            warnings.warn(f"row-update target rank clamped from {want_s} to {s} "
+                          "(block stage produced less derivable rank)")
+        f_rows, eng_r = row_update_device(f11, part.a21, s, low_rank_threshold=cfg.low_rank_threshold,
+                                          seed=cfg.seed + 1)
+    timings.append(StageTime("row_update", tm.seconds, f_rows.rank))
+
+    with _Timer() as tm:
+        r = min(math.ceil(cfg.alpha * n), f_rows.rank + n2, m)
+        f_full, eng_c = column_update_device(f_rows, part.T, part.Tt, r, low_rank_threshold=cfg.low_rank_threshold,
+                                             seed=cfg.seed + 2)
+    timings.append(StageTime("column_update", tm.seconds, f_full.rank))
+
+    with _Timer() as tm:
+        pv = _assemble(f_full, ordering.row_perm.device_forward(), ordering.col_perm.device_forward(),
+                       cfg.pinv_cutoff_factor)
+    timings.append(StageTime("pinv_assembly", tm.seconds, pv.retained_rank))
+    if stats is not None:
+        stats.update(engines=(eng_r, eng_c), s=s, r=r, rank11=f11.rank, m1=ordering.n_spoke_rows, n1=n1, m2=m2,
+                     n2=n2, T=ordering.n_iterations, nnz_a12=part.info.nnz_a12, nnz_a22=part.info.nnz_a22,
+                     nnz_a21=part.info.nnz_a21, nnz_a11=part.info.nnz_a11, f11=f11, f_rows=f_rows, part=part)
+    return FastpiResult(pv, f_full, ordering, timings)
+
+
+def _swap(res: FastpiResult) -> FastpiResult:
+    """pinv.py:291-303: results of fastpi(A^T) expressed for A."""
+    pv = res.pseudoinverse
+    d = pv._dev
+    # pinv(A) = pinv(A^T)^T : U_A = V_{A^T}, Vt_A = U_{A^T}^T  (reordered coordinates swap roles)
+    Ua = d.Vt.t().contiguous()
+    Vta = d.U.t().contiguous()
+    swapped = Pseudoinverse(sigma_dagger=pv.sigma_dagger.copy(), tolerance_used=pv.tolerance_used,
+                            all_filtered=pv.all_filtered, _dev=_DevPinv(Ua, d.sdag, Vta, d.col_fwd, d.row_fwd))
+    fd = res.factors.device()
+    factors = SvdFactors(_dev=_Dense(fd.Vt.t().contiguous(), fd.sigma, fd.U.t().contiguous()), is_sorted=True,
+                         _shape=(res.factors.shape[1], res.factors.shape[0]))
+    return FastpiResult(swapped, factors, res.reordering, res.timings)
+
+
+def fastpi(A, config: FastpiConfig | None = None) -> FastpiResult:
+    """pinv.py:278-347: reorder, block SVD, two incremental updates, assembly."""
+    cfg = config or FastpiConfig()
+    dev = A if isinstance(A, DeviceCSR) else DeviceCSR.from_host(A)
+    m, n = dev.shape
+    if m == 0 or n == 0:
+        raise ValueError("cannot factorize a zero-dimension matrix")
+    if m < n:
+        return _swap(fastpi_device(dev.transpose(), cfg))
+    return fastpi_device(dev, cfg)

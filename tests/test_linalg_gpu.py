@@ -1,0 +1,80 @@
+"""GPU: the FP64 building blocks (DMMA GEMM, SpMM, Cholesky, block-Jacobi eigensolver)
+against numpy fp64 references."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+pytestmark = pytest.mark.gpu
+
+
+def _t(a):
+    from paper_2011_04235_b200._device import h2d
+    return h2d(np.ascontiguousarray(a, dtype=np.float64))
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 53, 29), (130, 257, 64), (300, 200, 5000), (64, 64, 20000)])
+def test_gemm(ta, tb, M, N, K):
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import d2h
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = rng.standard_normal((K, M) if ta else (M, K))
+    B = rng.standard_normal((N, K) if tb else (K, N))
+    C0 = rng.standard_normal((M, N))
+    ref = 0.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 2.0 * C0
+    dA, dB, dC = _t(A), _t(B), _t(C0)
+    _lib.call("fpi_gemm", ta, tb, M, N, K, 0.5, _lib.ptr(dA), A.shape[1], _lib.ptr(dB), B.shape[1], -2.0,
+              _lib.ptr(dC), N)
+    got = d2h(dC)
+    assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
+
+
+def test_spmm():
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import DeviceCSR, d2h
+    rng = np.random.default_rng(3)
+    A = sp.random(500, 300, density=0.02, random_state=rng, format="csr")
+    for k in (1, 7, 128, 300):
+        X = rng.standard_normal((300, k))
+        dev = DeviceCSR.from_host(A)
+        Y = _t(np.zeros((500, k)))
+        _lib.call("fpi_spmm", 500, 300, k, _lib.ptr(dev.indptr), _lib.ptr(dev.indices), _lib.ptr(dev.values), 1.0,
+                  _lib.ptr(_t(X)), k, 0.0, _lib.ptr(Y), k)
+        assert np.abs(d2h(Y) - A @ X).max() < 1e-12
+
+
+def test_cholesky():
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import d2h
+    rng = np.random.default_rng(5)
+    for n in (1, 31, 100, 333):
+        B = rng.standard_normal((n + 20, n))
+        G = B.T @ B
+        dG = _t(G)
+        _lib.call("fpi_cholesky", n, _lib.ptr(dG), n)
+        L = np.tril(d2h(dG))
+        assert np.abs(L @ L.T - G).max() < 1e-10 * np.abs(G).max()
+    with pytest.raises(RuntimeError):
+        bad = _t(-np.eye(4))
+        _lib.call("fpi_cholesky", 4, _lib.ptr(bad), 4)
+
+
+@pytest.mark.parametrize("n", [1, 2, 17, 64, 150, 401])
+def test_sym_eig(n):
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import d2h, empty
+    rng = np.random.default_rng(n)
+    B = rng.standard_normal((n + 3, n)) * np.logspace(0, -4, n)
+    G = B.T @ B
+    w = empty(n)
+    V = empty((n, n))
+    sw = C.c_int32(0)
+    _lib.call("fpi_sym_eig", n, _lib.ptr(_t(G)), n, _lib.ptr(w), _lib.ptr(V), n, C.byref(sw))
+    wr = np.linalg.eigvalsh(G)[::-1]
+    assert np.abs(d2h(w) - wr).max() <= 1e-12 * wr[0]
+    Vh = d2h(V)
+    assert np.abs(Vh.T @ Vh - np.eye(n)).max() < 1e-12
+    assert np.abs(G @ Vh - Vh * d2h(w)).max() < 1e-11 * wr[0]
+    assert 0 < sw.value < 60

@@ -1,0 +1,93 @@
+"""GPU: SVD engines against the oracle / numpy (svd.py parity)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import problem
+from oracle import fastpi_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _rel_sigma(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape
+    return np.abs(a - b).max() / max(b.max(), 1e-300) if b.size else 0.0
+
+
+@pytest.mark.parametrize("p,q", [(1, 1), (5, 3), (3, 5), (200, 40), (40, 200), (1000, 333)])
+def test_dense_svd(p, q):
+    import paper_2011_04235_b200 as fp
+    rng = np.random.default_rng(p + 3 * q)
+    M = rng.standard_normal((p, q)) @ np.diag(np.logspace(0, -6, q))
+    f = fp.dense_svd(M)
+    s = np.linalg.svd(M, compute_uv=False)
+    assert _rel_sigma(f.sigma, s) < 1e-12
+    assert np.abs((f.U * f.sigma) @ f.Vt - M).max() < 1e-12 * s[0]
+    assert f.orthonormality_defect() < 1e-10
+
+
+def test_dense_svd_rank_deficient():
+    import paper_2011_04235_b200 as fp
+    A = np.zeros((8, 4))
+    A[:4, :4] = np.diag([5.0, 4.0, 3.0, 2.0])
+    A[:, 3] = 0.0
+    f = fp.dense_svd(A)
+    np.testing.assert_allclose(f.sigma, [5, 4, 3, 0], atol=1e-14)
+    assert f.orthonormality_defect() < 1e-12
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3r50"])
+def test_block_svd_matches_oracle(name):
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200._device import DeviceCSR
+    from paper_2011_04235_b200.reorder import partition_original
+    from paper_2011_04235_b200.svd import block_diagonal_svd_device
+    p = problem(name)
+    dev = DeviceCSR.from_host(p.A)
+    r = fp.reorder(fp.to_bipartite(dev), p.workload.k)
+    part = partition_original(dev, r)
+    alpha = p.workload.alpha
+    for a in (alpha, 1.0):
+        f = block_diagonal_svd_device(part.a11, r.spans_device(), a)
+        fo = orc.block_svd(part.a11.to_host(), r.spans, a)
+        assert f.rank == fo.rank
+        # per block: sigma relative to the block sigma_max
+        spans = r.spans
+        off = 0
+        for rs, h, cs, w in spans.tolist():
+            if not h or not w:
+                continue
+            kp = int(np.ceil(a * min(h, w)))
+            sg, so = f.sigma[off:off + kp], fo.sigma[off:off + kp]
+            assert np.abs(sg - so).max() <= 1e-9 * max(so[0], 1e-300), (rs, h, cs, w)
+            off += kp
+        # block-sparse structure identical, reconstruction of the kept part identical up to signs
+        Ug, Vg = f.U.toarray(), f.Vt.toarray()
+        Uo, Vo = fo.U.toarray(), fo.Vt.toarray()
+        assert np.abs((Ug * f.sigma) @ Vg - (Uo * fo.sigma) @ Vo).max() < 1e-9 * max(1.0, fo.sigma.max())
+        assert f.orthonormality_defect() < 1e-10
+
+
+def test_block_svd_spec_two_blocks():
+    import paper_2011_04235_b200 as fp
+    f = fp.block_diagonal_svd([np.diag([3.0, 1.0]), np.diag([2.0, 1.0])], 1.0)
+    np.testing.assert_allclose(f.sigma, [3.0, 1.0, 2.0, 1.0], rtol=0, atol=1e-15)
+    assert not f.is_sorted
+
+
+@pytest.mark.parametrize("seed,rank", [(1, 10), (7, 40)])
+def test_randomized_svd_matches_oracle(seed, rank):
+    """Same sketch bits -> same subspace: sigma and U S Vt agree to rounding."""
+    import paper_2011_04235_b200 as fp
+    rng = np.random.default_rng(seed)
+    A = sp.random(3000, 400, density=0.02, random_state=rng, format="csr") + \
+        sp.csr_matrix(rng.standard_normal((3000, 1)) @ rng.standard_normal((1, 400)))
+    A = sp.csr_matrix(A)
+    f = fp.randomized_svd(A, rank, seed)
+    fo = orc.randomized_svd(A, rank, seed)
+    assert _rel_sigma(f.sigma, fo.sigma) < 1e-10
+    Bg = (f.U * f.sigma) @ f.Vt
+    Bo = (fo.U * fo.sigma) @ fo.Vt
+    assert np.linalg.norm(Bg - Bo) <= 1e-9 * np.linalg.norm(Bo)
+    assert f.orthonormality_defect() < 1e-10
