@@ -114,15 +114,15 @@ __device__ __forceinline__ int rr_block(int pos, int round, int nb) {
 __device__ __forceinline__ int sub_to_global(int l, int bi, int bj) { return l < JB ? bi * JB + l : bj * JB + (l - JB); }
 
 __global__ void __launch_bounds__(JT)
-    k_jacobi(int nb, double* G, int64_t ldg, double* V, int64_t ldv, double* Jbuf, int* flags, int max_sweeps,
-             double tol, int inner_sweeps, int* sweeps_out) {
+    k_jacobi(int nb, double* G, int64_t ldg, double* V, int64_t ldv, double* Jbuf,
+             unsigned long long* offmax, int max_sweeps, double tol, int inner_sweeps, int* sweeps_out) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double S[JS][JS + 1];
   __shared__ double R[JS][JS + 1];
   __shared__ double T[JS][TILE + 1];
   __shared__ double cs_c[JS / 2], cs_s[JS / 2];
   __shared__ int pair_p[JS / 2], pair_q[JS / 2];
-  __shared__ int any_rot;
+  __shared__ unsigned long long blk_off;
   const int npairs = nb / 2;
   const int64_t npad = (int64_t)nb * JB;
   const int64_t ctiles = (npad + TILE - 1) / TILE;
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(JT)
           S[a][b] = G[(int64_t)sub_to_global(a, bi, bj) * ldg + sub_to_global(b, bi, bj)];
           R[a][b] = a == b ? 1.0 : 0.0;
         }
-        if (threadIdx.x == 0) any_rot = 0;
+        if (threadIdx.x == 0) blk_off = 0ull;
         __syncthreads();
         for (int isw = 0; isw < inner_sweeps; ++isw) {
           for (int step = 0; step < JS - 1; ++step) {
@@ -147,12 +147,14 @@ __global__ void __launch_bounds__(JT)
               const int p = rr_block(k, step, JS), q = rr_block(JS - 1 - k, step, JS);
               double app = S[p][p], aqq = S[q][q], apq = S[p][q];
               double c = 1.0, s = 0.0;
-              if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
+              const double den = sqrt(fabs(app) * fabs(aqq));
+              const double ratio = den > 0.0 ? fabs(apq) / den : (apq != 0.0 ? 1.0 : 0.0);
+              if (isw == 0 && ratio > 0.0) atomicMax(&blk_off, (unsigned long long)__double_as_longlong(ratio));
+              if (apq != 0.0 && ratio > tol) {
                 double zeta = (aqq - app) / (2.0 * apq);
                 double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                 c = 1.0 / sqrt(1.0 + t * t);
                 s = c * t;
-                any_rot = 1;
               }
               cs_c[k] = c;
               cs_s[k] = s;
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(JT)
         }
         double* Jp = Jbuf + (int64_t)pr * JS * JS;
         for (int e = threadIdx.x; e < JS * JS; e += JT) Jp[e] = R[e / JS][e % JS];
-        if (threadIdx.x == 0 && any_rot) atomicOr(flags + sweep, 1);
+        if (threadIdx.x == 0 && blk_off) atomicMax(offmax + sweep, blk_off);
         __syncthreads();
       }
       grid.sync();
@@ -249,7 +251,10 @@ __global__ void __launch_bounds__(JT)
       }
       grid.sync();
     }
-    if (flags[sweep] == 0) break;
+    // stop when converged, or when the off-diagonal measure stagnates at the rounding floor
+    const double cur = __longlong_as_double((long long)offmax[sweep]);
+    const double prev = sweep ? __longlong_as_double((long long)offmax[sweep - 1]) : 1e300;
+    if (cur <= tol || (cur < 1e-9 && cur > 0.25 * prev)) break;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep + 1;
 }
@@ -417,8 +422,9 @@ int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, 
   if (nb % 2) ++nb;
   const int64_t npad = (int64_t)nb * JB;
   Scratch<double> G(npad * npad, s), Vp(npad * npad, s), Jbuf((int64_t)(nb / 2) * JS * JS, s);
-  Scratch<int> flags(max_sweeps + 1, s), sweeps(1, s);
-  FPI_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int) * (max_sweeps + 1), s));
+  Scratch<unsigned long long> flags(max_sweeps + 1, s);
+  Scratch<int> sweeps(1, s);
+  FPI_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(unsigned long long) * (max_sweeps + 1), s));
   k_pad_copy<<<grid_for(npad * npad, 256, h->num_sms * 16), 256, 0, s>>>(n, npad, A, lda, G);
   k_set_identity<<<grid_for(npad * npad, 256, h->num_sms * 16), 256, 0, s>>>(npad, Vp, npad);
   FPI_LAUNCH_CHECK();
@@ -439,7 +445,7 @@ int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, 
   double* Vpp = Vp.get();
   int64_t ldvp = npad;
   double* Jb = Jbuf.get();
-  int* fl = flags.get();
+  unsigned long long* fl = flags.get();
   int* sw = sweeps.get();
   void* args[] = {&nb, &Gp, &ldg, &Vpp, &ldvp, &Jb, &fl, &max_sweeps, &tol, &inner, &sw};
   FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, 0, s));
