@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""FastPI pinv + regression solve on B200 -- the driver's benchmark contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c4]
+
+A step is one full FastPI solve on one synthetic problem: reorder + permute /
+partition + block SVD + row update + column update + pseudoinverse assembly
+(``fastpi``, reference pinv.py:278-347) followed by the regression solve
+Z = pinv @ Y (``Pseudoinverse.apply`` / ``fit``, pinv.py:72-81,
+regression.py:50-70).  The metric is seconds per solve (lower is better).
+
+* ``value``  -- device-resident inputs, CUDA events around each step, L2 flushed
+  (512 MB write) before every timed step, mean over K steps, max over ranks.
+* ``e2e``    -- the public API on host scipy inputs: fastpi(A) + apply(Y) -> numpy
+  Z, host->device copies of A and Y and the device->host copy of Z inside.
+* ``roofline`` -- the dominant kernel class of the step, timed live with CUDA
+  events on the library stream (a separate instrumented pass after the timed
+  region), algorithmic flops / bytes per SURVEY.md section 8(d).
+* ``cpu_baseline`` -- the oracle port (numpy/scipy restatement of the reference,
+  bit-identical to it on this image) timed on the host cores, rank 0, N=1.
+* ``--impl reference`` -- the reference's CPU path (the oracle port; the
+  Python reference itself cannot travel to the GPU box) on the same workload.
+
+Multi-GPU (torchrun): every rank runs an independent replica of the solve
+(weak scaling, no data-path collective) -- the sharded solve is future work
+(DESIGN.md).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "FastPI pinv+solve sec & FP64 TFLOP/s|HBM GB/s frac at 1/2/4/8 B200 vs CPU ref"
+CACHE = Path(os.environ.get("FASTPI_BENCH_CACHE", "/tmp/fastpi_b200_cache"))
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_problem(name):
+    from paper_2011_04235_b200 import workloads
+    import scipy.sparse as sp
+    CACHE.mkdir(parents=True, exist_ok=True)
+    f = CACHE / f"{name}.npz"
+    w = workloads.WORKLOADS[name]
+    if f.exists():
+        z = np.load(f)
+        A = sp.csr_matrix((z["Av"], z["Ai"], z["Ap"]), shape=(w.m, w.n))
+        Y = sp.csr_matrix((z["Yv"], z["Yi"], z["Yp"]), shape=(w.m, w.n_labels))
+        return workloads.Problem(w, A, Y)
+    t0 = time.time()
+    p = workloads.make_problem(name)
+    log(f"[bench] generated {name} in {time.time() - t0:.1f}s (nnz={p.A.nnz}, nnz_Y={p.Y.nnz})")
+    np.savez(f, Av=p.A.data, Ai=p.A.indices, Ap=p.A.indptr, Yv=p.Y.data, Yi=p.Y.indices, Yp=p.Y.indptr)
+    return p
+
+
+def measured_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        return json.loads(f.read_text()), "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_oracle_solve(p):
+    """One reference-path solve (oracle port) -> seconds."""
+    from oracle import fastpi_oracle as orc
+    w = p.workload
+    t0 = time.perf_counter()
+    out = orc.fastpi(p.A, w.alpha, w.k, w.seed, keep_stages=False)
+    orc.apply_pinv(out["pinv"], p.Y)
+    return time.perf_counter() - t0, out["timings"]
+
+
+def reference_arm(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return 0
+    from threadpoolctl import threadpool_limits
+    cores = cpu_cores()
+    p = load_problem(args.workload)
+    small = load_problem("c1")
+    with threadpool_limits(cores):
+        for _ in range(args.warmup):
+            run_oracle_solve(small)
+        times = []
+        budget = args.ref_budget
+        t_start = time.time()
+        for i in range(args.steps):
+            dt, stages = run_oracle_solve(p)
+            times.append(dt)
+            log(f"[bench:reference] step {i}: {dt:.2f}s {stages}")
+            if time.time() - t_start > budget:
+                break
+    v = statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+        "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator of the BASELINE.json configs)",
+        "config": workload_config(p),
+        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
+                         "sample": f"full {args.workload} solve (fastpi + apply) per step; warm-up on c1; "
+                                   f"{len(times)} of {args.steps} steps within a {budget:.0f}s budget"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(p):
+    w = p.workload
+    return {"workload": w.name, "m": w.m, "n": w.n, "nnz": int(p.A.nnz), "n_labels": w.n_labels,
+            "nnz_Y": int(p.Y.nnz), "rank": w.rank, "alpha": w.alpha, "k": w.k, "seed": w.seed,
+            "l2_flush": "512MB write before every timed step", "parallelism": "replicas"}
+
+
+def ours_arm(args):
+    import torch
+    world, rank, local = dist_setup()
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import DeviceCSR
+    from paper_2011_04235_b200.pinv import fastpi_device
+
+    p = load_problem(args.workload)
+    w = p.workload
+    cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
+    stream = torch.cuda.current_stream()
+    A_dev = DeviceCSR.from_host(p.A)
+    Y_dev = DeviceCSR.from_host(p.Y)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > L2 (126 MB)
+    stats = {}
+
+    def step():
+        res = fastpi_device(A_dev, cfg, stats=stats)
+        Z = res.pseudoinverse.apply_device(Y_dev)
+        return res, Z
+
+    for i in range(args.warmup):
+        t0 = time.perf_counter()
+        res, Z = step()
+        torch.cuda.synchronize()
+        log(f"[bench] warmup {i}: {time.perf_counter() - t0:.3f}s "
+            + " ".join(f"{s.stage}={s.seconds * 1e3:.1f}ms" for s in res.timings))
+    del res, Z
+    launches0 = _lib.kernel_launches()
+    times = []
+    stage_ms = {}
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res, Z = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            for s in res.timings:
+                stage_ms.setdefault(s.stage, []).append(s.seconds * 1e3)
+            del res, Z
+    barrier(world)
+    torch.cuda.synchronize()
+    launches = _lib.kernel_launches() - launches0
+    ms = statistics.mean(times)
+    ms_max = max_over_ranks(ms, world)
+    clocks = clk.summary()
+
+    # ---- roofline: instrumented pass (per kernel class, CUDA events on the library stream)
+    _lib.timing_enable(True)
+    flush.fill_(0.0)
+    res, Z = step()
+    rep = _lib.timing_report(reset=True)
+    _lib.timing_enable(False)
+    del res, Z
+    peaks, peak_src = measured_peaks()
+    fp64_peak = _lib.dmma_peak_tflops()
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    torch.matmul(a, a)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(3):
+        torch.matmul(a, a)
+    t1.record()
+    torch.cuda.synchronize()
+    cublas_dgemm = 3 * 2 * 8192 ** 3 / (t0.elapsed_time(t1) * 1e-3) / 1e12
+    del a
+    total_k = sum(v["ms"] for v in rep.values()) or 1.0
+    kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 3), "share_of_step": round(v["ms"] / ms, 4),
+                   "gflop": round(v["flops"] / 1e9, 3), "gbytes": round(v["bytes"] / 1e9, 4)}
+               for k, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
+    dom_name, dom = max(((k, v) for k, v in rep.items() if v["flops"] > 0 or v["bytes"] > 0),
+                        key=lambda kv: kv[1]["ms"], default=(None, None))
+    roofline = None
+    if dom is not None:
+        avg_ms = dom["ms"] / max(dom["launches"], 1)
+        if "gemm" in dom_name:
+            ach = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
+            peak = max(cublas_dgemm, fp64_peak)
+            roofline = {"kernel": dom_name, "bound": "tensor", "achieved": round(ach, 3), "peak": round(peak, 3),
+                        "unit": "TFLOP/s", "frac": round(ach / peak, 4), "traffic": None,
+                        "avg_launch_ms": round(avg_ms, 4), "launches": dom["launches"],
+                        "share_of_step": round(dom["ms"] / ms, 4),
+                        "peak_source": f"measured FP64 on this GPU: max(cuBLAS DGEMM 8192^3 = {cublas_dgemm:.1f}, "
+                                       f"DMMA issue-rate microbench = {fp64_peak:.1f}) TFLOP/s"}
+        else:
+            ach = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
+            peak = peaks["hbm_gbs"]
+            roofline = {"kernel": dom_name, "bound": "hbm", "achieved": round(ach, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": None,
+                        "avg_launch_ms": round(avg_ms, 4), "launches": dom["launches"],
+                        "share_of_step": round(dom["ms"] / ms, 4), "peak_source": peak_src}
+
+    # ---- e2e through the public API with host inputs
+    e2e = None
+    if not args.no_e2e:
+        h2d_bytes = (p.A.indptr.size * 8 + p.A.indices.size * 4 + p.A.data.size * 8
+                     + p.Y.indptr.size * 8 + p.Y.indices.size * 4 + p.Y.data.size * 8)
+        e2e_t = []
+        d2h_bytes = 0
+        for i in range(max(1, args.steps)):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = fp.fastpi(p.A, cfg)
+            Zh = res.pseudoinverse.apply(p.Y)
+            torch.cuda.synchronize()
+            e2e_t.append(time.perf_counter() - t0)
+            d2h_bytes = Zh.nbytes + 8 * (3 * res.factors.rank + 16)
+            del res, Zh
+        e2e = {"value": max_over_ranks(statistics.mean(e2e_t), world), "unit": "s",
+               "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
+               "note": "fastpi(A scipy) + pseudoinverse.apply(Y scipy) -> numpy Z; pinned staging inside"}
+
+    # ---- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from threadpoolctl import threadpool_limits
+        cores = cpu_cores()
+        with threadpool_limits(cores):
+            dt, _ = run_oracle_solve(p)
+        cpu = {"value": dt, "unit": "s", "cores": cores, "kind": "port",
+               "sample": f"one full {w.name} solve (oracle port: fastpi + apply), {cores} BLAS threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms_max / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator of the BASELINE.json configs; paper corpora unavailable)",
+            "config": workload_config(p), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks,
+            "stages_ms": {k: round(statistics.mean(v), 3) for k, v in stage_ms.items()},
+            "step_ms_all": [round(t, 3) for t in times],
+            "kernels": kernels,
+            "structure": {k: stats[k] for k in ("m1", "n1", "m2", "n2", "T", "s", "r", "rank11", "engines")
+                          if k in stats},
+            "fp64_peaks_tflops": {"cublas_dgemm_8192": round(cublas_dgemm, 2), "dmma_microbench": round(fp64_peak, 2)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=240.0, help="seconds of reference steps before stopping")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -197,6 +197,14 @@ int fpi_pinv_apply_dense(fpi_handle h, int64_t m, int64_t n, int64_t r, const do
                          const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
                          const int64_t* d_col_fwd, int64_t L, const double* d_Y, int64_t ldy, double* d_Z);
 
+/* ---- measurement (bench.py) ---------------------------------------------- */
+/* Record CUDA events around every kernel class launched on this handle. */
+int fpi_timing_enable(fpi_handle h, int on);
+/* "name\tlaunches\tms\tflops\tbytes\n" per kernel class (algorithmic flops / bytes). */
+int fpi_timing_report(fpi_handle h, char* h_buf, int64_t cap, int reset);
+/* FP64 tensor-pipe (DMMA) issue-rate peak of this GPU, TFLOP/s. */
+int fpi_dmma_peak(fpi_handle h, double* h_tflops);
+
 #ifdef __cplusplus
 }
 #endif

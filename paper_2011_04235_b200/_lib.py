@@ -82,6 +82,9 @@ SIGNATURES = {
     "fpi_unfold": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
     "fpi_pinv_apply_csr": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp]),
     "fpi_pinv_apply_dense": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp]),
+    "fpi_timing_enable": (C.c_int, [vp, C.c_int]),
+    "fpi_timing_report": (C.c_int, [vp, C.c_char_p, i64, C.c_int]),
+    "fpi_dmma_peak": (C.c_int, [vp, C.POINTER(f64)]),
 }
 
 _lib = None
@@ -172,3 +175,24 @@ def svd_diag() -> dict:
     load().fpi_get_svd_diag(handle(), C.byref(d))
     return {"engine": d.engine, "cholqr_passes": d.cholqr_passes, "cond_estimate": d.cond_estimate,
             "eig_sweeps": list(d.eig_sweeps), "null_completed": d.null_completed}
+
+
+def timing_enable(on: bool = True):
+    call("fpi_timing_enable", 1 if on else 0)
+
+
+def timing_report(reset: bool = True) -> dict:
+    """Per kernel class: launches, total ms, algorithmic flops and bytes (CUDA events)."""
+    buf = C.create_string_buffer(1 << 16)
+    call("fpi_timing_report", buf, len(buf), 1 if reset else 0)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, n, ms, fl, by = line.split("\t")
+        out[name] = {"launches": int(n), "ms": float(ms), "flops": float(fl), "bytes": float(by)}
+    return out
+
+
+def dmma_peak_tflops() -> float:
+    v = C.c_double(0.0)
+    call("fpi_dmma_peak", C.byref(v))
+    return float(v.value)

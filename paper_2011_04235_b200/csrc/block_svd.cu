@@ -23,6 +23,7 @@
 #include "capi_guard.cuh"
 #include "cub_util.cuh"
 #include "svd_engine.cuh"
+#include "instrument.cuh"
 
 namespace fpi {
 namespace {
@@ -404,6 +405,7 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
     for (int c = 0; c < 2; ++c) {
       const int64_t nsm = counts[c];
       if (!nsm) continue;
+      KTimer kt(h, c == 0 ? "block_svd_jacobi_tiny" : "block_svd_jacobi_smem", 0.0, 0.0);
       k_block_svd_small<<<(unsigned)(nsm < 65535 ? nsm : 65535), BT, smem[c], s>>>(
           lists[c], nsm, spans, st.keep, st.rank_off, st.u_off, st.v_off, a_ptr, a_idx, a_val, sigma, u_val, vt_val,
           60);

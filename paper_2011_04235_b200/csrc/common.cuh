@@ -53,6 +53,7 @@ struct fpi_context {
   fpi_svd_diag diag{};
   // counters
   int64_t kernel_launches = 0;
+  bool timing_on = false;
 };
 
 namespace fpi {

@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "capi_guard.cuh"
 #include "gemm.cuh"
+#include "instrument.cuh"
 
 namespace fpi {
 namespace {
@@ -256,6 +257,8 @@ void gemm(fpi_context* h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
     FPI_LAUNCH_CHECK();
     return;
   }
+  KTimer kt(h, "gemm_f64_dmma", 2.0 * (double)M * (double)N * (double)K,
+            8.0 * ((double)M * K + (double)K * N + (beta == 0.0 ? 1.0 : 2.0) * (double)M * N));
   if (!ta && !tb) launch<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
   else if (!ta && tb) launch<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
   else if (ta && !tb) launch<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);

@@ -1,0 +1,15 @@
+// CUDA-event timing of kernel classes (enabled per handle by fpi_timing_enable).
+#pragma once
+#include "common.cuh"
+
+namespace fpi {
+struct KTimer {
+  fpi_context* h;
+  const char* name;
+  double flops, bytes;
+  bool active = false;
+  void* ev_a = nullptr;
+  KTimer(fpi_context* h, const char* name, double flops, double bytes);
+  ~KTimer();
+};
+}  // namespace fpi

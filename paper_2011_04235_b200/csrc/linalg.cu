@@ -14,6 +14,7 @@
 #include "cub_util.cuh"
 #include "gemm.cuh"
 #include "linalg.cuh"
+#include "instrument.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -448,7 +449,10 @@ int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, 
   unsigned long long* fl = flags.get();
   int* sw = sweeps.get();
   void* args[] = {&nb, &Gp, &ldg, &Vpp, &ldvp, &Jb, &fl, &max_sweeps, &tol, &inner, &sw};
-  FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, 0, s));
+  {
+    KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
+    FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, 0, s));
+  }
   note_launch(h);
   // sort eigenvalues descending, gather vectors
   CubTemp tmp(s);

@@ -24,6 +24,7 @@
 #include "common.cuh"
 #include "capi_guard.cuh"
 #include "cub_util.cuh"
+#include "instrument.cuh"
 #include <cmath>
 
 namespace fpi {
@@ -459,6 +460,7 @@ extern "C" int fpi_reorder(fpi_handle h, int64_t m, int64_t n, int64_t nnz, cons
                            fpi_reorder_info* info) {
   FPI_API_BEGIN(h)
   fpi::ReorderOut o{};
+  fpi::KTimer kt(h, "reorder_loop(all kernels)", 0.0, 0.0);
   fpi::run_reorder(h, m, n, nnz, d_indptr, d_indices, k, d_row_fwd, d_col_fwd, o);
   if (info) {
     info->m1 = o.m1;

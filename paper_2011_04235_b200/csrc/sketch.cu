@@ -20,6 +20,7 @@
 #include "capi_guard.cuh"
 #include "log1p_ieee.cuh"
 #include "generated/ziggurat_tables.h"
+#include "instrument.cuh"
 
 namespace fpi {
 namespace {
@@ -392,6 +393,7 @@ void sketch_normal(fpi_context* h, int64_t seed, int64_t rows, int64_t cols, dou
       nchunks = (int64_t)((double)nchunks * 1.25) + 64;
       continue;
     }
+    KTimer kt(h, "sketch_pcg64_ziggurat_emit", 0.0, 8.0 * (double)N);
     k_emit<<<g1, T, 0, s>>>(st[0], st[1], st[2], st[3], nchunks, centry, cbase, N, cols, ld, d_out);
     FPI_LAUNCH_CHECK();
     note_launch(h, 1);

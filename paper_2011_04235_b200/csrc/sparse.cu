@@ -12,6 +12,7 @@
 #include "capi_guard.cuh"
 #include "cub_util.cuh"
 #include "sparse.cuh"
+#include "instrument.cuh"
 
 namespace fpi {
 namespace {
@@ -413,6 +414,7 @@ extern "C" int fpi_partition(fpi_handle h, int64_t m, int64_t n, int64_t nnz, co
   fpi::PartOut out{a11_ptr, a11_idx, a11_val, t_ptr, t_idx, t_val, tt_ptr, tt_idx, tt_val,
                    a21_ptr, a21_idx, a21_val, a21t_ptr, a21t_idx, a21t_val};
   fpi_partition_info info{};
+  fpi::KTimer kt(h, "permute_partition(all kernels)", 0.0, 2.0 * 12.0 * nnz + 8.0 * (m + n));
   fpi::partition(h, m, n, nnz, d_indptr, d_indices, d_values, d_row_fwd, d_col_fwd, m1, n1, n_spans, d_spans, &info,
                  &out);
   FPI_API_END(h)

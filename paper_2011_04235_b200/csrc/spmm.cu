@@ -11,6 +11,7 @@
 #include "common.cuh"
 #include "capi_guard.cuh"
 #include "spmm.cuh"
+#include "instrument.cuh"
 
 namespace fpi {
 namespace {
@@ -71,7 +72,6 @@ __global__ void __launch_bounds__(WARPS * 32)
 void spmm(fpi_context* h, int64_t p, int64_t q, int64_t k, const int64_t* indptr, const int32_t* indices,
           const double* values, const double* row_scale, double alpha, const double* X, int64_t ldx, double beta,
           double* Y, int64_t ldy) {
-  (void)q;
   if (p <= 0 || k <= 0) return;
   const int64_t slices = (k + SLICE - 1) / SLICE;
   FPI_REQUIRE(slices < 65536, FPI_ECAPACITY, "spmm: too many column slices");
@@ -79,6 +79,11 @@ void spmm(fpi_context* h, int64_t p, int64_t q, int64_t k, const int64_t* indptr
   const int64_t cap = (int64_t)h->num_sms * 16;
   if (gx > cap) gx = cap;
   dim3 grid((unsigned)gx, (unsigned)slices);
+  int64_t nnz = 0;
+  if (h->timing_on) nnz = host_read(indptr + p, h->stream);
+  // algorithmic bytes: 12 nnz + 4 (p + 1) + 8 q k + 8 p k
+  KTimer kt(h, "spmm_csr", 2.0 * (double)nnz * (double)k,
+            12.0 * nnz + 4.0 * (p + 1) + 8.0 * (double)q * k + 8.0 * (double)p * k);
   const bool vec = (ldx % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
   if (vec)
     k_spmm<true><<<grid, WARPS * 32, 0, h->stream>>>(p, k, indptr, indices, values, row_scale, alpha, X, ldx, beta,
