@@ -36,7 +36,13 @@ def h2d(arr: np.ndarray, dtype=None):
 
 
 def d2h(t_) -> np.ndarray:
-    return t_.detach().to("cpu").numpy()
+    """Device tensor -> numpy through page-locked memory (torch's caching host allocator)."""
+    t = torch()
+    if t_.numel() * t_.element_size() < (1 << 20):
+        return t_.detach().to("cpu").numpy()
+    host = t.empty(t_.shape, dtype=t_.dtype, pin_memory=True)
+    host.copy_(t_.detach())
+    return host.numpy()
 
 
 def empty(shape, dtype="f64"):

@@ -1,0 +1,408 @@
+// Symmetric eigensolver: parallel two-sided block Jacobi, one cooperative
+// kernel (replaces LAPACK's dsyevd / the eigen part of dgesdd, svd.py:105,136).
+//
+// The n x n matrix (padded to nb * 16) is split into 16-wide index blocks.
+// A sweep is nb - 1 rounds of the round-robin pairing of blocks; in a round
+// every block pair (I, J) owns the 32 x 32 sub-problem G[I u J, I u J]:
+//   phase A  one CTA per pair, the sub-problem in shared memory: 16 threads
+//            compute the 16 disjoint rotations of a step, all 256 threads apply
+//            them as independent 2 x 2 block updates.  Round 0 of a sweep
+//            rotates the within-block pairs (15 steps), every round the cross
+//            pairs (16 steps), so each index pair is visited once per sweep (a
+//            cyclic Jacobi ordering).
+//   phase B  every 32 x 32 block of G gets G'[P, P'] = R_P^T G[P, P'] R_P' and
+//            every 32-row tile of V gets V[:, P'] <- V[:, P'] R_P', as 32^3
+//            products on the FP64 tensor path (mma.sync m8n8k4 -> DMMA).
+// Grid-wide barriers separate the phases.  A sweep ends by checking the
+// largest off-diagonal measure seen (relative |a_pq| / sqrt(a_pp a_qq), or
+// absolute |a_pq| / max|a_ii| for Gram matrices) against the tolerance, or
+// its stagnation at the rounding floor.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "capi_guard.cuh"
+#include "cub_util.cuh"
+#include "instrument.cuh"
+#include "linalg.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace fpi {
+namespace {
+
+constexpr int JB = 16;      // index block
+constexpr int JS = 32;      // sub-problem (two blocks)
+constexpr int JT = 256;     // threads per CTA
+constexpr int LDS_ = 36;    // smem stride (doubles): conflict-free DMMA fragment loads
+
+__device__ __forceinline__ int rr_block(int pos, int round, int nb) {
+  return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (nb - 1));
+}
+__device__ __forceinline__ int sub_to_global(int l, int bi, int bj) { return l < JB ? bi * JB + l : bj * JB + (l - JB); }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// ---- phase A: cyclic Jacobi on one 32 x 32 sub-problem in shared memory ---
+// Step descriptors: within-block step t (circle method on 16, both halves:
+// pairs k < 8 in the first half, k >= 8 in the second) and cross step t
+// (k <-> 16 + (k + t) % 16).  Each step rotates 16 disjoint index pairs.
+__device__ __forceinline__ int pos16(int i, int t) { return i == 0 ? 0 : 1 + ((i - 1 + t) % 15); }
+__device__ __forceinline__ void step_pair(int mode, int t, int k, int& p, int& q) {
+  if (mode == 0) {
+    const int h = k < 8 ? 0 : 16, kk = k & 7;
+    p = h + pos16(kk, t);
+    q = h + pos16(15 - kk, t);
+  } else {
+    p = k;
+    q = 16 + ((k + t) & 15);
+  }
+}
+
+// S (JS x JS, stride LDS_), R accumulated rotation; returns this thread's max off-diagonal measure
+__device__ double subsolve(double* S, double* R, double* cs_c, double* cs_s, int* pp, int* pq, bool round0,
+                           double tol, double ascale, bool absolute) {
+  double om = 0.0;
+  const int nsteps0 = round0 ? 15 : 0;
+  for (int st = 0; st < nsteps0 + 16; ++st) {
+    const int mode = st < nsteps0 ? 0 : 1, t = st < nsteps0 ? st : st - nsteps0;
+    if (threadIdx.x < 16) {
+      const int k = threadIdx.x;
+      int p, q;
+      step_pair(mode, t, k, p, q);
+      const double app = S[p * LDS_ + p], aqq = S[q * LDS_ + q], apq = S[p * LDS_ + q];
+      // threshold test and the rotation are independent chains (the rotation is discarded when not needed)
+      const double den2 = absolute ? ascale * ascale : fabs(app) * fabs(aqq);
+      const double apq2 = apq * apq;
+      const double ratio = den2 > 0.0 ? sqrt(apq2 / den2) : (apq != 0.0 ? 1.0 : 0.0);
+      om = fmax(om, ratio);
+      // Rutishauser angle t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (aqq - app) / (2 apq),
+      // evaluated in FP32 (short MUFU chain): any t gives an exactly orthogonal FP64 rotation
+      // c = 1 / sqrt(1 + t^2), s = c t; an inexact angle only leaves a tiny off-diagonal that the
+      // 2x2 update below computes (it is not forced to zero) and the next sweep removes.
+      const float zf = (float)((aqq - app) / 1.0) * __frcp_rn((float)(2.0 * apq));
+      const float azf = fabsf(zf);
+      const float tf = azf > 1e18f ? 0.5f / zf : copysignf(__frcp_rn(azf + sqrtf(fmaf(zf, zf, 1.0f))), zf);
+      const double tt = isfinite(tf) ? (double)tf : 0.0;
+      const bool rot = apq != 0.0 && apq2 > tol * tol * den2 && tt != 0.0;
+      const double c = rot ? rsqrt(fma(tt, tt, 1.0)) : 1.0;
+      const double sn = rot ? c * tt : 0.0;
+      cs_c[k] = c;
+      cs_s[k] = sn;
+      pp[k] = p;
+      pq[k] = q;
+    }
+    __syncthreads();
+    // S <- J^T S J as independent 2x2 blocks (pair k rows x pair l cols); R <- R J
+    {
+      const int k = threadIdx.x >> 4, l = threadIdx.x & 15;
+      const double ck = cs_c[k], sk = cs_s[k], cl = cs_c[l], sl = cs_s[l];
+      const int pk = pp[k], qk = pq[k], pl = pp[l], ql = pq[l];
+      if (sk != 0.0 || sl != 0.0) {
+        const double a = S[pk * LDS_ + pl], b = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
+        const double ra = ck * a - sk * c2, rb = ck * b - sk * d;
+        const double rc = sk * a + ck * c2, rd = sk * b + ck * d;
+        const double na = ra * cl - rb * sl, nb = ra * sl + rb * cl, nc = rc * cl - rd * sl, nd = rc * sl + rd * cl;
+        S[pk * LDS_ + pl] = na;
+        S[pk * LDS_ + ql] = nb;
+        S[qk * LDS_ + pl] = nc;
+        S[qk * LDS_ + ql] = nd;
+      }
+      if (sk != 0.0) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int row = l + 16 * h2;
+          const double rp = R[row * LDS_ + pk], rq = R[row * LDS_ + qk];
+          R[row * LDS_ + pk] = ck * rp - sk * rq;
+          R[row * LDS_ + qk] = sk * rp + ck * rq;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return om;
+}
+
+// 32x32x32 product C = op(A) B on DMMA: A, B in smem (stride LDS_); TA: A stored transposed.
+template <bool TA>
+__device__ __forceinline__ void mm32(const double* A, const double* B, double (&acc)[2][2], int warp, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const int m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
+  acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
+#pragma unroll
+  for (int k0 = 0; k0 < JS; k0 += 4) {
+    const double a = TA ? A[(k0 + t) * LDS_ + m0 + g] : A[(m0 + g) * LDS_ + k0 + t];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double b = B[(k0 + t) * LDS_ + n0 + 8 * j + g];
+      dmma(acc[j][0], acc[j][1], a, b);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(JT, 3)
+    k_jacobi(int nb, double* G, int64_t ldg, double* V, int64_t ldv, double* Jbuf, int* jflag,
+             unsigned long long* offmax, int max_sweeps, double tol, int* sweeps_out, const double* abs_scale,
+             unsigned long long* prof) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ __align__(16) double Sa[JS * LDS_];
+  __shared__ __align__(16) double Ra[JS * LDS_];
+  __shared__ __align__(16) double Rb[JS * LDS_];
+  __shared__ __align__(16) double Tm[JS * LDS_];
+  __shared__ double cs_c[16], cs_s[16];
+  __shared__ int pp[16], pq[16];
+  const bool absolute = abs_scale != nullptr;
+  const double ascale = absolute ? *abs_scale : 0.0;
+  const int npairs = nb / 2;
+  const int64_t npad = (int64_t)nb * JB;
+  const int64_t rtiles = (npad + JS - 1) / JS;
+  const int64_t gitems = (int64_t)npairs * npairs;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    for (int round = 0; round < nb - 1; ++round) {
+      const unsigned long long t0 = prof ? gtimer() : 0;
+      // ---- phase A: one CTA per pair (sub-problem in smem)
+      for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+        const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
+        for (int e = threadIdx.x; e < JS * JS; e += JT) {
+          const int a = e >> 5, b = e & 31;
+          Sa[a * LDS_ + b] = G[(int64_t)sub_to_global(a, bi, bj) * ldg + sub_to_global(b, bi, bj)];
+          Ra[a * LDS_ + b] = a == b ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        const unsigned long long ts0 = prof ? gtimer() : 0;
+        double om = subsolve(Sa, Ra, cs_c, cs_s, pp, pq, round == 0, tol, ascale, absolute);
+        if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
+        double* Jp = Jbuf + (int64_t)pr * JS * JS;
+        int rot = 0;
+        for (int e = threadIdx.x; e < JS * JS; e += JT) {
+          const double v = Ra[(e >> 5) * LDS_ + (e & 31)];
+          Jp[e] = v;
+          rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
+        }
+        rot = __syncthreads_or(rot);
+        if (threadIdx.x == 0) jflag[pr] = rot;
+        if (threadIdx.x < 32) {
+          for (int o = 16; o; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
+          if (threadIdx.x == 0 && om > 0.0) atomicMax(offmax + sweep, (unsigned long long)__double_as_longlong(om));
+        }
+        __syncthreads();
+      }
+      const unsigned long long t1 = prof ? gtimer() : 0;
+      grid.sync();
+      const unsigned long long t2 = prof ? gtimer() : 0;
+      // ---- phase B
+      for (int64_t item = blockIdx.x; item < gitems + (int64_t)npairs * rtiles; item += gridDim.x) {
+        if (item < gitems) {
+          const int pa = (int)(item / npairs), pb = (int)(item % npairs);
+          const int ai = rr_block(pa, round, nb), aj = rr_block(nb - 1 - pa, round, nb);
+          const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
+          if (!jflag[pa] && !jflag[pb]) continue;  // both rotations are the identity
+          const double* Ja = Jbuf + (int64_t)pa * JS * JS;
+          const double* Jb2 = Jbuf + (int64_t)pb * JS * JS;
+          for (int e = threadIdx.x; e < JS * JS; e += JT) {
+            const int a = e >> 5, b = e & 31;
+            Sa[a * LDS_ + b] = G[(int64_t)sub_to_global(a, ai, aj) * ldg + sub_to_global(b, bi, bj)];
+            Ra[a * LDS_ + b] = Ja[e];
+            Rb[a * LDS_ + b] = Jb2[e];
+          }
+          __syncthreads();
+          double acc[2][2];
+          mm32<true>(Ra, Sa, acc, warp, lane);  // Tm = Ja^T S
+          {
+            const int g = lane >> 2, t = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              Tm[(m0 + g) * LDS_ + n0 + 8 * j + 2 * t] = acc[j][0];
+              Tm[(m0 + g) * LDS_ + n0 + 8 * j + 2 * t + 1] = acc[j][1];
+            }
+          }
+          __syncthreads();
+          mm32<false>(Tm, Rb, acc, warp, lane);  // G' = Tm Jb
+          {
+            const int g = lane >> 2, t = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
+            const int64_t row = sub_to_global(m0 + g, ai, aj);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int c0 = n0 + 8 * j + 2 * t;
+              G[row * ldg + sub_to_global(c0, bi, bj)] = acc[j][0];
+              G[row * ldg + sub_to_global(c0 + 1, bi, bj)] = acc[j][1];
+            }
+          }
+        } else {
+          const int64_t it2 = item - gitems;
+          const int pb = (int)(it2 / rtiles);
+          const int64_t r0 = (it2 % rtiles) * JS;
+          const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
+          if (!jflag[pb]) continue;
+          const double* Jb2 = Jbuf + (int64_t)pb * JS * JS;
+          for (int e = threadIdx.x; e < JS * JS; e += JT) {
+            const int a = e >> 5, b = e & 31;
+            Sa[a * LDS_ + b] = (r0 + a < npad) ? V[(r0 + a) * ldv + sub_to_global(b, bi, bj)] : 0.0;
+            Rb[a * LDS_ + b] = Jb2[e];
+          }
+          __syncthreads();
+          double acc[2][2];
+          mm32<false>(Sa, Rb, acc, warp, lane);  // V tile * Jb
+          const int g = lane >> 2, t = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
+          const int64_t row = r0 + m0 + g;
+          if (row < npad) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int c0 = n0 + 8 * j + 2 * t;
+              V[row * ldv + sub_to_global(c0, bi, bj)] = acc[j][0];
+              V[row * ldv + sub_to_global(c0 + 1, bi, bj)] = acc[j][1];
+            }
+          }
+        }
+        __syncthreads();
+      }
+      const unsigned long long t3 = prof ? gtimer() : 0;
+      grid.sync();
+      if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
+        prof[0] += t1 - t0;
+        prof[1] += t2 - t1;
+        prof[2] += t3 - t2;
+        prof[3] += gtimer() - t3;
+      }
+    }
+    const double cur = __longlong_as_double((long long)offmax[sweep]);
+    const double prev = sweep ? __longlong_as_double((long long)offmax[sweep - 1]) : 1e300;
+    if (cur <= tol || (cur < 1e-9 && cur > 0.25 * prev)) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep + 1;
+}
+
+__global__ void k_max_diag(int64_t n, const double* A, int64_t lda, double* out) {
+  __shared__ double red[256];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(A[i * lda + i]));
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0] > 0.0 ? red[0] : 1.0;
+}
+
+__global__ void k_pad_copy(int64_t n, int64_t npad, const double* A, int64_t lda, double* G) {
+  FPI_GRID_STRIDE(e, npad * npad) {
+    int64_t i = e / npad, j = e - i * npad;
+    G[e] = (i < n && j < n) ? A[i * lda + j] : 0.0;
+  }
+}
+
+__global__ void k_identity(int64_t n, double* A) {
+  FPI_GRID_STRIDE(e, n * n) A[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+__global__ void k_diag_keys(int64_t n, const double* G, int64_t npad, double* keys, int32_t* idx) {
+  FPI_GRID_STRIDE(i, n) {
+    keys[i] = G[i * npad + i];
+    idx[i] = (int32_t)i;
+  }
+}
+
+__global__ void k_gather_eig(int64_t n, const double* Vp, int64_t npad, const int32_t* order, const double* wsorted,
+                             double* w, double* V, int64_t ldv) {
+  FPI_GRID_STRIDE(e, n * n) {
+    int64_t i = e / n, k = e - i * n;
+    V[i * ldv + k] = Vp[i * npad + order[k]];
+    if (i == 0) w[k] = wsorted[k];
+  }
+}
+
+}  // namespace
+
+int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, double* V, int64_t ldv,
+            int max_sweeps, double tol, bool absolute) {
+  cudaStream_t s = h->stream;
+  if (n <= 0) return 0;
+  int nb = (int)((n + JB - 1) / JB);
+  if (nb < 2) nb = 2;
+  if (nb % 2) ++nb;
+  const int64_t npad = (int64_t)nb * JB;
+  Scratch<double> G(npad * npad, s), Vp(npad * npad, s), Jbuf((int64_t)(nb / 2) * JS * JS, s);
+  Scratch<int> jflag(nb / 2, s);
+  Scratch<unsigned long long> offm(max_sweeps + 1, s);
+  Scratch<int> sweeps(1, s);
+  Scratch<double> scale(1, s);
+  FPI_CUDA(cudaMemsetAsync(offm.get(), 0, sizeof(unsigned long long) * (max_sweeps + 1), s));
+  const unsigned G16 = (unsigned)(h->num_sms * 16);
+  k_pad_copy<<<grid_for(npad * npad, 256, G16), 256, 0, s>>>(n, npad, A, lda, G);
+  k_identity<<<grid_for(npad * npad, 256, G16), 256, 0, s>>>(npad, Vp);
+  double* scale_p = nullptr;
+  if (absolute) {
+    k_max_diag<<<1, 256, 0, s>>>(n, A, lda, scale);
+    scale_p = scale.get();
+  }
+  FPI_LAUNCH_CHECK();
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    int per_sm = 0;
+    FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, JT, 0));
+    max_blocks = per_sm * h->num_sms;
+  }
+  const int64_t rtiles = (npad + JS - 1) / JS;
+  const int64_t want = (int64_t)(nb / 2) * (nb / 2) + (int64_t)(nb / 2) * rtiles;
+  int cap_blocks = max_blocks;
+  if (const char* e = getenv("FPI_JACOBI_GRID")) cap_blocks = atoi(e) < max_blocks ? atoi(e) : max_blocks;
+  int grid = (int)(want < cap_blocks ? want : cap_blocks);
+  if (grid < nb / 2) grid = nb / 2 < max_blocks ? nb / 2 : max_blocks;
+  if (grid < 1) grid = 1;
+  Scratch<unsigned long long> prof(5, s);
+  FPI_CUDA(cudaMemsetAsync(prof.get(), 0, sizeof(unsigned long long) * 5, s));
+  unsigned long long* prof_p = getenv("FPI_JACOBI_PROFILE") ? prof.get() : nullptr;
+  double* Gp = G.get();
+  int64_t ldg = npad;
+  double* Vpp = Vp.get();
+  int64_t ldvp = npad;
+  double* Jb = Jbuf.get();
+  int* jf = jflag.get();
+  unsigned long long* om = offm.get();
+  int* sw = sweeps.get();
+  void* args[] = {&nb, &Gp, &ldg, &Vpp, &ldvp, &Jb, &jf, &om, &max_sweeps, &tol, &sw, &scale_p, &prof_p};
+  {
+    KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
+    FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, 0, s));
+  }
+  note_launch(h);
+  CubTemp tmp(s);
+  Scratch<double> keys(n, s), keys2(n, s);
+  Scratch<int32_t> idx(n, s), idx2(n, s);
+  k_diag_keys<<<grid_for(n, 256, h->num_sms * 4), 256, 0, s>>>(n, G, npad, keys, idx);
+  sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n, true, 0, 64, s);
+  k_gather_eig<<<grid_for(n * n, 256, G16), 256, 0, s>>>(n, Vp, npad, idx2, keys2, w, V, ldv);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 3);
+  if (prof_p) {
+    unsigned long long hp[5];
+    FPI_CUDA(cudaMemcpyAsync(hp, prof_p, sizeof(hp), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "[jacobi n=%lld grid=%d] phaseA %.3f (subsolve %.3f)  syncA %.3f  phaseB %.3f  syncB %.3f ms\n",
+            (long long)n, grid, hp[0] * 1e-6, hp[4] * 1e-6, hp[1] * 1e-6, hp[2] * 1e-6, hp[3] * 1e-6);
+  }
+  return host_read(sweeps.get(), s);
+}
+
+}  // namespace fpi
+
+extern "C" int fpi_sym_eig(fpi_handle h, int64_t n, const double* d_A, int64_t lda, double* d_w, double* d_V,
+                           int64_t ldv, int32_t* h_sweeps) {
+  FPI_API_BEGIN(h)
+  int sw = fpi::sym_eig(h, n, d_A, lda, d_w, d_V, ldv, 60, 1e-14, false);
+  if (h_sweeps) *h_sweeps = sw;
+  FPI_API_END(h)
+}

@@ -2,12 +2,10 @@
 //   * Cholesky (blocked, right-looking; trailing updates on the DMMA GEMM) and
 //     lower-triangular solves with many right-hand sides -- CholeskyQR of the
 //     sketch (replaces LAPACK dgeqrf+dorgqr, svd.py:134),
-//   * a symmetric eigensolver: parallel two-sided block Jacobi (cyclic
-//     round-robin over 16-wide column blocks) in one cooperative kernel with
-//     grid-wide barriers between the solve / row-rotate / column-rotate
-//     phases -- the small SVDs (replaces dgesdd, svd.py:105,136,166),
+//   * (the symmetric eigensolver lives in jacobi.cu),
 //   * small helpers: transpose, column norms, scaling, canonical signs.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "capi_guard.cuh"
@@ -99,187 +97,6 @@ __global__ void k_set_identity(int64_t n, double* A, int64_t lda) {
   FPI_GRID_STRIDE(e, n * n) {
     int64_t i = e / n, j = e - i * n;
     A[i * lda + j] = i == j ? 1.0 : 0.0;
-  }
-}
-
-// ---- symmetric block Jacobi ------------------------------------------------
-constexpr int JB = 16;         // column block width
-constexpr int JS = 2 * JB;     // sub-problem size
-constexpr int JT = 256;        // threads per CTA
-constexpr int TILE = 64;       // columns (phase B) / rows (phase C) per work item
-
-__device__ __forceinline__ int rr_block(int pos, int round, int nb) {
-  return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (nb - 1));
-}
-
-__device__ __forceinline__ int sub_to_global(int l, int bi, int bj) { return l < JB ? bi * JB + l : bj * JB + (l - JB); }
-
-__global__ void __launch_bounds__(JT)
-    k_jacobi(int nb, double* G, int64_t ldg, double* V, int64_t ldv, double* Jbuf,
-             unsigned long long* offmax, int max_sweeps, double tol, int inner_sweeps, int* sweeps_out) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ double S[JS][JS + 1];
-  __shared__ double R[JS][JS + 1];
-  __shared__ double T[JS][TILE + 1];
-  __shared__ double cs_c[JS / 2], cs_s[JS / 2];
-  __shared__ int pair_p[JS / 2], pair_q[JS / 2];
-  __shared__ unsigned long long blk_off;
-  const int npairs = nb / 2;
-  const int64_t npad = (int64_t)nb * JB;
-  const int64_t ctiles = (npad + TILE - 1) / TILE;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    for (int round = 0; round < nb - 1; ++round) {
-      // ---- phase A: solve each 2b x 2b sub-problem, accumulate its rotation
-      for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
-        const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
-        for (int e = threadIdx.x; e < JS * JS; e += JT) {
-          int a = e / JS, b = e % JS;
-          S[a][b] = G[(int64_t)sub_to_global(a, bi, bj) * ldg + sub_to_global(b, bi, bj)];
-          R[a][b] = a == b ? 1.0 : 0.0;
-        }
-        if (threadIdx.x == 0) blk_off = 0ull;
-        __syncthreads();
-        for (int isw = 0; isw < inner_sweeps; ++isw) {
-          for (int step = 0; step < JS - 1; ++step) {
-            if (threadIdx.x < JS / 2) {
-              const int k = threadIdx.x;
-              // round-robin (circle) pairing of the JS local indices
-              const int p = rr_block(k, step, JS), q = rr_block(JS - 1 - k, step, JS);
-              double app = S[p][p], aqq = S[q][q], apq = S[p][q];
-              double c = 1.0, s = 0.0;
-              const double den = sqrt(fabs(app) * fabs(aqq));
-              const double ratio = den > 0.0 ? fabs(apq) / den : (apq != 0.0 ? 1.0 : 0.0);
-              if (isw == 0 && ratio > 0.0) atomicMax(&blk_off, (unsigned long long)__double_as_longlong(ratio));
-              if (apq != 0.0 && ratio > tol) {
-                double zeta = (aqq - app) / (2.0 * apq);
-                double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                c = 1.0 / sqrt(1.0 + t * t);
-                s = c * t;
-              }
-              cs_c[k] = c;
-              cs_s[k] = s;
-              pair_p[k] = p;
-              pair_q[k] = q;
-            }
-            __syncthreads();
-            // rows
-            for (int e = threadIdx.x; e < (JS / 2) * JS; e += JT) {
-              int k = e / JS, col = e % JS;
-              double c = cs_c[k], s = cs_s[k];
-              if (s == 0.0) continue;
-              int p = pair_p[k], q = pair_q[k];
-              double ap = S[p][col], aq = S[q][col];
-              S[p][col] = c * ap - s * aq;
-              S[q][col] = s * ap + c * aq;
-            }
-            __syncthreads();
-            // columns (+ accumulated rotation)
-            for (int e = threadIdx.x; e < (JS / 2) * JS; e += JT) {
-              int k = e / JS, row = e % JS;
-              double c = cs_c[k], s = cs_s[k];
-              if (s == 0.0) continue;
-              int p = pair_p[k], q = pair_q[k];
-              double ap = S[row][p], aq = S[row][q];
-              S[row][p] = c * ap - s * aq;
-              S[row][q] = s * ap + c * aq;
-              double rp = R[row][p], rq = R[row][q];
-              R[row][p] = c * rp - s * rq;
-              R[row][q] = s * rp + c * rq;
-            }
-            __syncthreads();
-            if (threadIdx.x < JS / 2 && cs_s[threadIdx.x] != 0.0) {
-              S[pair_p[threadIdx.x]][pair_q[threadIdx.x]] = 0.0;
-              S[pair_q[threadIdx.x]][pair_p[threadIdx.x]] = 0.0;
-            }
-            __syncthreads();
-          }
-        }
-        double* Jp = Jbuf + (int64_t)pr * JS * JS;
-        for (int e = threadIdx.x; e < JS * JS; e += JT) Jp[e] = R[e / JS][e % JS];
-        if (threadIdx.x == 0 && blk_off) atomicMax(offmax + sweep, blk_off);
-        __syncthreads();
-      }
-      grid.sync();
-      // ---- phase B: G[I u J, :] <- J^T G[I u J, :]
-      for (int64_t item = blockIdx.x; item < (int64_t)npairs * ctiles; item += gridDim.x) {
-        const int pr = (int)(item / ctiles);
-        const int64_t c0 = (item % ctiles) * TILE;
-        const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
-        const double* Jp = Jbuf + (int64_t)pr * JS * JS;
-        for (int e = threadIdx.x; e < JS * JS; e += JT) R[e / JS][e % JS] = Jp[e];
-        for (int e = threadIdx.x; e < JS * TILE; e += JT) {
-          int a = e / TILE, c = e % TILE;
-          T[a][c] = (c0 + c < npad) ? G[(int64_t)sub_to_global(a, bi, bj) * ldg + c0 + c] : 0.0;
-        }
-        __syncthreads();
-        for (int e = threadIdx.x; e < JS * TILE; e += JT) {
-          int a = e / TILE, c = e % TILE;
-          if (c0 + c >= npad) continue;
-          double acc = 0.0;
-#pragma unroll 8
-          for (int kk = 0; kk < JS; ++kk) acc = fma(R[kk][a], T[kk][c], acc);
-          G[(int64_t)sub_to_global(a, bi, bj) * ldg + c0 + c] = acc;
-        }
-        __syncthreads();
-      }
-      grid.sync();
-      // ---- phase C: G[:, I u J] <- G[:, I u J] J ;  V[:, I u J] <- V[:, I u J] J
-      for (int64_t item = blockIdx.x; item < (int64_t)npairs * ctiles * 2; item += gridDim.x) {
-        const int which = (int)(item % 2);
-        const int64_t it2 = item / 2;
-        const int pr = (int)(it2 / ctiles);
-        const int64_t r0 = (it2 % ctiles) * TILE;
-        const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
-        double* M = which ? V : G;
-        const int64_t ldm = which ? ldv : ldg;
-        const double* Jp = Jbuf + (int64_t)pr * JS * JS;
-        for (int e = threadIdx.x; e < JS * JS; e += JT) R[e / JS][e % JS] = Jp[e];
-        for (int e = threadIdx.x; e < JS * TILE; e += JT) {
-          int r = e / JS, a = e % JS;  // T used as [a][r]
-          T[a][r] = (r0 + r < npad) ? M[(r0 + r) * ldm + sub_to_global(a, bi, bj)] : 0.0;
-        }
-        __syncthreads();
-        for (int e = threadIdx.x; e < JS * TILE; e += JT) {
-          int r = e / JS, a = e % JS;
-          if (r0 + r >= npad) continue;
-          double acc = 0.0;
-#pragma unroll 8
-          for (int kk = 0; kk < JS; ++kk) acc = fma(T[kk][r], R[kk][a], acc);
-          M[(r0 + r) * ldm + sub_to_global(a, bi, bj)] = acc;
-        }
-        __syncthreads();
-      }
-      grid.sync();
-    }
-    // stop when converged, or when the off-diagonal measure stagnates at the rounding floor
-    const double cur = __longlong_as_double((long long)offmax[sweep]);
-    const double prev = sweep ? __longlong_as_double((long long)offmax[sweep - 1]) : 1e300;
-    if (cur <= tol || (cur < 1e-9 && cur > 0.25 * prev)) break;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep + 1;
-}
-
-__global__ void k_pad_copy(int64_t n, int64_t npad, const double* A, int64_t lda, double* G) {
-  FPI_GRID_STRIDE(e, npad * npad) {
-    int64_t i = e / npad, j = e - i * npad;
-    G[e] = (i < n && j < n) ? A[i * lda + j] : 0.0;
-  }
-}
-
-__global__ void k_diag_keys(int64_t n, const double* G, int64_t npad, double* keys, int32_t* idx) {
-  FPI_GRID_STRIDE(i, n) {
-    keys[i] = G[i * npad + i];
-    idx[i] = (int32_t)i;
-  }
-}
-
-__global__ void k_gather_eig(int64_t n, const double* Vp, int64_t npad, const int32_t* order, const double* wsorted,
-                             double* w, double* V, int64_t ldv) {
-  FPI_GRID_STRIDE(e, n * n) {
-    int64_t i = e / n, k = e - i * n;
-    V[i * ldv + k] = Vp[i * npad + order[k]];
-    if (i == 0) w[k] = wsorted[k];
   }
 }
 
@@ -414,58 +231,6 @@ void lower_inverse(fpi_context* h, int64_t n, const double* L, int64_t ldl, doub
   trsm_lower_left(h, n, L, ldl, Linv, ldi, n);
 }
 
-int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, double* V, int64_t ldv,
-            int max_sweeps) {
-  cudaStream_t s = h->stream;
-  if (n <= 0) return 0;
-  int nb = (int)((n + JB - 1) / JB);
-  if (nb < 2) nb = 2;
-  if (nb % 2) ++nb;
-  const int64_t npad = (int64_t)nb * JB;
-  Scratch<double> G(npad * npad, s), Vp(npad * npad, s), Jbuf((int64_t)(nb / 2) * JS * JS, s);
-  Scratch<unsigned long long> flags(max_sweeps + 1, s);
-  Scratch<int> sweeps(1, s);
-  FPI_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(unsigned long long) * (max_sweeps + 1), s));
-  k_pad_copy<<<grid_for(npad * npad, 256, h->num_sms * 16), 256, 0, s>>>(n, npad, A, lda, G);
-  k_set_identity<<<grid_for(npad * npad, 256, h->num_sms * 16), 256, 0, s>>>(npad, Vp, npad);
-  FPI_LAUNCH_CHECK();
-  static int max_blocks = 0;
-  if (!max_blocks) {
-    int per_sm = 0;
-    FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, JT, 0));
-    max_blocks = per_sm * h->num_sms;
-  }
-  const int64_t ctiles = (npad + TILE - 1) / TILE;
-  int64_t want = (int64_t)(nb / 2) * ctiles * 2;
-  int grid = (int)(want < max_blocks ? want : max_blocks);
-  if (grid < 1) grid = 1;
-  double tol = 1e-14;
-  int inner = 1;
-  double* Gp = G.get();
-  int64_t ldg = npad;
-  double* Vpp = Vp.get();
-  int64_t ldvp = npad;
-  double* Jb = Jbuf.get();
-  unsigned long long* fl = flags.get();
-  int* sw = sweeps.get();
-  void* args[] = {&nb, &Gp, &ldg, &Vpp, &ldvp, &Jb, &fl, &max_sweeps, &tol, &inner, &sw};
-  {
-    KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
-    FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, 0, s));
-  }
-  note_launch(h);
-  // sort eigenvalues descending, gather vectors
-  CubTemp tmp(s);
-  Scratch<double> keys(n, s), keys2(n, s);
-  Scratch<int32_t> idx(n, s), idx2(n, s);
-  k_diag_keys<<<grid_for(n, 256, h->num_sms * 4), 256, 0, s>>>(n, G, npad, keys, idx);
-  sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n, true, 0, 64, s);
-  k_gather_eig<<<grid_for(n * n, 256, h->num_sms * 16), 256, 0, s>>>(n, Vp, npad, idx2, keys2, w, V, ldv);
-  FPI_LAUNCH_CHECK();
-  note_launch(h, 3);
-  return host_read(sweeps.get(), s);
-}
-
 void transpose(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* B, int64_t ldb) {
   if (M <= 0 || N <= 0) return;
   dim3 blk(32, 8);
@@ -515,10 +280,3 @@ extern "C" int fpi_cholesky(fpi_handle h, int64_t n, double* d_A, int64_t lda) {
   FPI_API_END(h)
 }
 
-extern "C" int fpi_sym_eig(fpi_handle h, int64_t n, const double* d_A, int64_t lda, double* d_w, double* d_V,
-                           int64_t ldv, int32_t* h_sweeps) {
-  FPI_API_BEGIN(h)
-  int sw = fpi::sym_eig(h, n, d_A, lda, d_w, d_V, ldv, 60);
-  if (h_sweeps) *h_sweeps = sw;
-  FPI_API_END(h)
-}

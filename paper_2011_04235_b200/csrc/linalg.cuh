@@ -7,8 +7,10 @@ void cholesky_lower(fpi_context* h, int64_t n, double* A, int64_t lda, int* h_in
 void trsm_lower_left(fpi_context* h, int64_t n, const double* L, int64_t ldl, double* X, int64_t ldx, int64_t nrhs);
 void lower_inverse(fpi_context* h, int64_t n, const double* L, int64_t ldl, double* Linv, int64_t ldi);
 // eigenvalues descending in w (n), eigenvectors as columns of V (n x n); returns Jacobi sweeps used
+// Converged when every |a_pq| <= tol * sqrt(|a_pp a_qq|) (relative), or, with `absolute`,
+// <= tol * max_i |a_ii|; also stops when the measure stagnates at rounding level.
 int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, double* V, int64_t ldv,
-            int max_sweeps);
+            int max_sweeps, double tol = 1e-14, bool absolute = false);
 void transpose(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* B, int64_t ldb);
 void col_sumsq(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* out);
 void scale_cols(fpi_context* h, int64_t M, int64_t N, double* A, int64_t lda, const double* s, bool divide);

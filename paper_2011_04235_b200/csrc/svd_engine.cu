@@ -216,17 +216,42 @@ static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M
                            double* U, double* sigma, double* Vt, fpi_svd_diag* diag) {
   cudaStream_t s = h->stream;
   const unsigned G = (unsigned)(h->num_sms * 16);
-  Scratch<double> Gm(q * q, s), W0(q * q, s), w0(q, s), M1(p * q, s), W1(q * q, s), w1(q, s), V(q * q, s);
+  Scratch<double> Gm(q * q, s), W0(q * q, s), w0(q, s);
   gemm(h, true, false, q, q, p, 1.0, M, ldm, M, ldm, 0.0, Gm, q);
-  int sw0 = sym_eig(h, q, Gm, q, w0, W0, q, 60);
-  gemm(h, false, false, p, q, q, 1.0, M, ldm, W0, q, 0.0, M1, q);
-  gemm(h, true, false, q, q, p, 1.0, M1, q, M1, q, 0.0, Gm, q);
-  int sw1 = sym_eig(h, q, Gm, q, w1, W1, q, 60);
-  gemm(h, false, false, q, q, q, 1.0, W0, q, W1, q, 0.0, V, q);
-  // candidate left vectors for the top `rank` (by w1) and their norms
+  // Gram entries are accurate to eps * ||G|| in absolute terms: converge to that (absolute criterion)
+  int sw0 = sym_eig(h, q, Gm, q, w0, W0, q, 60, 1e-15, true);
+  int sw1 = 0;
+  // sigma_i from the Gram eigenpairs carries absolute error ~eps sigma_1^2 / sigma_i; when the kept
+  // spectrum is wide (sigma_r / sigma_1 < 1e-3) refine once: M1 = M W0 has nearly orthogonal
+  // columns, and the Jacobi solve of its Gram then converges to relative accuracy in a few sweeps.
+  double lam[2];
+  FPI_CUDA(cudaMemcpyAsync(&lam[0], w0.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  FPI_CUDA(cudaMemcpyAsync(&lam[1], w0.get() + (rank - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+  FPI_CUDA(cudaStreamSynchronize(s));
+  const bool refine = !(lam[0] > 0.0) || lam[1] < 1e-6 * lam[0];
+  const double* Mr = M;  // columns whose directions are refined
+  int64_t ldr = ldm;
+  Scratch<double> M1, W1, w1, V;
+  const double* Vfin = W0.get();
+  const double* Wsel = W0.get();  // maps Mr's columns to the candidate left vectors
+  if (refine) {
+    M1.alloc(p * q, s);
+    W1.alloc(q * q, s);
+    w1.alloc(q, s);
+    V.alloc(q * q, s);
+    gemm(h, false, false, p, q, q, 1.0, M, ldm, W0, q, 0.0, M1, q);
+    gemm(h, true, false, q, q, p, 1.0, M1, q, M1, q, 0.0, Gm, q);
+    sw1 = sym_eig(h, q, Gm, q, w1, W1, q, 60, 1e-14, false);
+    gemm(h, false, false, q, q, q, 1.0, W0, q, W1, q, 0.0, V, q);
+    Mr = M1.get();
+    ldr = q;
+    Vfin = V.get();
+    Wsel = W1.get();
+  }
+  // candidate left vectors for the top `rank` and their norms (= sigma)
   Scratch<double> Uraw(p * rank, s), ss(rank, s), ss2(rank, s);
   Scratch<int32_t> ord(rank, s), ord2(rank, s);
-  gemm(h, false, false, p, rank, q, 1.0, M1, q, W1, q, 0.0, Uraw, rank);
+  gemm(h, false, false, p, rank, q, 1.0, Mr, ldr, Wsel, q, 0.0, Uraw, rank);
   col_sumsq(h, p, rank, Uraw, rank, ss);
   k_sqrt_clamp<<<grid_for(rank, 256, G), 256, 0, s>>>(rank, ss);
   // sort the kept sigma descending (ties keep order) so factors are flagged sorted
@@ -235,15 +260,16 @@ static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M
   sort_pairs(tmp, ss.get(), ss2.get(), ord.get(), ord2.get(), rank, true, 0, 64, s);
   FPI_CUDA(cudaMemcpyAsync(sigma, ss2.get(), sizeof(double) * rank, cudaMemcpyDeviceToDevice, s));
   k_gather_cols_div<<<grid_for(p * rank, 256, G), 256, 0, s>>>(p, rank, Uraw, rank, ord2, ss2, U, rank);
-  // Vt rows = columns of V for the same triplets: V column index = ord2 (within the first `rank`)
-  k_gather_vt<<<grid_for(rank * q, 256, G), 256, 0, s>>>(q, rank, V, q, ord2, Vt, q);
+  k_gather_vt<<<grid_for(rank * q, 256, G), 256, 0, s>>>(q, rank, Vfin, q, ord2, Vt, q);
   FPI_LAUNCH_CHECK();
   note_launch(h, 5);
   complete_null_left(h, p, rank, U, rank, sigma, diag);
   canonical_signs(h, rank, p, q, U, rank, Vt, q);
   if (diag) {
-    diag->eig_sweeps[0] = sw0;
-    diag->eig_sweeps[1] = sw1;
+    // slots 0/1: the first dense SVD of a stage, slots 2/3: the next one (sweeps of pass 1 / pass 2)
+    const int slot = diag->eig_sweeps[0] ? 2 : 0;
+    diag->eig_sweeps[slot] = sw0;
+    diag->eig_sweeps[slot + 1] = sw1;
   }
 }
 
@@ -404,7 +430,7 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   } else {
     // not numerically PD (B rank deficient): orthonormalise through the eigendecomposition
     Scratch<double> w(k, s), W(k * k, s);
-    sym_eig(h, k, Gm, k, w, W, k, 60);
+    sym_eig(h, k, Gm, k, w, W, k, 60, 1e-15, true);
     k_eig_orth<<<grid_for(k * k, 256, h->num_sms * 16), 256, 0, s>>>(k, w, W, 1e-26, Linv);
     FPI_LAUNCH_CHECK();
     if (diag) {

@@ -355,12 +355,14 @@ def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = Non
                           "(block stage produced less derivable rank)")
         f_rows, eng_r = row_update_device(f11, part.a21, s, low_rank_threshold=cfg.low_rank_threshold,
                                           seed=cfg.seed + 1)
+        diag_r = _lib.svd_diag() if stats is not None else None
     timings.append(StageTime("row_update", tm.seconds, f_rows.rank))
 
     with _Timer() as tm:
         r = min(math.ceil(cfg.alpha * n), f_rows.rank + n2, m)
         f_full, eng_c = column_update_device(f_rows, part.T, part.Tt, r, low_rank_threshold=cfg.low_rank_threshold,
                                              seed=cfg.seed + 2)
+        diag_c = _lib.svd_diag() if stats is not None else None
     timings.append(StageTime("column_update", tm.seconds, f_full.rank))
 
     with _Timer() as tm:
@@ -370,7 +372,8 @@ def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = Non
     if stats is not None:
         stats.update(engines=(eng_r, eng_c), s=s, r=r, rank11=f11.rank, m1=ordering.n_spoke_rows, n1=n1, m2=m2,
                      n2=n2, T=ordering.n_iterations, nnz_a12=part.info.nnz_a12, nnz_a22=part.info.nnz_a22,
-                     nnz_a21=part.info.nnz_a21, nnz_a11=part.info.nnz_a11, f11=f11, f_rows=f_rows, part=part)
+                     nnz_a21=part.info.nnz_a21, nnz_a11=part.info.nnz_a11, f11=f11, f_rows=f_rows, part=part,
+                     svd_diag_row=diag_r, svd_diag_col=diag_c)
     return FastpiResult(pv, f_full, ordering, timings)
 
 

@@ -35,14 +35,24 @@ def test_spmm():
     from paper_2011_04235_b200 import _lib
     from paper_2011_04235_b200._device import DeviceCSR, d2h
     rng = np.random.default_rng(3)
-    A = sp.random(500, 300, density=0.02, random_state=rng, format="csr")
-    for k in (1, 7, 128, 300):
+    A = sp.random(500, 300, density=0.02, random_state=rng, format="csr").tolil()
+    A[3, :] = rng.random(300) + 0.1        # long rows -> segmented path
+    A[77, :290] = rng.random(290) + 0.1
+    A = sp.csr_matrix(A)
+    AT = sp.csr_matrix(A.T)                 # 300 x 500 with long rows too
+    for k in (1, 7, 128, 300, 1000):
         X = rng.standard_normal((300, k))
         dev = DeviceCSR.from_host(A)
         Y = _t(np.zeros((500, k)))
         _lib.call("fpi_spmm", 500, 300, k, _lib.ptr(dev.indptr), _lib.ptr(dev.indices), _lib.ptr(dev.values), 1.0,
                   _lib.ptr(_t(X)), k, 0.0, _lib.ptr(Y), k)
         assert np.abs(d2h(Y) - A @ X).max() < 1e-12
+        X2 = rng.standard_normal((500, k))
+        dT = DeviceCSR.from_host(AT)
+        Y2 = _t(np.ones((300, k)))
+        _lib.call("fpi_spmm", 300, 500, k, _lib.ptr(dT.indptr), _lib.ptr(dT.indices), _lib.ptr(dT.values), 2.0,
+                  _lib.ptr(_t(X2)), k, -1.0, _lib.ptr(Y2), k)
+        assert np.abs(d2h(Y2) - (2.0 * (AT @ X2) - 1.0)).max() < 1e-11
 
 
 def test_cholesky():
