@@ -69,62 +69,114 @@ __device__ __forceinline__ void step_pair(int mode, int t, int k, int& p, int& q
   }
 }
 
-// S (JS x JS, stride LDS_), R accumulated rotation; returns this thread's max off-diagonal measure
-__device__ double subsolve(double* S, double* R, double* cs_c, double* cs_s, int* pp, int* pq, bool round0,
-                           double tol, double ascale, bool absolute) {
+// Per-step pairing tables (steps 0..14 within-block, 15..30 cross).
+struct StepTables {
+  signed char P[31][16], Q[31][16];
+  signed char pair_of[31][32];  // pair index of each local index
+  signed char is_p[31][32];     // 1 if the index is the pair's p
+};
+
+__device__ void build_tables(StepTables& tb) {
+  for (int e = threadIdx.x; e < 31 * 16; e += blockDim.x) {
+    const int st = e / 16, k = e % 16;
+    int p, q;
+    step_pair(st < 15 ? 0 : 1, st < 15 ? st : st - 15, k, p, q);
+    tb.P[st][k] = (signed char)p;
+    tb.Q[st][k] = (signed char)q;
+    tb.pair_of[st][p] = (signed char)k;
+    tb.pair_of[st][q] = (signed char)k;
+    tb.is_p[st][p] = 1;
+    tb.is_p[st][q] = 0;
+  }
+}
+
+// Rotation of one pair from (app, aqq, apq): FP32 angle, exactly orthogonal FP64 (c, s).
+__device__ __forceinline__ void rotation(double app, double aqq, double apq, double tol, double ascale, bool absolute,
+                                         double& c, double& sn) {
+  const double den2 = absolute ? ascale * ascale : fabs(app) * fabs(aqq);
+  const double apq2 = apq * apq;
+  const float zf = (float)(aqq - app) * __frcp_rn((float)(2.0 * apq));
+  const float azf = fabsf(zf);
+  const float tf = azf > 1e18f ? 0.5f / zf : copysignf(__frcp_rn(azf + sqrtf(fmaf(zf, zf, 1.0f))), zf);
+  const double tt = isfinite(tf) ? (double)tf : 0.0;
+  const bool rot = apq != 0.0 && apq2 > tol * tol * den2 && tt != 0.0;
+  c = rot ? rsqrt(fma(tt, tt, 1.0)) : 1.0;
+  sn = rot ? c * tt : 0.0;
+}
+
+struct PairBuf {
+  double c[2][16], s[2][16], app[2][16], aqq[2][16], apq[2][16];
+};
+
+// New diagonal entry of index x after its pair's rotation (2x2 congruence).
+__device__ __forceinline__ double new_diag(bool isp, double c, double sn, double app, double aqq, double apq) {
+  return isp ? c * c * app - 2.0 * c * sn * apq + sn * sn * aqq : sn * sn * app + 2.0 * c * sn * apq + c * c * aqq;
+}
+
+// One round's sub-problem: S (JS x JS, stride LDS_) <- J^T S J, R = J.  One barrier per step:
+// the thread that produces a next-step pair's off-diagonal entry also derives that pair's new
+// diagonals from this step's rotations and computes the next rotation.
+__device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& pb, bool round0, double tol,
+                           double ascale, bool absolute) {
+  const int st0 = round0 ? 0 : 15, st_end = 31;
+  // convergence measure of this sub-problem before rotating
   double om = 0.0;
-  const int nsteps0 = round0 ? 15 : 0;
-  for (int st = 0; st < nsteps0 + 16; ++st) {
-    const int mode = st < nsteps0 ? 0 : 1, t = st < nsteps0 ? st : st - nsteps0;
-    if (threadIdx.x < 16) {
-      const int k = threadIdx.x;
-      int p, q;
-      step_pair(mode, t, k, p, q);
-      const double app = S[p * LDS_ + p], aqq = S[q * LDS_ + q], apq = S[p * LDS_ + q];
-      // threshold test and the rotation are independent chains (the rotation is discarded when not needed)
-      const double den2 = absolute ? ascale * ascale : fabs(app) * fabs(aqq);
-      const double apq2 = apq * apq;
-      const double ratio = den2 > 0.0 ? sqrt(apq2 / den2) : (apq != 0.0 ? 1.0 : 0.0);
-      om = fmax(om, ratio);
-      // Rutishauser angle t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (aqq - app) / (2 apq),
-      // evaluated in FP32 (short MUFU chain): any t gives an exactly orthogonal FP64 rotation
-      // c = 1 / sqrt(1 + t^2), s = c t; an inexact angle only leaves a tiny off-diagonal that the
-      // 2x2 update below computes (it is not forced to zero) and the next sweep removes.
-      const float zf = (float)((aqq - app) / 1.0) * __frcp_rn((float)(2.0 * apq));
-      const float azf = fabsf(zf);
-      const float tf = azf > 1e18f ? 0.5f / zf : copysignf(__frcp_rn(azf + sqrtf(fmaf(zf, zf, 1.0f))), zf);
-      const double tt = isfinite(tf) ? (double)tf : 0.0;
-      const bool rot = apq != 0.0 && apq2 > tol * tol * den2 && tt != 0.0;
-      const double c = rot ? rsqrt(fma(tt, tt, 1.0)) : 1.0;
-      const double sn = rot ? c * tt : 0.0;
-      cs_c[k] = c;
-      cs_s[k] = sn;
-      pp[k] = p;
-      pq[k] = q;
+  for (int e = threadIdx.x; e < JS * JS; e += JT) {
+    const int x = e >> 5, y = e & 31;
+    if (x == y) continue;
+    const double sxy = S[x * LDS_ + y];
+    const double den2 = absolute ? ascale * ascale : fabs(S[x * LDS_ + x]) * fabs(S[y * LDS_ + y]);
+    if (sxy != 0.0) om = fmax(om, den2 > 0.0 ? sqrt(sxy * sxy / den2) : 1.0);
+  }
+  // prologue: rotations of the first step
+  if (threadIdx.x < 16) {
+    const int k = threadIdx.x, p = tb.P[st0][k], q = tb.Q[st0][k];
+    const double app = S[p * LDS_ + p], aqq = S[q * LDS_ + q], apq = S[p * LDS_ + q];
+    double c, sn;
+    rotation(app, aqq, apq, tol, ascale, absolute, c, sn);
+    const int b = st0 & 1;
+    pb.c[b][k] = c; pb.s[b][k] = sn; pb.app[b][k] = app; pb.aqq[b][k] = aqq; pb.apq[b][k] = apq;
+  }
+  __syncthreads();
+  const int k = threadIdx.x >> 4, l = threadIdx.x & 15;
+  for (int st = st0; st < st_end; ++st) {
+    const int b = st & 1, nbuf = b ^ 1;
+    const int pk = tb.P[st][k], qk = tb.Q[st][k], pl = tb.P[st][l], ql = tb.Q[st][l];
+    const double ck = pb.c[b][k], sk = pb.s[b][k], cl = pb.c[b][l], sl = pb.s[b][l];
+    // 2x2 block (rows pk,qk x cols pl,ql)
+    const double a = S[pk * LDS_ + pl], bb = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
+    const double ra = ck * a - sk * c2, rb = ck * bb - sk * d;
+    const double rc = sk * a + ck * c2, rd = sk * bb + ck * d;
+    const double out[4] = {ra * cl - rb * sl, ra * sl + rb * cl, rc * cl - rd * sl, rc * sl + rd * cl};
+    if (sk != 0.0 || sl != 0.0) {
+      S[pk * LDS_ + pl] = out[0];
+      S[pk * LDS_ + ql] = out[1];
+      S[qk * LDS_ + pl] = out[2];
+      S[qk * LDS_ + ql] = out[3];
     }
-    __syncthreads();
-    // S <- J^T S J as independent 2x2 blocks (pair k rows x pair l cols); R <- R J
-    {
-      const int k = threadIdx.x >> 4, l = threadIdx.x & 15;
-      const double ck = cs_c[k], sk = cs_s[k], cl = cs_c[l], sl = cs_s[l];
-      const int pk = pp[k], qk = pq[k], pl = pp[l], ql = pq[l];
-      if (sk != 0.0 || sl != 0.0) {
-        const double a = S[pk * LDS_ + pl], b = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
-        const double ra = ck * a - sk * c2, rb = ck * b - sk * d;
-        const double rc = sk * a + ck * c2, rd = sk * b + ck * d;
-        const double na = ra * cl - rb * sl, nb = ra * sl + rb * cl, nc = rc * cl - rd * sl, nd = rc * sl + rd * cl;
-        S[pk * LDS_ + pl] = na;
-        S[pk * LDS_ + ql] = nb;
-        S[qk * LDS_ + pl] = nc;
-        S[qk * LDS_ + ql] = nd;
-      }
-      if (sk != 0.0) {
+    if (sk != 0.0) {  // R is stored transposed (Rt[col][row]): conflict-free column updates
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int row = l + 16 * h2;
-          const double rp = R[row * LDS_ + pk], rq = R[row * LDS_ + qk];
-          R[row * LDS_ + pk] = ck * rp - sk * rq;
-          R[row * LDS_ + qk] = sk * rp + ck * rq;
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int row = l + 16 * h2;
+        const double rp = R[pk * LDS_ + row], rq = R[qk * LDS_ + row];
+        R[pk * LDS_ + row] = ck * rp - sk * rq;
+        R[qk * LDS_ + row] = sk * rp + ck * rq;
+      }
+    }
+    // rotations of the next step whose (p, q) entry this thread just produced
+    if (st + 1 < st_end && k != l) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int x = (e < 2) ? pk : qk, y = (e & 1) ? ql : pl;
+        const int kn = tb.pair_of[st + 1][x];
+        if (tb.is_p[st + 1][x] && tb.Q[st + 1][kn] == y) {
+          const double axy = out[e];
+          const double dx = new_diag(e < 2, ck, sk, pb.app[b][k], pb.aqq[b][k], pb.apq[b][k]);
+          const double dy = new_diag(!(e & 1), cl, sl, pb.app[b][l], pb.aqq[b][l], pb.apq[b][l]);
+          double c, sn;
+          rotation(dx, dy, axy, tol, ascale, absolute, c, sn);
+          pb.c[nbuf][kn] = c; pb.s[nbuf][kn] = sn; pb.app[nbuf][kn] = dx; pb.aqq[nbuf][kn] = dy;
+          pb.apq[nbuf][kn] = axy;
         }
       }
     }
@@ -159,8 +211,10 @@ __global__ void __launch_bounds__(JT, 3)
   __shared__ __align__(16) double Ra[JS * LDS_];
   __shared__ __align__(16) double Rb[JS * LDS_];
   __shared__ __align__(16) double Tm[JS * LDS_];
-  __shared__ double cs_c[16], cs_s[16];
-  __shared__ int pp[16], pq[16];
+  __shared__ StepTables tb;
+  __shared__ PairBuf pbuf;
+  build_tables(tb);
+  __syncthreads();
   const bool absolute = abs_scale != nullptr;
   const double ascale = absolute ? *abs_scale : 0.0;
   const int npairs = nb / 2;
@@ -182,12 +236,12 @@ __global__ void __launch_bounds__(JT, 3)
         }
         __syncthreads();
         const unsigned long long ts0 = prof ? gtimer() : 0;
-        double om = subsolve(Sa, Ra, cs_c, cs_s, pp, pq, round == 0, tol, ascale, absolute);
+        double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
         if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
         double* Jp = Jbuf + (int64_t)pr * JS * JS;
         int rot = 0;
         for (int e = threadIdx.x; e < JS * JS; e += JT) {
-          const double v = Ra[(e >> 5) * LDS_ + (e & 31)];
+          const double v = Ra[(e & 31) * LDS_ + (e >> 5)];  // Rt -> row-major J
           Jp[e] = v;
           rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
         }
@@ -404,5 +458,50 @@ extern "C" int fpi_sym_eig(fpi_handle h, int64_t n, const double* d_A, int64_t l
   FPI_API_BEGIN(h)
   int sw = fpi::sym_eig(h, n, d_A, lda, d_w, d_V, ldv, 60, 1e-14, false);
   if (h_sweeps) *h_sweeps = sw;
+  FPI_API_END(h)
+}
+
+// ---- internal microbenchmark (not part of the public ABI): one CTA runs the
+// sub-solve `iters` times on a fixed SPD 32 x 32 matrix; ns per step.
+namespace fpi {
+namespace {
+__global__ void __launch_bounds__(JT) k_subsolve_bench(int iters, double* out) {
+  __shared__ __align__(16) double S[JS * LDS_];
+  __shared__ __align__(16) double R[JS * LDS_];
+  __shared__ StepTables tb;
+  __shared__ PairBuf pbuf;
+  build_tables(tb);
+  __syncthreads();
+  const unsigned long long t0 = gtimer();
+  double acc = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    for (int e = threadIdx.x; e < JS * JS; e += JT) {
+      const int a = e >> 5, b = e & 31;
+      S[a * LDS_ + b] = (a == b) ? 32.0 + a : 1.0 / (1.0 + a + b);
+      R[a * LDS_ + b] = a == b ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    acc += subsolve(S, R, tb, pbuf, true, 1e-14, 0.0, false);
+  }
+  const unsigned long long t1 = gtimer();
+  if (threadIdx.x == 0) {
+    out[0] = (double)(t1 - t0) / (iters * 31.0);
+    out[1] = acc;
+  }
+}
+}  // namespace
+}  // namespace fpi
+
+extern "C" int fpi_dbg_subsolve_bench(fpi_handle h, int iters, double* h_ns_per_step) {
+  FPI_API_BEGIN(h)
+  double* d;
+  FPI_CUDA(cudaMallocAsync((void**)&d, 16, h->stream));
+  fpi::k_subsolve_bench<<<1, fpi::JT, 0, h->stream>>>(iters, d);
+  FPI_LAUNCH_CHECK();
+  double hv[2];
+  FPI_CUDA(cudaMemcpyAsync(hv, d, 16, cudaMemcpyDeviceToHost, h->stream));
+  FPI_CUDA(cudaStreamSynchronize(h->stream));
+  cudaFreeAsync(d, h->stream);
+  *h_ns_per_step = hv[0];
   FPI_API_END(h)
 }
