@@ -331,6 +331,10 @@ def ours_arm(args):
                      + p.Y.indptr.size * 8 + p.Y.indices.size * 4 + p.Y.data.size * 8)
         e2e_t = []
         d2h_bytes = 0
+        for i in range(args.warmup):  # first calls allocate the pinned host staging buffers
+            res = fp.fastpi(p.A, cfg)
+            Zh = res.pseudoinverse.apply(p.Y)
+            del res, Zh
         for i in range(max(1, args.steps)):
             flush.fill_(float(i))
             torch.cuda.synchronize()
