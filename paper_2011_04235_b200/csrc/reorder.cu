@@ -260,10 +260,133 @@ __global__ void k_assign_tail(const int32_t* __restrict__ act, int64_t cnt, int3
 
 }  // namespace
 
+// device-side kernels used by the one-sync-per-iteration driver
+namespace {
+
+// degrees over the compacted edge list whose length lives on the device
+__global__ void k_degree_dev(const uint64_t* __restrict__ edges, const int* __restrict__ ne_p, int32_t m,
+                             int32_t* __restrict__ deg) {
+  const int64_t ne = *ne_p;
+  FPI_GRID_STRIDE(e, ne) {
+    uint64_t ed = edges[e];
+    warp_agg_inc(deg, (int32_t)(ed >> 32));
+    warp_agg_inc(deg, (int32_t)(ed & 0xffffffffu) + m);
+  }
+}
+
+__global__ void k_hook_dev(const uint64_t* __restrict__ edges, const int* __restrict__ ne_p, int32_t m,
+                           const uint8_t* __restrict__ state, int32_t* parent) {
+  const int64_t ne = *ne_p;
+  FPI_GRID_STRIDE(e, ne) {
+    uint64_t ed = edges[e];
+    int32_t u = (int32_t)(ed >> 32);
+    int32_t v = (int32_t)(ed & 0xffffffffu) + m;
+    if (!state[u] || !state[v]) continue;
+    int32_t ru = find_root(u, parent), rv = find_root(v, parent);
+    while (ru != rv) {
+      if (ru < rv) {
+        int32_t old = atomicCAS(parent + rv, rv, ru);
+        if (old == rv) break;
+        rv = find_root(old, parent);
+      } else {
+        int32_t old = atomicCAS(parent + ru, ru, rv);
+        if (old == ru) break;
+        ru = find_root(old, parent);
+      }
+    }
+  }
+}
+
+__global__ void k_label_stats_dev(const int32_t* __restrict__ act, const int* __restrict__ cnt_p, int32_t m,
+                                  int32_t* parent, int32_t* __restrict__ csize, int32_t* __restrict__ crows) {
+  const int64_t cnt = *cnt_p;
+  FPI_GRID_STRIDE(i, cnt) {
+    int32_t v = act[i];
+    int32_t r = v;
+    while (parent[r] != r) r = parent[r];
+    parent[v] = r;
+    warp_agg_inc(csize, r);
+    if (v < m) warp_agg_inc(crows, r);
+  }
+}
+
+__global__ void k_pick_gcc_dev(const int32_t* __restrict__ act, const int* __restrict__ cnt_p,
+                               const int32_t* __restrict__ parent, const int32_t* __restrict__ csize,
+                               unsigned long long* best, int32_t* nroots) {
+  const int64_t cnt = *cnt_p;
+  unsigned long long local = 0;
+  int32_t nr = 0;
+  FPI_GRID_STRIDE(i, cnt) {
+    int32_t v = act[i];
+    if (parent[v] == v) {
+      unsigned long long key = ((unsigned long long)(uint32_t)csize[v] << 32) | (uint32_t)(0x7fffffff - v);
+      local = key > local ? key : local;
+      ++nr;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    unsigned long long other = __shfl_xor_sync(0xffffffffu, local, o);
+    local = other > local ? other : local;
+    nr += __shfl_xor_sync(0xffffffffu, nr, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(best, local);
+    atomicAdd(nroots, nr);
+  }
+}
+
+// Hubs: the first min(q, #positive) entries of the degree-descending (stable) active list.
+__global__ void k_assign_hubs_dev(const int32_t* __restrict__ sorted_ids, const uint32_t* __restrict__ sorted_deg,
+                                  int64_t q, int64_t hi, int32_t base, int64_t* __restrict__ fwd,
+                                  uint8_t* __restrict__ state, int* __restrict__ nhubs) {
+  FPI_GRID_STRIDE(i, q) {
+    if (sorted_deg[i] == 0) continue;
+    int32_t v = sorted_ids[i];
+    fwd[v - base] = hi - i;
+    state[v] = 0;
+    atomicAdd(nhubs, 1);
+  }
+}
+
+struct IterScalars {
+  unsigned long long best;
+  int32_t nroots, h_t, h_f, acnt, ne, gcc_rows, pad0, pad1;
+};
+
+__global__ void k_collect(IterScalars* out, const unsigned long long* best, const int32_t* nroots, const int* hubs,
+                          const int* acnt, const int* ne, const int32_t* crows) {
+  if (threadIdx.x || blockIdx.x) return;
+  out->best = *best;
+  out->nroots = *nroots;
+  out->h_t = hubs[0];
+  out->h_f = hubs[1];
+  out->acnt = *acnt;
+  out->ne = *ne;
+  const int32_t gcc = (int32_t)(0x7fffffff - (int64_t)(*best & 0xffffffffull));
+  out->gcc_rows = (*best) ? crows[gcc] : 0;
+}
+
+__global__ void k_reset_nodes_dev(const int32_t* __restrict__ act, int64_t cnt, int32_t* __restrict__ deg,
+                                  int32_t* __restrict__ parent, int32_t* __restrict__ csize,
+                                  int32_t* __restrict__ crows) {
+  FPI_GRID_STRIDE(i, cnt) {
+    int32_t v = act[i];
+    deg[v] = 0;
+    parent[v] = v;
+    csize[v] = 0;
+    crows[v] = 0;
+  }
+}
+
+}  // namespace
+
 struct ReorderOut {
   int64_t m1, n1, m2, n2, T;
 };
 
+// One host synchronisation per iteration: every count the host needs (hubs taken, active
+// nodes left, component count, giant component) is gathered into one pinned readback; edge
+// and node kernels take their lengths from device memory.
 static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const int64_t* d_indptr,
                         const int32_t* d_indices, double k, int64_t* d_row_fwd, int64_t* d_col_fwd,
                         ReorderOut& out) {
@@ -283,17 +406,12 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
   Scratch<int32_t> act(V, s), act2(V, s), cand(V, s), cand_sorted(V, s);
   Scratch<uint32_t> keys(V, s), keys_sorted(V, s);
   Scratch<int64_t> rows_c(V, s), cols_c(V, s), size_c(V, s), row_off(V, s), col_off(V, s), node_off(V, s);
-  Scratch<int32_t> d_count(4, s);
+  // device scalars: [0] hubs rows, [1] hubs cols, [2] active count, [3] edge count, [4] nroots, [5] scratch
+  Scratch<int32_t> dsc(8, s);
   Scratch<unsigned long long> d_best(1, s);
-  // pinned staging for the per-iteration scalars
-  struct Stage {
-    int32_t counts[4];
-    unsigned long long best;
-    int32_t nroots;
-    int32_t gcc_rows;
-  };
-  Stage* hs = nullptr;
-  FPI_CUDA(cudaMallocHost((void**)&hs, sizeof(Stage)));
+  Scratch<IterScalars> d_it(1, s);
+  IterScalars* hs = nullptr;
+  FPI_CUDA(cudaMallocHost((void**)&hs, sizeof(IterScalars)));
   struct HostFree {
     void* p;
     ~HostFree() { cudaFreeHost(p); }
@@ -307,19 +425,22 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
   h->n_spans = 0;
   h->gcc_sizes.clear();
 
-  if (nnz) {
-    k_expand_edges<<<G, T, 0, s>>>(m, d_indptr, d_indices, edges);
-    FPI_LAUNCH_CHECK();
-  }
+  if (nnz) k_expand_edges<<<G, T, 0, s>>>(m, d_indptr, d_indices, edges);
   k_set_u8<<<G, T, 0, s>>>(state, V, 1);
   k_fill_iota<<<G, T, 0, s>>>(act, V);
+  int32_t* ne_d = dsc.get() + 3;
+  {
+    int32_t v = (int32_t)nnz;
+    FPI_CUDA(cudaMemcpyAsync(ne_d, &v, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+  }
   FPI_LAUNCH_CHECK();
   note_launch(h, 3);
 
-  int64_t ne = nnz;
   int64_t cnt_t = m, cnt_f = n;
   int64_t lo_t = 0, lo_f = 0, hi_t = m - 1, hi_f = n - 1;
   int64_t iters = 0;
+  bool any_edges = nnz > 0;
   const int deg_bits = bits_for((uint64_t)(m > n ? m : n));
   const int rank_bits = bits_for((uint64_t)V);
 
@@ -330,74 +451,56 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
     const int64_t cnt = cnt_t + cnt_f;
 
     // 1. degrees over the compacted edge list
-    k_reset_nodes<<<grid_for(cnt, T, G), T, 0, s>>>(act, cnt, deg, parent, csize, crows);
-    if (ne) k_degree<<<grid_for(ne, T, G), T, 0, s>>>(edges, ne, (int32_t)m, deg);
-    FPI_LAUNCH_CHECK();
-    note_launch(h, 2);
-
-    // 2. hub candidates (ascending ids, positive degree), per side
-    select_if(tmp, act.get(), cand.get(), d_count.get() + 0, cnt_t, PositiveDeg{deg}, s);
-    select_if(tmp, act.get() + cnt_t, cand.get() + cnt_t, d_count.get() + 1, cnt_f, PositiveDeg{deg}, s);
-    FPI_CUDA(cudaMemcpyAsync(hs->counts, d_count.get(), 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaStreamSynchronize(s));
-    note_launch(h, 2);
-    const int64_t c_t = hs->counts[0], c_f = hs->counts[1];
-    const int64_t h_t = q_t > 0 ? (q_t < c_t ? q_t : c_t) : 0;
-    const int64_t h_f = q_f > 0 ? (q_f < c_f ? q_f : c_f) : 0;
+    k_reset_nodes_dev<<<grid_for(cnt, T, G), T, 0, s>>>(act, cnt, deg, parent, csize, crows);
+    FPI_CUDA(cudaMemsetAsync(dsc.get(), 0, sizeof(int32_t) * 2, s));
+    if (any_edges) k_degree_dev<<<G, T, 0, s>>>(edges, ne_d, (int32_t)m, deg);
+    // 2. hubs: stable degree-descending sort of each side's (ascending) active list
     for (int side = 0; side < 2; ++side) {
-      const int64_t c = side ? c_f : c_t;
-      const int64_t hcount = side ? h_f : h_t;
-      if (hcount == 0) continue;
-      int32_t* cnd = cand.get() + (side ? cnt_t : 0);
-      int32_t* cs = cand_sorted.get() + (side ? cnt_t : 0);
+      const int64_t c = side ? cnt_f : cnt_t, q = side ? q_f : q_t;
+      if (c == 0 || q <= 0) continue;
+      int32_t* ids = act.get() + (side ? cnt_t : 0);
       uint32_t* kk = keys.get() + (side ? cnt_t : 0);
       uint32_t* ks = keys_sorted.get() + (side ? cnt_t : 0);
-      k_gather_keys<<<grid_for(c, T, G), T, 0, s>>>(cnd, c, deg, kk);
-      sort_pairs(tmp, kk, ks, cnd, cs, c, /*descending=*/true, 0, deg_bits, s);
-      if (side == 0)
-        k_assign_hubs<<<grid_for(hcount, T, G), T, 0, s>>>(cs, hcount, hi_t, 0, d_row_fwd, state);
-      else
-        k_assign_hubs<<<grid_for(hcount, T, G), T, 0, s>>>(cs, hcount, hi_f, (int32_t)m, d_col_fwd, state);
-      FPI_LAUNCH_CHECK();
-      note_launch(h, 3);
+      int32_t* cs = cand_sorted.get() + (side ? cnt_t : 0);
+      k_gather_keys<<<grid_for(c, T, G), T, 0, s>>>(ids, c, deg, kk);
+      sort_pairs(tmp, kk, ks, ids, cs, c, /*descending=*/true, 0, deg_bits, s);
+      k_assign_hubs_dev<<<grid_for(q < c ? q : c, T, G), T, 0, s>>>(cs, ks, q < c ? q : c, side ? hi_f : hi_t,
+                                                                    side ? (int32_t)m : 0,
+                                                                    side ? d_col_fwd : d_row_fwd, state,
+                                                                    dsc.get() + side);
     }
+    // active list without the hubs (count on device)
+    select_if(tmp, act.get(), act2.get(), dsc.get() + 2, cnt, IsActive{state}, s);
+    std::swap(act, act2);
+    // 3. connected components of the residual
+    if (any_edges) k_hook_dev<<<G, T, 0, s>>>(edges, ne_d, (int32_t)m, state, parent);
+    k_label_stats_dev<<<grid_for(cnt, T, G), T, 0, s>>>(act, dsc.get() + 2, (int32_t)m, parent, csize, crows);
+    FPI_CUDA(cudaMemsetAsync(d_best.get(), 0, sizeof(unsigned long long), s));
+    FPI_CUDA(cudaMemsetAsync(dsc.get() + 4, 0, sizeof(int32_t), s));
+    k_pick_gcc_dev<<<grid_for(cnt, T, G), T, 0, s>>>(act, dsc.get() + 2, parent, csize, d_best, dsc.get() + 4);
+    k_collect<<<1, 1, 0, s>>>(d_it, d_best, dsc.get() + 4, dsc.get(), dsc.get() + 2, ne_d, crows);
+    FPI_CUDA(cudaMemcpyAsync(hs, d_it.get(), sizeof(IterScalars), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));  // the one host synchronisation of the iteration
+    FPI_LAUNCH_CHECK();
+    note_launch(h, 12);
+    const int64_t h_t = hs->h_t, h_f = hs->h_f;
     hi_t -= h_t;
     hi_f -= h_f;
     cnt_t -= h_t;
     cnt_f -= h_f;
-    // drop the hubs from the active list (keeps ascending order)
-    if (h_t + h_f) {
-      select_if(tmp, act.get(), act2.get(), d_count.get() + 2, cnt + 0, IsActive{state}, s);
-      std::swap(act, act2);
-      note_launch(h, 1);
-    }
     const int64_t acnt = cnt_t + cnt_f;
     if (acnt == 0) {  // reorder.py:224-226
       h->gcc_sizes.push_back(0);
       break;
     }
-
-    // 3. connected components of the residual
-    if (ne) k_hook<<<grid_for(ne, T, G), T, 0, s>>>(edges, ne, (int32_t)m, state, parent);
-    k_label_stats<<<grid_for(acnt, T, G), T, 0, s>>>(act, acnt, (int32_t)m, parent, csize, crows);
-    FPI_CUDA(cudaMemsetAsync(d_best.get(), 0, sizeof(unsigned long long), s));
-    FPI_CUDA(cudaMemsetAsync(d_count.get() + 3, 0, sizeof(int32_t), s));
-    k_pick_gcc<<<grid_for(acnt, T, G), T, 0, s>>>(act, acnt, parent, csize, d_best, d_count.get() + 3);
-    FPI_LAUNCH_CHECK();
-    note_launch(h, 3);
-    FPI_CUDA(cudaMemcpyAsync(&hs->best, d_best.get(), sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaMemcpyAsync(&hs->nroots, d_count.get() + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaStreamSynchronize(s));
     const int32_t gcc = (int32_t)(0x7fffffff - (int64_t)(hs->best & 0xffffffffull));
     const int64_t gcc_size = (int64_t)(hs->best >> 32);
-    FPI_CUDA(cudaMemcpyAsync(&hs->gcc_rows, crows.get() + gcc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaStreamSynchronize(s));
     const int64_t gcc_t = hs->gcc_rows, gcc_f = gcc_size - gcc_t;
     const int64_t nsc = (int64_t)hs->nroots - 1;
 
     // 4. spoke components -> blocks, members ascending within each side
     if (nsc > 0) {
-      select_if(tmp, act.get(), cand.get(), d_count.get() + 0, acnt, IsSpokeRoot{parent, gcc}, s);
+      select_if(tmp, act.get(), cand.get(), dsc.get() + 5, acnt, IsSpokeRoot{parent, gcc}, s);
       k_gather_keys<<<grid_for(nsc, T, G), T, 0, s>>>(cand, nsc, csize, keys);
       sort_pairs(tmp, keys.get(), keys_sorted.get(), cand.get(), cand_sorted.get(), nsc, true, 0, rank_bits, s);
       k_comp_table<<<grid_for(nsc, T, G), T, 0, s>>>(cand_sorted, nsc, csize, crows, rank_of_root, rows_c, cols_c,
@@ -408,7 +511,7 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
       k_write_spans<<<grid_for(nsc, T, G), T, 0, s>>>(nsc, row_off, rows_c, col_off, cols_c, lo_t, lo_f,
                                                       h->d_spans + 4 * h->n_spans);
       const int64_t nsp = acnt - gcc_size;
-      select_if(tmp, act.get(), cand.get(), d_count.get() + 1, acnt, IsSpokeNode{parent, gcc}, s);
+      select_if(tmp, act.get(), cand.get(), dsc.get() + 5, acnt, IsSpokeNode{parent, gcc}, s);
       k_node_rank_keys<<<grid_for(nsp, T, G), T, 0, s>>>(cand, nsp, parent, rank_of_root, keys);
       sort_pairs(tmp, keys.get(), keys_sorted.get(), cand.get(), cand_sorted.get(), nsp, false, 0, rank_bits, s);
       k_emit_spokes<<<grid_for(nsp, T, G), T, 0, s>>>(cand_sorted, keys_sorted, nsp, (int32_t)m, node_off, row_off,
@@ -420,20 +523,17 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
     lo_t += cnt_t - gcc_t;
     lo_f += cnt_f - gcc_f;
 
-    // 5. giant component becomes the active set
-    select_if(tmp, act.get(), act2.get(), d_count.get() + 2, acnt, InComp{parent, gcc}, s);
+    // 5. giant component becomes the active set (count = gcc_size, also kept on device)
+    select_if(tmp, act.get(), act2.get(), dsc.get() + 2, acnt, InComp{parent, gcc}, s);
     std::swap(act, act2);
     note_launch(h, 1);
     h->gcc_sizes.push_back(gcc_size);
     cnt_t = gcc_t;
     cnt_f = gcc_f;
     if (gcc_t < q_t || gcc_f < q_f) break;  // reorder.py:268-269
-    // compact edges to the new active set
-    if (ne) {
-      select_if(tmp, edges.get(), edges2.get(), d_count.get() + 3, ne, EdgeLive{state, (int32_t)m}, s);
-      FPI_CUDA(cudaMemcpyAsync(hs->counts + 3, d_count.get() + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      FPI_CUDA(cudaStreamSynchronize(s));
-      ne = hs->counts[3];
+    // compact edges to the new active set (length stays on the device)
+    if (any_edges) {
+      select_if(tmp, edges.get(), edges2.get(), ne_d, hs->ne, EdgeLive{state, (int32_t)m}, s);
       std::swap(edges, edges2);
       note_launch(h, 1);
     }
