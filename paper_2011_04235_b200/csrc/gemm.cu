@@ -92,7 +92,9 @@ template <bool TA, bool TB>
 __global__ void __launch_bounds__(NT, 1)
     k_gemm(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
            const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
-           int64_t k_per_split, double* __restrict__ partial) {
+           int64_t k_per_split, double* __restrict__ partial, int sym) {
+  // sym: C is symmetric (A == B, op(A) = op(B)^T): only tiles on / below the diagonal are computed
+  if (sym && blockIdx.x > blockIdx.y) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * A_STAGE;
@@ -181,6 +183,10 @@ __global__ void __launch_bounds__(NT, 1)
           double v = alpha * acc[i][j][q];
           double* dst = C + r * ldc + c + q;
           *dst = beta == 0.0 ? v : v + beta * *dst;
+          if (sym && blockIdx.x < blockIdx.y) {  // mirror strictly-lower tiles
+            double* mir = C + (c + q) * ldc + r;
+            *mir = beta == 0.0 ? v : v + beta * *mir;
+          }
         }
       }
     }
@@ -188,11 +194,13 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 __global__ void k_reduce_split(int64_t M, int64_t N, int splits, const double* __restrict__ P, double alpha,
-                               double beta, double* __restrict__ C, int64_t ldc) {
+                               double beta, double* __restrict__ C, int64_t ldc, int sym) {
   FPI_GRID_STRIDE(e, M * N) {
     int64_t r = e / N, c = e - r * N;
+    // upper tiles of a symmetric product were not computed: read the mirrored partials
+    const int64_t src = (sym && (c / BN) > (r / BM)) ? c * N + r : e;
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += P[(int64_t)z * M * N + e];
+    for (int z = 0; z < splits; ++z) s += P[(int64_t)z * M * N + src];
     double* dst = C + r * ldc + c;
     double v = alpha * s;
     *dst = beta == 0.0 ? v : v + beta * *dst;
@@ -209,7 +217,7 @@ __global__ void k_scale(int64_t M, int64_t N, double beta, double* __restrict__ 
 
 template <bool TA, bool TB>
 void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
-            const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+            const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int sym) {
   static bool attr_set = false;
   if (!attr_set) {
     FPI_CUDA(cudaFuncSetAttribute(k_gemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
@@ -217,7 +225,7 @@ void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const
   }
   cudaStream_t s = h->stream;
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
-  const int64_t tiles = tm * tn;
+  const int64_t tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
   int splits = 1;
   const int64_t want = 2LL * h->num_sms;
   if (tiles < want && K >= 4 * BK * 8) {
@@ -230,7 +238,7 @@ void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const
   FPI_REQUIRE(tm < 65536 && tn < (1LL << 31), FPI_ECAPACITY, "gemm grid too large");
   if (splits == 1) {
     dim3 grid((unsigned)tn, (unsigned)tm, 1);
-    k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, K, nullptr);
+    k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, K, nullptr, sym);
     FPI_LAUNCH_CHECK();
     note_launch(h);
     return;
@@ -240,9 +248,9 @@ void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const
   splits = (int)((K + kps - 1) / kps);
   Scratch<double> part((size_t)splits * M * N, s);
   dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)splits);
-  k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps, part);
+  k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps, part, sym);
   k_reduce_split<<<grid_for(M * N, 256, (int64_t)h->num_sms * 16), 256, 0, s>>>(M, N, splits, part, alpha, beta, C,
-                                                                                 ldc);
+                                                                                 ldc, sym);
   FPI_LAUNCH_CHECK();
   note_launch(h, 2);
 }
@@ -250,19 +258,20 @@ void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const
 }  // namespace
 
 void gemm(fpi_context* h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
-          int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+          int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, bool sym) {
   if (M <= 0 || N <= 0) return;
+  const int sy = (sym && M == N && A == B && ta != tb) ? 1 : 0;
   if (K <= 0) {
     k_scale<<<grid_for(M * N, 256, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(M, N, beta, C, ldc);
     FPI_LAUNCH_CHECK();
     return;
   }
-  KTimer kt(h, "gemm_f64_dmma", 2.0 * (double)M * (double)N * (double)K,
+  KTimer kt(h, "gemm_f64_dmma", (sy ? 1.0 : 2.0) * (double)M * (double)N * (double)K,
             8.0 * ((double)M * K + (double)K * N + (beta == 0.0 ? 1.0 : 2.0) * (double)M * N));
-  if (!ta && !tb) launch<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else if (!ta && tb) launch<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else if (ta && !tb) launch<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-  else launch<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (!ta && !tb) launch<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+  else if (!ta && tb) launch<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sy);
+  else if (ta && !tb) launch<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sy);
+  else launch<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
 }
 
 }  // namespace fpi

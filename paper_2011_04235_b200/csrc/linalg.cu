@@ -204,7 +204,7 @@ void cholesky_lower(fpi_context* h, int64_t n, double* A, int64_t lda, int* h_in
       int64_t rows = n - j - jb;
       k_trsm_panel<<<grid_for(rows, 128, h->num_sms * 4), 128, 0, s>>>(A, lda, j, jb, n);
       gemm(h, false, true, rows, rows, jb, -1.0, A + (j + jb) * lda + j, lda, A + (j + jb) * lda + j, lda, 1.0,
-           A + (j + jb) * lda + j + jb, lda);
+           A + (j + jb) * lda + j + jb, lda, /*sym=*/true);
     }
     note_launch(h, 2);
   }

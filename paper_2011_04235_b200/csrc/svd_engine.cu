@@ -112,6 +112,45 @@ __global__ void k_csr_to_dense(int64_t rows, const int64_t* __restrict__ ptr, co
     for (int64_t p = ptr[r] + lane; p < ptr[r + 1]; p += 32) D[r * ld + col0 + idx[p]] = val[p];
 }
 
+// 1 if row i of D (m x s) has a nonzero entry
+__global__ void k_row_nonzero(int64_t m, int64_t sd, const double* __restrict__ D, int64_t ldd,
+                              int32_t* __restrict__ flag) {
+  int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < m; r += nw) {
+    bool nz = false;
+    for (int64_t c = lane; c < sd; c += 32) nz |= D[r * ldd + c] != 0.0;
+    nz = __any_sync(0xffffffffu, nz);
+    if (lane == 0) flag[r] = nz ? 1 : 0;
+  }
+}
+
+struct FlagSet {
+  const int32_t* f;
+  __device__ bool operator()(int32_t i) const { return f[i] != 0; }
+};
+
+__global__ void k_gather_rows32(int64_t nr, int64_t k, const double* __restrict__ src, int64_t lds,
+                                const int32_t* __restrict__ rows, double* __restrict__ dst, int64_t ldd) {
+  FPI_GRID_STRIDE(e, nr * k) {
+    const int64_t i = e / k, c = e - i * k;
+    dst[i * ldd + c] = src[(int64_t)rows[i] * lds + c];
+  }
+}
+
+__global__ void k_scatter_add_rows32(int64_t nr, int64_t k, const double* __restrict__ src, int64_t lds,
+                                     const int32_t* __restrict__ rows, double* __restrict__ dst, int64_t ldd) {
+  FPI_GRID_STRIDE(e, nr * k) {
+    const int64_t i = e / k, c = e - i * k;
+    dst[(int64_t)rows[i] * ldd + c] += src[i * lds + c];
+  }
+}
+
+__global__ void k_iota_i32(int32_t* a, int64_t n) {
+  FPI_GRID_STRIDE(i, n) a[i] = (int32_t)i;
+}
+
 __global__ void k_fill(int64_t n, double* a, double v) {
   FPI_GRID_STRIDE(i, n) a[i] = v;
 }
@@ -217,7 +256,7 @@ static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M
   cudaStream_t s = h->stream;
   const unsigned G = (unsigned)(h->num_sms * 16);
   Scratch<double> Gm(q * q, s), W0(q * q, s), w0(q, s);
-  gemm(h, true, false, q, q, p, 1.0, M, ldm, M, ldm, 0.0, Gm, q);
+  gemm(h, true, false, q, q, p, 1.0, M, ldm, M, ldm, 0.0, Gm, q, /*sym=*/true);
   // Gram entries are accurate to eps * ||G|| in absolute terms: converge to that (absolute criterion)
   int sw0 = sym_eig(h, q, Gm, q, w0, W0, q, 60, 1e-15, true);
   int sw1 = 0;
@@ -240,7 +279,7 @@ static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M
     w1.alloc(q, s);
     V.alloc(q * q, s);
     gemm(h, false, false, p, q, q, 1.0, M, ldm, W0, q, 0.0, M1, q);
-    gemm(h, true, false, q, q, p, 1.0, M1, q, M1, q, 0.0, Gm, q);
+    gemm(h, true, false, q, q, p, 1.0, M1, q, M1, q, 0.0, Gm, q, /*sym=*/true);
     sw1 = sym_eig(h, q, Gm, q, w1, W1, q, 60, 1e-14, false);
     gemm(h, false, false, q, q, q, 1.0, W0, q, W1, q, 0.0, V, q);
     Mr = M1.get();
@@ -354,9 +393,30 @@ struct InnerOp {
   const int64_t* st_ptr = nullptr;
   const int32_t* st_idx = nullptr;
   const double* st_val = nullptr;  // (q - sd) x p
+  // optional: only nzr rows of D are nonzero (rows listed in nz_rows, gathered into Dnz)
+  int64_t nzr = -1;
+  const int32_t* nz_rows = nullptr;
+  const double* Dnz = nullptr;
 
   // B (p x k) = inner * X (q x k)
   void apply(fpi_context* h, const double* X, int64_t k, double* B) const {
+    if (D && sd > 0 && nzr >= 0) {
+      cudaStream_t s = h->stream;
+      const unsigned G = (unsigned)(h->num_sms * 16);
+      if (q > sd)
+        spmm(h, p, q - sd, k, s_ptr, s_idx, s_val, nullptr, 1.0, X + sd * k, k, 0.0, B, k);
+      else
+        FPI_CUDA(cudaMemsetAsync(B, 0, sizeof(double) * p * k, s));
+      if (nzr > 0) {
+        Scratch<double> Xs(sd * k, s), tmp(nzr * k, s);
+        FPI_CUDA(cudaMemcpyAsync(Xs.get(), X, sizeof(double) * sd * k, cudaMemcpyDeviceToDevice, s));
+        if (dscale) scale_rows(h, sd, k, Xs, k, dscale);
+        gemm(h, false, false, nzr, k, sd, 1.0, Dnz, sd, Xs, k, 0.0, tmp, k);
+        k_scatter_add_rows32<<<grid_for(nzr * k, 256, G), 256, 0, s>>>(nzr, k, tmp, k, nz_rows, B, k);
+        FPI_LAUNCH_CHECK();
+      }
+      return;
+    }
     if (D && sd > 0) {
       Scratch<double> Xs(sd * k, h->stream);
       FPI_CUDA(cudaMemcpyAsync(Xs.get(), X, sizeof(double) * sd * k, cudaMemcpyDeviceToDevice, h->stream));
@@ -369,6 +429,21 @@ struct InnerOp {
   }
   // Z (q x k) = inner^T * B (p x k)
   void applyT(fpi_context* h, const double* B, int64_t k, double* Z) const {
+    if (D && sd > 0 && nzr >= 0) {
+      cudaStream_t s = h->stream;
+      const unsigned G = (unsigned)(h->num_sms * 16);
+      if (nzr > 0) {
+        Scratch<double> Bg(nzr * k, s);
+        k_gather_rows32<<<grid_for(nzr * k, 256, G), 256, 0, s>>>(nzr, k, B, k, nz_rows, Bg, k);
+        FPI_LAUNCH_CHECK();
+        gemm(h, true, false, sd, k, nzr, 1.0, Dnz, sd, Bg, k, 0.0, Z, k);
+        if (dscale) scale_rows(h, sd, k, Z, k, dscale);
+      } else {
+        FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * sd * k, s));
+      }
+      if (q > sd) spmm(h, q - sd, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z + sd * k, k);
+      return;
+    }
     if (D && sd > 0) {
       gemm(h, true, false, sd, k, p, 1.0, D, ldd, B, k, 0.0, Z, k);
       if (dscale) scale_rows(h, sd, k, Z, k, dscale);
@@ -413,7 +488,7 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   op.apply(h, X, k, B);                 // svd.py:133
   X.release();
   // CholeskyQR: B^T B = L L^T, Q = B L^-T   (svd.py:134)
-  gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k);
+  gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k, /*sym=*/true);
   Scratch<double> Gc(k * k, s);
   FPI_CUDA(cudaMemcpyAsync(Gc.get(), Gm.get(), sizeof(double) * k * k, cudaMemcpyDeviceToDevice, s));
   int info = 0;
@@ -552,6 +627,32 @@ void column_update(fpi_context* h, int64_t m, int64_t s_prev, int64_t n1, const 
   op.st_ptr = tt_ptr;
   op.st_idx = tt_idx;
   op.st_val = tt_val;
+  // rows of U_prev that are identically zero (spoke rows of column-free blocks): skip them in the
+  // dense products of the randomized engine when they are the majority
+  Scratch<int32_t> flag, ids, nzl, cntd;
+  Scratch<double> Dnz;
+  if (s_prev > 0 && (double)r < thr * (double)q) {
+    const unsigned G = (unsigned)(h->num_sms * 16);
+    flag.alloc(m, s);
+    ids.alloc(m, s);
+    nzl.alloc(m, s);
+    cntd.alloc(1, s);
+    k_row_nonzero<<<grid_for(m * 32, 256, G), 256, 0, s>>>(m, s_prev, U_prev, s_prev, flag);
+    k_iota_i32<<<grid_for(m, 256, G), 256, 0, s>>>(ids, m);
+    CubTemp tmp(s);
+    select_if(tmp, ids.get(), nzl.get(), cntd.get(), m, FlagSet{flag.get()}, s);
+    const int64_t nzr = host_read(cntd.get(), s);
+    if (nzr < (m * 6) / 10) {
+      Dnz.alloc(nzr * s_prev + 1, s);
+      if (nzr)
+        k_gather_rows32<<<grid_for(nzr * s_prev, 256, G), 256, 0, s>>>(nzr, s_prev, U_prev, s_prev, nzl, Dnz,
+                                                                       s_prev);
+      FPI_LAUNCH_CHECK();
+      op.nzr = nzr;
+      op.nz_rows = nzl.get();
+      op.Dnz = Dnz.get();
+    }
+  }
   Scratch<double> Vti(r * q, s);
   inner_svd(h, op, r, q, thr, seed, U, sigma, Vti, engine, &h->diag);
   // lift: Vt = [Vti[:, :s] Vt_prev | Vti[:, s:]]   (pinv.py:205-207)
