@@ -141,18 +141,28 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
   const int k = threadIdx.x >> 4, l = threadIdx.x & 15;
   for (int st = st0; st < st_end; ++st) {
     const int b = st & 1, nbuf = b ^ 1;
-    const int pk = tb.P[st][k], qk = tb.Q[st][k], pl = tb.P[st][l], ql = tb.Q[st][l];
+    const bool cross = st >= 15;
+    const int t = st - 15;
+    int pk, qk, pl, ql;
+    if (cross) {  // closed form: pair k = (k, 16 + (k + t) % 16)
+      pk = k; qk = 16 + ((k + t) & 15); pl = l; ql = 16 + ((l + t) & 15);
+    } else {
+      pk = tb.P[st][k]; qk = tb.Q[st][k]; pl = tb.P[st][l]; ql = tb.Q[st][l];
+    }
     const double ck = pb.c[b][k], sk = pb.s[b][k], cl = pb.c[b][l], sl = pb.s[b][l];
-    // 2x2 block (rows pk,qk x cols pl,ql)
-    const double a = S[pk * LDS_ + pl], bb = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
-    const double ra = ck * a - sk * c2, rb = ck * bb - sk * d;
-    const double rc = sk * a + ck * c2, rd = sk * bb + ck * d;
-    const double out[4] = {ra * cl - rb * sl, ra * sl + rb * cl, rc * cl - rd * sl, rc * sl + rd * cl};
+    double o1 = 0.0;
     if (sk != 0.0 || sl != 0.0) {
-      S[pk * LDS_ + pl] = out[0];
-      S[pk * LDS_ + ql] = out[1];
-      S[qk * LDS_ + pl] = out[2];
-      S[qk * LDS_ + ql] = out[3];
+      const double a = S[pk * LDS_ + pl], bb = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
+      const double ra = ck * a - sk * c2, rb = ck * bb - sk * d;
+      const double rc = sk * a + ck * c2, rd = sk * bb + ck * d;
+      const double o0 = ra * cl - rb * sl, o2 = rc * cl - rd * sl, o3 = rc * sl + rd * cl;
+      o1 = ra * sl + rb * cl;
+      S[pk * LDS_ + pl] = o0;
+      S[pk * LDS_ + ql] = o1;
+      S[qk * LDS_ + pl] = o2;
+      S[qk * LDS_ + ql] = o3;
+    } else if (cross && l == ((k + 1) & 15)) {
+      o1 = S[pk * LDS_ + ql];
     }
     if (sk != 0.0) {  // R is stored transposed (Rt[col][row]): conflict-free column updates
 #pragma unroll
@@ -163,20 +173,34 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
         R[qk * LDS_ + row] = sk * rp + ck * rq;
       }
     }
-    // rotations of the next step whose (p, q) entry this thread just produced
-    if (st + 1 < st_end && k != l) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int x = (e < 2) ? pk : qk, y = (e & 1) ? ql : pl;
-        const int kn = tb.pair_of[st + 1][x];
-        if (tb.is_p[st + 1][x] && tb.Q[st + 1][kn] == y) {
-          const double axy = out[e];
-          const double dx = new_diag(e < 2, ck, sk, pb.app[b][k], pb.aqq[b][k], pb.apq[b][k]);
-          const double dy = new_diag(!(e & 1), cl, sl, pb.app[b][l], pb.aqq[b][l], pb.apq[b][l]);
+    // rotations of the next step, computed by the thread that produced the pair's entry
+    if (st + 1 < st_end) {
+      if (cross) {
+        // next cross pair k is (k, 16 + (k + t + 1) % 16) = (pk, ql) with l = k + 1: entry o1
+        if (l == ((k + 1) & 15)) {
+          const double dx = new_diag(true, ck, sk, pb.app[b][k], pb.aqq[b][k], pb.apq[b][k]);
+          const double dy = new_diag(false, cl, sl, pb.app[b][l], pb.aqq[b][l], pb.apq[b][l]);
           double c, sn;
-          rotation(dx, dy, axy, tol, ascale, absolute, c, sn);
-          pb.c[nbuf][kn] = c; pb.s[nbuf][kn] = sn; pb.app[nbuf][kn] = dx; pb.aqq[nbuf][kn] = dy;
-          pb.apq[nbuf][kn] = axy;
+          rotation(dx, dy, o1, tol, ascale, absolute, c, sn);
+          pb.c[nbuf][k] = c; pb.s[nbuf][k] = sn; pb.app[nbuf][k] = dx; pb.aqq[nbuf][k] = dy;
+          pb.apq[nbuf][k] = o1;
+        }
+      } else if (k != l) {
+        // within-block steps (round 0 only): generic producer lookup
+        const bool any = (sk != 0.0 || sl != 0.0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int x = (e < 2) ? pk : qk, y = (e & 1) ? ql : pl;
+          const int kn = tb.pair_of[st + 1][x];
+          if (tb.is_p[st + 1][x] && tb.Q[st + 1][kn] == y) {
+            const double axy = any ? S[x * LDS_ + y] : S[x * LDS_ + y];
+            const double dx = new_diag(e < 2, ck, sk, pb.app[b][k], pb.aqq[b][k], pb.apq[b][k]);
+            const double dy = new_diag(!(e & 1), cl, sl, pb.app[b][l], pb.aqq[b][l], pb.apq[b][l]);
+            double c, sn;
+            rotation(dx, dy, axy, tol, ascale, absolute, c, sn);
+            pb.c[nbuf][kn] = c; pb.s[nbuf][kn] = sn; pb.app[nbuf][kn] = dx; pb.aqq[nbuf][kn] = dy;
+            pb.apq[nbuf][kn] = axy;
+          }
         }
       }
     }
