@@ -364,8 +364,8 @@ void dense_svd(fpi_context* h, int64_t p, int64_t q, const double* M, int64_t ld
                double* sigma, double* Vt, fpi_svd_diag* diag) {
   FPI_REQUIRE(rank >= 1 && rank <= (p < q ? p : q), FPI_EDOMAIN,
               "target rank " + std::to_string(rank) + " out of range [1, " + std::to_string(p < q ? p : q) + "]");
-  FPI_REQUIRE(p * q <= 100000000LL, FPI_ECAPACITY,
-              "dense SVD of a " + std::to_string(p) + "x" + std::to_string(q) + " matrix exceeds the 100000000-entry guard");
+  // (no capacity guard here: the reference guards only the user-facing dense_svd, svd.py:98-102,
+  //  not the small SVD inside randomized_svd, svd.py:136; fpi_dense_svd applies it)
   cudaStream_t s = h->stream;
   if (p >= q) {
     dense_svd_tall(h, p, q, M, ldm, rank, U, sigma, Vt, diag);
@@ -756,6 +756,9 @@ extern "C" int fpi_dense_svd(fpi_handle h, int64_t p, int64_t q, const double* d
   FPI_API_BEGIN(h)
   h->diag = fpi_svd_diag{};
   h->diag.engine = 2;
+  FPI_REQUIRE(p * q <= 100000000LL, FPI_ECAPACITY,
+              "dense SVD of a " + std::to_string(p) + "x" + std::to_string(q) +
+                  " matrix exceeds the 100000000-entry guard");
   fpi::dense_svd(h, p, q, d_M, ldm, rank, d_U, d_sigma, d_Vt, &h->diag);
   FPI_API_END(h)
 }
