@@ -296,19 +296,30 @@ __global__ void k_iota64(int64_t* a, int64_t n) {
 // scatter one block (rows rs.., cols cs..) into a zeroed row-major h x w buffer
 __global__ void k_scatter_block(int64_t rs, int64_t h, int64_t cs, int64_t w, const int64_t* __restrict__ a_ptr,
                                 const int32_t* __restrict__ a_idx, const double* __restrict__ a_val,
-                                double* __restrict__ D) {
+                                double* __restrict__ D, int transposed) {
   int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t i = warp; i < h; i += nw)
-    for (int64_t p = a_ptr[rs + i] + lane; p < a_ptr[rs + i + 1]; p += 32) D[i * w + (a_idx[p] - cs)] = a_val[p];
+    for (int64_t p = a_ptr[rs + i] + lane; p < a_ptr[rs + i + 1]; p += 32) {
+      const int64_t j = a_idx[p] - cs;
+      if (transposed) D[j * h + i] = a_val[p]; else D[i * w + j] = a_val[p];
+    }
 }
 
-// copy a dense (h x kp) U and (kp x w) Vt into the CSR value arrays
-__global__ void k_store_large(int64_t h, int64_t w, int64_t kp, const double* __restrict__ U, const double* __restrict__ Vt,
-                              double* __restrict__ u_val, double* __restrict__ vt_val) {
-  FPI_GRID_STRIDE(e, h * kp) u_val[e] = U[e];
-  FPI_GRID_STRIDE(e2, kp * w) vt_val[e2] = Vt[e2];
+// copy the oriented factors of one block into the CSR value arrays: U11 part (h x kp), Vt11 part (kp x w).
+// not transposed: Uo (h x kp), Vto (kp x w).  transposed (oriented panel = A^T): Uo (w x kp), Vto (kp x h).
+__global__ void k_store_large(int64_t h, int64_t w, int64_t kp, const double* __restrict__ Uo,
+                              const double* __restrict__ Vto, int transposed, double* __restrict__ u_val,
+                              double* __restrict__ vt_val) {
+  FPI_GRID_STRIDE(e, h * kp) {
+    const int64_t i = e / kp, t = e - i * kp;
+    u_val[e] = transposed ? Vto[t * h + i] : Uo[e];
+  }
+  FPI_GRID_STRIDE(e2, kp * w) {
+    const int64_t t = e2 / w, j = e2 - t * w;
+    vt_val[e2] = transposed ? Uo[j * kp + t] : Vto[e2];
+  }
 }
 
 }  // namespace
@@ -425,22 +436,58 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
     FPI_CUDA(cudaMemcpyAsync(huoff.data(), st.u_off.get(), sizeof(int64_t) * nspans, cudaMemcpyDeviceToHost, s));
     FPI_CUDA(cudaMemcpyAsync(hvoff.data(), st.v_off.get(), sizeof(int64_t) * nspans, cudaMemcpyDeviceToHost, s));
     FPI_CUDA(cudaStreamSynchronize(s));
-    for (int64_t b : lg) {
-      const int64_t rs = hspans[4 * b], hh = hspans[4 * b + 1], cs = hspans[4 * b + 2], ww = hspans[4 * b + 3];
-      const int64_t kp = hkeep[b];
+    // dense, oriented (rows >= cols) copies of every large block, one batched SVD for all of them
+    const int nl = (int)lg.size();
+    std::vector<int64_t> pp(nl), qq(nl), kk(nl), ldm(nl);
+    std::vector<int> tr(nl);
+    int64_t tot = 0;
+    for (int i = 0; i < nl; ++i) {
+      const int64_t b = lg[i], hh = hspans[4 * b + 1], ww = hspans[4 * b + 3];
       FPI_REQUIRE(hh * ww <= 4000000, FPI_ECAPACITY,
                   "diagonal block of " + std::to_string(hh) + "x" + std::to_string(ww) +
                       " entries exceeds the 4000000-entry guard; reordering produced a pathological block");
-      Scratch<double> D(hh * ww, s), U(hh * kp, s), Vt(kp * ww, s);
-      FPI_CUDA(cudaMemsetAsync(D.get(), 0, sizeof(double) * hh * ww, s));
-      k_scatter_block<<<grid_for(hh * 32, T, G), T, 0, s>>>(rs, hh, cs, ww, a_ptr, a_idx, a_val, D);
-      FPI_LAUNCH_CHECK();
-      dense_svd(h, hh, ww, D, ww, kp, U, sigma + hroff[b], Vt, nullptr);
-      k_store_large<<<grid_for(hh * kp + kp * ww, T, G), T, 0, s>>>(hh, ww, kp, U, Vt, u_val + huoff[b],
-                                                                     vt_val + hvoff[b]);
-      FPI_LAUNCH_CHECK();
+      tr[i] = hh < ww;
+      pp[i] = tr[i] ? ww : hh;
+      qq[i] = tr[i] ? hh : ww;
+      kk[i] = hkeep[b];
+      ldm[i] = qq[i];
+      tot += hh * ww;
+    }
+    Scratch<double> Dall(tot, s);
+    FPI_CUDA(cudaMemsetAsync(Dall.get(), 0, sizeof(double) * tot, s));
+    std::vector<const double*> Mp(nl);
+    std::vector<double*> Up(nl), Sp(nl), Vp(nl);
+    int64_t tu = 0, tv = 0;
+    for (int i = 0; i < nl; ++i) {
+      tu += pp[i] * kk[i];
+      tv += kk[i] * qq[i];
+    }
+    Scratch<double> Uall(tu, s), Vall(tv, s);
+    int64_t od = 0, ou = 0, ov = 0;
+    for (int i = 0; i < nl; ++i) {
+      const int64_t b = lg[i], rs = hspans[4 * b], hh = hspans[4 * b + 1], cs = hspans[4 * b + 2],
+                    ww = hspans[4 * b + 3];
+      double* D = Dall.get() + od;
+      k_scatter_block<<<grid_for(hh * 32, T, G), T, 0, s>>>(rs, hh, cs, ww, a_ptr, a_idx, a_val, D, tr[i]);
+      Mp[i] = D;
+      Up[i] = Uall.get() + ou;
+      Vp[i] = Vall.get() + ov;
+      Sp[i] = sigma + hroff[b];
+      od += hh * ww;
+      ou += pp[i] * kk[i];
+      ov += kk[i] * qq[i];
+    }
+    FPI_LAUNCH_CHECK();
+    dense_svd_batched(h, nl, pp.data(), qq.data(), Mp.data(), ldm.data(), kk.data(), Up.data(), Sp.data(),
+                      Vp.data());
+    for (int i = 0; i < nl; ++i) {
+      const int64_t b = lg[i], hh = hspans[4 * b + 1], ww = hspans[4 * b + 3];
+      // oriented M = U' S V'^T; for a transposed block A = V' S U'^T
+      k_store_large<<<grid_for(hh * kk[i] + kk[i] * ww, T, G), T, 0, s>>>(hh, ww, kk[i], Up[i], Vp[i], tr[i],
+                                                                           u_val + huoff[b], vt_val + hvoff[b]);
       note_launch(h, 2);
     }
+    FPI_LAUNCH_CHECK();
   }
   if (out_plan) *out_plan = fpi_block_plan{st.rank11, st.nnz_u, st.nnz_v, st.n_small + st.n_large, st.n_large};
 }

@@ -19,6 +19,7 @@
 // its stagnation at the rounding floor.
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "capi_guard.cuh"
@@ -226,10 +227,33 @@ __device__ __forceinline__ void mm32(const double* A, const double* B, double (&
   }
 }
 
+// One eigenproblem of a batch (device descriptor).
+struct EigProb {
+  int nb;                        // padded block count (even)
+  int done;                      // converged (written on the device)
+  int sweeps;
+  int pad;
+  double* G;                     // npad x npad
+  double* V;                     // npad x npad
+  double* Jbuf;                  // npairs * JS * JS
+  int* jflag;                    // npairs
+  unsigned long long* offmax;    // per sweep
+  const double* abs_scale;       // null: relative criterion
+  int64_t pair_off, item_off;    // prefix sums over the batch
+};
+
+__device__ __forceinline__ int find_prob(const EigProb* P, int nprob, int64_t idx, bool items) {
+  int lo = 0, hi = nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((items ? P[mid].item_off : P[mid].pair_off) <= idx) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 __global__ void __launch_bounds__(JT, 3)
-    k_jacobi(int nb, double* G, int64_t ldg, double* V, int64_t ldv, double* Jbuf, int* jflag,
-             unsigned long long* offmax, int max_sweeps, double tol, int* sweeps_out, const double* abs_scale,
-             unsigned long long* prof) {
+    k_jacobi(EigProb* P, int nprob, int64_t total_pairs, int64_t total_items, int max_rounds, int max_sweeps,
+             double tol, unsigned long long* prof) {
   cg::grid_group grid = cg::this_grid();
   __shared__ __align__(16) double Sa[JS * LDS_];
   __shared__ __align__(16) double Ra[JS * LDS_];
@@ -239,19 +263,22 @@ __global__ void __launch_bounds__(JT, 3)
   __shared__ PairBuf pbuf;
   build_tables(tb);
   __syncthreads();
-  const bool absolute = abs_scale != nullptr;
-  const double ascale = absolute ? *abs_scale : 0.0;
-  const int npairs = nb / 2;
-  const int64_t npad = (int64_t)nb * JB;
-  const int64_t rtiles = (npad + JS - 1) / JS;
-  const int64_t gitems = (int64_t)npairs * npairs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int sweep = 0;
   for (; sweep < max_sweeps; ++sweep) {
-    for (int round = 0; round < nb - 1; ++round) {
+    for (int round = 0; round < max_rounds; ++round) {
       const unsigned long long t0 = prof ? gtimer() : 0;
       // ---- phase A: one CTA per pair (sub-problem in smem)
-      for (int pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+      for (int64_t gp = blockIdx.x; gp < total_pairs; gp += gridDim.x) {
+        const int pi = find_prob(P, nprob, gp, false);
+        const EigProb& pr_ = P[pi];
+        const int nb = pr_.nb;
+        if (pr_.done || round >= nb - 1) continue;
+        const int pr = (int)(gp - pr_.pair_off);
+        const int64_t ldg = (int64_t)nb * JB;
+        double* G = pr_.G;
+        const bool absolute = pr_.abs_scale != nullptr;
+        const double ascale = absolute ? *pr_.abs_scale : 0.0;
         const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
         for (int e = threadIdx.x; e < JS * JS; e += JT) {
           const int a = e >> 5, b = e & 31;
@@ -262,7 +289,7 @@ __global__ void __launch_bounds__(JT, 3)
         const unsigned long long ts0 = prof ? gtimer() : 0;
         double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
         if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
-        double* Jp = Jbuf + (int64_t)pr * JS * JS;
+        double* Jp = pr_.Jbuf + (int64_t)pr * JS * JS;
         int rot = 0;
         for (int e = threadIdx.x; e < JS * JS; e += JT) {
           const double v = Ra[(e & 31) * LDS_ + (e >> 5)];  // Rt -> row-major J
@@ -270,10 +297,11 @@ __global__ void __launch_bounds__(JT, 3)
           rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
         }
         rot = __syncthreads_or(rot);
-        if (threadIdx.x == 0) jflag[pr] = rot;
+        if (threadIdx.x == 0) pr_.jflag[pr] = rot;
         if (threadIdx.x < 32) {
           for (int o = 16; o; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
-          if (threadIdx.x == 0 && om > 0.0) atomicMax(offmax + sweep, (unsigned long long)__double_as_longlong(om));
+          if (threadIdx.x == 0 && om > 0.0)
+            atomicMax(pr_.offmax + sweep, (unsigned long long)__double_as_longlong(om));
         }
         __syncthreads();
       }
@@ -281,14 +309,26 @@ __global__ void __launch_bounds__(JT, 3)
       grid.sync();
       const unsigned long long t2 = prof ? gtimer() : 0;
       // ---- phase B
-      for (int64_t item = blockIdx.x; item < gitems + (int64_t)npairs * rtiles; item += gridDim.x) {
+      for (int64_t gi = blockIdx.x; gi < total_items; gi += gridDim.x) {
+        const int pi = find_prob(P, nprob, gi, true);
+        const EigProb& pr_ = P[pi];
+        const int nb = pr_.nb;
+        if (pr_.done || round >= nb - 1) continue;
+        const int npairs = nb / 2;
+        const int64_t npad = (int64_t)nb * JB;
+        const int64_t rtiles = (npad + JS - 1) / JS;
+        const int64_t gitems = (int64_t)npairs * npairs;
+        const int64_t item = gi - pr_.item_off;
+        double* G = pr_.G;
+        double* V = pr_.V;
+        const int64_t ldg = npad, ldv = npad;
         if (item < gitems) {
           const int pa = (int)(item / npairs), pb = (int)(item % npairs);
           const int ai = rr_block(pa, round, nb), aj = rr_block(nb - 1 - pa, round, nb);
           const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
-          if (!jflag[pa] && !jflag[pb]) continue;  // both rotations are the identity
-          const double* Ja = Jbuf + (int64_t)pa * JS * JS;
-          const double* Jb2 = Jbuf + (int64_t)pb * JS * JS;
+          if (!pr_.jflag[pa] && !pr_.jflag[pb]) continue;  // both rotations are the identity
+          const double* Ja = pr_.Jbuf + (int64_t)pa * JS * JS;
+          const double* Jb2 = pr_.Jbuf + (int64_t)pb * JS * JS;
           for (int e = threadIdx.x; e < JS * JS; e += JT) {
             const int a = e >> 5, b = e & 31;
             Sa[a * LDS_ + b] = G[(int64_t)sub_to_global(a, ai, aj) * ldg + sub_to_global(b, bi, bj)];
@@ -323,8 +363,8 @@ __global__ void __launch_bounds__(JT, 3)
           const int pb = (int)(it2 / rtiles);
           const int64_t r0 = (it2 % rtiles) * JS;
           const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
-          if (!jflag[pb]) continue;
-          const double* Jb2 = Jbuf + (int64_t)pb * JS * JS;
+          if (!pr_.jflag[pb]) continue;
+          const double* Jb2 = pr_.Jbuf + (int64_t)pb * JS * JS;
           for (int e = threadIdx.x; e < JS * JS; e += JT) {
             const int a = e >> 5, b = e & 31;
             Sa[a * LDS_ + b] = (r0 + a < npad) ? V[(r0 + a) * ldv + sub_to_global(b, bi, bj)] : 0.0;
@@ -355,11 +395,24 @@ __global__ void __launch_bounds__(JT, 3)
         prof[3] += gtimer() - t3;
       }
     }
-    const double cur = __longlong_as_double((long long)offmax[sweep]);
-    const double prev = sweep ? __longlong_as_double((long long)offmax[sweep - 1]) : 1e300;
-    if (cur <= tol || (cur < 1e-9 && cur > 0.25 * prev)) break;
+    // per-problem convergence: converged, or the off-diagonal measure stagnates at the rounding floor
+    if (blockIdx.x == 0) {
+      for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) {
+        EigProb& pr_ = P[pi];
+        if (pr_.done) continue;
+        const double cur = __longlong_as_double((long long)pr_.offmax[sweep]);
+        const double prev = sweep ? __longlong_as_double((long long)pr_.offmax[sweep - 1]) : 1e300;
+        if (cur <= tol || (cur < 1e-9 && cur > 0.25 * prev) || sweep + 1 == max_sweeps) {
+          pr_.done = 1;
+          pr_.sweeps = sweep + 1;
+        }
+      }
+    }
+    grid.sync();
+    bool all = true;
+    for (int pi = 0; pi < nprob; ++pi) all &= (P[pi].done != 0);
+    if (all) break;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep + 1;
 }
 
 __global__ void k_max_diag(int64_t n, const double* A, int64_t lda, double* out) {
@@ -404,28 +457,54 @@ __global__ void k_gather_eig(int64_t n, const double* Vp, int64_t npad, const in
 
 }  // namespace
 
-int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, double* V, int64_t ldv,
-            int max_sweeps, double tol, bool absolute) {
+void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* const* A, const int64_t* lda,
+                     double* const* w, double* const* V, const int64_t* ldv, int max_sweeps, double tol,
+                     bool absolute, int* sweeps_out) {
   cudaStream_t s = h->stream;
-  if (n <= 0) return 0;
-  int nb = (int)((n + JB - 1) / JB);
-  if (nb < 2) nb = 2;
-  if (nb % 2) ++nb;
-  const int64_t npad = (int64_t)nb * JB;
-  Scratch<double> G(npad * npad, s), Vp(npad * npad, s), Jbuf((int64_t)(nb / 2) * JS * JS, s);
-  Scratch<int> jflag(nb / 2, s);
-  Scratch<unsigned long long> offm(max_sweeps + 1, s);
-  Scratch<int> sweeps(1, s);
-  Scratch<double> scale(1, s);
-  FPI_CUDA(cudaMemsetAsync(offm.get(), 0, sizeof(unsigned long long) * (max_sweeps + 1), s));
-  const unsigned G16 = (unsigned)(h->num_sms * 16);
-  k_pad_copy<<<grid_for(npad * npad, 256, G16), 256, 0, s>>>(n, npad, A, lda, G);
-  k_identity<<<grid_for(npad * npad, 256, G16), 256, 0, s>>>(npad, Vp);
-  double* scale_p = nullptr;
-  if (absolute) {
-    k_max_diag<<<1, 256, 0, s>>>(n, A, lda, scale);
-    scale_p = scale.get();
+  if (nprob <= 0) return;
+  std::vector<EigProb> hp(nprob);
+  std::vector<int64_t> npad(nprob);
+  int64_t gsz = 0, jsz = 0, fsz = 0, tot_pairs = 0, tot_items = 0;
+  int max_rounds = 0;
+  for (int i = 0; i < nprob; ++i) {
+    int nb = (int)((n[i] + JB - 1) / JB);
+    if (nb < 2) nb = 2;
+    if (nb % 2) ++nb;
+    npad[i] = (int64_t)nb * JB;
+    hp[i] = EigProb{};
+    hp[i].nb = nb;
+    hp[i].pair_off = tot_pairs;
+    hp[i].item_off = tot_items;
+    const int64_t np = nb / 2, rt = (npad[i] + JS - 1) / JS;
+    tot_pairs += np;
+    tot_items += np * np + np * rt;
+    gsz += npad[i] * npad[i];
+    jsz += np * JS * JS;
+    fsz += np;
+    if (nb - 1 > max_rounds) max_rounds = nb - 1;
   }
+  Scratch<double> Gall(gsz, s), Vall(gsz, s), Jall(jsz, s), scales(nprob, s);
+  Scratch<int> fall(fsz, s);
+  Scratch<unsigned long long> offm((int64_t)nprob * (max_sweeps + 1), s);
+  Scratch<EigProb> dP(nprob, s);
+  FPI_CUDA(cudaMemsetAsync(offm.get(), 0, sizeof(unsigned long long) * nprob * (max_sweeps + 1), s));
+  const unsigned G16 = (unsigned)(h->num_sms * 16);
+  int64_t go = 0, jo = 0, fo = 0;
+  for (int i = 0; i < nprob; ++i) {
+    hp[i].G = Gall.get() + go;
+    hp[i].V = Vall.get() + go;
+    hp[i].Jbuf = Jall.get() + jo;
+    hp[i].jflag = fall.get() + fo;
+    hp[i].offmax = offm.get() + (int64_t)i * (max_sweeps + 1);
+    hp[i].abs_scale = absolute ? scales.get() + i : nullptr;
+    k_pad_copy<<<grid_for(npad[i] * npad[i], 256, G16), 256, 0, s>>>(n[i], npad[i], A[i], lda[i], hp[i].G);
+    k_identity<<<grid_for(npad[i] * npad[i], 256, G16), 256, 0, s>>>(npad[i], hp[i].V);
+    if (absolute) k_max_diag<<<1, 256, 0, s>>>(n[i], A[i], lda[i], scales.get() + i);
+    go += npad[i] * npad[i];
+    jo += (int64_t)(hp[i].nb / 2) * JS * JS;
+    fo += hp[i].nb / 2;
+  }
+  FPI_CUDA(cudaMemcpyAsync(dP.get(), hp.data(), sizeof(EigProb) * nprob, cudaMemcpyHostToDevice, s));
   FPI_LAUNCH_CHECK();
   static int max_blocks = 0;
   if (!max_blocks) {
@@ -433,46 +512,53 @@ int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, 
     FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, JT, 0));
     max_blocks = per_sm * h->num_sms;
   }
-  const int64_t rtiles = (npad + JS - 1) / JS;
-  const int64_t want = (int64_t)(nb / 2) * (nb / 2) + (int64_t)(nb / 2) * rtiles;
   int cap_blocks = max_blocks;
   if (const char* e = getenv("FPI_JACOBI_GRID")) cap_blocks = atoi(e) < max_blocks ? atoi(e) : max_blocks;
-  int grid = (int)(want < cap_blocks ? want : cap_blocks);
-  if (grid < nb / 2) grid = nb / 2 < max_blocks ? nb / 2 : max_blocks;
+  int grid = (int)(tot_items < cap_blocks ? tot_items : cap_blocks);
+  if (grid < tot_pairs) grid = (int)(tot_pairs < max_blocks ? tot_pairs : max_blocks);
   if (grid < 1) grid = 1;
   Scratch<unsigned long long> prof(5, s);
   FPI_CUDA(cudaMemsetAsync(prof.get(), 0, sizeof(unsigned long long) * 5, s));
   unsigned long long* prof_p = getenv("FPI_JACOBI_PROFILE") ? prof.get() : nullptr;
-  double* Gp = G.get();
-  int64_t ldg = npad;
-  double* Vpp = Vp.get();
-  int64_t ldvp = npad;
-  double* Jb = Jbuf.get();
-  int* jf = jflag.get();
-  unsigned long long* om = offm.get();
-  int* sw = sweeps.get();
-  void* args[] = {&nb, &Gp, &ldg, &Vpp, &ldvp, &Jb, &jf, &om, &max_sweeps, &tol, &sw, &scale_p, &prof_p};
+  EigProb* Pp = dP.get();
+  void* args[] = {&Pp, &nprob, &tot_pairs, &tot_items, &max_rounds, &max_sweeps, &tol, &prof_p};
   {
     KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
     FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, 0, s));
   }
   note_launch(h);
+  // eigenvalues descending + gathered eigenvectors, per problem
+  FPI_CUDA(cudaMemcpyAsync(hp.data(), dP.get(), sizeof(EigProb) * nprob, cudaMemcpyDeviceToHost, s));
   CubTemp tmp(s);
-  Scratch<double> keys(n, s), keys2(n, s);
-  Scratch<int32_t> idx(n, s), idx2(n, s);
-  k_diag_keys<<<grid_for(n, 256, h->num_sms * 4), 256, 0, s>>>(n, G, npad, keys, idx);
-  sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n, true, 0, 64, s);
-  k_gather_eig<<<grid_for(n * n, 256, G16), 256, 0, s>>>(n, Vp, npad, idx2, keys2, w, V, ldv);
-  FPI_LAUNCH_CHECK();
-  note_launch(h, 3);
-  if (prof_p) {
-    unsigned long long hp[5];
-    FPI_CUDA(cudaMemcpyAsync(hp, prof_p, sizeof(hp), cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[jacobi n=%lld grid=%d] phaseA %.3f (subsolve %.3f)  syncA %.3f  phaseB %.3f  syncB %.3f ms\n",
-            (long long)n, grid, hp[0] * 1e-6, hp[4] * 1e-6, hp[1] * 1e-6, hp[2] * 1e-6, hp[3] * 1e-6);
+  for (int i = 0; i < nprob; ++i) {
+    Scratch<double> keys(n[i], s), keys2(n[i], s);
+    Scratch<int32_t> idx(n[i], s), idx2(n[i], s);
+    k_diag_keys<<<grid_for(n[i], 256, h->num_sms * 4), 256, 0, s>>>(n[i], Gall.get() + (hp[i].G - Gall.get()),
+                                                                   npad[i], keys, idx);
+    sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n[i], true, 0, 64, s);
+    k_gather_eig<<<grid_for(n[i] * n[i], 256, G16), 256, 0, s>>>(n[i], hp[i].V, npad[i], idx2, keys2, w[i], V[i],
+                                                                 ldv[i]);
+    note_launch(h, 3);
   }
-  return host_read(sweeps.get(), s);
+  FPI_LAUNCH_CHECK();
+  FPI_CUDA(cudaStreamSynchronize(s));
+  if (sweeps_out)
+    for (int i = 0; i < nprob; ++i) sweeps_out[i] = hp[i].sweeps;
+  if (prof_p) {
+    unsigned long long hq[5];
+    FPI_CUDA(cudaMemcpyAsync(hq, prof_p, sizeof(hq), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+    fprintf(stderr, "[jacobi nprob=%d n0=%lld grid=%d] phaseA %.3f (subsolve %.3f)  syncA %.3f  phaseB %.3f  syncB %.3f ms\n",
+            nprob, (long long)n[0], grid, hq[0] * 1e-6, hq[4] * 1e-6, hq[1] * 1e-6, hq[2] * 1e-6, hq[3] * 1e-6);
+  }
+}
+
+int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, double* V, int64_t ldv,
+            int max_sweeps, double tol, bool absolute) {
+  if (n <= 0) return 0;
+  int sw = 0;
+  sym_eig_batched(h, 1, &n, &A, &lda, &w, &V, &ldv, max_sweeps, tol, absolute, &sw);
+  return sw;
 }
 
 }  // namespace fpi

@@ -11,6 +11,10 @@ void lower_inverse(fpi_context* h, int64_t n, const double* L, int64_t ldl, doub
 // <= tol * max_i |a_ii|; also stops when the measure stagnates at rounding level.
 int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, double* V, int64_t ldv,
             int max_sweeps, double tol = 1e-14, bool absolute = false);
+// Independent eigenproblems in one cooperative launch (all solved concurrently).
+void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* const* A, const int64_t* lda,
+                     double* const* w, double* const* V, const int64_t* ldv, int max_sweeps, double tol,
+                     bool absolute, int* sweeps_out);
 void transpose(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* B, int64_t ldb);
 void col_sumsq(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* out);
 void scale_cols(fpi_context* h, int64_t M, int64_t N, double* A, int64_t lda, const double* s, bool divide);

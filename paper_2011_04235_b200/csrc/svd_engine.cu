@@ -312,6 +312,66 @@ static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M
   }
 }
 
+// Many tall panels (p_i >= q_i) at once: Grams -> one batched eigensolve -> per-panel finish.
+// Panels whose kept spectrum is wide fall back to the refined single-panel path.
+void dense_svd_batched(fpi_context* h, int nb, const int64_t* p, const int64_t* q, const double* const* M,
+                       const int64_t* ldm, const int64_t* rank, double* const* U, double* const* sigma,
+                       double* const* Vt) {
+  if (nb <= 0) return;
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  int64_t tq2 = 0, tq = 0;
+  for (int i = 0; i < nb; ++i) {
+    tq2 += q[i] * q[i];
+    tq += q[i];
+  }
+  Scratch<double> Gall(tq2, s), Wall(tq2, s), wall(tq, s);
+  std::vector<const double*> Gp(nb);
+  std::vector<double*> Wp(nb), wp(nb);
+  std::vector<int64_t> ldq(nb);
+  int64_t o2 = 0, o1 = 0;
+  for (int i = 0; i < nb; ++i) {
+    double* Gi = Gall.get() + o2;
+    gemm(h, true, false, q[i], q[i], p[i], 1.0, M[i], ldm[i], M[i], ldm[i], 0.0, Gi, q[i], /*sym=*/true);
+    Gp[i] = Gi;
+    Wp[i] = Wall.get() + o2;
+    wp[i] = wall.get() + o1;
+    ldq[i] = q[i];
+    o2 += q[i] * q[i];
+    o1 += q[i];
+  }
+  std::vector<int> sw(nb);
+  sym_eig_batched(h, nb, q, Gp.data(), ldq.data(), wp.data(), Wp.data(), ldq.data(), 60, 1e-15, true, sw.data());
+  std::vector<double> hl(2 * nb);
+  for (int i = 0; i < nb; ++i) {
+    FPI_CUDA(cudaMemcpyAsync(&hl[2 * i], wp[i], sizeof(double), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaMemcpyAsync(&hl[2 * i + 1], wp[i] + rank[i] - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  FPI_CUDA(cudaStreamSynchronize(s));
+  CubTemp tmp(s);
+  for (int i = 0; i < nb; ++i) {
+    const int64_t r = rank[i];
+    if (!(hl[2 * i] > 0.0) || hl[2 * i + 1] < 1e-6 * hl[2 * i]) {  // wide spectrum: refined path
+      dense_svd(h, p[i], q[i], M[i], ldm[i], r, U[i], sigma[i], Vt[i], nullptr);
+      continue;
+    }
+    Scratch<double> Uraw(p[i] * r, s), ss(r, s), ss2(r, s);
+    Scratch<int32_t> ord(r, s), ord2(r, s);
+    gemm(h, false, false, p[i], r, q[i], 1.0, M[i], ldm[i], Wp[i], q[i], 0.0, Uraw, r);
+    col_sumsq(h, p[i], r, Uraw, r, ss);
+    k_sqrt_clamp<<<grid_for(r, 256, G), 256, 0, s>>>(r, ss);
+    k_iota32<<<grid_for(r, 256, G), 256, 0, s>>>(ord, r);
+    sort_pairs(tmp, ss.get(), ss2.get(), ord.get(), ord2.get(), r, true, 0, 64, s);
+    FPI_CUDA(cudaMemcpyAsync(sigma[i], ss2.get(), sizeof(double) * r, cudaMemcpyDeviceToDevice, s));
+    k_gather_cols_div<<<grid_for(p[i] * r, 256, G), 256, 0, s>>>(p[i], r, Uraw, r, ord2, ss2, U[i], r);
+    k_gather_vt<<<grid_for(r * q[i], 256, G), 256, 0, s>>>(q[i], r, Wp[i], q[i], ord2, Vt[i], q[i]);
+    FPI_LAUNCH_CHECK();
+    note_launch(h, 5);
+    complete_null_left(h, p[i], r, U[i], r, sigma[i], nullptr);
+    canonical_signs(h, r, p[i], q[i], U[i], r, Vt[i], q[i]);
+  }
+}
+
 // Orthonormal completion of left vectors whose sigma is numerically zero
 // (LAPACK returns some orthonormal completion there; any is valid).
 void complete_null_left(fpi_context* h, int64_t p, int64_t rank, double* U, int64_t ldu, const double* sigma,

@@ -91,3 +91,33 @@ def test_randomized_svd_matches_oracle(seed, rank):
     Bo = (fo.U * fo.sigma) @ fo.Vt
     assert np.linalg.norm(Bg - Bo) <= 1e-9 * np.linalg.norm(Bo)
     assert f.orthonormality_defect() < 1e-10
+
+
+def test_block_svd_large_tier_batched():
+    """Blocks too large for shared memory (both orientations) go through the batched Gram path."""
+    import paper_2011_04235_b200 as fp
+    rng = np.random.default_rng(11)
+    blocks = [sp.random(600, 90, density=0.3, random_state=rng, format="csr"),
+              sp.random(80, 700, density=0.3, random_state=rng, format="csr"),
+              sp.csr_matrix(rng.standard_normal((5, 4))),
+              sp.random(450, 120, density=0.5, random_state=rng, format="csr")]
+    for alpha in (0.03, 0.5):
+        f = fp.block_diagonal_svd(blocks, alpha)
+        spoke = sp.block_diag(blocks).tocsr()
+        spans, ro, co = [], 0, 0
+        for b in blocks:
+            spans.append((ro, b.shape[0], co, b.shape[1]))
+            ro += b.shape[0]
+            co += b.shape[1]
+        fo = orc.block_svd(spoke, np.array(spans), alpha)
+        assert f.rank == fo.rank
+        off = 0
+        for b in blocks:
+            kp = int(np.ceil(alpha * min(b.shape)))
+            so = fo.sigma[off:off + kp]
+            assert np.abs(f.sigma[off:off + kp] - so).max() <= 1e-9 * so[0]
+            off += kp
+        Ug, Vg = f.U.toarray(), f.Vt.toarray()
+        Uo, Vo = fo.U.toarray(), fo.Vt.toarray()
+        assert np.abs((Ug * f.sigma) @ Vg - (Uo * fo.sigma) @ Vo).max() < 1e-9 * fo.sigma.max()
+        assert f.orthonormality_defect() < 1e-10
