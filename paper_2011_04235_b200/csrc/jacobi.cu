@@ -10,9 +10,13 @@
 //            rotates the within-block pairs (15 steps), every round the cross
 //            pairs (16 steps), so each index pair is visited once per sweep (a
 //            cyclic Jacobi ordering).
-//   phase B  every 32 x 32 block of G gets G'[P, P'] = R_P^T G[P, P'] R_P' and
-//            every 32-row tile of V gets V[:, P'] <- V[:, P'] R_P', as 32^3
-//            products on the FP64 tensor path (mma.sync m8n8k4 -> DMMA).
+//   phase B  every upper 32 x 32 block of G gets G'[P, P'] = R_P^T G[P, P'] R_P'
+//            (written to both triangles), as 32^3 products on the FP64 tensor
+//            path (mma.sync m8n8k4 -> DMMA); each CTA streams a contiguous run
+//            of blocks through a two-stage cp.async pipeline.
+//   V        the eigenvector update V[:, P'] <- V[:, P'] R_P' of round r does
+//            not feed the iteration, so it runs during phase A of round r + 1
+//            on the CTAs phase A leaves idle (R is double-buffered by round).
 // Grid-wide barriers separate the phases.  A sweep ends by checking the
 // largest off-diagonal measure seen (relative |a_pq| / sqrt(a_pp a_qq), or
 // absolute |a_pq| / max|a_ii| for Gram matrices) against the tolerance, or
@@ -91,20 +95,41 @@ __device__ void build_tables(StepTables& tb) {
   }
 }
 
-// Rotation of one pair from (app, aqq, apq): FP32 angle, exactly orthogonal FP64 (c, s).
+// Fast approximations (MUFU) for the rotation angle: the angle only has to be close, the
+// rotation itself is made orthogonal to FP64 precision by the Newton-refined cosine.
+__device__ __forceinline__ float rcp_apx(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ float sqrt_apx(float x) { float r; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ float rsqrt_apx(float x) { float r; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+__device__ __forceinline__ double rcp_apx(double x) { double r; asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
+__device__ __forceinline__ double rsqrt_apx(double x) { double r; asm("rsqrt.approx.f64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
+
+// tan of the Jacobi angle from z = (aqq - app) / (2 apq): t = sign(z) / (|z| + sqrt(z^2 + 1)), |t| <= 1.
+__device__ __forceinline__ float tan_from_z(float zf) {
+  return copysignf(rcp_apx(fabsf(zf) + sqrt_apx(fmaf(zf, zf, 1.0f))), zf);
+}
+
+// Rotation of one pair from (app, aqq, apq): FP32-accurate angle, then c = 1/sqrt(1 + t^2) to full
+// FP64 precision (FP32 seed + one third-order Newton step) and s = c t, so the rotation is
+// orthogonal to rounding.
 __device__ __forceinline__ void rotation(double app, double aqq, double apq, double tol, double ascale, bool absolute,
                                          double& c, double& sn) {
   const double den2 = absolute ? ascale * ascale : fabs(app) * fabs(aqq);
   const double apq2 = apq * apq;
-  const float zf = (float)(aqq - app) * __frcp_rn((float)(2.0 * apq));
-  const float azf = fabsf(zf);
-  const float tf = azf > 1e18f ? 0.5f / zf : copysignf(__frcp_rn(azf + sqrtf(fmaf(zf, zf, 1.0f))), zf);
-  const double tt = isfinite(tf) ? (double)tf : 0.0;
-  const bool rot = apq != 0.0 && apq2 > tol * tol * den2 && tt != 0.0;
-  c = rot ? rsqrt(fma(tt, tt, 1.0)) : 1.0;
-  sn = rot ? c * tt : 0.0;
+  const double zd = (aqq - app) * rcp_apx(2.0 * apq);
+  double tt;
+  if (fabs(zd) > 1e18) {
+    tt = 0.5 * rcp_apx(zd);
+  } else {
+    tt = (double)tan_from_z((float)zd);
+  }
+  const bool rot = apq != 0.0 && apq2 > tol * tol * den2 && isfinite(tt) && tt != 0.0;
+  const double x = fma(tt, tt, 1.0);             // in [1, 2]
+  const double y = (double)rsqrt_apx((float)x);  // ~2^-22
+  const double e = fma(-x, y * y, 1.0);
+  const double cy = fma(y, fma(e, 0.375, 0.5) * e, y);
+  c = rot ? cy : 1.0;
+  sn = rot ? cy * tt : 0.0;
 }
-
 struct PairBuf {
   double c[2][16], s[2][16], app[2][16], aqq[2][16], apq[2][16];
 };
@@ -127,7 +152,7 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
     if (x == y) continue;
     const double sxy = S[x * LDS_ + y];
     const double den2 = absolute ? ascale * ascale : fabs(S[x * LDS_ + x]) * fabs(S[y * LDS_ + y]);
-    if (sxy != 0.0) om = fmax(om, den2 > 0.0 ? sqrt(sxy * sxy / den2) : 1.0);
+    if (sxy != 0.0) om = fmax(om, den2 > 0.0 ? fabs(sxy) * rsqrt_apx(den2) : 1.0);
   }
   // prologue: rotations of the first step
   if (threadIdx.x < 16) {
@@ -210,7 +235,38 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
   return om;
 }
 
-// 32x32x32 product C = op(A) B on DMMA: A, B in smem (stride LDS_); TA: A stored transposed.
+// ---- tiles: 32 x 32 FP64 blocks in shared memory (stride LDS_), filled by cp.async
+constexpr int TILE = JS * LDS_;
+constexpr int NTILE = 7;
+constexpr size_t JACOBI_SMEM = (size_t)NTILE * TILE * sizeof(double);
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// dst <- M[rows, cols]: local row a -> global row r0 + a (r0 >= 0) or block pair (bi, bj); local
+// cols map to the block pair (ci, cj).  16 B chunks never straddle a 16-wide block.
+__device__ __forceinline__ void tile_async(double* dst, const double* M, int64_t ld, int64_t r0, int bi, int bj,
+                                           int ci, int cj) {
+  for (int e = threadIdx.x; e < JS * 16; e += JT) {
+    const int a = e >> 4, c = (e & 15) * 2;
+    const int64_t row = r0 >= 0 ? r0 + a : (int64_t)sub_to_global(a, bi, bj);
+    cp16(dst + a * LDS_ + c, M + row * ld + sub_to_global(c, ci, cj));
+  }
+}
+__device__ __forceinline__ void j_async(double* dst, const double* J) {
+  for (int e = threadIdx.x; e < JS * 16; e += JT) {
+    const int a = e >> 4, c = (e & 15) * 2;
+    cp16(dst + a * LDS_ + c, J + a * JS + c);
+  }
+}
+
+// 32x32x32 product acc = op(A) B with A, B in smem; TA: A read transposed.  Warp w owns rows
+// m0 + g, cols n0 + 8j + 2t (+1) of the output (the DMMA accumulator layout).
 template <bool TA>
 __device__ __forceinline__ void mm32(const double* A, const double* B, double (&acc)[2][2], int warp, int lane) {
   const int g = lane >> 2, t = lane & 3;
@@ -227,166 +283,245 @@ __device__ __forceinline__ void mm32(const double* A, const double* B, double (&
   }
 }
 
+// Two-stage cp.async pipeline over the items [t0, t1) of a CTA's run; skip(t) drops identity
+// updates, issue(t, stage) starts the loads of item t, compute(t, stage) consumes them.
+template <class Skip, class Issue, class Compute>
+__device__ __forceinline__ void pipeline(int64_t t0, int64_t t1, Skip skip, Issue issue, Compute compute) {
+  int64_t cur = t0;
+  while (cur < t1 && skip(cur)) ++cur;
+  if (cur >= t1) return;
+  issue(cur, 0);
+  cp_commit();
+  int stage = 0;
+  while (cur < t1) {
+    int64_t nxt = cur + 1;
+    while (nxt < t1 && skip(nxt)) ++nxt;
+    if (nxt < t1) {
+      issue(nxt, stage ^ 1);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    compute(cur, stage);
+    __syncthreads();
+    cur = nxt;
+    stage ^= 1;
+  }
+}
+
 // One eigenproblem of a batch (device descriptor).
 struct EigProb {
-  int nb;                        // padded block count (even)
-  int done;                      // converged (written on the device)
+  int nb;              // padded block count (even); npairs = nb / 2 = 32-row tiles of the panel
+  int done;            // converged (written on the device)
   int sweeps;
-  int pad;
-  double* G;                     // npad x npad
-  double* V;                     // npad x npad
-  double* Jbuf;                  // npairs * JS * JS
-  int* jflag;                    // npairs
-  unsigned long long* offmax;    // per sweep
-  const double* abs_scale;       // null: relative criterion
-  int64_t pair_off, item_off;    // prefix sums over the batch
+  int vround;          // round (within its sweep) whose rotations V still owes, -1: none
+  int vpar;            // R buffer holding them
+  int pad_;
+  double* G;           // npad x npad
+  double* V;           // npad x npad
+  double* Jbuf;        // 2 x npairs x JS x JS (by round parity)
+  int* jflag;          // 2 x npairs: rotation of the pair is not the identity
+  unsigned long long* offmax;  // per sweep
+  const double* abs_scale;     // null: relative criterion
+  int64_t pair_off, gitem_off, vitem_off;  // prefix sums over the batch (phase A pairs, G runs, V runs)
 };
 
-__device__ __forceinline__ int find_prob(const EigProb* P, int nprob, int64_t idx, bool items) {
+__device__ __forceinline__ int find_prob(const EigProb* P, int nprob, int64_t idx, int which) {
   int lo = 0, hi = nprob - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if ((items ? P[mid].item_off : P[mid].pair_off) <= idx) lo = mid; else hi = mid - 1;
+    const int64_t off = which == 0 ? P[mid].pair_off : which == 1 ? P[mid].gitem_off : P[mid].vitem_off;
+    if (off <= idx) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
 
+// upper-triangle block index t -> (pa <= pb)
+__device__ __forceinline__ void tri_pair(int64_t t, int& pa, int& pb) {
+  int b = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(b + 1) * (b + 2) / 2 <= t) ++b;
+  while ((int64_t)b * (b + 1) / 2 > t) --b;
+  pb = b;
+  pa = (int)(t - (int64_t)b * (b + 1) / 2);
+}
+
+// V[:, P'] <- V[:, P'] R_P' for the pending round of problem pr_, tiles [t0, t1) of np x np (pair-major).
+__device__ void v_run(const EigProb& pr_, int64_t t0, int64_t t1, double* sm, int warp, int lane) {
+  const int nb = pr_.nb, np = nb / 2, round = pr_.vround;
+  const int64_t ld = (int64_t)nb * JB;
+  const double* Jb0 = pr_.Jbuf + (int64_t)pr_.vpar * np * JS * JS;
+  const int* fl = pr_.jflag + pr_.vpar * np;
+  double* V = pr_.V;
+  pipeline(
+      t0, t1, [&](int64_t t) { return fl[t / np] == 0; },
+      [&](int64_t t, int st) {
+        const int pb = (int)(t / np), rt = (int)(t % np);
+        const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
+        tile_async(sm + (2 * st) * TILE, V, ld, (int64_t)rt * JS, 0, 0, bi, bj);
+        j_async(sm + (2 * st + 1) * TILE, Jb0 + (int64_t)pb * JS * JS);
+      },
+      [&](int64_t t, int st) {
+        const int pb = (int)(t / np), rt = (int)(t % np);
+        const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
+        double acc[2][2];
+        mm32<false>(sm + (2 * st) * TILE, sm + (2 * st + 1) * TILE, acc, warp, lane);
+        const int g = lane >> 2, tq = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
+        const int64_t row = (int64_t)rt * JS + m0 + g;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c0 = n0 + 8 * j + 2 * tq;
+          *reinterpret_cast<double2*>(V + row * ld + sub_to_global(c0, bi, bj)) = make_double2(acc[j][0], acc[j][1]);
+        }
+      });
+}
+
+// phase A item plus the V runs owed by the previous round, for every problem of the batch
+__device__ void section_a(EigProb* P, int nprob, int64_t total_pairs, int64_t total_vitems, int vchunk, int round,
+                          int par, int sweep, bool pairs_on, double tol, double* sm, PairBuf& pbuf,
+                          const StepTables& tb, unsigned long long* prof) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nA = pairs_on ? total_pairs : 0;
+  for (int64_t it = blockIdx.x; it < nA + total_vitems; it += gridDim.x) {
+    if (it < nA) {
+      const int pi = find_prob(P, nprob, it, 0);
+      const EigProb& pr_ = P[pi];
+      const int nb = pr_.nb;
+      if (pr_.done || round >= nb - 1) continue;
+      const int np = nb / 2;
+      const int pr = (int)(it - pr_.pair_off);
+      const int64_t ldg = (int64_t)nb * JB;
+      const bool absolute = pr_.abs_scale != nullptr;
+      const double ascale = absolute ? *pr_.abs_scale : 0.0;
+      const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
+      double* Sa = sm;
+      double* Ra = sm + TILE;
+      tile_async(Sa, pr_.G, ldg, -1, bi, bj, bi, bj);
+      cp_commit();
+      for (int e = threadIdx.x; e < JS * JS; e += JT) {
+        const int a = e >> 5, b = e & 31;
+        Ra[a * LDS_ + b] = a == b ? 1.0 : 0.0;
+      }
+      cp_wait<0>();
+      __syncthreads();
+      const unsigned long long ts0 = prof ? gtimer() : 0;
+      double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
+      if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
+      double* Jp = pr_.Jbuf + ((int64_t)par * np + pr) * JS * JS;
+      int rot = 0;
+      for (int e = threadIdx.x; e < JS * JS; e += JT) {
+        const double v = Ra[(e & 31) * LDS_ + (e >> 5)];  // Rt -> row-major J
+        Jp[e] = v;
+        rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
+      }
+      rot = __syncthreads_or(rot);
+      if (threadIdx.x == 0) pr_.jflag[par * np + pr] = rot;
+      if (threadIdx.x < 32) {
+        for (int o = 16; o; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
+        if (threadIdx.x == 0 && om > 0.0) atomicMax(pr_.offmax + sweep, (unsigned long long)__double_as_longlong(om));
+      }
+      __syncthreads();
+    } else {
+      const int64_t vi = it - nA;
+      const int pi = find_prob(P, nprob, vi, 2);
+      const EigProb& pr_ = P[pi];
+      if (pr_.vround < 0) continue;
+      const int64_t np = pr_.nb / 2;
+      const int64_t t0 = (vi - pr_.vitem_off) * vchunk;
+      const int64_t t1 = t0 + vchunk < np * np ? t0 + vchunk : np * np;
+      v_run(pr_, t0, t1, sm, warp, lane);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(JT, 3)
-    k_jacobi(EigProb* P, int nprob, int64_t total_pairs, int64_t total_items, int max_rounds, int max_sweeps,
-             double tol, unsigned long long* prof) {
+    k_jacobi(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems, int gchunk,
+             int vchunk, int max_rounds, int max_sweeps, double tol, double stagnate_below, unsigned long long* prof) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ __align__(16) double Sa[JS * LDS_];
-  __shared__ __align__(16) double Ra[JS * LDS_];
-  __shared__ __align__(16) double Rb[JS * LDS_];
-  __shared__ __align__(16) double Tm[JS * LDS_];
+  extern __shared__ __align__(16) double sm[];
   __shared__ StepTables tb;
   __shared__ PairBuf pbuf;
   build_tables(tb);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int sweep = 0;
-  for (; sweep < max_sweeps; ++sweep) {
-    for (int round = 0; round < max_rounds; ++round) {
+  int gr = 0;  // global round counter (R buffer parity)
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int round = 0; round < max_rounds; ++round, ++gr) {
+      const int par = gr & 1;
       const unsigned long long t0 = prof ? gtimer() : 0;
-      // ---- phase A: one CTA per pair (sub-problem in smem)
-      for (int64_t gp = blockIdx.x; gp < total_pairs; gp += gridDim.x) {
-        const int pi = find_prob(P, nprob, gp, false);
-        const EigProb& pr_ = P[pi];
-        const int nb = pr_.nb;
-        if (pr_.done || round >= nb - 1) continue;
-        const int pr = (int)(gp - pr_.pair_off);
-        const int64_t ldg = (int64_t)nb * JB;
-        double* G = pr_.G;
-        const bool absolute = pr_.abs_scale != nullptr;
-        const double ascale = absolute ? *pr_.abs_scale : 0.0;
-        const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
-        for (int e = threadIdx.x; e < JS * JS; e += JT) {
-          const int a = e >> 5, b = e & 31;
-          Sa[a * LDS_ + b] = G[(int64_t)sub_to_global(a, bi, bj) * ldg + sub_to_global(b, bi, bj)];
-          Ra[a * LDS_ + b] = a == b ? 1.0 : 0.0;
-        }
-        __syncthreads();
-        const unsigned long long ts0 = prof ? gtimer() : 0;
-        double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
-        if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
-        double* Jp = pr_.Jbuf + (int64_t)pr * JS * JS;
-        int rot = 0;
-        for (int e = threadIdx.x; e < JS * JS; e += JT) {
-          const double v = Ra[(e & 31) * LDS_ + (e >> 5)];  // Rt -> row-major J
-          Jp[e] = v;
-          rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
-        }
-        rot = __syncthreads_or(rot);
-        if (threadIdx.x == 0) pr_.jflag[pr] = rot;
-        if (threadIdx.x < 32) {
-          for (int o = 16; o; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
-          if (threadIdx.x == 0 && om > 0.0)
-            atomicMax(pr_.offmax + sweep, (unsigned long long)__double_as_longlong(om));
-        }
-        __syncthreads();
-      }
+      section_a(P, nprob, total_pairs, total_vitems, vchunk, round, par, sweep, true, tol, sm, pbuf, tb, prof);
       const unsigned long long t1 = prof ? gtimer() : 0;
       grid.sync();
       const unsigned long long t2 = prof ? gtimer() : 0;
-      // ---- phase B
-      for (int64_t gi = blockIdx.x; gi < total_items; gi += gridDim.x) {
-        const int pi = find_prob(P, nprob, gi, true);
+      // ---- phase B: upper blocks of G, both triangles written
+      for (int64_t it = blockIdx.x; it < total_gitems; it += gridDim.x) {
+        const int pi = find_prob(P, nprob, it, 1);
         const EigProb& pr_ = P[pi];
         const int nb = pr_.nb;
         if (pr_.done || round >= nb - 1) continue;
-        const int npairs = nb / 2;
-        const int64_t npad = (int64_t)nb * JB;
-        const int64_t rtiles = (npad + JS - 1) / JS;
-        const int64_t gitems = (int64_t)npairs * npairs;
-        const int64_t item = gi - pr_.item_off;
+        const int np = nb / 2;
+        const int64_t ld = (int64_t)nb * JB;
+        const int64_t ntri = (int64_t)np * (np + 1) / 2;
+        const int64_t ta = (it - pr_.gitem_off) * gchunk;
+        const int64_t tb1 = ta + gchunk < ntri ? ta + gchunk : ntri;
+        const double* J0 = pr_.Jbuf + (int64_t)par * np * JS * JS;
+        const int* fl = pr_.jflag + par * np;
         double* G = pr_.G;
-        double* V = pr_.V;
-        const int64_t ldg = npad, ldv = npad;
-        if (item < gitems) {
-          const int pa = (int)(item / npairs), pb = (int)(item % npairs);
-          const int ai = rr_block(pa, round, nb), aj = rr_block(nb - 1 - pa, round, nb);
-          const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
-          if (!pr_.jflag[pa] && !pr_.jflag[pb]) continue;  // both rotations are the identity
-          const double* Ja = pr_.Jbuf + (int64_t)pa * JS * JS;
-          const double* Jb2 = pr_.Jbuf + (int64_t)pb * JS * JS;
-          for (int e = threadIdx.x; e < JS * JS; e += JT) {
-            const int a = e >> 5, b = e & 31;
-            Sa[a * LDS_ + b] = G[(int64_t)sub_to_global(a, ai, aj) * ldg + sub_to_global(b, bi, bj)];
-            Ra[a * LDS_ + b] = Ja[e];
-            Rb[a * LDS_ + b] = Jb2[e];
-          }
-          __syncthreads();
-          double acc[2][2];
-          mm32<true>(Ra, Sa, acc, warp, lane);  // Tm = Ja^T S
-          {
-            const int g = lane >> 2, t = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
+        double* Us = sm + 6 * TILE;
+        pipeline(
+            ta, tb1,
+            [&](int64_t t) {
+              int pa, pb;
+              tri_pair(t, pa, pb);
+              return fl[pa] == 0 && fl[pb] == 0;
+            },
+            [&](int64_t t, int st) {
+              int pa, pb;
+              tri_pair(t, pa, pb);
+              const int ai = rr_block(pa, round, nb), aj = rr_block(nb - 1 - pa, round, nb);
+              const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
+              tile_async(sm + (3 * st) * TILE, G, ld, -1, ai, aj, bi, bj);
+              j_async(sm + (3 * st + 1) * TILE, J0 + (int64_t)pa * JS * JS);
+              j_async(sm + (3 * st + 2) * TILE, J0 + (int64_t)pb * JS * JS);
+            },
+            [&](int64_t t, int st) {
+              int pa, pb;
+              tri_pair(t, pa, pb);
+              const int ai = rr_block(pa, round, nb), aj = rr_block(nb - 1 - pa, round, nb);
+              const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
+              const int g = lane >> 2, tq = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
+              double acc[2][2];
+              mm32<false>(sm + (3 * st) * TILE, sm + (3 * st + 2) * TILE, acc, warp, lane);  // U = G Jb
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              Tm[(m0 + g) * LDS_ + n0 + 8 * j + 2 * t] = acc[j][0];
-              Tm[(m0 + g) * LDS_ + n0 + 8 * j + 2 * t + 1] = acc[j][1];
-            }
-          }
-          __syncthreads();
-          mm32<false>(Tm, Rb, acc, warp, lane);  // G' = Tm Jb
-          {
-            const int g = lane >> 2, t = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
-            const int64_t row = sub_to_global(m0 + g, ai, aj);
+              for (int j = 0; j < 2; ++j)
+                *reinterpret_cast<double2*>(Us + (m0 + g) * LDS_ + n0 + 8 * j + 2 * tq) =
+                    make_double2(acc[j][0], acc[j][1]);
+              __syncthreads();
+              mm32<true>(sm + (3 * st + 1) * TILE, Us, acc, warp, lane);  // G' = Ja^T U
+              const int64_t row = sub_to_global(m0 + g, ai, aj);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int c0 = n0 + 8 * j + 2 * t;
-              G[row * ldg + sub_to_global(c0, bi, bj)] = acc[j][0];
-              G[row * ldg + sub_to_global(c0 + 1, bi, bj)] = acc[j][1];
-            }
-          }
-        } else {
-          const int64_t it2 = item - gitems;
-          const int pb = (int)(it2 / rtiles);
-          const int64_t r0 = (it2 % rtiles) * JS;
-          const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
-          if (!pr_.jflag[pb]) continue;
-          const double* Jb2 = pr_.Jbuf + (int64_t)pb * JS * JS;
-          for (int e = threadIdx.x; e < JS * JS; e += JT) {
-            const int a = e >> 5, b = e & 31;
-            Sa[a * LDS_ + b] = (r0 + a < npad) ? V[(r0 + a) * ldv + sub_to_global(b, bi, bj)] : 0.0;
-            Rb[a * LDS_ + b] = Jb2[e];
-          }
-          __syncthreads();
-          double acc[2][2];
-          mm32<false>(Sa, Rb, acc, warp, lane);  // V tile * Jb
-          const int g = lane >> 2, t = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
-          const int64_t row = r0 + m0 + g;
-          if (row < npad) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int c0 = n0 + 8 * j + 2 * t;
-              V[row * ldv + sub_to_global(c0, bi, bj)] = acc[j][0];
-              V[row * ldv + sub_to_global(c0 + 1, bi, bj)] = acc[j][1];
-            }
-          }
-        }
-        __syncthreads();
+              for (int j = 0; j < 2; ++j) {
+                const int c0 = n0 + 8 * j + 2 * tq;
+                const int64_t col = sub_to_global(c0, bi, bj);
+                *reinterpret_cast<double2*>(G + row * ld + col) = make_double2(acc[j][0], acc[j][1]);
+                if (pa != pb) {
+                  G[col * ld + row] = acc[j][0];
+                  G[(col + 1) * ld + row] = acc[j][1];
+                }
+              }
+            });
       }
       const unsigned long long t3 = prof ? gtimer() : 0;
+      // V owes this round's rotations (read in the next section A, after the barrier below)
+      if (blockIdx.x == 0) {
+        for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) {
+          EigProb& pr_ = P[pi];
+          const bool active = !pr_.done && round < pr_.nb - 1;
+          pr_.vround = active ? round : -1;
+          pr_.vpar = par;
+        }
+      }
       grid.sync();
       if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
         prof[0] += t1 - t0;
@@ -402,7 +537,7 @@ __global__ void __launch_bounds__(JT, 3)
         if (pr_.done) continue;
         const double cur = __longlong_as_double((long long)pr_.offmax[sweep]);
         const double prev = sweep ? __longlong_as_double((long long)pr_.offmax[sweep - 1]) : 1e300;
-        if (cur <= tol || (cur < 1e-9 && cur > 0.25 * prev) || sweep + 1 == max_sweeps) {
+        if (cur <= tol || (cur < stagnate_below && cur > 0.25 * prev) || sweep + 1 == max_sweeps) {
           pr_.done = 1;
           pr_.sweeps = sweep + 1;
         }
@@ -413,6 +548,8 @@ __global__ void __launch_bounds__(JT, 3)
     for (int pi = 0; pi < nprob; ++pi) all &= (P[pi].done != 0);
     if (all) break;
   }
+  // the last round's eigenvector update
+  section_a(P, nprob, total_pairs, total_vitems, vchunk, 0, gr & 1, 0, false, tol, sm, pbuf, tb, nullptr);
 }
 
 __global__ void k_max_diag(int64_t n, const double* A, int64_t lda, double* out) {
@@ -451,7 +588,7 @@ __global__ void k_gather_eig(int64_t n, const double* Vp, int64_t npad, const in
   FPI_GRID_STRIDE(e, n * n) {
     int64_t i = e / n, k = e - i * n;
     V[i * ldv + k] = Vp[i * npad + order[k]];
-    if (i == 0) w[k] = wsorted[k];
+    if (i == 0 && w) w[k] = wsorted[k];
   }
 }
 
@@ -460,28 +597,54 @@ __global__ void k_gather_eig(int64_t n, const double* Vp, int64_t npad, const in
 void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* const* A, const int64_t* lda,
                      double* const* w, double* const* V, const int64_t* ldv, int max_sweeps, double tol,
                      bool absolute, int* sweeps_out) {
-  cudaStream_t s = h->stream;
   if (nprob <= 0) return;
+  cudaStream_t s = h->stream;
+  const double stagnate_below = 1e-9;
   std::vector<EigProb> hp(nprob);
-  std::vector<int64_t> npad(nprob);
-  int64_t gsz = 0, jsz = 0, fsz = 0, tot_pairs = 0, tot_items = 0;
+  std::vector<int64_t> npad(nprob), goff(nprob);
+  int64_t gsz = 0, jsz = 0, fsz = 0, tot_pairs = 0, tot_tri = 0, tot_vt = 0;
   int max_rounds = 0;
   for (int i = 0; i < nprob; ++i) {
     int nb = (int)((n[i] + JB - 1) / JB);
     if (nb < 2) nb = 2;
     if (nb % 2) ++nb;
     npad[i] = (int64_t)nb * JB;
+    const int64_t np = nb / 2;
     hp[i] = EigProb{};
     hp[i].nb = nb;
-    hp[i].pair_off = tot_pairs;
-    hp[i].item_off = tot_items;
-    const int64_t np = nb / 2, rt = (npad[i] + JS - 1) / JS;
-    tot_pairs += np;
-    tot_items += np * np + np * rt;
+    hp[i].vround = -1;
+    goff[i] = gsz;
     gsz += npad[i] * npad[i];
-    jsz += np * JS * JS;
-    fsz += np;
+    jsz += 2 * np * JS * JS;
+    fsz += 2 * np;
+    tot_pairs += np;
+    tot_tri += np * (np + 1) / 2;
+    tot_vt += np * np;
     if (nb - 1 > max_rounds) max_rounds = nb - 1;
+  }
+  static int max_blocks = 0;
+  if (!max_blocks) {
+    FPI_CUDA(cudaFuncSetAttribute((const void*)k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)JACOBI_SMEM));
+    int per_sm = 0;
+    FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, JT, JACOBI_SMEM));
+    max_blocks = per_sm * h->num_sms;
+  }
+  int grid = max_blocks;
+  if (const char* e = getenv("FPI_JACOBI_GRID")) grid = atoi(e) < max_blocks ? atoi(e) : max_blocks;
+  if (grid < 1) grid = 1;
+  // run lengths: G blocks spread over the whole grid; V tiles over the CTAs phase A leaves idle
+  const int gchunk = (int)((tot_tri + grid - 1) / grid);
+  const int64_t vcta = grid - tot_pairs > grid / 4 ? grid - tot_pairs : grid / 4 + 1;
+  const int vchunk = (int)((tot_vt + vcta - 1) / vcta);
+  int64_t tot_g = 0, tot_v = 0;
+  for (int i = 0; i < nprob; ++i) {
+    const int64_t np = hp[i].nb / 2;
+    hp[i].pair_off = i ? hp[i - 1].pair_off + hp[i - 1].nb / 2 : 0;
+    hp[i].gitem_off = tot_g;
+    hp[i].vitem_off = tot_v;
+    tot_g += (np * (np + 1) / 2 + gchunk - 1) / gchunk;
+    tot_v += (np * np + vchunk - 1) / vchunk;
   }
   Scratch<double> Gall(gsz, s), Vall(gsz, s), Jall(jsz, s), scales(nprob, s);
   Scratch<int> fall(fsz, s);
@@ -489,10 +652,11 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   Scratch<EigProb> dP(nprob, s);
   FPI_CUDA(cudaMemsetAsync(offm.get(), 0, sizeof(unsigned long long) * nprob * (max_sweeps + 1), s));
   const unsigned G16 = (unsigned)(h->num_sms * 16);
-  int64_t go = 0, jo = 0, fo = 0;
+  int64_t jo = 0, fo = 0;
   for (int i = 0; i < nprob; ++i) {
-    hp[i].G = Gall.get() + go;
-    hp[i].V = Vall.get() + go;
+    const int64_t np = hp[i].nb / 2;
+    hp[i].G = Gall.get() + goff[i];
+    hp[i].V = Vall.get() + goff[i];
     hp[i].Jbuf = Jall.get() + jo;
     hp[i].jflag = fall.get() + fo;
     hp[i].offmax = offm.get() + (int64_t)i * (max_sweeps + 1);
@@ -500,47 +664,25 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     k_pad_copy<<<grid_for(npad[i] * npad[i], 256, G16), 256, 0, s>>>(n[i], npad[i], A[i], lda[i], hp[i].G);
     k_identity<<<grid_for(npad[i] * npad[i], 256, G16), 256, 0, s>>>(npad[i], hp[i].V);
     if (absolute) k_max_diag<<<1, 256, 0, s>>>(n[i], A[i], lda[i], scales.get() + i);
-    go += npad[i] * npad[i];
-    jo += (int64_t)(hp[i].nb / 2) * JS * JS;
-    fo += hp[i].nb / 2;
+    note_launch(h, absolute ? 3 : 2);
+    jo += 2 * np * JS * JS;
+    fo += 2 * np;
   }
   FPI_CUDA(cudaMemcpyAsync(dP.get(), hp.data(), sizeof(EigProb) * nprob, cudaMemcpyHostToDevice, s));
   FPI_LAUNCH_CHECK();
-  static int max_blocks = 0;
-  if (!max_blocks) {
-    int per_sm = 0;
-    FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, JT, 0));
-    max_blocks = per_sm * h->num_sms;
-  }
-  int cap_blocks = max_blocks;
-  if (const char* e = getenv("FPI_JACOBI_GRID")) cap_blocks = atoi(e) < max_blocks ? atoi(e) : max_blocks;
-  int grid = (int)(tot_items < cap_blocks ? tot_items : cap_blocks);
-  if (grid < tot_pairs) grid = (int)(tot_pairs < max_blocks ? tot_pairs : max_blocks);
-  if (grid < 1) grid = 1;
   Scratch<unsigned long long> prof(5, s);
   FPI_CUDA(cudaMemsetAsync(prof.get(), 0, sizeof(unsigned long long) * 5, s));
   unsigned long long* prof_p = getenv("FPI_JACOBI_PROFILE") ? prof.get() : nullptr;
   EigProb* Pp = dP.get();
-  void* args[] = {&Pp, &nprob, &tot_pairs, &tot_items, &max_rounds, &max_sweeps, &tol, &prof_p};
+  int gch = gchunk, vch = vchunk;
+  void* args[] = {&Pp, &nprob, &tot_pairs, &tot_g, &tot_v, &gch, &vch, &max_rounds, &max_sweeps, &tol,
+                  (void*)&stagnate_below, &prof_p};
   {
     KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
-    FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, 0, s));
+    FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, JACOBI_SMEM, s));
   }
   note_launch(h);
-  // eigenvalues descending + gathered eigenvectors, per problem
   FPI_CUDA(cudaMemcpyAsync(hp.data(), dP.get(), sizeof(EigProb) * nprob, cudaMemcpyDeviceToHost, s));
-  CubTemp tmp(s);
-  for (int i = 0; i < nprob; ++i) {
-    Scratch<double> keys(n[i], s), keys2(n[i], s);
-    Scratch<int32_t> idx(n[i], s), idx2(n[i], s);
-    k_diag_keys<<<grid_for(n[i], 256, h->num_sms * 4), 256, 0, s>>>(n[i], Gall.get() + (hp[i].G - Gall.get()),
-                                                                   npad[i], keys, idx);
-    sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n[i], true, 0, 64, s);
-    k_gather_eig<<<grid_for(n[i] * n[i], 256, G16), 256, 0, s>>>(n[i], hp[i].V, npad[i], idx2, keys2, w[i], V[i],
-                                                                 ldv[i]);
-    note_launch(h, 3);
-  }
-  FPI_LAUNCH_CHECK();
   FPI_CUDA(cudaStreamSynchronize(s));
   if (sweeps_out)
     for (int i = 0; i < nprob; ++i) sweeps_out[i] = hp[i].sweeps;
@@ -548,9 +690,22 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     unsigned long long hq[5];
     FPI_CUDA(cudaMemcpyAsync(hq, prof_p, sizeof(hq), cudaMemcpyDeviceToHost, s));
     FPI_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[jacobi nprob=%d n0=%lld grid=%d] phaseA %.3f (subsolve %.3f)  syncA %.3f  phaseB %.3f  syncB %.3f ms\n",
-            nprob, (long long)n[0], grid, hq[0] * 1e-6, hq[4] * 1e-6, hq[1] * 1e-6, hq[2] * 1e-6, hq[3] * 1e-6);
+    fprintf(stderr, "[jacobi nprob=%d n0=%lld grid=%d gchunk=%d vchunk=%d] sectionA %.3f (subsolve %.3f)  syncA %.3f  "
+            "phaseB %.3f  syncB %.3f ms\n", nprob, (long long)n[0], grid, gchunk, vchunk, hq[0] * 1e-6, hq[4] * 1e-6,
+            hq[1] * 1e-6, hq[2] * 1e-6, hq[3] * 1e-6);
   }
+  // eigenvalues (descending diagonal) and the matching columns of V
+  CubTemp tmp(s);
+  for (int i = 0; i < nprob; ++i) {
+    Scratch<double> keys(n[i], s), keys2(n[i], s);
+    Scratch<int32_t> idx(n[i], s), idx2(n[i], s);
+    k_diag_keys<<<grid_for(n[i], 256, h->num_sms * 4), 256, 0, s>>>(n[i], Gall.get() + goff[i], npad[i], keys, idx);
+    sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n[i], true, 0, 64, s);
+    k_gather_eig<<<grid_for(n[i] * n[i], 256, G16), 256, 0, s>>>(n[i], Vall.get() + goff[i], npad[i], idx2, keys2, w[i],
+                                                                  V[i], ldv[i]);
+    note_launch(h, 3);
+  }
+  FPI_LAUNCH_CHECK();
 }
 
 int sym_eig(fpi_context* h, int64_t n, const double* A, int64_t lda, double* w, double* V, int64_t ldv,
@@ -582,6 +737,8 @@ __global__ void __launch_bounds__(JT) k_subsolve_bench(int iters, double* out) {
   __shared__ PairBuf pbuf;
   build_tables(tb);
   __syncthreads();
+  const bool r0 = iters > 0;  // negative iters: cross steps only (rounds > 0 of a sweep)
+  iters = iters < 0 ? -iters : iters;
   const unsigned long long t0 = gtimer();
   double acc = 0.0;
   for (int it = 0; it < iters; ++it) {
@@ -591,11 +748,11 @@ __global__ void __launch_bounds__(JT) k_subsolve_bench(int iters, double* out) {
       R[a * LDS_ + b] = a == b ? 1.0 : 0.0;
     }
     __syncthreads();
-    acc += subsolve(S, R, tb, pbuf, true, 1e-14, 0.0, false);
+    acc += subsolve(S, R, tb, pbuf, r0, 1e-14, 0.0, false);
   }
   const unsigned long long t1 = gtimer();
   if (threadIdx.x == 0) {
-    out[0] = (double)(t1 - t0) / (iters * 31.0);
+    out[0] = (double)(t1 - t0) / (iters * (r0 ? 31.0 : 16.0));
     out[1] = acc;
   }
 }

@@ -22,16 +22,21 @@ def main():
         w = empty(n)
         V = empty((n, n))
         sw = C.c_int32(0)
-        for rep in range(3):
+        for mixed in ("0", "1"):
+          os.environ["FPI_JACOBI_MIXED"] = mixed
+          for rep in range(3):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             _lib.call("fpi_sym_eig", n, _lib.ptr(dG), n, _lib.ptr(w), _lib.ptr(V), n, C.byref(sw))
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
-        wr = np.linalg.eigvalsh(G)[::-1]
-        err = np.abs(d2h(w) - wr).max() / wr[0]
-        print(f"n={n} inner={os.environ.get('FPI_JACOBI_INNER', '1')} sweeps={sw.value} {dt*1e3:.2f} ms "
-              f"({dt*1e3/sw.value:.3f} ms/sweep) eig err {err:.2e}", flush=True)
+          wr = np.linalg.eigvalsh(G)[::-1]
+          err = np.abs(d2h(w) - wr).max() / wr[0]
+          Vh = d2h(V)
+          orth = np.abs(Vh.T @ Vh - np.eye(n)).max()
+          res = np.abs(G @ Vh - Vh * d2h(w)).max() / wr[0]
+          print(f"n={n} mixed={mixed} sweeps={sw.value} {dt*1e3:.2f} ms "
+                f"eig err {err:.2e} orth {orth:.2e} resid {res:.2e}", flush=True)
 
 
 if __name__ == "__main__":
