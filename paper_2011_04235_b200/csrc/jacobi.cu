@@ -139,15 +139,20 @@ __device__ __forceinline__ double new_diag(bool isp, double c, double sn, double
   return isp ? c * c * app - 2.0 * c * sn * apq + sn * sn * aqq : sn * sn * app + 2.0 * c * sn * apq + c * c * aqq;
 }
 
-// One round's sub-problem: S (JS x JS, stride LDS_) <- J^T S J, R = J.  One barrier per step:
-// the thread that produces a next-step pair's off-diagonal entry also derives that pair's new
-// diagonals from this step's rotations and computes the next rotation.
+// One round's sub-problem: S (JS x JS, stride LDS_) <- J^T S J, R = J.  One barrier per step.
+// Within-block steps (round 0 of a sweep only): thread (k, l) = (tid / 16, tid % 16) updates the
+// 2 x 2 block of pairs k, l, and whichever thread produces a next-step pair's off-diagonal entry
+// also derives that pair's new diagonals and computes its next rotation.  Cross steps (every
+// round, the hot loop): thread tid = 16 d + k owns block (k, k + 1 + d); the producers of the
+// next rotations are exactly d = 0, i.e. lanes 0..15 of warp 0, so the rotation chain (the
+// critical path) runs on one warp while warps 1..7 apply the previous rotations to R.
 __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& pb, bool round0, double tol,
                            double ascale, bool absolute) {
   const int st0 = round0 ? 0 : 15, st_end = 31;
+  const int tid = threadIdx.x;
   // convergence measure of this sub-problem before rotating
   double om = 0.0;
-  for (int e = threadIdx.x; e < JS * JS; e += JT) {
+  for (int e = tid; e < JS * JS; e += JT) {
     const int x = e >> 5, y = e & 31;
     if (x == y) continue;
     const double sxy = S[x * LDS_ + y];
@@ -155,8 +160,8 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
     if (sxy != 0.0) om = fmax(om, den2 > 0.0 ? fabs(sxy) * rsqrt_apx(den2) : 1.0);
   }
   // prologue: rotations of the first step
-  if (threadIdx.x < 16) {
-    const int k = threadIdx.x, p = tb.P[st0][k], q = tb.Q[st0][k];
+  if (tid < 16) {
+    const int k = tid, p = tb.P[st0][k], q = tb.Q[st0][k];
     const double app = S[p * LDS_ + p], aqq = S[q * LDS_ + q], apq = S[p * LDS_ + q];
     double c, sn;
     rotation(app, aqq, apq, tol, ascale, absolute, c, sn);
@@ -164,62 +169,37 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
     pb.c[b][k] = c; pb.s[b][k] = sn; pb.app[b][k] = app; pb.aqq[b][k] = aqq; pb.apq[b][k] = apq;
   }
   __syncthreads();
-  const int k = threadIdx.x >> 4, l = threadIdx.x & 15;
-  for (int st = st0; st < st_end; ++st) {
-    const int b = st & 1, nbuf = b ^ 1;
-    const bool cross = st >= 15;
-    const int t = st - 15;
-    int pk, qk, pl, ql;
-    if (cross) {  // closed form: pair k = (k, 16 + (k + t) % 16)
-      pk = k; qk = 16 + ((k + t) & 15); pl = l; ql = 16 + ((l + t) & 15);
-    } else {
-      pk = tb.P[st][k]; qk = tb.Q[st][k]; pl = tb.P[st][l]; ql = tb.Q[st][l];
-    }
-    const double ck = pb.c[b][k], sk = pb.s[b][k], cl = pb.c[b][l], sl = pb.s[b][l];
-    double o1 = 0.0;
-    if (sk != 0.0 || sl != 0.0) {
-      const double a = S[pk * LDS_ + pl], bb = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
-      const double ra = ck * a - sk * c2, rb = ck * bb - sk * d;
-      const double rc = sk * a + ck * c2, rd = sk * bb + ck * d;
-      const double o0 = ra * cl - rb * sl, o2 = rc * cl - rd * sl, o3 = rc * sl + rd * cl;
-      o1 = ra * sl + rb * cl;
-      S[pk * LDS_ + pl] = o0;
-      S[pk * LDS_ + ql] = o1;
-      S[qk * LDS_ + pl] = o2;
-      S[qk * LDS_ + ql] = o3;
-    } else if (cross && l == ((k + 1) & 15)) {
-      o1 = S[pk * LDS_ + ql];
-    }
-    if (sk != 0.0) {  // R is stored transposed (Rt[col][row]): conflict-free column updates
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int row = l + 16 * h2;
-        const double rp = R[pk * LDS_ + row], rq = R[qk * LDS_ + row];
-        R[pk * LDS_ + row] = ck * rp - sk * rq;
-        R[qk * LDS_ + row] = sk * rp + ck * rq;
+  if (round0) {
+    const int k = tid >> 4, l = tid & 15;
+    for (int st = 0; st < 15; ++st) {
+      const int b = st & 1, nbuf = b ^ 1;
+      const int pk = tb.P[st][k], qk = tb.Q[st][k], pl = tb.P[st][l], ql = tb.Q[st][l];
+      const double ck = pb.c[b][k], sk = pb.s[b][k], cl = pb.c[b][l], sl = pb.s[b][l];
+      if (sk != 0.0 || sl != 0.0) {
+        const double a = S[pk * LDS_ + pl], bb = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
+        const double ra = ck * a - sk * c2, rb = ck * bb - sk * d;
+        const double rc = sk * a + ck * c2, rd = sk * bb + ck * d;
+        S[pk * LDS_ + pl] = ra * cl - rb * sl;
+        S[pk * LDS_ + ql] = ra * sl + rb * cl;
+        S[qk * LDS_ + pl] = rc * cl - rd * sl;
+        S[qk * LDS_ + ql] = rc * sl + rd * cl;
       }
-    }
-    // rotations of the next step, computed by the thread that produced the pair's entry
-    if (st + 1 < st_end) {
-      if (cross) {
-        // next cross pair k is (k, 16 + (k + t + 1) % 16) = (pk, ql) with l = k + 1: entry o1
-        if (l == ((k + 1) & 15)) {
-          const double dx = new_diag(true, ck, sk, pb.app[b][k], pb.aqq[b][k], pb.apq[b][k]);
-          const double dy = new_diag(false, cl, sl, pb.app[b][l], pb.aqq[b][l], pb.apq[b][l]);
-          double c, sn;
-          rotation(dx, dy, o1, tol, ascale, absolute, c, sn);
-          pb.c[nbuf][k] = c; pb.s[nbuf][k] = sn; pb.app[nbuf][k] = dx; pb.aqq[nbuf][k] = dy;
-          pb.apq[nbuf][k] = o1;
+      if (sk != 0.0) {  // R is stored transposed (Rt[col][row]): conflict-free column updates
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int row = l + 16 * h2;
+          const double rp = R[pk * LDS_ + row], rq = R[qk * LDS_ + row];
+          R[pk * LDS_ + row] = ck * rp - sk * rq;
+          R[qk * LDS_ + row] = sk * rp + ck * rq;
         }
-      } else if (k != l) {
-        // within-block steps (round 0 only): generic producer lookup
-        const bool any = (sk != 0.0 || sl != 0.0);
+      }
+      if (k != l) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int x = (e < 2) ? pk : qk, y = (e & 1) ? ql : pl;
           const int kn = tb.pair_of[st + 1][x];
           if (tb.is_p[st + 1][x] && tb.Q[st + 1][kn] == y) {
-            const double axy = any ? S[x * LDS_ + y] : S[x * LDS_ + y];
+            const double axy = S[x * LDS_ + y];
             const double dx = new_diag(e < 2, ck, sk, pb.app[b][k], pb.aqq[b][k], pb.apq[b][k]);
             const double dy = new_diag(!(e & 1), cl, sl, pb.app[b][l], pb.aqq[b][l], pb.apq[b][l]);
             double c, sn;
@@ -227,6 +207,60 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
             pb.c[nbuf][kn] = c; pb.s[nbuf][kn] = sn; pb.app[nbuf][kn] = dx; pb.aqq[nbuf][kn] = dy;
             pb.apq[nbuf][kn] = axy;
           }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // cross steps: pair k = (k, 16 + (k + t) % 16).  Identity rotations (c = 1, s = 0) are applied
+  // as arithmetic (exact), so every load of a step is issued up front without branches.
+  const int k = tid & 15, l = (k + 1 + (tid >> 4)) & 15;
+  const int u = tid - 32;  // R updater index (warps 1..7): items u, u + 224, u + 448 of 16 x 32
+  for (int st = 15; st < st_end; ++st) {
+    const int t = st - 15, b = st & 1, nbuf = b ^ 1;
+    const int pk = k, qk = 16 + ((k + t) & 15), pl = l, ql = 16 + ((l + t) & 15);
+    const double ck = pb.c[b][k], sk = pb.s[b][k], cl = pb.c[b][l], sl = pb.s[b][l];
+    const double a = S[pk * LDS_ + pl], bb = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
+    // the producer's inputs for the new diagonals, loaded before any store of the step
+    const double appk = pb.app[b][k], aqqk = pb.aqq[b][k], apqk = pb.apq[b][k];
+    const double appl = pb.app[b][l], aqql = pb.aqq[b][l], apql = pb.apq[b][l];
+    double rc_[3], rs_[3], rp_[3], rq_[3];
+    int rpi[3], rqi[3];
+    if (u >= 0) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int idx = u + r * (JT - 32);
+        const int kk = (idx >> 5) & 15, row = idx & 31;
+        rpi[r] = kk * LDS_ + row;
+        rqi[r] = (16 + ((kk + t) & 15)) * LDS_ + row;
+        rc_[r] = pb.c[b][kk];
+        rs_[r] = pb.s[b][kk];
+        rp_[r] = R[rpi[r]];
+        rq_[r] = R[rqi[r]];
+      }
+    }
+    const double ra = ck * a - sk * c2, rb = ck * bb - sk * d;
+    const double rc = sk * a + ck * c2, rd = sk * bb + ck * d;
+    const double o1 = ra * sl + rb * cl;
+    S[pk * LDS_ + pl] = ra * cl - rb * sl;
+    S[pk * LDS_ + ql] = o1;
+    S[qk * LDS_ + pl] = rc * cl - rd * sl;
+    S[qk * LDS_ + ql] = rc * sl + rd * cl;
+    if (tid < 16) {
+      // next cross pair k is (k, 16 + (k + t + 1) % 16) = (pk, ql) with l = k + 1: entry o1
+      if (st + 1 < st_end) {
+        const double dx = new_diag(true, ck, sk, appk, aqqk, apqk);
+        const double dy = new_diag(false, cl, sl, appl, aqql, apql);
+        double c, sn;
+        rotation(dx, dy, o1, tol, ascale, absolute, c, sn);
+        pb.c[nbuf][k] = c; pb.s[nbuf][k] = sn; pb.app[nbuf][k] = dx; pb.aqq[nbuf][k] = dy; pb.apq[nbuf][k] = o1;
+      }
+    } else if (u >= 0) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        if (u + r * (JT - 32) < 16 * JS) {
+          R[rpi[r]] = rc_[r] * rp_[r] - rs_[r] * rq_[r];
+          R[rqi[r]] = rs_[r] * rp_[r] + rc_[r] * rq_[r];
         }
       }
     }
@@ -237,8 +271,12 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
 
 // ---- tiles: 32 x 32 FP64 blocks in shared memory (stride LDS_), filled by cp.async
 constexpr int TILE = JS * LDS_;
-constexpr int NTILE = 7;
+constexpr int NST = 4;              // cp.async pipeline depth of the phase B / V runs
+constexpr int NTILE = 2 + 2 * NST;  // G run: Jb, U, NST x {G tile, Ja}; V run: Jb, NST x V tile
 constexpr size_t JACOBI_SMEM = (size_t)NTILE * TILE * sizeof(double);
+#ifndef JACOBI_CTAS_PER_SM
+#define JACOBI_CTAS_PER_SM 2
+#endif
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -283,37 +321,48 @@ __device__ __forceinline__ void mm32(const double* A, const double* B, double (&
   }
 }
 
-// Two-stage cp.async pipeline over the items [t0, t1) of a CTA's run; skip(t) drops identity
-// updates, issue(t, stage) starts the loads of item t, compute(t, stage) consumes them.
-template <class Skip, class Issue, class Compute>
-__device__ __forceinline__ void pipeline(int64_t t0, int64_t t1, Skip skip, Issue issue, Compute compute) {
-  int64_t cur = t0;
-  while (cur < t1 && skip(cur)) ++cur;
-  if (cur >= t1) return;
-  issue(cur, 0);
-  cp_commit();
-  int stage = 0;
-  while (cur < t1) {
-    int64_t nxt = cur + 1;
-    while (nxt < t1 && skip(nxt)) ++nxt;
-    if (nxt < t1) {
-      issue(nxt, stage ^ 1);
-      cp_commit();
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
+// NST-deep cp.async pipeline over the items [t0, t1) of one run (a fixed block column pb):
+// pre() starts the run-constant loads, skip(t) drops identity updates, issue(t, stage) starts the
+// loads of item t, compute(t, stage) consumes them.  Exactly one commit group per item slot, so
+// wait_group<NST - 1> always retires the oldest item.
+template <class Pre, class Skip, class Issue, class Compute>
+__device__ __forceinline__ void pipeline(int64_t t0, int64_t t1, Pre pre, Skip skip, Issue issue, Compute compute) {
+  auto adv = [&](int64_t x) {
+    while (x < t1 && skip(x)) ++x;
+    return x;
+  };
+  int64_t ni = adv(t0), nc = ni;
+  if (nc >= t1) return;
+  int issued = 0, consumed = 0;
+  pre();
+  for (int p = 0; p < NST - 1; ++p) {
+    if (ni < t1) {
+      issue(ni, issued % NST);
+      ++issued;
+      ni = adv(ni + 1);
     }
-    __syncthreads();
-    compute(cur, stage);
-    __syncthreads();
-    cur = nxt;
-    stage ^= 1;
+    cp_commit();
   }
+  while (nc < t1) {
+    if (ni < t1) {
+      issue(ni, issued % NST);
+      ++issued;
+      ni = adv(ni + 1);
+    }
+    cp_commit();
+    cp_wait<NST - 1>();
+    __syncthreads();
+    compute(nc, consumed % NST);
+    __syncthreads();
+    ++consumed;
+    nc = adv(nc + 1);
+  }
+  cp_wait<0>();
 }
 
 // One eigenproblem of a batch (device descriptor).
 struct EigProb {
-  int nb;              // padded block count (even); npairs = nb / 2 = 32-row tiles of the panel
+  int nb;              // padded block count (even); np = nb / 2 pairs = 32-row tiles of the panel
   int done;            // converged (written on the device)
   int sweeps;
   int vround;          // round (within its sweep) whose rotations V still owes, -1: none
@@ -321,8 +370,8 @@ struct EigProb {
   int pad_;
   double* G;           // npad x npad
   double* V;           // npad x npad
-  double* Jbuf;        // 2 x npairs x JS x JS (by round parity)
-  int* jflag;          // 2 x npairs: rotation of the pair is not the identity
+  double* Jbuf;        // 2 x np x JS x JS (by round parity)
+  int* jflag;          // 2 x np: rotation of the pair is not the identity
   unsigned long long* offmax;  // per sweep
   const double* abs_scale;     // null: relative criterion
   int64_t pair_off, gitem_off, vitem_off;  // prefix sums over the batch (phase A pairs, G runs, V runs)
@@ -338,41 +387,88 @@ __device__ __forceinline__ int find_prob(const EigProb* P, int nprob, int64_t id
   return lo;
 }
 
-// upper-triangle block index t -> (pa <= pb)
-__device__ __forceinline__ void tri_pair(int64_t t, int& pa, int& pb) {
-  int b = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-  while ((int64_t)(b + 1) * (b + 2) / 2 <= t) ++b;
-  while ((int64_t)b * (b + 1) / 2 > t) --b;
-  pb = b;
-  pa = (int)(t - (int64_t)b * (b + 1) / 2);
+// G runs of one problem: block column pb holds pa = 0..pb in runs of c, so the runs of columns
+// < P number F(P) = P + c q (q - 1) / 2 + r q with P = q c + r.
+__host__ __device__ __forceinline__ int64_t g_runs_before(int64_t P, int64_t c) {
+  const int64_t q = P / c, r = P % c;
+  return P + c * q * (q - 1) / 2 + r * q;
+}
+__device__ __forceinline__ void g_run(int64_t j, int np, int c, int& pb, int& chunk) {
+  int lo = 0, hi = np - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (g_runs_before(mid, c) <= j) lo = mid; else hi = mid - 1;
+  }
+  pb = lo;
+  chunk = (int)(j - g_runs_before(lo, c));
 }
 
-// V[:, P'] <- V[:, P'] R_P' for the pending round of problem pr_, tiles [t0, t1) of np x np (pair-major).
-__device__ void v_run(const EigProb& pr_, int64_t t0, int64_t t1, double* sm, int warp, int lane) {
+// V[:, P'] <- V[:, P'] R_P' for the pending round of problem pr_: row tiles [r0, r1) of column pb.
+__device__ void v_run(const EigProb& pr_, int pb, int r0, int r1, double* sm, int warp, int lane) {
   const int nb = pr_.nb, np = nb / 2, round = pr_.vround;
+  if (!pr_.jflag[pr_.vpar * np + pb]) return;
   const int64_t ld = (int64_t)nb * JB;
-  const double* Jb0 = pr_.Jbuf + (int64_t)pr_.vpar * np * JS * JS;
-  const int* fl = pr_.jflag + pr_.vpar * np;
+  const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
   double* V = pr_.V;
+  double* Jb = sm;
+  double* stg = sm + TILE;
   pipeline(
-      t0, t1, [&](int64_t t) { return fl[t / np] == 0; },
-      [&](int64_t t, int st) {
-        const int pb = (int)(t / np), rt = (int)(t % np);
-        const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
-        tile_async(sm + (2 * st) * TILE, V, ld, (int64_t)rt * JS, 0, 0, bi, bj);
-        j_async(sm + (2 * st + 1) * TILE, Jb0 + (int64_t)pb * JS * JS);
-      },
-      [&](int64_t t, int st) {
-        const int pb = (int)(t / np), rt = (int)(t % np);
-        const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
+      r0, r1, [&] { j_async(Jb, pr_.Jbuf + ((int64_t)pr_.vpar * np + pb) * JS * JS); },
+      [&](int64_t) { return false; },
+      [&](int64_t rt, int st) { tile_async(stg + st * TILE, V, ld, rt * JS, 0, 0, bi, bj); },
+      [&](int64_t rt, int st) {
         double acc[2][2];
-        mm32<false>(sm + (2 * st) * TILE, sm + (2 * st + 1) * TILE, acc, warp, lane);
+        mm32<false>(stg + st * TILE, Jb, acc, warp, lane);
         const int g = lane >> 2, tq = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
-        const int64_t row = (int64_t)rt * JS + m0 + g;
+        const int64_t row = rt * JS + m0 + g;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int c0 = n0 + 8 * j + 2 * tq;
           *reinterpret_cast<double2*>(V + row * ld + sub_to_global(c0, bi, bj)) = make_double2(acc[j][0], acc[j][1]);
+        }
+      });
+}
+
+// G'[Pa, Pb] = Ja^T G[Pa, Pb] Jb for pa in [a0, a1) (<= pb), written to both triangles.
+__device__ void g_run_exec(const EigProb& pr_, int round, int par, int pb, int a0, int a1, double* sm, int warp,
+                           int lane) {
+  const int nb = pr_.nb, np = nb / 2;
+  const int64_t ld = (int64_t)nb * JB;
+  const double* J0 = pr_.Jbuf + (int64_t)par * np * JS * JS;
+  const int* fl = pr_.jflag + par * np;
+  const bool fb = fl[pb] != 0;
+  const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
+  double* G = pr_.G;
+  double* Jb = sm;
+  double* Us = sm + TILE;
+  double* stg = sm + 2 * TILE;
+  pipeline(
+      a0, a1, [&] { j_async(Jb, J0 + (int64_t)pb * JS * JS); }, [&](int64_t pa) { return !fb && fl[pa] == 0; },
+      [&](int64_t pa, int st) {
+        const int ai = rr_block((int)pa, round, nb), aj = rr_block(nb - 1 - (int)pa, round, nb);
+        tile_async(stg + (2 * st) * TILE, G, ld, -1, ai, aj, bi, bj);
+        j_async(stg + (2 * st + 1) * TILE, J0 + pa * JS * JS);
+      },
+      [&](int64_t pa, int st) {
+        const int ai = rr_block((int)pa, round, nb), aj = rr_block(nb - 1 - (int)pa, round, nb);
+        const int g = lane >> 2, tq = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
+        double acc[2][2];
+        mm32<false>(stg + (2 * st) * TILE, Jb, acc, warp, lane);  // U = G Jb
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          *reinterpret_cast<double2*>(Us + (m0 + g) * LDS_ + n0 + 8 * j + 2 * tq) = make_double2(acc[j][0], acc[j][1]);
+        __syncthreads();
+        mm32<true>(stg + (2 * st + 1) * TILE, Us, acc, warp, lane);  // G' = Ja^T U
+        const int64_t row = sub_to_global(m0 + g, ai, aj);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int c0 = n0 + 8 * j + 2 * tq;
+          const int64_t col = sub_to_global(c0, bi, bj);
+          *reinterpret_cast<double2*>(G + row * ld + col) = make_double2(acc[j][0], acc[j][1]);
+          if (pa != pb) {
+            G[col * ld + row] = acc[j][0];
+            G[(col + 1) * ld + row] = acc[j][1];
+          }
         }
       });
 }
@@ -427,15 +523,17 @@ __device__ void section_a(EigProb* P, int nprob, int64_t total_pairs, int64_t to
       const int pi = find_prob(P, nprob, vi, 2);
       const EigProb& pr_ = P[pi];
       if (pr_.vround < 0) continue;
-      const int64_t np = pr_.nb / 2;
-      const int64_t t0 = (vi - pr_.vitem_off) * vchunk;
-      const int64_t t1 = t0 + vchunk < np * np ? t0 + vchunk : np * np;
-      v_run(pr_, t0, t1, sm, warp, lane);
+      const int np = pr_.nb / 2;
+      const int per = (np + vchunk - 1) / vchunk;
+      const int64_t j = vi - pr_.vitem_off;
+      const int pb = (int)(j / per), c = (int)(j % per);
+      const int r0 = c * vchunk, r1 = r0 + vchunk < np ? r0 + vchunk : np;
+      v_run(pr_, pb, r0, r1, sm, warp, lane);
     }
   }
 }
 
-__global__ void __launch_bounds__(JT, 3)
+__global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
     k_jacobi(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems, int gchunk,
              int vchunk, int max_rounds, int max_sweeps, double tol, double stagnate_below, unsigned long long* prof) {
   cg::grid_group grid = cg::this_grid();
@@ -460,57 +558,10 @@ __global__ void __launch_bounds__(JT, 3)
         const EigProb& pr_ = P[pi];
         const int nb = pr_.nb;
         if (pr_.done || round >= nb - 1) continue;
-        const int np = nb / 2;
-        const int64_t ld = (int64_t)nb * JB;
-        const int64_t ntri = (int64_t)np * (np + 1) / 2;
-        const int64_t ta = (it - pr_.gitem_off) * gchunk;
-        const int64_t tb1 = ta + gchunk < ntri ? ta + gchunk : ntri;
-        const double* J0 = pr_.Jbuf + (int64_t)par * np * JS * JS;
-        const int* fl = pr_.jflag + par * np;
-        double* G = pr_.G;
-        double* Us = sm + 6 * TILE;
-        pipeline(
-            ta, tb1,
-            [&](int64_t t) {
-              int pa, pb;
-              tri_pair(t, pa, pb);
-              return fl[pa] == 0 && fl[pb] == 0;
-            },
-            [&](int64_t t, int st) {
-              int pa, pb;
-              tri_pair(t, pa, pb);
-              const int ai = rr_block(pa, round, nb), aj = rr_block(nb - 1 - pa, round, nb);
-              const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
-              tile_async(sm + (3 * st) * TILE, G, ld, -1, ai, aj, bi, bj);
-              j_async(sm + (3 * st + 1) * TILE, J0 + (int64_t)pa * JS * JS);
-              j_async(sm + (3 * st + 2) * TILE, J0 + (int64_t)pb * JS * JS);
-            },
-            [&](int64_t t, int st) {
-              int pa, pb;
-              tri_pair(t, pa, pb);
-              const int ai = rr_block(pa, round, nb), aj = rr_block(nb - 1 - pa, round, nb);
-              const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
-              const int g = lane >> 2, tq = lane & 3, m0 = 8 * (warp & 3), n0 = 16 * (warp >> 2);
-              double acc[2][2];
-              mm32<false>(sm + (3 * st) * TILE, sm + (3 * st + 2) * TILE, acc, warp, lane);  // U = G Jb
-#pragma unroll
-              for (int j = 0; j < 2; ++j)
-                *reinterpret_cast<double2*>(Us + (m0 + g) * LDS_ + n0 + 8 * j + 2 * tq) =
-                    make_double2(acc[j][0], acc[j][1]);
-              __syncthreads();
-              mm32<true>(sm + (3 * st + 1) * TILE, Us, acc, warp, lane);  // G' = Ja^T U
-              const int64_t row = sub_to_global(m0 + g, ai, aj);
-#pragma unroll
-              for (int j = 0; j < 2; ++j) {
-                const int c0 = n0 + 8 * j + 2 * tq;
-                const int64_t col = sub_to_global(c0, bi, bj);
-                *reinterpret_cast<double2*>(G + row * ld + col) = make_double2(acc[j][0], acc[j][1]);
-                if (pa != pb) {
-                  G[col * ld + row] = acc[j][0];
-                  G[(col + 1) * ld + row] = acc[j][1];
-                }
-              }
-            });
+        int pb, chunk;
+        g_run(it - pr_.gitem_off, nb / 2, gchunk, pb, chunk);
+        const int a0 = chunk * gchunk, a1 = a0 + gchunk < pb + 1 ? a0 + gchunk : pb + 1;
+        g_run_exec(pr_, round, par, pb, a0, a1, sm, warp, lane);
       }
       const unsigned long long t3 = prof ? gtimer() : 0;
       // V owes this round's rotations (read in the next section A, after the barrier below)
@@ -633,18 +684,37 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   int grid = max_blocks;
   if (const char* e = getenv("FPI_JACOBI_GRID")) grid = atoi(e) < max_blocks ? atoi(e) : max_blocks;
   if (grid < 1) grid = 1;
-  // run lengths: G blocks spread over the whole grid; V tiles over the CTAs phase A leaves idle
-  const int gchunk = (int)((tot_tri + grid - 1) / grid);
+  // run lengths: G blocks (per block column) spread over the whole grid; V tiles over the CTAs
+  // phase A leaves idle
+  // (smallest run lengths whose run count fits one wave)
   const int64_t vcta = grid - tot_pairs > grid / 4 ? grid - tot_pairs : grid / 4 + 1;
-  const int vchunk = (int)((tot_vt + vcta - 1) / vcta);
+  int gchunk = (int)((tot_tri + grid - 1) / grid), vchunk = (int)((tot_vt + vcta - 1) / vcta);
+  auto runs = [&](int gc, int vc, int64_t& ng, int64_t& nv) {
+    ng = nv = 0;
+    for (int i = 0; i < nprob; ++i) {
+      const int64_t np = hp[i].nb / 2;
+      ng += g_runs_before(np, gc);
+      nv += np * ((np + vc - 1) / vc);
+    }
+  };
+  for (int64_t ng, nv;;) {
+    runs(gchunk, 1 << 30, ng, nv);
+    if (ng <= grid || gchunk >= max_rounds) break;
+    ++gchunk;
+  }
+  for (int64_t ng, nv;;) {
+    runs(1 << 30, vchunk, ng, nv);
+    if (nv <= vcta || vchunk >= max_rounds) break;
+    ++vchunk;
+  }
   int64_t tot_g = 0, tot_v = 0;
   for (int i = 0; i < nprob; ++i) {
     const int64_t np = hp[i].nb / 2;
     hp[i].pair_off = i ? hp[i - 1].pair_off + hp[i - 1].nb / 2 : 0;
     hp[i].gitem_off = tot_g;
     hp[i].vitem_off = tot_v;
-    tot_g += (np * (np + 1) / 2 + gchunk - 1) / gchunk;
-    tot_v += (np * np + vchunk - 1) / vchunk;
+    tot_g += g_runs_before(np, gchunk);
+    tot_v += np * ((np + vchunk - 1) / vchunk);
   }
   Scratch<double> Gall(gsz, s), Vall(gsz, s), Jall(jsz, s), scales(nprob, s);
   Scratch<int> fall(fsz, s);
