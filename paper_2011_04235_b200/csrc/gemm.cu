@@ -4,15 +4,22 @@
 //
 //   C = alpha * op(A) * op(B) + beta * C,   all row-major, op = identity / transpose
 //
-// CTA tile 128 x 128 x 16, 8 warps (2 x 4), warp tile 64 x 32 = 8 x 4 DMMA
-// tiles (64 accumulator doubles per thread).  Operands stream global -> smem
-// with a 3-stage cp.async ring; the smem layouts are padded so every
-// fragment load is bank-conflict free for all four transpose combinations.
-// Split-K (deterministic: partial tiles + ordered reduction) covers the
-// tall-skinny Gram / projection shapes where M x N alone cannot fill 148 SMs.
+// CTA tile 128 x 64 x 16, 8 warps (4 x 2), warp tile 32 x 32 = 4 x 4 DMMA tiles
+// (32 accumulator doubles per thread), two CTAs per SM: 4 warps per SM
+// sub-partition keep the DMMA pipe fed, and while one CTA sits at its k-tile
+// barrier the other keeps issuing.  Operands stream global -> smem with a
+// 3-stage cp.async ring (16-byte copies when the operands are 16-byte aligned
+// along their contiguous dimension, 8-byte otherwise); the smem layouts are
+// padded so every fragment load is bank-conflict free for all four transpose
+// combinations.  Split-K (deterministic: partial tiles + ordered reduction)
+// covers the tall-skinny Gram / projection shapes where M x N alone cannot fill
+// 148 SMs; the split count minimises a wave-quantisation + reduction model.
 // Used for: U.Sigma x X1 and Q^T inner (svd.py:133,135 dense parts), the
 // Gram matrices of CholeskyQR and of the small SVD, the lifts
 // (pinv.py:169,206) and V (Sigma+ U^T Y) (pinv.py:81).
+#include <cstdint>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "capi_guard.cuh"
 #include "gemm.cuh"
@@ -21,7 +28,8 @@
 namespace fpi {
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, NT = 256;
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, NT = 256;
+constexpr int WARPS_N = BN / 32;  // warp grid (BM / 32) x (BN / 32)
 constexpr int PAD = 4;
 // smem strides (doubles)
 constexpr int LDA_MK = BK + PAD;   // As[m][k]
@@ -31,11 +39,18 @@ constexpr int LDB_NK = BK + PAD;   // Bs[n][k]
 constexpr int A_STAGE = (BM * LDA_MK > BK * LDA_KM) ? BM * LDA_MK : BK * LDA_KM;
 constexpr int B_STAGE = (BN * LDB_NK > BK * LDB_KN) ? BN * LDB_NK : BK * LDB_KN;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+static_assert((BM / 32) * (BN / 32) * 32 == NT, "one warp per 32 x 32 warp tile");
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
   unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
   int sz = pred ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
+}
+// 16-byte copy of up to two doubles (nvalid in 0..2; the rest zero-filled)
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, int nvalid) {
+  unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = nvalid * 8;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(sz));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -49,52 +64,64 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// Load one BMxBK tile of op(A) and one BKxBN tile of op(B) into stage buffers.
-template <bool TA, bool TB>
+// Load one BM x BK tile of op(A) and one BK x BN tile of op(B) into stage buffers.  V16: pairs of
+// doubles along each operand's contiguous dimension (16-byte aligned by the caller's check).
+template <bool TA, bool TB, bool V16>
 __device__ __forceinline__ void load_tiles(double* As, double* Bs, const double* A, int64_t lda, const double* B,
                                            int64_t ldb, int64_t M, int64_t N, int64_t K, int64_t m0, int64_t n0,
                                            int64_t k0) {
   const int tid = threadIdx.x;
-  // A: 128 x 16 doubles = 2048 elements, 8 per thread
+  constexpr int W = V16 ? 2 : 1;
 #pragma unroll
-  for (int i = 0; i < (BM * BK) / NT; ++i) {
-    int e = tid + i * NT;
-    if (!TA) {  // A[m][k], k contiguous
-      int m = e / BK, k = e % BK;
-      int64_t gm = m0 + m, gk = k0 + k;
-      bool p = gm < M && gk < K;
-      cp_async8(As + m * LDA_MK + k, p ? A + gm * lda + gk : A, p);
-    } else {    // stored K x M, m contiguous
-      int k = e / BM, m = e % BM;
-      int64_t gm = m0 + m, gk = k0 + k;
-      bool p = gm < M && gk < K;
-      cp_async8(As + k * LDA_KM + m, p ? A + gk * lda + gm : A, p);
+  for (int i = 0; i < (BM * BK) / (NT * W); ++i) {
+    const int e = (tid + i * NT) * W;
+    int m, k;
+    if (!TA) { m = e / BK; k = e % BK; } else { k = e / BM; m = e % BM; }
+    const int64_t gm = m0 + m, gk = k0 + k;
+    double* dst = TA ? As + k * LDA_KM + m : As + m * LDA_MK + k;
+    if (V16) {
+      // contiguous dimension: k (A[m][k]) or m (A^T stored K x M)
+      const int64_t lim = TA ? M - gm : K - gk;
+      const bool row_ok = TA ? gk < K : gm < M;
+      const int nv = !row_ok || lim <= 0 ? 0 : (lim >= 2 ? 2 : 1);
+      cp_async16(dst, nv ? (TA ? A + gk * lda + gm : A + gm * lda + gk) : A, nv);
+    } else {
+      const bool p = gm < M && gk < K;
+      cp_async8(dst, p ? (TA ? A + gk * lda + gm : A + gm * lda + gk) : A, p);
     }
   }
 #pragma unroll
-  for (int i = 0; i < (BN * BK) / NT; ++i) {
-    int e = tid + i * NT;
-    if (!TB) {  // B[k][n], n contiguous
-      int k = e / BN, n = e % BN;
-      int64_t gn = n0 + n, gk = k0 + k;
-      bool p = gn < N && gk < K;
-      cp_async8(Bs + k * LDB_KN + n, p ? B + gk * ldb + gn : B, p);
-    } else {    // stored N x K, k contiguous
-      int n = e / BK, k = e % BK;
-      int64_t gn = n0 + n, gk = k0 + k;
-      bool p = gn < N && gk < K;
-      cp_async8(Bs + n * LDB_NK + k, p ? B + gn * ldb + gk : B, p);
+  for (int i = 0; i < (BN * BK) / (NT * W); ++i) {
+    const int e = (tid + i * NT) * W;
+    int n, k;
+    if (!TB) { k = e / BN; n = e % BN; } else { n = e / BK; k = e % BK; }
+    const int64_t gn = n0 + n, gk = k0 + k;
+    double* dst = TB ? Bs + n * LDB_NK + k : Bs + k * LDB_KN + n;
+    if (V16) {
+      const int64_t lim = TB ? K - gk : N - gn;
+      const bool row_ok = TB ? gn < N : gk < K;
+      const int nv = !row_ok || lim <= 0 ? 0 : (lim >= 2 ? 2 : 1);
+      cp_async16(dst, nv ? (TB ? B + gn * ldb + gk : B + gk * ldb + gn) : B, nv);
+    } else {
+      const bool p = gn < N && gk < K;
+      cp_async8(dst, p ? (TB ? B + gn * ldb + gk : B + gk * ldb + gn) : B, p);
     }
   }
 }
 
-template <bool TA, bool TB>
-__global__ void __launch_bounds__(NT, 1)
+// sym: C is symmetric (A == B, op(A) = op(B)^T).  Tiles entirely above the diagonal are skipped;
+// every computed element (r, c) with c <= r is stored, and mirrored to (c, r) when c < r, so each
+// upper element has exactly one (deterministic) writer.
+__host__ __device__ __forceinline__ bool tile_above_diag(int64_t bx, int64_t by) {
+  return bx * BN >= (by + 1) * BM;
+}
+
+template <bool TA, bool TB, bool V16>
+__global__ void __launch_bounds__(NT, 2)
     k_gemm(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
            const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
            int64_t k_per_split, double* __restrict__ partial, int sym) {
-  // sym: C is symmetric (A == B, op(A) = op(B)^T): only tiles on / below the diagonal are computed
-  if (sym && blockIdx.x > blockIdx.y) return;
+  if (sym && tile_above_diag(blockIdx.x, blockIdx.y)) return;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + STAGES * A_STAGE;
@@ -103,12 +130,12 @@ __global__ void __launch_bounds__(NT, 1)
   const int64_t ke = kb + k_per_split < K ? kb + k_per_split : K;
   const int64_t ntiles = ke > kb ? (ke - kb + BK - 1) / BK : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;  // 2 x 4 warps
+  const int wm = (warp / WARPS_N) * 32, wn = (warp % WARPS_N) * 32;
   const int g = lane >> 2, t = lane & 3;
 
-  double acc[8][4][2];
+  double acc[4][4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -116,7 +143,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ntiles)
-      load_tiles<TA, TB>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, ke, m0, n0, kb + s * BK);
+      load_tiles<TA, TB, V16>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, M, N, ke, m0, n0, kb + s * BK);
     cp_async_commit();
   }
   for (int64_t kt = 0; kt < ntiles; ++kt) {
@@ -127,17 +154,17 @@ __global__ void __launch_bounds__(NT, 1)
       int64_t nk = kt + STAGES - 1;
       int slot = (int)(nk % STAGES);
       if (nk < ntiles)
-        load_tiles<TA, TB>(As + slot * A_STAGE, Bs + slot * B_STAGE, A, lda, B, ldb, M, N, ke, m0, n0,
-                           kb + nk * BK);
+        load_tiles<TA, TB, V16>(As + slot * A_STAGE, Bs + slot * B_STAGE, A, lda, B, ldb, M, N, ke, m0, n0,
+                                kb + nk * BK);
       cp_async_commit();
     }
     const double* as = As + (kt % STAGES) * A_STAGE;
     const double* bs = Bs + (kt % STAGES) * B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[8], bf[4];
+      double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 4; ++i) {
         int m = wm + i * 8 + g;
         af[i] = TA ? as[(kk + t) * LDA_KM + m] : as[m * LDA_MK + kk + t];
       }
@@ -147,7 +174,7 @@ __global__ void __launch_bounds__(NT, 1)
         bf[j] = TB ? bs[n * LDB_NK + kk + t] : bs[(kk + t) * LDB_KN + n];
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
@@ -158,20 +185,20 @@ __global__ void __launch_bounds__(NT, 1)
   if (partial) {
     double* P = partial + (int64_t)blockIdx.z * M * N;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 4; ++i) {
       int64_t r = m0 + wm + i * 8 + g;
       if (r >= M) continue;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         int64_t c = n0 + wn + j * 8 + 2 * t;
-        if (c < N) P[r * N + c] = acc[i][j][0];
-        if (c + 1 < N) P[r * N + c + 1] = acc[i][j][1];
+        if (c < N && (!sym || c <= r)) P[r * N + c] = acc[i][j][0];
+        if (c + 1 < N && (!sym || c + 1 <= r)) P[r * N + c + 1] = acc[i][j][1];
       }
     }
     return;
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 4; ++i) {
     int64_t r = m0 + wm + i * 8 + g;
     if (r >= M) continue;
 #pragma unroll
@@ -179,12 +206,13 @@ __global__ void __launch_bounds__(NT, 1)
       int64_t c = n0 + wn + j * 8 + 2 * t;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        if (c + q < N) {
+        const int64_t cq = c + q;
+        if (cq < N && (!sym || cq <= r)) {
           double v = alpha * acc[i][j][q];
-          double* dst = C + r * ldc + c + q;
+          double* dst = C + r * ldc + cq;
           *dst = beta == 0.0 ? v : v + beta * *dst;
-          if (sym && blockIdx.x < blockIdx.y) {  // mirror strictly-lower tiles
-            double* mir = C + (c + q) * ldc + r;
+          if (sym && cq < r) {
+            double* mir = C + cq * ldc + r;
             *mir = beta == 0.0 ? v : v + beta * *mir;
           }
         }
@@ -197,8 +225,8 @@ __global__ void k_reduce_split(int64_t M, int64_t N, int splits, const double* _
                                double beta, double* __restrict__ C, int64_t ldc, int sym) {
   FPI_GRID_STRIDE(e, M * N) {
     int64_t r = e / N, c = e - r * N;
-    // upper tiles of a symmetric product were not computed: read the mirrored partials
-    const int64_t src = (sym && (c / BN) > (r / BM)) ? c * N + r : e;
+    // upper elements of a symmetric product were not computed: read the mirrored partials
+    const int64_t src = (sym && c > r) ? c * N + r : e;
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += P[(int64_t)z * M * N + src];
     double* dst = C + r * ldc + c;
@@ -215,30 +243,52 @@ __global__ void k_scale(int64_t M, int64_t N, double beta, double* __restrict__ 
   }
 }
 
-template <bool TA, bool TB>
+// Split count: minimise (waves of CTAs) x (K per CTA) + the partial-tile reduction traffic.
+int choose_splits(int64_t tiles, int64_t M, int64_t N, int64_t K, int num_sms) {
+  const int64_t slots = 2LL * num_sms;  // resident CTAs
+  const double cta_flops = 36.0e12 / (double)slots, red_bw = 4.0e12;
+  int best = 1;
+  double best_t = 1e300;
+  const int64_t max_splits = K / (BK * 8) < 64 ? K / (BK * 8) : 64;
+  for (int sp = 1; sp <= (max_splits > 1 ? max_splits : 1); ++sp) {
+    const int64_t kps = ((K + sp - 1) / sp + BK - 1) / BK * BK;
+    const int64_t real = (K + kps - 1) / kps;
+    if (real != sp) continue;
+    const int64_t waves = (tiles * sp + slots - 1) / slots;
+    double t = (double)waves * 2.0 * BM * BN * (double)kps / cta_flops;
+    if (sp > 1) t += (double)M * N * (sp + 1) * 8.0 / red_bw;
+    if (t < best_t * 0.98) {
+      best_t = t;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+template <bool TA, bool TB, bool V16>
 void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
             const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int sym) {
   static bool attr_set = false;
   if (!attr_set) {
-    FPI_CUDA(cudaFuncSetAttribute(k_gemm<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+    FPI_CUDA(cudaFuncSetAttribute(k_gemm<TA, TB, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
     attr_set = true;
   }
   cudaStream_t s = h->stream;
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
-  const int64_t tiles = sym ? tm * (tm + 1) / 2 : tm * tn;
-  int splits = 1;
-  const int64_t want = 2LL * h->num_sms;
-  if (tiles < want && K >= 4 * BK * 8) {
-    splits = (int)((want + tiles - 1) / tiles);
-    int64_t max_splits = K / (BK * 8);
-    if (splits > max_splits) splits = (int)max_splits;
-    if (splits > 64) splits = 64;
-    if (splits < 1) splits = 1;
+  int64_t tiles = tm * tn;
+  if (sym) {
+    tiles = 0;
+    for (int64_t by = 0; by < tm; ++by) {
+      const int64_t lim = ((by + 1) * BM + BN - 1) / BN;  // bx < lim are not entirely above the diagonal
+      tiles += lim < tn ? lim : tn;
+    }
   }
+  int splits = choose_splits(tiles, M, N, K, h->num_sms);
+  if (const char* e = getenv("FPI_GEMM_SPLITS")) splits = atoi(e) > 0 ? atoi(e) : splits;
   FPI_REQUIRE(tm < 65536 && tn < (1LL << 31), FPI_ECAPACITY, "gemm grid too large");
   if (splits == 1) {
     dim3 grid((unsigned)tn, (unsigned)tm, 1);
-    k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, K, nullptr, sym);
+    k_gemm<TA, TB, V16><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, K, nullptr, sym);
     FPI_LAUNCH_CHECK();
     note_launch(h);
     return;
@@ -248,11 +298,20 @@ void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const
   splits = (int)((K + kps - 1) / kps);
   Scratch<double> part((size_t)splits * M * N, s);
   dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)splits);
-  k_gemm<TA, TB><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps, part, sym);
+  k_gemm<TA, TB, V16><<<grid, NT, SMEM_BYTES, s>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kps, part, sym);
   k_reduce_split<<<grid_for(M * N, 256, (int64_t)h->num_sms * 16), 256, 0, s>>>(M, N, splits, part, alpha, beta, C,
                                                                                  ldc, sym);
   FPI_LAUNCH_CHECK();
   note_launch(h, 2);
+}
+
+template <bool TA, bool TB>
+void launch_any(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int sym) {
+  const bool v16 = ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) && lda % 2 == 0 && ldb % 2 == 0 &&
+                   !getenv("FPI_GEMM_NO_V16");
+  if (v16) launch<TA, TB, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym);
+  else launch<TA, TB, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym);
 }
 
 }  // namespace
@@ -268,10 +327,10 @@ void gemm(fpi_context* h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
   }
   KTimer kt(h, "gemm_f64_dmma", (sy ? 1.0 : 2.0) * (double)M * (double)N * (double)K,
             8.0 * ((double)M * K + (double)K * N + (beta == 0.0 ? 1.0 : 2.0) * (double)M * N));
-  if (!ta && !tb) launch<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
-  else if (!ta && tb) launch<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sy);
-  else if (ta && !tb) launch<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sy);
-  else launch<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+  if (!ta && !tb) launch_any<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+  else if (!ta && tb) launch_any<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sy);
+  else if (ta && !tb) launch_any<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sy);
+  else launch_any<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
 }
 
 }  // namespace fpi

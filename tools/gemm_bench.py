@@ -13,6 +13,10 @@ SHAPES = [  # (name, ta, tb, M, N, K)
     ("Z_VtT_WT_c4", 1, 1, 50000, 4000, 500),
     ("gram_Yt_c4", 1, 0, 1000, 1000, 10684),
     ("square_4096", 0, 0, 4096, 4096, 4096),
+    ("Y_eq_U_X_c5", 0, 0, 2000000, 2000, 1000),
+    ("gram_YtY_c5", 1, 0, 2000, 2000, 2000000),
+    ("YtU_c5", 1, 0, 2000, 1000, 2000000),
+    ("U_eq_Y_X_c5", 0, 0, 2000000, 1000, 2000),
 ]
 
 
@@ -37,8 +41,16 @@ def main():
         ms = e0.elapsed_time(e1) / reps
         ref = (A.t() if ta else A) @ (B.t() if tb else B)
         err = (C - ref).abs().max().item() / ref.abs().max().item()
-        print(f"{name:16s} M={M} N={N} K={K}: {ms:.3f} ms  {2*M*N*K/ms/1e9:.2f} TFLOP/s  relerr {err:.1e}", flush=True)
-        del A, B, C, ref
+        e0.record()
+        for _ in range(reps):
+            torch.matmul(A.t() if ta else A, B.t() if tb else B, out=C)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_cublas = e0.elapsed_time(e1) / reps
+        print(f"{name:16s} M={M} N={N} K={K}: {ms:.3f} ms  {2*M*N*K/ms/1e9:.2f} TFLOP/s  relerr {err:.1e}  "
+              f"(cuBLAS {2*M*N*K/ms_cublas/1e9:.2f} TFLOP/s)", flush=True)
+        A = B = C = ref = None
+        A = B = C = ref = None
 
 
 if __name__ == "__main__":
