@@ -6,7 +6,21 @@
 #include "capi_guard.cuh"
 #include "instrument.cuh"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace fpi {
+void trace_point(fpi_context* h, const char* label) {
+  static const bool on = getenv("FPI_TRACE") != nullptr;
+  if (!on) return;
+  static auto last = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(h->stream);
+  const auto now = std::chrono::steady_clock::now();
+  fprintf(stderr, "[trace] %-28s %9.3f ms\n", label, std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
+
 
 struct TimingState {
   struct Rec {

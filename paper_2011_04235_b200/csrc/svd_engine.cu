@@ -23,6 +23,7 @@
 #include "cub_util.cuh"
 #include "gemm.cuh"
 #include "linalg.cuh"
+#include "instrument.cuh"
 #include "sparse.cuh"
 #include "spmm.cuh"
 #include "svd_engine.cuh"
@@ -543,12 +544,17 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
     dense_svd(h, p, q, Dn, q, rank, U, sigma, Vt, diag);
     return;
   }
+  trace_point(h, "rsvd:start");
   Scratch<double> X(q * k, s), B(p * k, s), Gm(k * k, s), Linv(k * k, s);
+  trace_point(h, "rsvd:alloc X,B");
   sketch_normal(h, seed, q, k, X, k);   // svd.py:131-132
+  trace_point(h, "rsvd:sketch");
   op.apply(h, X, k, B);                 // svd.py:133
+  trace_point(h, "rsvd:B = M X");
   X.release();
   // CholeskyQR: B^T B = L L^T, Q = B L^-T   (svd.py:134)
   gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k, /*sym=*/true);
+  trace_point(h, "rsvd:gram B^T B");
   Scratch<double> Gc(k * k, s);
   FPI_CUDA(cudaMemcpyAsync(Gc.get(), Gm.get(), sizeof(double) * k * k, cudaMemcpyDeviceToDevice, s));
   int info = 0;
@@ -575,21 +581,28 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   }
   Gc.release();
   Gm.release();
+  trace_point(h, "rsvd:cholesky/inverse");
   // Y^T = (inner^T B) L^-T   (svd.py:135: Y = Q^T inner)
   Scratch<double> Z(q * k, s), Yt(q * k, s);
   op.applyT(h, B, k, Z);
+  trace_point(h, "rsvd:Z = M^T B");
   gemm(h, false, true, q, k, k, 1.0, Z, k, Linv, k, 0.0, Yt, k);
   Z.release();
+  trace_point(h, "rsvd:Yt = Z L^-T");
   // SVD of Y (k x q) through its transpose Y^T = Vy S Uy^T   (svd.py:136)
   Scratch<double> Vy(q * rank, s), Uyt(rank * k, s);
   dense_svd(h, q, k, Yt, k, rank, Vy, sigma, Uyt, diag);
+  trace_point(h, "rsvd:dense_svd(Yt)");
   Yt.release();
   transpose(h, q, rank, Vy, rank, Vt, q);                   // Vt = Vy^T
+  trace_point(h, "rsvd:transpose Vy");
   // U = Q U~ = B L^-T U~ ,  U~ = Uyt^T   (svd.py:137)
   Scratch<double> Mx(k * rank, s);
   gemm(h, true, true, k, rank, k, 1.0, Linv, k, Uyt, k, 0.0, Mx, rank);
   gemm(h, false, false, p, rank, k, 1.0, B, k, Mx, rank, 0.0, U, rank);
+  trace_point(h, "rsvd:U = B Mx");
   canonical_signs(h, rank, p, q, U, rank, Vt, q);
+  trace_point(h, "rsvd:canonical signs");
   if (diag) diag->engine = 1;
 }
 
@@ -713,8 +726,10 @@ void column_update(fpi_context* h, int64_t m, int64_t s_prev, int64_t n1, const 
       op.Dnz = Dnz.get();
     }
   }
+  trace_point(h, "col: zero-row scan");
   Scratch<double> Vti(r * q, s);
   inner_svd(h, op, r, q, thr, seed, U, sigma, Vti, engine, &h->diag);
+  trace_point(h, "col: inner svd");
   // lift: Vt = [Vti[:, :s] Vt_prev | Vti[:, s:]]   (pinv.py:205-207)
   const int64_t n = n1 + n2;
   if (n1) {
@@ -726,6 +741,7 @@ void column_update(fpi_context* h, int64_t m, int64_t s_prev, int64_t n1, const 
   if (n2)
     FPI_CUDA(cudaMemcpy2DAsync(Vt + n1, n * sizeof(double), Vti.get() + s_prev, q * sizeof(double),
                                n2 * sizeof(double), r, cudaMemcpyDeviceToDevice, s));
+  trace_point(h, "col: lift");
 }
 
 void pinv_assemble(fpi_context* h, int64_t r, const double* sigma, int64_t p, int64_t q, double cutoff,
