@@ -222,6 +222,18 @@ def workload_config(p):
             "l2_flush": "512MB write before every timed step", "parallelism": "replicas"}
 
 
+def _ncu_traffic():
+    """DRAM bytes of one representative launch of the dominant kernel, from the committed
+    `ncu --set full` capture summary (profiles/); None when absent."""
+    f = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full_summary.json"
+    try:
+        g = json.loads(f.read_text())["r01_gemm_gram_c4"]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"source": f"profiles/{f.name}", "launch": g.get("launch"), "traffic_bytes": g.get("traffic_bytes"),
+            "algorithmic_bytes": g.get("algorithmic_bytes"), "dmma_pipe_active": g.get("dmma_pipe_active_pct")}
+
+
 def ours_arm(args):
     import torch
     world, rank, local = dist_setup()
@@ -305,13 +317,16 @@ def ours_arm(args):
     dom_name, dom = max(((k, v) for k, v in rep.items() if v["flops"] > 0 or v["bytes"] > 0),
                         key=lambda kv: kv[1]["ms"], default=(None, None))
     roofline = None
+    ncu_traffic = _ncu_traffic()
     if dom is not None:
         avg_ms = dom["ms"] / max(dom["launches"], 1)
         if "gemm" in dom_name:
             ach = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
             peak = max(cublas_dgemm, fp64_peak)
             roofline = {"kernel": dom_name, "bound": "tensor", "achieved": round(ach, 3), "peak": round(peak, 3),
-                        "unit": "TFLOP/s", "frac": round(ach / peak, 4), "traffic": None,
+                        "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                        "traffic": ncu_traffic.get("traffic_bytes") if ncu_traffic else None,
+                        "traffic_launch": ncu_traffic,
                         "avg_launch_ms": round(avg_ms, 4), "launches": dom["launches"],
                         "share_of_step": round(dom["ms"] / ms, 4),
                         "peak_source": f"measured FP64 on this GPU: max(cuBLAS DGEMM 8192^3 = {cublas_dgemm:.1f}, "
