@@ -144,20 +144,26 @@ def handle():
     return h
 
 
+def raise_for_status(rc: int, msg: str, name: str = "") -> None:
+    """Map a C-ABI status code to the reference's exception types (validation.py:22-35)."""
+    if rc == FPI_OK:
+        return
+    if rc == FPI_EDOMAIN:
+        raise ValueError(msg)
+    if rc == FPI_ECAPACITY:
+        raise CapacityError(msg)
+    if rc == FPI_ESTRUCT:
+        raise StructuralViolationError(msg)
+    raise RuntimeError(f"{name}: {msg}" if name else msg)
+
+
 def call(name, *args):
     """Invoke ``name(handle, *args)`` and map its status code to the reference's exceptions."""
     lib = load()
     h = handle()
     rc = getattr(lib, name)(h, *args)
     if rc != FPI_OK:
-        msg = lib.fpi_last_error(h).decode(errors="replace")
-        if rc == FPI_EDOMAIN:
-            raise ValueError(msg)
-        if rc == FPI_ECAPACITY:
-            raise CapacityError(msg)
-        if rc == FPI_ESTRUCT:
-            raise StructuralViolationError(msg)
-        raise RuntimeError(f"{name}: {msg}")
+        raise_for_status(rc, lib.fpi_last_error(h).decode(errors="replace"), name)
     return h
 
 
