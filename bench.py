@@ -21,9 +21,10 @@ regression.py:50-70).  The metric is seconds per solve (lower is better).
 * ``--impl reference`` -- the reference's CPU path (the oracle port; the
   Python reference itself cannot travel to the GPU box) on the same workload.
 
-Multi-GPU (torchrun): every rank runs an independent replica of the solve
-(weak scaling, no data-path collective) -- the sharded solve is future work
-(DESIGN.md).
+Multi-GPU (torchrun, one rank per GPU, NCCL): the same problem is solved by all
+ranks together (strong scaling) -- reorder, block SVD and row update
+replicated, column update and apply row-sharded with NCCL all-reduces
+(paper_2011_04235_b200/sharded.py).
 """
 
 from __future__ import annotations
@@ -139,8 +140,15 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one rank per GPU over NCCL; FPI_DIST_BACKEND=gloo is a functional check of the multi-rank
+        # path on a box with fewer GPUs than ranks (never a measurement)
+        backend = os.environ.get("FPI_DIST_BACKEND", "nccl")
+        dev = local % max(torch.cuda.device_count(), 1)
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
     return world, rank, local
@@ -203,9 +211,9 @@ def reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
         "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator of the BASELINE.json configs)",
-        "config": workload_config(p),
+        "config": workload_config(p, world),
         "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
                          "sample": f"full {args.workload} solve (fastpi + apply) per step; warm-up on c1; "
                                    f"{len(times)} of {args.steps} steps within a {budget:.0f}s budget"},
@@ -215,11 +223,14 @@ def reference_arm(args):
     return 0
 
 
-def workload_config(p):
+def workload_config(p, world=1):
     w = p.workload
     return {"workload": w.name, "m": w.m, "n": w.n, "nnz": int(p.A.nnz), "n_labels": w.n_labels,
             "nnz_Y": int(p.Y.nnz), "rank": w.rank, "alpha": w.alpha, "k": w.k, "seed": w.seed,
-            "l2_flush": "512MB write before every timed step", "parallelism": "replicas"}
+            "l2_flush": "512MB write before every timed step",
+            "parallelism": "1 GPU" if world == 1 else
+            f"{world} ranks: column update + apply row-sharded (NCCL all-reduce of the 2r x 2r Gram, "
+            "of M^T B and of U^T Y); reorder, block SVD, row update replicated"}
 
 
 def _ncu_traffic():
@@ -251,8 +262,15 @@ def ours_arm(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device="cuda")  # 512 MB > L2 (126 MB)
     stats = {}
 
+    if world > 1:
+        from paper_2011_04235_b200.sharded import Comm, apply_distributed, fastpi_distributed, fastpi_sharded
+        comm = Comm()
+
     def step():
-        res = fastpi_device(A_dev, cfg, stats=stats)
+        if world > 1:
+            res = fastpi_sharded(A_dev, cfg, comm, stats=stats)
+        else:
+            res = fastpi_device(A_dev, cfg, stats=stats)
         Z = res.pseudoinverse.apply_device(Y_dev)
         return res, Z
 
@@ -346,19 +364,25 @@ def ours_arm(args):
                      + p.Y.indptr.size * 8 + p.Y.indices.size * 4 + p.Y.data.size * 8)
         e2e_t = []
         d2h_bytes = 0
-        for i in range(args.warmup):  # first calls allocate the pinned host staging buffers
+        def e2e_step():
+            if world > 1:
+                res = fastpi_distributed(p.A, cfg, comm)
+                return res, apply_distributed(res.pseudoinverse, p.Y), int(res.sigma.shape[0])
             res = fp.fastpi(p.A, cfg)
-            Zh = res.pseudoinverse.apply(p.Y)
+            return res, res.pseudoinverse.apply(p.Y), res.factors.rank
+
+        for i in range(args.warmup):  # first calls allocate the pinned host staging buffers
+            res, Zh, _ = e2e_step()
             del res, Zh
         for i in range(max(1, args.steps)):
             flush.fill_(float(i))
             torch.cuda.synchronize()
+            barrier(world)
             t0 = time.perf_counter()
-            res = fp.fastpi(p.A, cfg)
-            Zh = res.pseudoinverse.apply(p.Y)
+            res, Zh, rk = e2e_step()
             torch.cuda.synchronize()
             e2e_t.append(time.perf_counter() - t0)
-            d2h_bytes = Zh.nbytes + 8 * (3 * res.factors.rank + 16)
+            d2h_bytes = Zh.nbytes + 8 * (3 * rk + 16)
             del res, Zh
         e2e = {"value": max_over_ranks(statistics.mean(e2e_t), world), "unit": "s",
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
@@ -377,10 +401,10 @@ def ours_arm(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_max / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": False, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator of the BASELINE.json configs; paper corpora unavailable)",
-            "config": workload_config(p), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "config": workload_config(p, world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks,
             "stages_ms": {k: round(statistics.mean(v), 3) for k, v in stage_ms.items()},
             "step_ms_all": [round(t, 3) for t in times],

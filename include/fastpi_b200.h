@@ -163,6 +163,24 @@ int fpi_randomized_svd(fpi_handle h, int64_t p, int64_t q, const int64_t* a_ptr,
                        const double* a_val, const int64_t* at_ptr, const int32_t* at_idx, const double* at_val,
                        int64_t rank, int64_t seed, double* d_U, double* d_sigma, double* d_Vt);
 
+/* ---- building blocks of the row-sharded randomized SVD (multi-GPU, sharded.py) ------------ */
+/* C = op(A) op(A)^T (n x n, symmetric: lower tiles computed and mirrored); op(A) is n x k.
+ * The Gram of svd.py:134's QR (B^T B with trans_a = 1), summed across row shards by the caller. */
+int fpi_gram(fpi_handle h, int trans_a, int64_t n, int64_t k, const double* d_A, int64_t lda, double* d_C,
+             int64_t ldc);
+/* Linv (k x k) with Q = B Linv^T orthonormal, from G = B^T B: CholeskyQR (svd.py:134's QR without
+ * forming Q) or an eigen-based factor when G is not numerically positive definite. */
+int fpi_orth_factor(fpi_handle h, int64_t k, const double* d_G, double* d_Linv, double* h_cond);
+/* A[i, :] *= scale[i] (the diag(sigma) factors of pinv.py:133,194). */
+int fpi_scale_rows(fpi_handle h, int64_t rows, int64_t cols, double* d_A, int64_t lda, const double* d_scale);
+/* Sign rule applied by every SVD of the library: the largest-|.| entry of each row of Vt is made
+ * positive, U's columns flipped to match (U may be a row shard: the sign depends on Vt only). */
+int fpi_canonical_signs(fpi_handle h, int64_t r, int64_t p, int64_t q, double* d_U, int64_t ldu, double* d_Vt,
+                        int64_t ldv);
+/* At = A^T (A rows x cols). */
+int fpi_transpose(fpi_handle h, int64_t rows, int64_t cols, const double* d_A, int64_t lda, double* d_At,
+                  int64_t ldat);
+
 /* ---- pinv.py FastPI stages ---------------------------------------------- */
 /* pinv.py:131-171 row_update: f11 = (sigma11, U11 CSR m1 x rank11, Vt11 CSR rank11 x n1), A21 CSR m2 x n1.
  * Outputs U (m1+m2) x s, sigma s, Vt s x n1; *h_engine = 1 randomized / 2 dense. */
@@ -192,6 +210,15 @@ int fpi_pinv_apply_csr(fpi_handle h, int64_t m, int64_t n, int64_t r, const doub
                        const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
                        const int64_t* d_col_fwd, int64_t L, int64_t nnz, const int64_t* y_ptr,
                        const int32_t* y_idx, const double* y_val, double* d_Z);
+/* One row shard of pinv.py:75's U^T Y: W (L x r) = sum over the rows of Y whose reordered index lies
+ * in [r0, r0 + m_loc) of Y[i, :]^T U_loc[row_fwd[i] - r0, :]; the shards' W sum to the full product
+ * (the multi-GPU all-reduce operand).  Y is CSR (m x L) in original row order. */
+int fpi_pinv_project_csr(fpi_handle h, int64_t r0, int64_t m_loc, int64_t r, const double* d_U_loc,
+                         const int64_t* d_row_fwd, int64_t m, int64_t L, int64_t nnz, const int64_t* y_ptr,
+                         const int32_t* y_idx, const double* y_val, double* d_W);
+/* pinv.py:81's lift: Z (n x L, original column order) = V diag(sigma+) W^T; W is scaled in place. */
+int fpi_pinv_lift(fpi_handle h, int64_t n, int64_t r, const double* d_sigma_dagger, const double* d_Vt,
+                  const int64_t* d_col_fwd, int64_t L, double* d_W, double* d_Z);
 /* Dense right-hand side variant (Y m x L row-major). */
 int fpi_pinv_apply_dense(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U,
                          const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,

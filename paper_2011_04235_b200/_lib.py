@@ -74,6 +74,11 @@ SIGNATURES = {
                                 C.POINTER(BlockPlan)]),
     "fpi_dense_svd": (C.c_int, [vp, i64, i64, vp, i64, i64, vp, vp, vp]),
     "fpi_randomized_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp]),
+    "fpi_gram": (C.c_int, [vp, C.c_int, i64, i64, vp, i64, vp, i64]),
+    "fpi_orth_factor": (C.c_int, [vp, i64, vp, vp, C.POINTER(f64)]),
+    "fpi_scale_rows": (C.c_int, [vp, i64, i64, vp, i64, vp]),
+    "fpi_canonical_signs": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, i64]),
+    "fpi_transpose": (C.c_int, [vp, i64, i64, vp, i64, vp, i64]),
     "fpi_row_update": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, i64, f64, i64,
                                  vp, vp, vp, C.POINTER(i32)]),
     "fpi_column_update": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp, i64, f64, i64,
@@ -81,6 +86,8 @@ SIGNATURES = {
     "fpi_pinv_assemble": (C.c_int, [vp, i64, vp, i64, i64, f64, vp, C.POINTER(f64), C.POINTER(i32)]),
     "fpi_unfold": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
     "fpi_pinv_apply_csr": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp]),
+    "fpi_pinv_project_csr": (C.c_int, [vp, i64, i64, i64, vp, vp, i64, i64, i64, vp, vp, vp, vp]),
+    "fpi_pinv_lift": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, vp]),
     "fpi_pinv_apply_dense": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp]),
     "fpi_timing_enable": (C.c_int, [vp, C.c_int]),
     "fpi_timing_report": (C.c_int, [vp, C.c_char_p, i64, C.c_int]),

@@ -158,7 +158,7 @@ __global__ void k_scale_rows(int64_t M, int64_t N, double* A, int64_t lda, const
 // Canonical sign per singular triplet: the largest-|.| entry of the right
 // vector (row j of Vt, length q) is made positive (ties -> lowest index);
 // the matching left vector (column j of U) flips with it.
-__global__ void k_canon_sign(int64_t r, int64_t p, int64_t q, double* U, int64_t ldu, double* Vt, int64_t ldvt) {
+__global__ void k_canon_sign(int64_t r, int64_t q, double* Vt, int64_t ldvt, double* sign) {
   __shared__ double best[32];
   __shared__ int64_t bidx[32];
   for (int64_t j = blockIdx.x; j < r; j += gridDim.x) {
@@ -181,13 +181,20 @@ __global__ void k_canon_sign(int64_t r, int64_t p, int64_t q, double* U, int64_t
         if (best[k] > best[0] || (best[k] == best[0] && bidx[k] < bidx[0])) { best[0] = best[k]; bidx[0] = bidx[k]; }
     }
     __syncthreads();
-    const bool flip = Vt[j * ldvt + bidx[0]] < 0.0;
+    const bool flip = q > 0 && Vt[j * ldvt + bidx[0]] < 0.0;
     __syncthreads();
-    if (flip) {
+    if (flip)
       for (int64_t c = threadIdx.x; c < q; c += blockDim.x) Vt[j * ldvt + c] = -Vt[j * ldvt + c];
-      for (int64_t i = threadIdx.x; i < p; i += blockDim.x) U[i * ldu + j] = -U[i * ldu + j];
-    }
-    __syncthreads();
+    if (threadIdx.x == 0) sign[j] = flip ? -1.0 : 1.0;
+  }
+}
+
+// U[:, j] *= sign[j], row-major and coalesced (the left vectors follow their right vectors)
+__global__ void k_apply_col_signs(int64_t p, int64_t r, double* U, int64_t ldu, const double* sign) {
+  FPI_GRID_STRIDE(e, p * r) {
+    const int64_t i = e / r, j = e - i * r;
+    const double sg = sign[j];
+    if (sg < 0.0) U[i * ldu + j] = -U[i * ldu + j];
   }
 }
 
@@ -265,9 +272,12 @@ void scale_rows(fpi_context* h, int64_t M, int64_t N, double* A, int64_t lda, co
 void canonical_signs(fpi_context* h, int64_t r, int64_t p, int64_t q, double* U, int64_t ldu, double* Vt,
                      int64_t ldvt) {
   if (r <= 0) return;
-  k_canon_sign<<<(unsigned)(r < 4096 ? r : 4096), 256, 0, h->stream>>>(r, p, q, U, ldu, Vt, ldvt);
+  Scratch<double> sign(r, h->stream);
+  k_canon_sign<<<(unsigned)(r < 4096 ? r : 4096), 256, 0, h->stream>>>(r, q, Vt, ldvt, sign);
+  if (p > 0)
+    k_apply_col_signs<<<grid_for(p * r, 256, (int64_t)h->num_sms * 16), 256, 0, h->stream>>>(p, r, U, ldu, sign);
   FPI_LAUNCH_CHECK();
-  note_launch(h);
+  note_launch(h, 2);
 }
 
 }  // namespace fpi

@@ -227,6 +227,22 @@ __global__ void k_remap_rows_i32(int64_t nnz, const int32_t* __restrict__ rows, 
   FPI_GRID_STRIDE(e, nnz) out[e] = (int32_t)fwd[rows[e]];
 }
 
+__global__ void k_rows_in_range(int64_t nnz, const int32_t* __restrict__ rr, int64_t r0, int64_t len,
+                                int32_t* __restrict__ flag) {
+  FPI_GRID_STRIDE(e, nnz) flag[e] = (rr[e] >= r0 && rr[e] < r0 + len) ? 1 : 0;
+}
+
+__global__ void k_gather_triplets(int64_t cnt, const int32_t* __restrict__ picked, const int32_t* __restrict__ major,
+                                  const int32_t* __restrict__ minor, const double* __restrict__ val, int64_t r0,
+                                  int32_t* __restrict__ omaj, int32_t* __restrict__ omin, double* __restrict__ oval) {
+  FPI_GRID_STRIDE(e, cnt) {
+    const int32_t i = picked[e];
+    omaj[e] = major[i];
+    omin[e] = (int32_t)(minor[i] - r0);
+    oval[e] = val[i];
+  }
+}
+
 __global__ void k_diag_ratio(int64_t n, const double* __restrict__ L, int64_t ld, double* out) {
   if (blockIdx.x || threadIdx.x) return;
   double mx = 0.0, mn = 1e308;
@@ -528,6 +544,36 @@ struct InnerOp {
   }
 };
 
+// Q = B L^-T orthonormal from the Gram G = B^T B (k x k, preserved): CholeskyQR (svd.py:134's QR
+// without forming Q), or, when G is not numerically positive definite, an eigen-based factor.
+void orth_factor(fpi_context* h, int64_t k, const double* Gm, double* Linv, fpi_svd_diag* diag) {
+  cudaStream_t s = h->stream;
+  Scratch<double> Gc(k * k, s);
+  FPI_CUDA(cudaMemcpyAsync(Gc.get(), Gm, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, s));
+  int info = 0;
+  cholesky_lower(h, k, Gc, k, &info);
+  if (info == 0) {
+    Scratch<double> ratio(1, s);
+    k_diag_ratio<<<1, 1, 0, s>>>(k, Gc, k, ratio);
+    double r = host_read(ratio.get(), s);
+    if (diag) {
+      diag->cond_estimate = r;
+      diag->cholqr_passes = 1;
+    }
+    lower_inverse(h, k, Gc, k, Linv, k);
+  } else {
+    // not numerically PD (B rank deficient): orthonormalise through the eigendecomposition
+    Scratch<double> w(k, s), W(k * k, s);
+    sym_eig(h, k, Gm, k, w, W, k, 60, 1e-15, true);
+    k_eig_orth<<<grid_for(k * k, 256, h->num_sms * 16), 256, 0, s>>>(k, w, W, 1e-26, Linv);
+    FPI_LAUNCH_CHECK();
+    if (diag) {
+      diag->cond_estimate = INFINITY;
+      diag->cholqr_passes = 0;
+    }
+  }
+}
+
 static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int64_t seed, double* U, double* sigma,
                            double* Vt, fpi_svd_diag* diag) {
   const int64_t p = op.p, q = op.q;
@@ -555,31 +601,7 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   // CholeskyQR: B^T B = L L^T, Q = B L^-T   (svd.py:134)
   gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k, /*sym=*/true);
   trace_point(h, "rsvd:gram B^T B");
-  Scratch<double> Gc(k * k, s);
-  FPI_CUDA(cudaMemcpyAsync(Gc.get(), Gm.get(), sizeof(double) * k * k, cudaMemcpyDeviceToDevice, s));
-  int info = 0;
-  cholesky_lower(h, k, Gc, k, &info);
-  if (info == 0) {
-    Scratch<double> ratio(1, s);
-    k_diag_ratio<<<1, 1, 0, s>>>(k, Gc, k, ratio);
-    double r = host_read(ratio.get(), s);
-    if (diag) {
-      diag->cond_estimate = r;
-      diag->cholqr_passes = 1;
-    }
-    lower_inverse(h, k, Gc, k, Linv, k);
-  } else {
-    // not numerically PD (B rank deficient): orthonormalise through the eigendecomposition
-    Scratch<double> w(k, s), W(k * k, s);
-    sym_eig(h, k, Gm, k, w, W, k, 60, 1e-15, true);
-    k_eig_orth<<<grid_for(k * k, 256, h->num_sms * 16), 256, 0, s>>>(k, w, W, 1e-26, Linv);
-    FPI_LAUNCH_CHECK();
-    if (diag) {
-      diag->cond_estimate = INFINITY;
-      diag->cholqr_passes = 0;
-    }
-  }
-  Gc.release();
+  orth_factor(h, k, Gm, Linv, diag);
   Gm.release();
   trace_point(h, "rsvd:cholesky/inverse");
   // Y^T = (inner^T B) L^-T   (svd.py:135: Y = Q^T inner)
@@ -774,9 +796,58 @@ void unfold_transpose(fpi_context* h, int64_t m, int64_t n, int64_t r, const dou
 }
 
 // Z (n x L) = V diag(sdag) U^T Y  with U, Vt in reordered coordinates and Y (m x L) CSR in original rows
-void pinv_apply_csr(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* sdag,
-                    const double* Vt, const int64_t* row_fwd, const int64_t* col_fwd, int64_t L, int64_t nnz,
-                    const int64_t* y_ptr, const int32_t* y_idx, const double* y_val, double* Z) {
+// W (L x r) = Y'^T U_loc for the reordered rows [r0, r0 + m_loc) that U_loc holds (pinv.py:75's U^T Y,
+// one row shard of it; the shards' W sum to the full product).  Y is CSR in original row order.
+void pinv_project_csr(fpi_context* h, int64_t r0, int64_t m_loc, int64_t r, const double* U_loc,
+                      const int64_t* row_fwd, int64_t m, int64_t L, int64_t nnz, const int64_t* y_ptr,
+                      const int32_t* y_idx, const double* y_val, double* W) {
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  if (L == 0 || r == 0) return;
+  FPI_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * L * r, s));
+  if (nnz == 0 || m_loc == 0) return;
+  CubTemp tmp(s);
+  Scratch<int32_t> rows(nnz, s), rrows(nnz, s);
+  expand_rows(h, m, y_ptr, rows);
+  k_remap_rows_i32<<<grid_for(nnz, 256, G), 256, 0, s>>>(nnz, rows, row_fwd, rrows);
+  const int32_t* major = y_idx;
+  const int32_t* minor = rrows.get();
+  const double* vals = y_val;
+  int64_t cnt = nnz;
+  Scratch<int32_t> flag, ids, sel_major, sel_minor;
+  Scratch<int> dcnt;
+  Scratch<double> sel_val;
+  if (r0 > 0 || m_loc < m) {
+    flag.alloc(nnz, s);
+    ids.alloc(nnz, s);
+    sel_major.alloc(nnz, s);
+    sel_minor.alloc(nnz, s);
+    sel_val.alloc(nnz, s);
+    dcnt.alloc(1, s);
+    k_rows_in_range<<<grid_for(nnz, 256, G), 256, 0, s>>>(nnz, rrows, r0, m_loc, flag);
+    k_iota_i32<<<grid_for(nnz, 256, G), 256, 0, s>>>(ids, nnz);
+    Scratch<int32_t> picked(nnz, s);
+    select_if(tmp, ids.get(), picked.get(), dcnt.get(), nnz, FlagSet{flag.get()}, s);
+    cnt = host_read(dcnt.get(), s);
+    if (cnt == 0) return;
+    k_gather_triplets<<<grid_for(cnt, 256, G), 256, 0, s>>>(cnt, picked, y_idx, rrows, y_val, r0, sel_major, sel_minor,
+                                                             sel_val);
+    FPI_LAUNCH_CHECK();
+    major = sel_major.get();
+    minor = sel_minor.get();
+    vals = sel_val.get();
+  }
+  Scratch<int64_t> yt_ptr(L + 1, s);
+  Scratch<int32_t> yt_idx(cnt, s);
+  Scratch<double> yt_val(cnt, s);
+  build_csr(h, tmp, cnt, major, minor, vals, L, m_loc, yt_ptr, yt_idx, yt_val);
+  spmm(h, L, m_loc, r, yt_ptr, yt_idx, yt_val, nullptr, 1.0, U_loc, r, 0.0, W, r);
+  note_launch(h, 2);
+}
+
+// Z (n x L, original column order) = V diag(sigma+) W^T from the summed W (pinv.py:81); W is scaled in place.
+void pinv_lift(fpi_context* h, int64_t n, int64_t r, const double* sdag, const double* Vt, const int64_t* col_fwd,
+               int64_t L, double* W, double* Z) {
   cudaStream_t s = h->stream;
   const unsigned G = (unsigned)(h->num_sms * 16);
   if (n == 0 || L == 0) return;
@@ -784,24 +855,26 @@ void pinv_apply_csr(fpi_context* h, int64_t m, int64_t n, int64_t r, const doubl
     FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * n * L, s));
     return;
   }
-  // Y^T with rows remapped into reordered coordinates: CSR (L x m), column = row_fwd[i]
-  CubTemp tmp(s);
-  Scratch<int32_t> rows(nnz, s), rrows(nnz, s);
-  Scratch<int64_t> yt_ptr(L + 1, s);
-  Scratch<int32_t> yt_idx(nnz, s);
-  Scratch<double> yt_val(nnz, s);
-  expand_rows(h, m, y_ptr, rows);
-  if (nnz) k_remap_rows_i32<<<grid_for(nnz, 256, G), 256, 0, s>>>(nnz, rows, row_fwd, rrows);
-  build_csr(h, tmp, nnz, y_idx, rrows, y_val, L, m, yt_ptr, yt_idx, yt_val);
-  // W (L x r) = Y'^T U ; scale columns by sigma+   (pinv.py:75, 81)
-  Scratch<double> W(L * r, s), Zr(n * L, s);
-  spmm(h, L, m, r, yt_ptr, yt_idx, yt_val, nullptr, 1.0, U, r, 0.0, W, r);
   scale_cols(h, L, r, W, r, sdag, false);
-  // Z_reordered (n x L) = Vt^T W^T ; then Z[j] = Z_reordered[col_fwd[j]]
+  Scratch<double> Zr(n * L, s);
   gemm(h, true, true, n, L, r, 1.0, Vt, n, W, r, 0.0, Zr, L);
   k_gather_rows<<<grid_for(n * L, 256, G), 256, 0, s>>>(n, L, Zr, L, col_fwd, Z, L);
   FPI_LAUNCH_CHECK();
-  note_launch(h, 2);
+  note_launch(h);
+}
+
+void pinv_apply_csr(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* sdag,
+                    const double* Vt, const int64_t* row_fwd, const int64_t* col_fwd, int64_t L, int64_t nnz,
+                    const int64_t* y_ptr, const int32_t* y_idx, const double* y_val, double* Z) {
+  cudaStream_t s = h->stream;
+  if (n == 0 || L == 0) return;
+  if (r == 0) {
+    FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * n * L, s));
+    return;
+  }
+  Scratch<double> W(L * r, s);
+  pinv_project_csr(h, 0, m, r, U, row_fwd, m, L, nnz, y_ptr, y_idx, y_val, W);
+  pinv_lift(h, n, r, sdag, Vt, col_fwd, L, W, Z);
 }
 
 void pinv_apply_dense(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* sdag,
@@ -836,6 +909,48 @@ extern "C" int fpi_dense_svd(fpi_handle h, int64_t p, int64_t q, const double* d
               "dense SVD of a " + std::to_string(p) + "x" + std::to_string(q) +
                   " matrix exceeds the 100000000-entry guard");
   fpi::dense_svd(h, p, q, d_M, ldm, rank, d_U, d_sigma, d_Vt, &h->diag);
+  FPI_API_END(h)
+}
+
+// ---- building blocks of the row-sharded randomized SVD (sharded.py) ----
+extern "C" int fpi_gram(fpi_handle h, int trans_a, int64_t n, int64_t k, const double* d_A, int64_t lda, double* d_C,
+                        int64_t ldc) {
+  FPI_API_BEGIN(h)
+  FPI_REQUIRE(n >= 0 && k >= 0, FPI_EDOMAIN, "negative Gram dimension");
+  // C = op(A) op(A)^T, op(A) n x k: the symmetric (SYRK-style) product of svd.py:134's CholeskyQR
+  fpi::gemm(h, trans_a != 0, trans_a == 0, n, n, k, 1.0, d_A, lda, d_A, lda, 0.0, d_C, ldc, /*sym=*/true);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_orth_factor(fpi_handle h, int64_t k, const double* d_G, double* d_Linv, double* h_cond) {
+  FPI_API_BEGIN(h)
+  FPI_REQUIRE(k >= 1, FPI_EDOMAIN, "orth_factor needs k >= 1");
+  fpi_svd_diag dg{};
+  fpi::orth_factor(h, k, d_G, d_Linv, &dg);
+  h->diag.cond_estimate = dg.cond_estimate;
+  h->diag.cholqr_passes = dg.cholqr_passes;
+  if (h_cond) *h_cond = dg.cond_estimate;
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_scale_rows(fpi_handle h, int64_t rows, int64_t cols, double* d_A, int64_t lda,
+                              const double* d_scale) {
+  FPI_API_BEGIN(h)
+  if (rows > 0 && cols > 0) fpi::scale_rows(h, rows, cols, d_A, lda, d_scale);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_canonical_signs(fpi_handle h, int64_t r, int64_t p, int64_t q, double* d_U, int64_t ldu,
+                                   double* d_Vt, int64_t ldv) {
+  FPI_API_BEGIN(h)
+  if (r > 0) fpi::canonical_signs(h, r, p, q, d_U, ldu, d_Vt, ldv);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_transpose(fpi_handle h, int64_t rows, int64_t cols, const double* d_A, int64_t lda, double* d_At,
+                             int64_t ldat) {
+  FPI_API_BEGIN(h)
+  if (rows > 0 && cols > 0) fpi::transpose(h, rows, cols, d_A, lda, d_At, ldat);
   FPI_API_END(h)
 }
 
@@ -910,6 +1025,22 @@ extern "C" int fpi_pinv_apply_csr(fpi_handle h, int64_t m, int64_t n, int64_t r,
                                   const int32_t* y_idx, const double* y_val, double* d_Z) {
   FPI_API_BEGIN(h)
   fpi::pinv_apply_csr(h, m, n, r, d_U, d_sigma_dagger, d_Vt, d_row_fwd, d_col_fwd, L, nnz, y_ptr, y_idx, y_val, d_Z);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_pinv_project_csr(fpi_handle h, int64_t r0, int64_t m_loc, int64_t r, const double* d_U_loc,
+                                    const int64_t* d_row_fwd, int64_t m, int64_t L, int64_t nnz, const int64_t* y_ptr,
+                                    const int32_t* y_idx, const double* y_val, double* d_W) {
+  FPI_API_BEGIN(h)
+  FPI_REQUIRE(r0 >= 0 && m_loc >= 0 && r0 + m_loc <= m, FPI_EDOMAIN, "row shard out of range");
+  fpi::pinv_project_csr(h, r0, m_loc, r, d_U_loc, d_row_fwd, m, L, nnz, y_ptr, y_idx, y_val, d_W);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_pinv_lift(fpi_handle h, int64_t n, int64_t r, const double* d_sigma_dagger, const double* d_Vt,
+                             const int64_t* d_col_fwd, int64_t L, double* d_W, double* d_Z) {
+  FPI_API_BEGIN(h)
+  fpi::pinv_lift(h, n, r, d_sigma_dagger, d_Vt, d_col_fwd, L, d_W, d_Z);
   FPI_API_END(h)
 }
 
