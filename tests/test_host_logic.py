@@ -164,3 +164,46 @@ def test_public_names_cover_reference_hot_path(ref):
                     "from_matrix"}
     missing = set(ref.__all__) - set(fp.__all__) - out_of_scope
     assert not missing, missing
+
+
+# ---- artefact formats (svd.py:226-250, pinv.py:242-268, reorder.py:340-370): byte-compatible both ways
+
+def test_factor_and_pinv_files_roundtrip_with_reference(ref, tmp_path):
+    import importlib
+    osvd = importlib.import_module("paper_2011_04235_b200.svd")
+    opinv = importlib.import_module("paper_2011_04235_b200.pinv")
+    rng = np.random.default_rng(3)
+    U, s, Vt = rng.standard_normal((7, 3)), np.array([3.0, 2.0, 0.5]), rng.standard_normal((3, 5))
+    ours = fp.SvdFactors(U, s, Vt, is_sorted=True)
+    osvd.save_factors(ours, tmp_path / "a.bin")
+    rsvd, rpinv = importlib.import_module("fastpi.svd"), importlib.import_module("fastpi.pinv")
+    rsvd.save_factors(ref.SvdFactors(U, s, Vt, is_sorted=True), tmp_path / "b.bin")
+    assert (tmp_path / "a.bin").read_bytes() == (tmp_path / "b.bin").read_bytes()
+    back = rsvd.load_factors(tmp_path / "a.bin")
+    np.testing.assert_array_equal(back.U, U)
+    mine = osvd.load_factors(tmp_path / "b.bin")
+    np.testing.assert_array_equal(mine.Vt, Vt)
+    assert mine.is_sorted
+
+    V, sd, Ut = rng.standard_normal((5, 3)), np.array([0.5, 1.0, 0.0]), rng.standard_normal((3, 7))
+    opinv.save_pseudoinverse(fp.Pseudoinverse(V, sd, Ut, 1.25e-13, False), tmp_path / "p.bin")
+    rpinv.save_pseudoinverse(ref.Pseudoinverse(V, sd, Ut, 1.25e-13, False), tmp_path / "q.bin")
+    assert (tmp_path / "p.bin").read_bytes() == (tmp_path / "q.bin").read_bytes()
+    pl = opinv.load_pseudoinverse(tmp_path / "q.bin")
+    np.testing.assert_array_equal(pl.sigma_dagger, sd)
+    assert pl.tolerance_used == 1.25e-13 and not pl.all_filtered
+
+
+def test_reorder_file_roundtrip_with_reference(ref, tmp_path):
+    import importlib
+    oreo = importlib.import_module("paper_2011_04235_b200.reorder")  # the package name is the function
+    rmod = importlib.import_module("fastpi.reorder")
+    A = sp.random(30, 20, density=0.2, random_state=4, format="csr")
+    res = ref.reorder(ref.to_bipartite(A), 0.1)
+    rmod.save_reorder_result(res, tmp_path / "r.txt")
+    mine = oreo.load_reorder_result(tmp_path / "r.txt")
+    np.testing.assert_array_equal(mine.row_perm.forward, res.row_perm.forward)
+    np.testing.assert_array_equal(mine.col_perm.forward, res.col_perm.forward)
+    assert [tuple(b) for b in mine.blocks] == [tuple(b) for b in res.blocks]
+    oreo.save_reorder_result(mine, tmp_path / "s.txt")
+    assert (tmp_path / "s.txt").read_text() == (tmp_path / "r.txt").read_text()
