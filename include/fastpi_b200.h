@@ -163,6 +163,13 @@ int fpi_randomized_svd(fpi_handle h, int64_t p, int64_t q, const int64_t* a_ptr,
                        const double* a_val, const int64_t* at_ptr, const int32_t* at_idx, const double* at_val,
                        int64_t rank, int64_t seed, double* d_U, double* d_sigma, double* d_Vt);
 
+/* ---- regression harness (regression.py:89-124) -------------------------------------------- */
+/* For each row of the dense score block S (rows x L): the top-kmax labels in the reference's order
+ * (score descending, ties by ascending index: np.argsort(-s, kind="stable")) and whether each is in
+ * the row's label set (label CSR rows x L, sorted indices).  d_hits: rows x kmax of 0/1. */
+int fpi_topk_hits(fpi_handle h, int64_t rows, int64_t L, const double* d_S, int64_t lds, const int64_t* d_lab_ptr,
+                  const int32_t* d_lab_idx, int32_t kmax, uint8_t* d_hits);
+
 /* ---- building blocks of the row-sharded randomized SVD (multi-GPU, sharded.py) ------------ */
 /* C = op(A) op(A)^T (n x n, symmetric: lower tiles computed and mirrored); op(A) is n x k.
  * The Gram of svd.py:134's QR (B^T B with trans_a = 1), summed across row shards by the caller. */

@@ -74,6 +74,7 @@ SIGNATURES = {
                                 C.POINTER(BlockPlan)]),
     "fpi_dense_svd": (C.c_int, [vp, i64, i64, vp, i64, i64, vp, vp, vp]),
     "fpi_randomized_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp]),
+    "fpi_topk_hits": (C.c_int, [vp, i64, i64, vp, i64, vp, vp, i32, vp]),
     "fpi_gram": (C.c_int, [vp, C.c_int, i64, i64, vp, i64, vp, i64]),
     "fpi_orth_factor": (C.c_int, [vp, i64, vp, vp, C.POINTER(f64)]),
     "fpi_scale_rows": (C.c_int, [vp, i64, i64, vp, i64, vp]),
