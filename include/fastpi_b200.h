@@ -163,6 +163,43 @@ int fpi_randomized_svd(fpi_handle h, int64_t p, int64_t q, const int64_t* a_ptr,
                        const double* a_val, const int64_t* at_ptr, const int32_t* at_idx, const double* at_val,
                        int64_t rank, int64_t seed, double* d_U, double* d_sigma, double* d_Vt);
 
+/* ---- dataset text format (datasets.py:81-167), host-side native parser ---------------------- */
+enum fpi_dataset_error {
+  FPI_DS_OK = 0,
+  FPI_DS_EMPTY,           /* empty file */
+  FPI_DS_HEADER_SHAPE,    /* header is not three fields */
+  FPI_DS_HEADER_INT,      /* a header field is not an integer */
+  FPI_DS_HEADER_RANGE,    /* a header integer exceeds int64 */
+  FPI_DS_HEADER_NEG,      /* negative header count */
+  FPI_DS_LINE_COUNT,      /* instance-line count differs from m */
+  FPI_DS_BAD_LABEL,       /* label token is not an integer */
+  FPI_DS_LABEL_RANGE,     /* label index outside [0, L) */
+  FPI_DS_LABEL_DUP,       /* repeated label in a row */
+  FPI_DS_FEAT_TOKEN,      /* feature token without ':value' */
+  FPI_DS_FEAT_PARSE,      /* feature index / value does not parse */
+  FPI_DS_FEAT_RANGE,      /* feature index outside [0, n) */
+  FPI_DS_FEAT_DUP,        /* repeated feature index */
+  FPI_DS_FEAT_ORDER,      /* feature indices not increasing (tok2 = previous index) */
+  FPI_DS_FEAT_NONFINITE,  /* inf / nan value */
+  FPI_DS_FEAT_ZERO        /* explicit zero value */
+};
+typedef struct {
+  int64_t m, n, L, nnz_feat, nnz_lab, n_lines;
+  int32_t err_kind; /* fpi_dataset_error */
+  int32_t pad_;
+  int64_t err_line;              /* 1-based line of the rejection */
+  int64_t tok_begin, tok_end;    /* byte span of the offending token (-1 if none) */
+  int64_t tok2_begin, tok2_end;  /* second span (the previous index of FPI_DS_FEAT_ORDER) */
+} fpi_dataset_info;
+/* Parse a dataset file image (UTF-8 bytes).  On FPI_OK *h_out holds the parsed CSR arrays (sizes in
+ * *info); on FPI_EDOMAIN the rejection is described in *info (the caller renders load_dataset's
+ * ParseError message).  Host-only: no handle, no device. */
+int fpi_dataset_parse(const char* buf, int64_t len, void** h_out, fpi_dataset_info* info);
+/* Copy the parsed arrays out: features CSR (m+1, nnz_feat, nnz_feat), labels CSR (m+1, nnz_lab). */
+int fpi_dataset_fetch(void* h, int64_t* feat_ptr, int64_t* feat_idx, double* feat_val, int64_t* lab_ptr,
+                      int64_t* lab_idx);
+int fpi_dataset_free(void* h);
+
 /* ---- regression harness (regression.py:89-124) -------------------------------------------- */
 /* For each row of the dense score block S (rows x L): the top-kmax labels in the reference's order
  * (score descending, ties by ascending index: np.argsort(-s, kind="stable")) and whether each is in

@@ -40,6 +40,13 @@ class BlockPlan(C.Structure):
                 ("n_blocks_svd", i64), ("n_blocks_large", i64)]
 
 
+class DatasetInfo(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("L", C.c_int64), ("nnz_feat", C.c_int64),
+                ("nnz_lab", C.c_int64), ("n_lines", C.c_int64), ("err_kind", C.c_int32), ("pad_", C.c_int32),
+                ("err_line", C.c_int64), ("tok_begin", C.c_int64), ("tok_end", C.c_int64),
+                ("tok2_begin", C.c_int64), ("tok2_end", C.c_int64)]
+
+
 class SvdDiag(C.Structure):
     _fields_ = [("engine", i32), ("cholqr_passes", i32), ("cond_estimate", f64),
                 ("eig_sweeps", i32 * 4), ("null_completed", i32)]
@@ -74,6 +81,9 @@ SIGNATURES = {
                                 C.POINTER(BlockPlan)]),
     "fpi_dense_svd": (C.c_int, [vp, i64, i64, vp, i64, i64, vp, vp, vp]),
     "fpi_randomized_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp]),
+    "fpi_dataset_parse": (C.c_int, [C.c_char_p, i64, C.POINTER(vp), C.POINTER(DatasetInfo)]),
+    "fpi_dataset_fetch": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    "fpi_dataset_free": (C.c_int, [vp]),
     "fpi_topk_hits": (C.c_int, [vp, i64, i64, vp, i64, vp, vp, i32, vp]),
     "fpi_gram": (C.c_int, [vp, C.c_int, i64, i64, vp, i64, vp, i64]),
     "fpi_orth_factor": (C.c_int, [vp, i64, vp, vp, C.POINTER(f64)]),
