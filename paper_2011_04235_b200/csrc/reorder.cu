@@ -50,18 +50,6 @@ __global__ void k_set_u8(uint8_t* __restrict__ a, int64_t n, uint8_t v) {
   FPI_GRID_STRIDE(i, n) a[i] = v;
 }
 
-// deg[v] = 0 and parent[v] = v for the active list.
-__global__ void k_reset_nodes(const int32_t* __restrict__ act, int64_t cnt, int32_t* __restrict__ deg,
-                              int32_t* __restrict__ parent, int32_t* __restrict__ csize, int32_t* __restrict__ crows) {
-  FPI_GRID_STRIDE(i, cnt) {
-    int32_t v = act[i];
-    deg[v] = 0;
-    parent[v] = v;
-    csize[v] = 0;
-    crows[v] = 0;
-  }
-}
-
 __device__ __forceinline__ void warp_agg_inc(int32_t* ctr, int32_t key) {
   unsigned mask = __activemask();
   unsigned peers = __match_any_sync(mask, key);
@@ -69,30 +57,9 @@ __device__ __forceinline__ void warp_agg_inc(int32_t* ctr, int32_t key) {
   if ((int)(threadIdx.x & 31) == leader) atomicAdd(ctr + key, __popc(peers));
 }
 
-// Degrees over the compacted edge list (both endpoints active at loop entry).
-__global__ void k_degree(const uint64_t* __restrict__ edges, int64_t ne, int32_t m, int32_t* __restrict__ deg) {
-  FPI_GRID_STRIDE(e, ne) {
-    uint64_t ed = edges[e];
-    int32_t r = (int32_t)(ed >> 32);
-    int32_t c = (int32_t)(ed & 0xffffffffu) + m;
-    warp_agg_inc(deg, r);
-    warp_agg_inc(deg, c);
-  }
-}
-
 __global__ void k_gather_keys(const int32_t* __restrict__ ids, int64_t n, const int32_t* __restrict__ deg,
                               uint32_t* __restrict__ keys) {
   FPI_GRID_STRIDE(i, n) keys[i] = (uint32_t)deg[ids[i]];
-}
-
-// Hub i (in sorted order) gets id hi - i and leaves the active set.
-__global__ void k_assign_hubs(const int32_t* __restrict__ sorted_ids, int64_t cnt, int64_t hi, int32_t base,
-                              int64_t* __restrict__ fwd, uint8_t* __restrict__ state) {
-  FPI_GRID_STRIDE(i, cnt) {
-    int32_t v = sorted_ids[i];
-    fwd[v - base] = hi - i;
-    state[v] = 0;
-  }
 }
 
 // Union-find: parent[x] <= x always, so a root is the smallest id of its set.
@@ -107,65 +74,6 @@ __device__ __forceinline__ int32_t find_root(int32_t x, int32_t* parent) {
     }
   }
   return cur;
-}
-
-__global__ void k_hook(const uint64_t* __restrict__ edges, int64_t ne, int32_t m, const uint8_t* __restrict__ state,
-                       int32_t* parent) {
-  FPI_GRID_STRIDE(e, ne) {
-    uint64_t ed = edges[e];
-    int32_t u = (int32_t)(ed >> 32);
-    int32_t v = (int32_t)(ed & 0xffffffffu) + m;
-    if (!state[u] || !state[v]) continue;
-    int32_t ru = find_root(u, parent), rv = find_root(v, parent);
-    while (ru != rv) {
-      if (ru < rv) {
-        int32_t old = atomicCAS(parent + rv, rv, ru);
-        if (old == rv) break;
-        rv = find_root(old, parent);
-      } else {
-        int32_t old = atomicCAS(parent + ru, ru, rv);
-        if (old == ru) break;
-        ru = find_root(old, parent);
-      }
-    }
-  }
-}
-
-// Full compression + per-root size / row counts.
-__global__ void k_label_stats(const int32_t* __restrict__ act, int64_t cnt, int32_t m, int32_t* parent,
-                              int32_t* __restrict__ csize, int32_t* __restrict__ crows) {
-  FPI_GRID_STRIDE(i, cnt) {
-    int32_t v = act[i];
-    int32_t r = v;
-    while (parent[r] != r) r = parent[r];
-    parent[v] = r;
-    warp_agg_inc(csize, r);
-    if (v < m) warp_agg_inc(crows, r);
-  }
-}
-
-// Giant component: max size, ties by smallest root (= smallest member id).
-__global__ void k_pick_gcc(const int32_t* __restrict__ act, int64_t cnt, const int32_t* __restrict__ parent,
-                           const int32_t* __restrict__ csize, unsigned long long* best, int32_t* nroots) {
-  unsigned long long local = 0;
-  int32_t nr = 0;
-  FPI_GRID_STRIDE(i, cnt) {
-    int32_t v = act[i];
-    if (parent[v] == v) {
-      unsigned long long key = ((unsigned long long)(uint32_t)csize[v] << 32) | (uint32_t)(0x7fffffff - v);
-      local = key > local ? key : local;
-      ++nr;
-    }
-  }
-  for (int o = 16; o; o >>= 1) {
-    unsigned long long other = __shfl_xor_sync(0xffffffffu, local, o);
-    local = other > local ? other : local;
-    nr += __shfl_xor_sync(0xffffffffu, nr, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    atomicMax(best, local);
-    atomicAdd(nroots, nr);
-  }
 }
 
 struct IsSpokeRoot {
@@ -186,10 +94,6 @@ struct InComp {
 struct IsActive {
   const uint8_t* state;
   __device__ bool operator()(int32_t v) const { return state[v] != 0; }
-};
-struct PositiveDeg {
-  const int32_t* deg;
-  __device__ bool operator()(int32_t v) const { return deg[v] > 0; }
 };
 struct EdgeLive {
   const uint8_t* state;

@@ -70,11 +70,6 @@ __global__ void k_iota32(int32_t* a, int64_t n) {
   FPI_GRID_STRIDE(i, n) a[i] = (int32_t)i;
 }
 
-__global__ void k_gather_f64(int64_t n, const double* __restrict__ src, const int32_t* __restrict__ ord,
-                             double* __restrict__ dst) {
-  FPI_GRID_STRIDE(i, n) dst[i] = src[ord[i]];
-}
-
 // rows [0, rank11) of the inner CSR: Vt11 rows scaled by sigma; rows after: A21
 __global__ void k_inner_rows(int64_t rank11, int64_t m2, const int64_t* __restrict__ vptr,
                              const int64_t* __restrict__ aptr, int64_t nnz_v, int64_t* __restrict__ iptr) {
