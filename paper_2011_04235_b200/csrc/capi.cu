@@ -38,6 +38,7 @@ int fpi_create(fpi_handle* out, int device) {
 int fpi_destroy(fpi_handle h) {
   if (!h) return FPI_OK;
   if (h->d_spans) cudaFree(h->d_spans);
+  if (h->host_scalars) cudaFreeHost(h->host_scalars);
   delete h;
   return FPI_OK;
 }

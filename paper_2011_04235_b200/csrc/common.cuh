@@ -49,6 +49,7 @@ struct fpi_context {
   int64_t* d_spans = nullptr;
   int64_t n_spans = 0;
   int64_t spans_cap = 0;
+  void* host_scalars = nullptr;  // pinned scratch for per-iteration device scalars (reorder)
   // numerics diagnostics of the last randomized / dense SVD
   fpi_svd_diag diag{};
   // counters

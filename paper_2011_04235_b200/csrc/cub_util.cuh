@@ -52,6 +52,24 @@ void exclusive_sum(CubTemp& tmp, InIt in, OutIt out, int64_t n, cudaStream_t s) 
   FPI_CUDA(cub::DeviceScan::ExclusiveSum(tmp.need(b), b, in, out, (int)n, s));
 }
 
+// Three-way partition: first / second parts in input order, the rest through `rest`; the two counts
+// land on the device.
+template <typename InIt, typename T, typename RestIt, typename P1, typename P2>
+void three_way_partition(CubTemp& tmp, InIt in, T* first, T* second, RestIt rest, int* d_counts, int64_t n, P1 p1,
+                         P2 p2, cudaStream_t s) {
+  size_t b = 0;
+  FPI_CUDA(cub::DevicePartition::If(nullptr, b, in, first, second, rest, d_counts, (int)n, p1, p2, s));
+  FPI_CUDA(cub::DevicePartition::If(tmp.need(b), b, in, first, second, rest, d_counts, (int)n, p1, p2, s));
+}
+
+// Exclusive scan with a custom associative operator.
+template <typename InIt, typename OutIt, typename Op, typename T>
+void exclusive_scan(CubTemp& tmp, InIt in, OutIt out, Op op, T init, int64_t n, cudaStream_t s) {
+  size_t b = 0;
+  FPI_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, b, in, out, op, init, (int)n, s));
+  FPI_CUDA(cub::DeviceScan::ExclusiveScan(tmp.need(b), b, in, out, op, init, (int)n, s));
+}
+
 template <typename InIt, typename OutIt>
 void inclusive_sum(CubTemp& tmp, InIt in, OutIt out, int64_t n, cudaStream_t s) {
   size_t b = 0;

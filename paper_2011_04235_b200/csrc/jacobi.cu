@@ -95,41 +95,37 @@ __device__ void build_tables(StepTables& tb) {
   }
 }
 
-// Fast approximations (MUFU) for the rotation angle: the angle only has to be close, the
-// rotation itself is made orthogonal to FP64 precision by the Newton-refined cosine.
-__device__ __forceinline__ float rcp_apx(float x) { float r; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
-__device__ __forceinline__ float sqrt_apx(float x) { float r; asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
-__device__ __forceinline__ float rsqrt_apx(float x) { float r; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x)); return r; }
+// MUFU approximations for the rotation (measured on B200: rsqrt.approx.f64 ~2^-52.4 -- ptxas
+// refines MUFU.RSQ64H -- and rcp.approx.ftz.f64 ~2^-20).
 __device__ __forceinline__ double rcp_apx(double x) { double r; asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
 __device__ __forceinline__ double rsqrt_apx(double x) { double r; asm("rsqrt.approx.f64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
 
-// tan of the Jacobi angle from z = (aqq - app) / (2 apq): t = sign(z) / (|z| + sqrt(z^2 + 1)), |t| <= 1.
-__device__ __forceinline__ float tan_from_z(float zf) {
-  return copysignf(rcp_apx(fabsf(zf) + sqrt_apx(fmaf(zf, zf, 1.0f))), zf);
-}
-
-// Rotation of one pair from (app, aqq, apq): FP32-accurate angle, then c = 1/sqrt(1 + t^2) to full
-// FP64 precision (FP32 seed + one third-order Newton step) and s = c t, so the rotation is
-// orthogonal to rounding.
+// Rotation of one pair from (app, aqq, apq), without the z = (aqq - app) / (2 apq) division:
+//   t = tan(theta) = sign(d) 2 apq / (|d| + sqrt(d^2 + 4 apq^2)),  d = aqq - app,
+// with sqrt through rsqrt.approx.f64 (MUFU + refinement, ~2^-52) and the reciprocal through the
+// raw MUFU (2^-20: only the angle needs it), then c = 1/sqrt(1 + t^2) to full precision and
+// s = c t, so the rotation is orthogonal to rounding whatever the angle error.  Operands outside
+// [1e-150, 1e150] are rescaled first (the ratio d : apq is all the angle depends on).
 __device__ __forceinline__ void rotation(double app, double aqq, double apq, double tol, double ascale, bool absolute,
                                          double& c, double& sn) {
   const double den2 = absolute ? ascale * ascale : fabs(app) * fabs(aqq);
-  const double apq2 = apq * apq;
-  const double zd = (aqq - app) * rcp_apx(2.0 * apq);
-  double tt;
-  if (fabs(zd) > 1e18) {
-    tt = 0.5 * rcp_apx(zd);
-  } else {
-    tt = (double)tan_from_z((float)zd);
+  const bool rot = apq != 0.0 && apq * apq > tol * tol * den2;
+  double d = aqq - app, f2 = 2.0 * apq;
+  const double mx = fmax(fabs(d), fabs(f2));
+  if (mx > 1e150 || mx < 1e-150) {
+    const double sc = mx > 0.0 ? rcp_apx(mx) : 1.0;
+    d *= sc;
+    f2 *= sc;
   }
-  const bool rot = apq != 0.0 && apq2 > tol * tol * den2 && isfinite(tt) && tt != 0.0;
-  const double x = fma(tt, tt, 1.0);             // in [1, 2]
-  const double y = (double)rsqrt_apx((float)x);  // ~2^-22
-  const double e = fma(-x, y * y, 1.0);
-  const double cy = fma(y, fma(e, 0.375, 0.5) * e, y);
+  const double v = fma(d, d, f2 * f2);
+  const double hyp = v * rsqrt_apx(v);
+  const double t0 = f2 * rcp_apx(fabs(d) + hyp);
+  const double tt = d < 0.0 ? -t0 : t0;
+  const double cy = rsqrt_apx(fma(tt, tt, 1.0));
   c = rot ? cy : 1.0;
   sn = rot ? cy * tt : 0.0;
 }
+
 struct PairBuf {
   double c[2][16], s[2][16], app[2][16], aqq[2][16], apq[2][16];
 };

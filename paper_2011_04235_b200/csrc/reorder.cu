@@ -21,6 +21,10 @@
 //   5. next active set = giant component; stop when it is below the quota
 //      (reorder.py:259-269).  The terminal GCC takes the middle ids
 //      (reorder.py:271-275).
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "capi_guard.cuh"
 #include "cub_util.cuh"
@@ -81,11 +85,6 @@ struct IsSpokeRoot {
   int32_t gcc;
   __device__ bool operator()(int32_t v) const { return parent[v] == v && v != gcc; }
 };
-struct IsSpokeNode {
-  const int32_t* parent;
-  int32_t gcc;
-  __device__ bool operator()(int32_t v) const { return parent[v] != gcc; }
-};
 struct InComp {
   const int32_t* parent;
   int32_t gcc;
@@ -103,28 +102,32 @@ struct EdgeLive {
   }
 };
 
-// Per spoke component (rank order): rows, cols, and the size key.
+// Per spoke component (rank order): rows, cols and size, laid out by one exclusive scan of triples.
+struct Tri {
+  int64_t r, c, n;
+};
+struct TriSum {
+  __host__ __device__ Tri operator()(const Tri& a, const Tri& b) const { return Tri{a.r + b.r, a.c + b.c, a.n + b.n}; }
+};
+
 __global__ void k_comp_table(const int32_t* __restrict__ roots_sorted, int64_t nc, const int32_t* __restrict__ csize,
                              const int32_t* __restrict__ crows, int32_t* __restrict__ rank_of_root,
-                             int64_t* __restrict__ rows_c, int64_t* __restrict__ cols_c, int64_t* __restrict__ size_c) {
+                             Tri* __restrict__ tri) {
   FPI_GRID_STRIDE(i, nc) {
     int32_t r = roots_sorted[i];
     rank_of_root[r] = (int32_t)i;
     int64_t rows = crows[r], sz = csize[r];
-    rows_c[i] = rows;
-    cols_c[i] = sz - rows;
-    size_c[i] = sz;
+    tri[i] = Tri{rows, sz - rows, sz};
   }
 }
 
-__global__ void k_write_spans(int64_t nc, const int64_t* __restrict__ row_off, const int64_t* __restrict__ rows_c,
-                              const int64_t* __restrict__ col_off, const int64_t* __restrict__ cols_c, int64_t lo_t,
+__global__ void k_write_spans(int64_t nc, const Tri* __restrict__ off, const Tri* __restrict__ tri, int64_t lo_t,
                               int64_t lo_f, int64_t* __restrict__ spans) {
   FPI_GRID_STRIDE(i, nc) {
-    spans[4 * i + 0] = lo_t + row_off[i];
-    spans[4 * i + 1] = rows_c[i];
-    spans[4 * i + 2] = lo_f + col_off[i];
-    spans[4 * i + 3] = cols_c[i];
+    spans[4 * i + 0] = lo_t + off[i].r;
+    spans[4 * i + 1] = tri[i].r;
+    spans[4 * i + 2] = lo_f + off[i].c;
+    spans[4 * i + 3] = tri[i].c;
   }
 }
 
@@ -134,20 +137,49 @@ __global__ void k_node_rank_keys(const int32_t* __restrict__ nodes, int64_t cnt,
 }
 
 __global__ void k_emit_spokes(const int32_t* __restrict__ nodes, const uint32_t* __restrict__ ranks, int64_t cnt,
-                              int32_t m, const int64_t* __restrict__ node_off, const int64_t* __restrict__ row_off,
-                              const int64_t* __restrict__ col_off, const int64_t* __restrict__ rows_c, int64_t lo_t,
+                              int32_t m, const Tri* __restrict__ off, const Tri* __restrict__ tri, int64_t lo_t,
                               int64_t lo_f, int64_t* __restrict__ row_fwd, int64_t* __restrict__ col_fwd,
                               uint8_t* __restrict__ state) {
   FPI_GRID_STRIDE(p, cnt) {
     int32_t v = nodes[p];
     uint32_t c = ranks[p];
-    int64_t pos = p - node_off[c];
+    int64_t pos = p - off[c].n;
     if (v < m) {
-      row_fwd[v] = lo_t + row_off[c] + pos;
+      row_fwd[v] = lo_t + off[c].r + pos;
     } else {
-      col_fwd[v - m] = lo_f + col_off[c] + pos - rows_c[c];
+      col_fwd[v - m] = lo_f + off[c].c + pos - tri[c].r;
     }
     state[v] = 0;
+  }
+}
+
+// Hub sort keys of both sides in one list: ascending (side, mask - degree) = rows first, each side
+// degree-descending; the radix sort is stable, so ties keep the ascending id order.
+__global__ void k_hub_keys(const int32_t* __restrict__ act, int64_t cnt_t, int64_t cnt, const int32_t* __restrict__ deg,
+                           int deg_bits, uint32_t* __restrict__ keys) {
+  const uint32_t mask = (deg_bits >= 32) ? 0xffffffffu : ((1u << deg_bits) - 1u);
+  FPI_GRID_STRIDE(i, cnt) keys[i] = ((uint32_t)(i >= cnt_t) << deg_bits) | (mask - (uint32_t)deg[act[i]]);
+}
+
+// Hubs of both sides: the first min(q, #positive) of each side's segment of the sorted list; hub i
+// of a side takes the id hi - i (reorder.py:206-212).
+__global__ void k_assign_hubs2(const int32_t* __restrict__ ids, const uint32_t* __restrict__ keys, int64_t cnt_t,
+                               int64_t qt, int64_t qf, int64_t hi_t, int64_t hi_f, int32_t m, int deg_bits,
+                               int64_t* __restrict__ row_fwd, int64_t* __restrict__ col_fwd,
+                               uint8_t* __restrict__ state, int* __restrict__ nhubs) {
+  const uint32_t mask = (deg_bits >= 32) ? 0xffffffffu : ((1u << deg_bits) - 1u);
+  FPI_GRID_STRIDE(i, qt + qf) {
+    const bool col = i >= qt;
+    const int64_t j = col ? i - qt : i;
+    const int64_t pos = col ? cnt_t + j : j;
+    if ((keys[pos] & mask) == mask) continue;  // degree 0: not a hub
+    const int32_t v = ids[pos];
+    if (col)
+      col_fwd[v - m] = hi_f - j;
+    else
+      row_fwd[v] = hi_t - j;
+    state[v] = 0;
+    atomicAdd(nhubs + (col ? 1 : 0), 1);
   }
 }
 
@@ -270,9 +302,15 @@ __global__ void k_collect(IterScalars* out, const unsigned long long* best, cons
   out->gcc_rows = (*best) ? crows[gcc] : 0;
 }
 
+// also clears the iteration's device counters (hub counts, GCC key, root count)
 __global__ void k_reset_nodes_dev(const int32_t* __restrict__ act, int64_t cnt, int32_t* __restrict__ deg,
                                   int32_t* __restrict__ parent, int32_t* __restrict__ csize,
-                                  int32_t* __restrict__ crows) {
+                                  int32_t* __restrict__ crows, int32_t* __restrict__ dsc,
+                                  unsigned long long* __restrict__ best) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    dsc[0] = dsc[1] = dsc[4] = 0;
+    *best = 0ull;
+  }
   FPI_GRID_STRIDE(i, cnt) {
     int32_t v = act[i];
     deg[v] = 0;
@@ -295,6 +333,7 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
                         const int32_t* d_indices, double k, int64_t* d_row_fwd, int64_t* d_col_fwd,
                         ReorderOut& out) {
   cudaStream_t s = h->stream;
+  const auto t_enter = std::chrono::steady_clock::now();
   FPI_REQUIRE(k > 0.0 && k < 1.0, FPI_EDOMAIN, "hub selection ratio k must be in (0, 1)");
   FPI_REQUIRE(m > 0 && n > 0, FPI_EDOMAIN, "graph has an empty node side");
   FPI_REQUIRE(m + n < (int64_t)INT32_MAX, FPI_ECAPACITY, "m + n exceeds the int32 node-id range");
@@ -309,17 +348,16 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
   Scratch<int32_t> deg(V, s), parent(V, s), csize(V, s), crows(V, s), rank_of_root(V, s);
   Scratch<int32_t> act(V, s), act2(V, s), cand(V, s), cand_sorted(V, s);
   Scratch<uint32_t> keys(V, s), keys_sorted(V, s);
-  Scratch<int64_t> rows_c(V, s), cols_c(V, s), size_c(V, s), row_off(V, s), col_off(V, s), node_off(V, s);
-  // device scalars: [0] hubs rows, [1] hubs cols, [2] active count, [3] edge count, [4] nroots, [5] scratch
+  Scratch<Tri> tri(V, s), tri_off(V, s);
+  // device scalars: [0] hubs rows, [1] hubs cols, [2] active count, [3] spoke roots (partition),
+  // [4] nroots, [5] edge count
   Scratch<int32_t> dsc(8, s);
   Scratch<unsigned long long> d_best(1, s);
   Scratch<IterScalars> d_it(1, s);
-  IterScalars* hs = nullptr;
-  FPI_CUDA(cudaMallocHost((void**)&hs, sizeof(IterScalars)));
-  struct HostFree {
-    void* p;
-    ~HostFree() { cudaFreeHost(p); }
-  } hf{hs};
+  // pinned once per handle: a per-call cudaMallocHost / cudaFreeHost costs milliseconds and the
+  // free synchronises the device
+  if (!h->host_scalars) FPI_CUDA(cudaMallocHost(&h->host_scalars, 256));
+  IterScalars* hs = static_cast<IterScalars*>(h->host_scalars);
 
   if (h->spans_cap < V) {
     if (h->d_spans) cudaFree(h->d_spans);
@@ -332,7 +370,7 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
   if (nnz) k_expand_edges<<<G, T, 0, s>>>(m, d_indptr, d_indices, edges);
   k_set_u8<<<G, T, 0, s>>>(state, V, 1);
   k_fill_iota<<<G, T, 0, s>>>(act, V);
-  int32_t* ne_d = dsc.get() + 3;
+  int32_t* ne_d = dsc.get() + 5;
   {
     int32_t v = (int32_t)nnz;
     FPI_CUDA(cudaMemcpyAsync(ne_d, &v, sizeof(int32_t), cudaMemcpyHostToDevice, s));
@@ -348,6 +386,9 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
   const int deg_bits = bits_for((uint64_t)(m > n ? m : n));
   const int rank_bits = bits_for((uint64_t)V);
 
+  const bool trace = getenv("FPI_TRACE_REORDER") != nullptr;
+  auto titer = std::chrono::steady_clock::now();
+  if (trace) fprintf(stderr, "[reorder] setup %.2f ms\n", std::chrono::duration<double, std::milli>(titer - t_enter).count());
   while (true) {
     ++iters;
     const int64_t q_t = (int64_t)std::ceil(k * (double)cnt_t);  // math.ceil(k * cnt), reorder.py:198-199
@@ -355,23 +396,20 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
     const int64_t cnt = cnt_t + cnt_f;
 
     // 1. degrees over the compacted edge list
-    k_reset_nodes_dev<<<grid_for(cnt, T, G), T, 0, s>>>(act, cnt, deg, parent, csize, crows);
-    FPI_CUDA(cudaMemsetAsync(dsc.get(), 0, sizeof(int32_t) * 2, s));
+    k_reset_nodes_dev<<<grid_for(cnt, T, G), T, 0, s>>>(act, cnt, deg, parent, csize, crows, dsc, d_best);
     if (any_edges) k_degree_dev<<<G, T, 0, s>>>(edges, ne_d, (int32_t)m, deg);
-    // 2. hubs: stable degree-descending sort of each side's (ascending) active list
-    for (int side = 0; side < 2; ++side) {
-      const int64_t c = side ? cnt_f : cnt_t, q = side ? q_f : q_t;
-      if (c == 0 || q <= 0) continue;
-      int32_t* ids = act.get() + (side ? cnt_t : 0);
-      uint32_t* kk = keys.get() + (side ? cnt_t : 0);
-      uint32_t* ks = keys_sorted.get() + (side ? cnt_t : 0);
-      int32_t* cs = cand_sorted.get() + (side ? cnt_t : 0);
-      k_gather_keys<<<grid_for(c, T, G), T, 0, s>>>(ids, c, deg, kk);
-      sort_pairs(tmp, kk, ks, ids, cs, c, /*descending=*/true, 0, deg_bits, s);
-      k_assign_hubs_dev<<<grid_for(q < c ? q : c, T, G), T, 0, s>>>(cs, ks, q < c ? q : c, side ? hi_f : hi_t,
-                                                                    side ? (int32_t)m : 0,
-                                                                    side ? d_col_fwd : d_row_fwd, state,
-                                                                    dsc.get() + side);
+    // 2. hubs of both sides from one stable sort of the (ascending) active list
+    {
+      const int64_t qt = (cnt_t > 0 && q_t > 0) ? (q_t < cnt_t ? q_t : cnt_t) : 0;
+      const int64_t qf = (cnt_f > 0 && q_f > 0) ? (q_f < cnt_f ? q_f : cnt_f) : 0;
+      if (qt + qf > 0) {
+        k_hub_keys<<<grid_for(cnt, T, G), T, 0, s>>>(act, cnt_t, cnt, deg, deg_bits, keys);
+        sort_pairs(tmp, keys.get(), keys_sorted.get(), act.get(), cand_sorted.get(), cnt, /*descending=*/false, 0,
+                   deg_bits + 1, s);
+        k_assign_hubs2<<<grid_for(qt + qf, T, G), T, 0, s>>>(cand_sorted, keys_sorted, cnt_t, qt, qf, hi_t, hi_f,
+                                                             (int32_t)m, deg_bits, d_row_fwd, d_col_fwd, state,
+                                                             dsc.get());
+      }
     }
     // active list without the hubs (count on device)
     select_if(tmp, act.get(), act2.get(), dsc.get() + 2, cnt, IsActive{state}, s);
@@ -379,14 +417,20 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
     // 3. connected components of the residual
     if (any_edges) k_hook_dev<<<G, T, 0, s>>>(edges, ne_d, (int32_t)m, state, parent);
     k_label_stats_dev<<<grid_for(cnt, T, G), T, 0, s>>>(act, dsc.get() + 2, (int32_t)m, parent, csize, crows);
-    FPI_CUDA(cudaMemsetAsync(d_best.get(), 0, sizeof(unsigned long long), s));
-    FPI_CUDA(cudaMemsetAsync(dsc.get() + 4, 0, sizeof(int32_t), s));
     k_pick_gcc_dev<<<grid_for(cnt, T, G), T, 0, s>>>(act, dsc.get() + 2, parent, csize, d_best, dsc.get() + 4);
     k_collect<<<1, 1, 0, s>>>(d_it, d_best, dsc.get() + 4, dsc.get(), dsc.get() + 2, ne_d, crows);
     FPI_CUDA(cudaMemcpyAsync(hs, d_it.get(), sizeof(IterScalars), cudaMemcpyDeviceToHost, s));
+    const auto tsync0 = std::chrono::steady_clock::now();
     FPI_CUDA(cudaStreamSynchronize(s));  // the one host synchronisation of the iteration
+    if (trace) {
+      const auto now = std::chrono::steady_clock::now();
+      const double it_ms = std::chrono::duration<double, std::milli>(now - titer).count();
+      const double sy_ms = std::chrono::duration<double, std::milli>(now - tsync0).count();
+      if (it_ms > 2.0) fprintf(stderr, "[reorder] iteration %lld: %.2f ms (sync wait %.2f ms)\n", (long long)iters, it_ms, sy_ms);
+      titer = now;
+    }
     FPI_LAUNCH_CHECK();
-    note_launch(h, 12);
+    note_launch(h, 8);
     const int64_t h_t = hs->h_t, h_f = hs->h_f;
     hi_t -= h_t;
     hi_f -= h_f;
@@ -401,36 +445,35 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
     const int64_t gcc_size = (int64_t)(hs->best >> 32);
     const int64_t gcc_t = hs->gcc_rows, gcc_f = gcc_size - gcc_t;
     const int64_t nsc = (int64_t)hs->nroots - 1;
+    const int64_t nsp = acnt - gcc_size;
 
-    // 4. spoke components -> blocks, members ascending within each side
+    // 4. one pass over the active list: the giant component (next active set) | spoke roots |
+    //    other spoke nodes, each in ascending id order (this CUB writes the unselected part in input
+    //    order; tests/test_reorder_gpu.py pins it); roots and other spokes land contiguously in
+    //    cand (roots first), which orders every component root-first = ascending.
+    three_way_partition(tmp, act.get(), act2.get(), cand.get(), cand.get() + nsc,
+                        dsc.get() + 2, acnt, InComp{parent, gcc}, IsSpokeRoot{parent, gcc}, s);
+    note_launch(h, 2);
     if (nsc > 0) {
-      select_if(tmp, act.get(), cand.get(), dsc.get() + 5, acnt, IsSpokeRoot{parent, gcc}, s);
+      // spoke components -> blocks (size desc, min id asc), members ascending within each side
       k_gather_keys<<<grid_for(nsc, T, G), T, 0, s>>>(cand, nsc, csize, keys);
       sort_pairs(tmp, keys.get(), keys_sorted.get(), cand.get(), cand_sorted.get(), nsc, true, 0, rank_bits, s);
-      k_comp_table<<<grid_for(nsc, T, G), T, 0, s>>>(cand_sorted, nsc, csize, crows, rank_of_root, rows_c, cols_c,
-                                                     size_c);
-      exclusive_sum(tmp, rows_c.get(), row_off.get(), nsc, s);
-      exclusive_sum(tmp, cols_c.get(), col_off.get(), nsc, s);
-      exclusive_sum(tmp, size_c.get(), node_off.get(), nsc, s);
-      k_write_spans<<<grid_for(nsc, T, G), T, 0, s>>>(nsc, row_off, rows_c, col_off, cols_c, lo_t, lo_f,
-                                                      h->d_spans + 4 * h->n_spans);
-      const int64_t nsp = acnt - gcc_size;
-      select_if(tmp, act.get(), cand.get(), dsc.get() + 5, acnt, IsSpokeNode{parent, gcc}, s);
+      k_comp_table<<<grid_for(nsc, T, G), T, 0, s>>>(cand_sorted, nsc, csize, crows, rank_of_root, tri);
+      exclusive_scan(tmp, tri.get(), tri_off.get(), TriSum{}, Tri{0, 0, 0}, nsc, s);
+      k_write_spans<<<grid_for(nsc, T, G), T, 0, s>>>(nsc, tri_off, tri, lo_t, lo_f, h->d_spans + 4 * h->n_spans);
       k_node_rank_keys<<<grid_for(nsp, T, G), T, 0, s>>>(cand, nsp, parent, rank_of_root, keys);
       sort_pairs(tmp, keys.get(), keys_sorted.get(), cand.get(), cand_sorted.get(), nsp, false, 0, rank_bits, s);
-      k_emit_spokes<<<grid_for(nsp, T, G), T, 0, s>>>(cand_sorted, keys_sorted, nsp, (int32_t)m, node_off, row_off,
-                                                      col_off, rows_c, lo_t, lo_f, d_row_fwd, d_col_fwd, state);
+      k_emit_spokes<<<grid_for(nsp, T, G), T, 0, s>>>(cand_sorted, keys_sorted, nsp, (int32_t)m, tri_off, tri, lo_t,
+                                                      lo_f, d_row_fwd, d_col_fwd, state);
       FPI_LAUNCH_CHECK();
-      note_launch(h, 12);
+      note_launch(h, 8);
       h->n_spans += nsc;
     }
     lo_t += cnt_t - gcc_t;
     lo_f += cnt_f - gcc_f;
 
-    // 5. giant component becomes the active set (count = gcc_size, also kept on device)
-    select_if(tmp, act.get(), act2.get(), dsc.get() + 2, acnt, InComp{parent, gcc}, s);
+    // 5. giant component becomes the active set (its count was written to dsc[2] by the partition)
     std::swap(act, act2);
-    note_launch(h, 1);
     h->gcc_sizes.push_back(gcc_size);
     cnt_t = gcc_t;
     cnt_f = gcc_f;
@@ -450,6 +493,9 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
     note_launch(h, 1);
   }
   FPI_CUDA(cudaStreamSynchronize(s));
+  if (trace)
+    fprintf(stderr, "[reorder] loop+tail done %.2f ms after entry\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enter).count());
   out.m1 = lo_t;
   out.n1 = lo_f;
   out.m2 = m - lo_t;

@@ -333,12 +333,23 @@ class _Timer:
         self.seconds = time.perf_counter() - self.t0
 
 
+_TRACE = bool(__import__("os").environ.get("FPI_TRACE_REORDER"))
+
+
+def _trace_mark(label, tm):
+    import sys
+    torch().cuda.synchronize()
+    print(f"[fastpi] {label} done at {(time.perf_counter() - tm.t0) * 1e3:.2f} ms", file=sys.stderr)
+
+
 def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = None) -> FastpiResult:
     """Algorithm 1 on a canonical device CSR (m >= n); everything stays in HBM."""
     m, n = dev.shape
     timings = []
     with _Timer() as tm:
         ordering = reorder_device(dev, cfg.k)
+        if _TRACE:
+            _trace_mark("reorder_device", tm)
         part = partition_original(dev, ordering, transposes=True)
     timings.append(StageTime("reorder", tm.seconds, 0))
 
