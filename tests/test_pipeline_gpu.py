@@ -149,3 +149,33 @@ def test_public_api_fit_and_spec_examples():
     # estimator front-end
     reg = fp.PseudoinverseRegressor(alpha=w.alpha, k=w.k, seed=w.seed).fit(p.A, p.Y)
     assert np.linalg.norm(reg.coef_ - g1["Z"]) <= REC_TOL * np.linalg.norm(g1["Z"])
+
+
+def _lowrank_rel_factored(fa, fb):
+    """||A - B||_F / ||B||_F for A = Ua Sa Vta, B = Ub Sb Vtb without forming them and without the
+    cancellation of ||A||^2 + ||B||^2 - 2<A, B>: A - B = [Ua Sa, -Ub Sb] [Vta; Vtb] = Q (R N)."""
+    Ua, Vta, Ub, Vtb = (np.asarray(x) for x in (fa.U, fa.Vt, fb.U, fb.Vt))
+    M = np.hstack([Ua * fa.sigma, -(Ub * fb.sigma)])
+    _, R = np.linalg.qr(M)
+    D = R @ np.vstack([Vta, Vtb])
+    return np.linalg.norm(D) / np.linalg.norm(fb.sigma)  # B's factors are orthonormal
+
+
+def test_stagewise_parity_c4():
+    """P3 at the benchmark size (c4, 200k x 50k): oracle row / column updates fed the GPU's own
+    upstream factors; the reorder sizes against the live oracle."""
+    p, res, st = _run("c4")
+    w = p.workload
+    Ac = orc.canonical_csr(p.A)
+    o = orc.reorder(Ac.shape[0], Ac.shape[1], Ac.indptr, Ac.indices, w.k)
+    assert (st["m1"], st["n1"], st["m2"], st["n2"], st["T"]) == (o.m1, o.n1, o.m2, o.n2, o.n_iterations)
+    np.testing.assert_array_equal(res.reordering.row_perm.forward, o.row_fwd)
+    part = st["part"]
+    fo_rows, _ = orc.row_update(_host_factors(st["f11"]), part.a21.to_host(), st["s"], 0.3, w.seed + 1)
+    fr = st["f_rows"]
+    assert np.abs(fr.sigma - fo_rows.sigma).max() <= SIG_TOL * fo_rows.sigma[0]
+    assert _lowrank_rel_factored(fr, fo_rows) <= REC_TOL
+    fo_full, _ = orc.column_update(_host_factors(fr), part.T.to_host(), st["r"], 0.3, w.seed + 2)
+    ff = res.factors
+    assert np.abs(ff.sigma - fo_full.sigma).max() <= SIG_TOL * fo_full.sigma[0]
+    assert _lowrank_rel_factored(ff, fo_full) <= REC_TOL
