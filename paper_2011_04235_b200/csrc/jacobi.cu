@@ -22,6 +22,7 @@
 // absolute |a_pq| / max|a_ii| for Gram matrices) against the tolerance, or
 // its stagnation at the rounding floor.
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -356,15 +357,20 @@ __device__ __forceinline__ void pipeline(int64_t t0, int64_t t1, Pre pre, Skip s
   cp_wait<0>();
 }
 
-// One eigenproblem of a batch (device descriptor).
+// One eigenproblem of a batch (device descriptor).  G is double-buffered: the update of round r - 1
+// (phase B, old buffer -> new buffer) runs while phase A of round r builds its sub-problems from the
+// old buffer and round r - 1's rotations.  The per-round bookkeeping is double-buffered by round
+// parity q: during round gr the CTAs read slot q = gr & 1 and block 0 writes slot q ^ 1.
 struct EigProb {
   int nb;              // padded block count (even); np = nb / 2 pairs = 32-row tiles of the panel
   int done;            // converged (written on the device)
   int sweeps;
-  int vround;          // round (within its sweep) whose rotations V still owes, -1: none
-  int vpar;            // R buffer holding them
-  int pad_;
-  double* G;           // npad x npad
+  int gfinal;          // buffer holding the final G (written on the device)
+  int pend[2];         // the previous round's rotations are not yet applied to G and V
+  int pround[2];       // their round within the sweep (the pairing)
+  int ppar[2];         // their R buffer
+  int gcur[2];         // buffer holding the latest complete G (the pre-update G while pending)
+  double* G[2];        // npad x npad each
   double* V;           // npad x npad
   double* Jbuf;        // 2 x np x JS x JS (by round parity)
   int* jflag;          // 2 x np: rotation of the pair is not the identity
@@ -400,16 +406,16 @@ __device__ __forceinline__ void g_run(int64_t j, int np, int c, int& pb, int& ch
 }
 
 // V[:, P'] <- V[:, P'] R_P' for the pending round of problem pr_: row tiles [r0, r1) of column pb.
-__device__ void v_run(const EigProb& pr_, int pb, int r0, int r1, double* sm, int warp, int lane) {
-  const int nb = pr_.nb, np = nb / 2, round = pr_.vround;
-  if (!pr_.jflag[pr_.vpar * np + pb]) return;
+__device__ void v_run(const EigProb& pr_, int q, int pb, int r0, int r1, double* sm, int warp, int lane) {
+  const int nb = pr_.nb, np = nb / 2, round = pr_.pround[q], vpar = pr_.ppar[q];
+  if (!pr_.jflag[vpar * np + pb]) return;
   const int64_t ld = (int64_t)nb * JB;
   const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
   double* V = pr_.V;
   double* Jb = sm;
   double* stg = sm + TILE;
   pipeline(
-      r0, r1, [&] { j_async(Jb, pr_.Jbuf + ((int64_t)pr_.vpar * np + pb) * JS * JS); },
+      r0, r1, [&] { j_async(Jb, pr_.Jbuf + ((int64_t)vpar * np + pb) * JS * JS); },
       [&](int64_t) { return false; },
       [&](int64_t rt, int st) { tile_async(stg + st * TILE, V, ld, rt * JS, 0, 0, bi, bj); },
       [&](int64_t rt, int st) {
@@ -425,24 +431,23 @@ __device__ void v_run(const EigProb& pr_, int pb, int r0, int r1, double* sm, in
       });
 }
 
-// G'[Pa, Pb] = Ja^T G[Pa, Pb] Jb for pa in [a0, a1) (<= pb), written to both triangles.
-__device__ void g_run_exec(const EigProb& pr_, int round, int par, int pb, int a0, int a1, double* sm, int warp,
-                           int lane) {
-  const int nb = pr_.nb, np = nb / 2;
+// G'[Pa, Pb] = Ja^T G[Pa, Pb] Jb for pa in [a0, a1) (<= pb), read from the pre-update buffer and
+// written (both triangles) to the other one -- every tile, identity rotations included.
+__device__ void g_run_exec(const EigProb& pr_, int q, int pb, int a0, int a1, double* sm, int warp, int lane) {
+  const int nb = pr_.nb, np = nb / 2, round = pr_.pround[q], par = pr_.ppar[q];
   const int64_t ld = (int64_t)nb * JB;
   const double* J0 = pr_.Jbuf + (int64_t)par * np * JS * JS;
-  const int* fl = pr_.jflag + par * np;
-  const bool fb = fl[pb] != 0;
   const int bi = rr_block(pb, round, nb), bj = rr_block(nb - 1 - pb, round, nb);
-  double* G = pr_.G;
+  const double* Gs = pr_.G[pr_.gcur[q]];
+  double* G = pr_.G[pr_.gcur[q] ^ 1];
   double* Jb = sm;
   double* Us = sm + TILE;
   double* stg = sm + 2 * TILE;
   pipeline(
-      a0, a1, [&] { j_async(Jb, J0 + (int64_t)pb * JS * JS); }, [&](int64_t pa) { return !fb && fl[pa] == 0; },
+      a0, a1, [&] { j_async(Jb, J0 + (int64_t)pb * JS * JS); }, [&](int64_t) { return false; },
       [&](int64_t pa, int st) {
         const int ai = rr_block((int)pa, round, nb), aj = rr_block(nb - 1 - (int)pa, round, nb);
-        tile_async(stg + (2 * st) * TILE, G, ld, -1, ai, aj, bi, bj);
+        tile_async(stg + (2 * st) * TILE, Gs, ld, -1, ai, aj, bi, bj);
         j_async(stg + (2 * st + 1) * TILE, J0 + pa * JS * JS);
       },
       [&](int64_t pa, int st) {
@@ -469,112 +474,220 @@ __device__ void g_run_exec(const EigProb& pr_, int round, int par, int pb, int a
       });
 }
 
-// phase A item plus the V runs owed by the previous round, for every problem of the batch
-__device__ void section_a(EigProb* P, int nprob, int64_t total_pairs, int64_t total_vitems, int vchunk, int round,
-                          int par, int sweep, bool pairs_on, double tol, double* sm, PairBuf& pbuf,
-                          const StepTables& tb, unsigned long long* prof) {
+// Position of block x in the round-robin pairing of round rho (inverse of rr_block).
+__device__ __forceinline__ int rr_pos(int x, int rho, int nb) {
+  if (x == 0) return 0;
+  const int m = nb - 1;
+  return 1 + (((x - 1 - rho) % m) + m) % m;
+}
+
+// C (M x N) = op(A) (M x 32) B (32 x N), all in shared memory with explicit strides; M, N multiples
+// of 8.  8 x 8 output tiles are dealt round-robin to the warps (DMMA m8n8k4, K = 32).
+__device__ __forceinline__ void mm_k32(const double* A, int lda, bool ta, const double* B, int ldb, double* C, int ldc,
+                                       int M, int N, int tile0, int warp, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const int tn = N / 8, nt = (M / 8) * tn;
+  for (int tl = (warp + 8 - tile0 % 8) % 8; tl < nt; tl += 8) {
+    const int m0 = 8 * (tl / tn), n0 = 8 * (tl % tn);
+    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < JS; k0 += 4) {
+      const double a = ta ? A[(k0 + t) * lda + m0 + g] : A[(m0 + g) * lda + k0 + t];
+      const double b = B[(k0 + t) * ldb + n0 + g];
+      dmma(d0, d1, a, b);
+    }
+    C[(m0 + g) * ldc + n0 + 2 * t] = d0;
+    C[(m0 + g) * ldc + n0 + 2 * t + 1] = d1;
+  }
+}
+
+// The sub-problem of pair pr in round rho (blocks X, Y) from the pre-update G and the previous
+// round's rotations: S[x, y] = J_{P(x)}[:, x half]^T G[P(x), P(y)] J_{P(y)}[:, y half] for x, y in
+// {X, Y}, where P(x) is x's pair in the previous round.  S[Y, X] = S[X, Y]^T.  Uses tiles 0..7.
+__device__ void build_subproblem(const EigProb& pr_, int q, int pr, int rho, double* sm, int warp, int lane) {
+  const int nb = pr_.nb, np = nb / 2, prho = pr_.pround[q], par = pr_.ppar[q];
+  const int64_t ld = (int64_t)nb * JB;
+  const double* Gs = pr_.G[pr_.gcur[q]];
+  const double* J0 = pr_.Jbuf + (int64_t)par * np * JS * JS;
+  const int blk[2] = {rr_block(pr, rho, nb), rr_block(nb - 1 - pr, rho, nb)};
+  int pp[2], hh[2];
+  for (int i = 0; i < 2; ++i) {
+    const int pos = rr_pos(blk[i], prho, nb);
+    pp[i] = pos < np ? pos : nb - 1 - pos;
+    hh[i] = pos < np ? 0 : 1;
+  }
+  double* S = sm;               // tile 0: the sub-problem
+  double* Jx = sm + 2 * TILE;   // tiles 2, 3: previous rotations of X's and Y's pairs
+  double* Jy = sm + 3 * TILE;
+  double* T = sm + 4 * TILE;    // tiles 4, 5, 6: G[P(X), P(X)], G[P(X), P(Y)], G[P(Y), P(Y)]
+  double* W = sm + 7 * TILE;    // tile 7: three 32 x 16 products, stride 48
+  const int combos[3][2] = {{0, 0}, {0, 1}, {1, 1}};
+  j_async(Jx, J0 + (int64_t)pp[0] * JS * JS);
+  j_async(Jy, J0 + (int64_t)pp[1] * JS * JS);
+  for (int c = 0; c < 3; ++c) {
+    const int pa = pp[combos[c][0]], pb = pp[combos[c][1]];
+    tile_async(T + c * TILE, Gs, ld, -1, rr_block(pa, prho, nb), rr_block(nb - 1 - pa, prho, nb),
+               rr_block(pb, prho, nb), rr_block(nb - 1 - pb, prho, nb));
+  }
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  // W_c = T_c J_b[:, 16 h_b : +16]   (32 x 16)
+  for (int c = 0; c < 3; ++c) {
+    const int b = combos[c][1];
+    mm_k32(T + c * TILE, LDS_, false, (b ? Jy : Jx) + 16 * hh[b], LDS_, W + 16 * c, 48, 32, 16, 8 * c, warp, lane);
+  }
+  __syncthreads();
+  // S[a, b] = J_a[:, 16 h_a : +16]^T W_c   (16 x 16)
+  for (int c = 0; c < 3; ++c) {
+    const int a = combos[c][0], b = combos[c][1];
+    mm_k32((a ? Jy : Jx) + 16 * hh[a], LDS_, true, W + 16 * c, 48, S + (16 * a) * LDS_ + 16 * b, LDS_, 16, 16,
+           4 * c, warp, lane);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 256; e += JT) {  // S[Y, X] = S[X, Y]^T
+    const int i = e >> 4, j = e & 15;
+    S[(16 + i) * LDS_ + j] = S[j * LDS_ + 16 + i];
+  }
+  __syncthreads();
+}
+
+// phase A of one pair: the rotations of the 32 x 32 sub-problem (J into Jbuf[par])
+__device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par, int sweep, double tol, double* sm,
+                          PairBuf& pbuf, const StepTables& tb, unsigned long long* prof) {
+  const int nb = pr_.nb, np = nb / 2;
+  const bool absolute = pr_.abs_scale != nullptr;
+  const double ascale = absolute ? *pr_.abs_scale : 0.0;
+  double* Sa = sm;
+  double* Ra = sm + TILE;
+  if (pr_.pend[q]) {
+    build_subproblem(pr_, q, pr, round, sm, threadIdx.x >> 5, threadIdx.x & 31);
+  } else {
+    const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
+    tile_async(Sa, pr_.G[pr_.gcur[q]], (int64_t)nb * JB, -1, bi, bj, bi, bj);
+    cp_commit();
+    cp_wait<0>();
+  }
+  for (int e = threadIdx.x; e < JS * JS; e += JT) {
+    const int a = e >> 5, b = e & 31;
+    Ra[a * LDS_ + b] = a == b ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const unsigned long long ts0 = prof ? gtimer() : 0;
+  double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
+  if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
+  double* Jp = pr_.Jbuf + ((int64_t)par * np + pr) * JS * JS;
+  int rot = 0;
+  for (int e = threadIdx.x; e < JS * JS; e += JT) {
+    const double v = Ra[(e & 31) * LDS_ + (e >> 5)];  // Rt -> row-major J
+    Jp[e] = v;
+    rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
+  }
+  rot = __syncthreads_or(rot);
+  if (threadIdx.x == 0) pr_.jflag[par * np + pr] = rot;
+  if (threadIdx.x < 32) {
+    for (int o = 16; o; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
+    if (threadIdx.x == 0 && om > 0.0) atomicMax(pr_.offmax + sweep, (unsigned long long)__double_as_longlong(om));
+  }
+  __syncthreads();
+}
+
+// One round's parallel section: phase A of every active problem's pairs, and -- on the CTAs phase A
+// leaves idle -- the G (phase B) and V updates owed by the previous round.
+__device__ void section(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems,
+                        int gchunk, int vchunk, int q, int round, int par, int sweep, bool pairs_on, double tol,
+                        double* sm, PairBuf& pbuf, const StepTables& tb, unsigned long long* prof,
+                        unsigned long long* work, bool join) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nA = pairs_on ? total_pairs : 0;
-  for (int64_t it = blockIdx.x; it < nA + total_vitems; it += gridDim.x) {
-    if (it < nA) {
-      const int pi = find_prob(P, nprob, it, 0);
+  const int64_t nX = total_gitems + total_vitems;
+  auto extra = [&](int64_t x) {
+    if (x < total_gitems) {
+      const int pi = find_prob(P, nprob, x, 1);
       const EigProb& pr_ = P[pi];
-      const int nb = pr_.nb;
-      if (pr_.done || round >= nb - 1) continue;
-      const int np = nb / 2;
-      const int pr = (int)(it - pr_.pair_off);
-      const int64_t ldg = (int64_t)nb * JB;
-      const bool absolute = pr_.abs_scale != nullptr;
-      const double ascale = absolute ? *pr_.abs_scale : 0.0;
-      const int bi = rr_block(pr, round, nb), bj = rr_block(nb - 1 - pr, round, nb);
-      double* Sa = sm;
-      double* Ra = sm + TILE;
-      tile_async(Sa, pr_.G, ldg, -1, bi, bj, bi, bj);
-      cp_commit();
-      for (int e = threadIdx.x; e < JS * JS; e += JT) {
-        const int a = e >> 5, b = e & 31;
-        Ra[a * LDS_ + b] = a == b ? 1.0 : 0.0;
-      }
-      cp_wait<0>();
-      __syncthreads();
-      const unsigned long long ts0 = prof ? gtimer() : 0;
-      double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
-      if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
-      double* Jp = pr_.Jbuf + ((int64_t)par * np + pr) * JS * JS;
-      int rot = 0;
-      for (int e = threadIdx.x; e < JS * JS; e += JT) {
-        const double v = Ra[(e & 31) * LDS_ + (e >> 5)];  // Rt -> row-major J
-        Jp[e] = v;
-        rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
-      }
-      rot = __syncthreads_or(rot);
-      if (threadIdx.x == 0) pr_.jflag[par * np + pr] = rot;
-      if (threadIdx.x < 32) {
-        for (int o = 16; o; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
-        if (threadIdx.x == 0 && om > 0.0) atomicMax(pr_.offmax + sweep, (unsigned long long)__double_as_longlong(om));
-      }
-      __syncthreads();
+      if (!pr_.pend[q]) return;
+      int pb, chunk;
+      g_run(x - pr_.gitem_off, pr_.nb / 2, gchunk, pb, chunk);
+      const int a0 = chunk * gchunk, a1 = a0 + gchunk < pb + 1 ? a0 + gchunk : pb + 1;
+      g_run_exec(pr_, q, pb, a0, a1, sm, warp, lane);
     } else {
-      const int64_t vi = it - nA;
+      const int64_t vi = x - total_gitems;
       const int pi = find_prob(P, nprob, vi, 2);
       const EigProb& pr_ = P[pi];
-      if (pr_.vround < 0) continue;
+      if (!pr_.pend[q]) return;
       const int np = pr_.nb / 2;
       const int per = (np + vchunk - 1) / vchunk;
       const int64_t j = vi - pr_.vitem_off;
       const int pb = (int)(j / per), c = (int)(j % per);
       const int r0 = c * vchunk, r1 = r0 + vchunk < np ? r0 + vchunk : np;
-      v_run(pr_, pb, r0, r1, sm, warp, lane);
+      v_run(pr_, q, pb, r0, r1, sm, warp, lane);
     }
+  };
+  auto pair = [&](int64_t it) {
+    const int pi = find_prob(P, nprob, it, 0);
+    const EigProb& pr_ = P[pi];
+    if (pr_.done || round >= pr_.nb - 1) return;
+    pair_exec(pr_, q, (int)(it - pr_.pair_off), round, par, sweep, tol, sm, pbuf, tb, prof);
+  };
+  // pairs first (one per CTA while they last), then the G / V queue (heaviest items first), drained
+  // through a shared counter by the CTAs without a pair -- and by the pair CTAs too when the extra
+  // work outweighs a phase-A sub-solve (join)
+  bool had_pair = false;
+  for (int64_t it = blockIdx.x; it < nA; it += gridDim.x) {
+    pair(it);
+    had_pair = true;
+  }
+  if (had_pair && !join && nA < (int64_t)gridDim.x) return;
+  __shared__ int64_t grab;
+  while (true) {
+    if (threadIdx.x == 0) grab = (int64_t)atomicAdd(work, 1ull);
+    __syncthreads();
+    const int64_t x = grab;
+    __syncthreads();
+    if (x >= nX) break;
+    extra(x);
+  }
+}
+
+// Block 0, after its own section work: the next round's bookkeeping slot (q ^ 1) and work counter.
+__device__ void advance_slots(EigProb* P, int nprob, int q, int round, int par, unsigned long long* work) {
+  if (blockIdx.x != 0) return;
+  if (threadIdx.x == 0) work[q ^ 1] = 0ull;
+  for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) {
+    EigProb& pr_ = P[pi];
+    const int cur = pr_.pend[q] ? pr_.gcur[q] ^ 1 : pr_.gcur[q];
+    const bool active = !pr_.done && round < pr_.nb - 1;
+    pr_.gcur[q ^ 1] = cur;
+    pr_.pend[q ^ 1] = active ? 1 : 0;
+    pr_.pround[q ^ 1] = round;
+    pr_.ppar[q ^ 1] = par;
+    pr_.gfinal = cur;
   }
 }
 
 __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
     k_jacobi(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems, int gchunk,
-             int vchunk, int max_rounds, int max_sweeps, double tol, double stagnate_below, unsigned long long* prof) {
+             int vchunk, int max_rounds, int max_sweeps, double tol, double stagnate_below, unsigned long long* prof,
+             unsigned long long* work, int join) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   __shared__ StepTables tb;
   __shared__ PairBuf pbuf;
   build_tables(tb);
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int gr = 0;  // global round counter (R buffer parity)
+  int gr = 0;  // global round counter (R buffer and bookkeeping parity)
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int round = 0; round < max_rounds; ++round, ++gr) {
-      const int par = gr & 1;
+      const int q = gr & 1;
       const unsigned long long t0 = prof ? gtimer() : 0;
-      section_a(P, nprob, total_pairs, total_vitems, vchunk, round, par, sweep, true, tol, sm, pbuf, tb, prof);
+      section(P, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, round, q, sweep, true, tol, sm, pbuf,
+              tb, prof, work + q, join != 0);
       const unsigned long long t1 = prof ? gtimer() : 0;
-      grid.sync();
-      const unsigned long long t2 = prof ? gtimer() : 0;
-      // ---- phase B: upper blocks of G, both triangles written
-      for (int64_t it = blockIdx.x; it < total_gitems; it += gridDim.x) {
-        const int pi = find_prob(P, nprob, it, 1);
-        const EigProb& pr_ = P[pi];
-        const int nb = pr_.nb;
-        if (pr_.done || round >= nb - 1) continue;
-        int pb, chunk;
-        g_run(it - pr_.gitem_off, nb / 2, gchunk, pb, chunk);
-        const int a0 = chunk * gchunk, a1 = a0 + gchunk < pb + 1 ? a0 + gchunk : pb + 1;
-        g_run_exec(pr_, round, par, pb, a0, a1, sm, warp, lane);
-      }
-      const unsigned long long t3 = prof ? gtimer() : 0;
-      // V owes this round's rotations (read in the next section A, after the barrier below)
-      if (blockIdx.x == 0) {
-        for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) {
-          EigProb& pr_ = P[pi];
-          const bool active = !pr_.done && round < pr_.nb - 1;
-          pr_.vround = active ? round : -1;
-          pr_.vpar = par;
-        }
-      }
+      advance_slots(P, nprob, q, round, q, work);
       grid.sync();
       if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
         prof[0] += t1 - t0;
-        prof[1] += t2 - t1;
-        prof[2] += t3 - t2;
-        prof[3] += gtimer() - t3;
+        prof[1] += gtimer() - t1;
       }
     }
     // per-problem convergence: converged, or the off-diagonal measure stagnates at the rounding floor
@@ -595,8 +708,11 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
     for (int pi = 0; pi < nprob; ++pi) all &= (P[pi].done != 0);
     if (all) break;
   }
-  // the last round's eigenvector update
-  section_a(P, nprob, total_pairs, total_vitems, vchunk, 0, gr & 1, 0, false, tol, sm, pbuf, tb, nullptr);
+  // the last round's G and V updates
+  const int q = gr & 1;
+  section(P, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, 0, q, 0, false, tol, sm, pbuf, tb,
+          nullptr, work + q, true);
+  advance_slots(P, nprob, q, 0, q, work);
 }
 
 __global__ void k_max_diag(int64_t n, const double* A, int64_t lda, double* out) {
@@ -659,7 +775,6 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     const int64_t np = nb / 2;
     hp[i] = EigProb{};
     hp[i].nb = nb;
-    hp[i].vround = -1;
     goff[i] = gsz;
     gsz += npad[i] * npad[i];
     jsz += 2 * np * JS * JS;
@@ -680,29 +795,14 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   int grid = max_blocks;
   if (const char* e = getenv("FPI_JACOBI_GRID")) grid = atoi(e) < max_blocks ? atoi(e) : max_blocks;
   if (grid < 1) grid = 1;
-  // run lengths: G blocks (per block column) spread over the whole grid; V tiles over the CTAs
-  // phase A leaves idle
-  // (smallest run lengths whose run count fits one wave)
-  const int64_t vcta = grid - tot_pairs > grid / 4 ? grid - tot_pairs : grid / 4 + 1;
-  int gchunk = (int)((tot_tri + grid - 1) / grid), vchunk = (int)((tot_vt + vcta - 1) / vcta);
-  auto runs = [&](int gc, int vc, int64_t& ng, int64_t& nv) {
-    ng = nv = 0;
-    for (int i = 0; i < nprob; ++i) {
-      const int64_t np = hp[i].nb / 2;
-      ng += g_runs_before(np, gc);
-      nv += np * ((np + vc - 1) / vc);
-    }
-  };
-  for (int64_t ng, nv;;) {
-    runs(gchunk, 1 << 30, ng, nv);
-    if (ng <= grid || gchunk >= max_rounds) break;
-    ++gchunk;
-  }
-  for (int64_t ng, nv;;) {
-    runs(1 << 30, vchunk, ng, nv);
-    if (nv <= vcta || vchunk >= max_rounds) break;
-    ++vchunk;
-  }
+  // run lengths of the G (phase B) and V updates of round r - 1: a few 32 x 32 tiles per queue item,
+  // enough items to balance across the grid (a G tile costs two 32^3 products, a V tile one)
+  int gchunk = 4, vchunk = 8;
+  if (const char* e = getenv("FPI_JACOBI_CHUNKS")) sscanf(e, "%d,%d", &gchunk, &vchunk);
+  // pair CTAs join the queue when the extra work per idle CTA exceeds ~20 tile products (~ one sub-solve)
+  const int64_t xcta = grid - tot_pairs > 1 ? grid - tot_pairs : 1;
+  int join = (2 * tot_tri + tot_vt) > 20 * xcta ? 1 : 0;
+  if (const char* e = getenv("FPI_JACOBI_JOIN")) join = atoi(e);
   int64_t tot_g = 0, tot_v = 0;
   for (int i = 0; i < nprob; ++i) {
     const int64_t np = hp[i].nb / 2;
@@ -712,7 +812,7 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     tot_g += g_runs_before(np, gchunk);
     tot_v += np * ((np + vchunk - 1) / vchunk);
   }
-  Scratch<double> Gall(gsz, s), Vall(gsz, s), Jall(jsz, s), scales(nprob, s);
+  Scratch<double> Gall(gsz, s), Gall2(gsz, s), Vall(gsz, s), Jall(jsz, s), scales(nprob, s);
   Scratch<int> fall(fsz, s);
   Scratch<unsigned long long> offm((int64_t)nprob * (max_sweeps + 1), s);
   Scratch<EigProb> dP(nprob, s);
@@ -721,13 +821,14 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   int64_t jo = 0, fo = 0;
   for (int i = 0; i < nprob; ++i) {
     const int64_t np = hp[i].nb / 2;
-    hp[i].G = Gall.get() + goff[i];
+    hp[i].G[0] = Gall.get() + goff[i];
+    hp[i].G[1] = Gall2.get() + goff[i];
     hp[i].V = Vall.get() + goff[i];
     hp[i].Jbuf = Jall.get() + jo;
     hp[i].jflag = fall.get() + fo;
     hp[i].offmax = offm.get() + (int64_t)i * (max_sweeps + 1);
     hp[i].abs_scale = absolute ? scales.get() + i : nullptr;
-    k_pad_copy<<<grid_for(npad[i] * npad[i], 256, G16), 256, 0, s>>>(n[i], npad[i], A[i], lda[i], hp[i].G);
+    k_pad_copy<<<grid_for(npad[i] * npad[i], 256, G16), 256, 0, s>>>(n[i], npad[i], A[i], lda[i], hp[i].G[0]);
     k_identity<<<grid_for(npad[i] * npad[i], 256, G16), 256, 0, s>>>(npad[i], hp[i].V);
     if (absolute) k_max_diag<<<1, 256, 0, s>>>(n[i], A[i], lda[i], scales.get() + i);
     note_launch(h, absolute ? 3 : 2);
@@ -736,13 +837,16 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   }
   FPI_CUDA(cudaMemcpyAsync(dP.get(), hp.data(), sizeof(EigProb) * nprob, cudaMemcpyHostToDevice, s));
   FPI_LAUNCH_CHECK();
+  Scratch<unsigned long long> work(2, s);
+  FPI_CUDA(cudaMemsetAsync(work.get(), 0, sizeof(unsigned long long) * 2, s));
   Scratch<unsigned long long> prof(5, s);
   FPI_CUDA(cudaMemsetAsync(prof.get(), 0, sizeof(unsigned long long) * 5, s));
   unsigned long long* prof_p = getenv("FPI_JACOBI_PROFILE") ? prof.get() : nullptr;
   EigProb* Pp = dP.get();
   int gch = gchunk, vch = vchunk;
+  unsigned long long* work_p = work.get();
   void* args[] = {&Pp, &nprob, &tot_pairs, &tot_g, &tot_v, &gch, &vch, &max_rounds, &max_sweeps, &tol,
-                  (void*)&stagnate_below, &prof_p};
+                  (void*)&stagnate_below, &prof_p, &work_p, &join};
   {
     KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
     FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, JACOBI_SMEM, s));
@@ -756,16 +860,16 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     unsigned long long hq[5];
     FPI_CUDA(cudaMemcpyAsync(hq, prof_p, sizeof(hq), cudaMemcpyDeviceToHost, s));
     FPI_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[jacobi nprob=%d n0=%lld grid=%d gchunk=%d vchunk=%d] sectionA %.3f (subsolve %.3f)  syncA %.3f  "
-            "phaseB %.3f  syncB %.3f ms\n", nprob, (long long)n[0], grid, gchunk, vchunk, hq[0] * 1e-6, hq[4] * 1e-6,
-            hq[1] * 1e-6, hq[2] * 1e-6, hq[3] * 1e-6);
+    fprintf(stderr, "[jacobi nprob=%d n0=%lld grid=%d gchunk=%d vchunk=%d] section %.3f (subsolve %.3f)  sync %.3f ms\n",
+            nprob, (long long)n[0], grid, gchunk, vchunk, hq[0] * 1e-6, hq[4] * 1e-6, hq[1] * 1e-6);
   }
   // eigenvalues (descending diagonal) and the matching columns of V
   CubTemp tmp(s);
   for (int i = 0; i < nprob; ++i) {
     Scratch<double> keys(n[i], s), keys2(n[i], s);
     Scratch<int32_t> idx(n[i], s), idx2(n[i], s);
-    k_diag_keys<<<grid_for(n[i], 256, h->num_sms * 4), 256, 0, s>>>(n[i], Gall.get() + goff[i], npad[i], keys, idx);
+    k_diag_keys<<<grid_for(n[i], 256, h->num_sms * 4), 256, 0, s>>>(n[i], hp[i].G[hp[i].gfinal], npad[i], keys,
+                                                                       idx);
     sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n[i], true, 0, 64, s);
     k_gather_eig<<<grid_for(n[i] * n[i], 256, G16), 256, 0, s>>>(n[i], Vall.get() + goff[i], npad[i], idx2, keys2, w[i],
                                                                   V[i], ldv[i]);
