@@ -469,6 +469,13 @@ struct InnerOp {
   int64_t nzr = -1;
   const int32_t* nz_rows = nullptr;
   const double* Dnz = nullptr;
+  int64_t s_nnz = 0;  // stored entries of the sparse part (cost model only)
+
+  // flop-equivalent cost of apply() with k columns (a gathered SpMM byte ~ 10 flops on B200)
+  double apply_cost(int64_t k) const {
+    const double dense_rows = (double)(nzr >= 0 ? nzr : p);
+    return (D && sd > 0 ? 2.0 * dense_rows * (double)sd * (double)k : 0.0) + 10.0 * 8.0 * (double)s_nnz * (double)k;
+  }
 
   // B (p x k) = inner * X (q x k)
   void apply(fpi_context* h, const double* X, int64_t k, double* B) const {
@@ -592,7 +599,6 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   trace_point(h, "rsvd:sketch");
   op.apply(h, X, k, B);                 // svd.py:133
   trace_point(h, "rsvd:B = M X");
-  X.release();
   // CholeskyQR: B^T B = L L^T, Q = B L^-T   (svd.py:134)
   gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k, /*sym=*/true);
   trace_point(h, "rsvd:gram B^T B");
@@ -616,8 +622,18 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   // U = Q U~ = B L^-T U~ ,  U~ = Uyt^T   (svd.py:137)
   Scratch<double> Mx(k * rank, s);
   gemm(h, true, true, k, rank, k, 1.0, Linv, k, Uyt, k, 0.0, Mx, rank);
-  gemm(h, false, false, p, rank, k, 1.0, B, k, Mx, rank, 0.0, U, rank);
-  trace_point(h, "rsvd:U = B Mx");
+  if (op.apply_cost(rank) + 2.0 * (double)q * (double)k * (double)rank < 2.0 * (double)p * (double)k * (double)rank) {
+    // = inner (X L^-T U~): the thin q x r factor first, then one pass of the inner operator -- about
+    // half the flops of the p x 2r x r product with B when inner is [U Sigma | T] with a tall U
+    B.release();
+    Scratch<double> XM(q * rank, s);
+    gemm(h, false, false, q, rank, k, 1.0, X, k, Mx, rank, 0.0, XM, rank);
+    X.release();
+    op.apply(h, XM, rank, U);
+  } else {
+    gemm(h, false, false, p, rank, k, 1.0, B, k, Mx, rank, 0.0, U, rank);
+  }
+  trace_point(h, "rsvd:U");
   canonical_signs(h, rank, p, q, U, rank, Vt, q);
   trace_point(h, "rsvd:canonical signs");
   if (diag) diag->engine = 1;
@@ -672,6 +688,7 @@ void row_update(fpi_context* h, int64_t m1, int64_t n1, int64_t rank11, const do
   InnerOp op;
   op.p = p;
   op.q = q;
+  op.s_nnz = nnz;
   op.s_ptr = iptr;
   op.s_idx = iidx;
   op.s_val = ival;
@@ -717,6 +734,7 @@ void column_update(fpi_context* h, int64_t m, int64_t s_prev, int64_t n1, const 
   op.st_ptr = tt_ptr;
   op.st_idx = tt_idx;
   op.st_val = tt_val;
+  op.s_nnz = (n2 && m) ? host_read(t_ptr + m, s) : 0;
   // rows of U_prev that are identically zero (spoke rows of column-free blocks): skip them in the
   // dense products of the randomized engine when they are the majority
   Scratch<int32_t> flag, ids, nzl, cntd;
@@ -964,6 +982,7 @@ extern "C" int fpi_randomized_svd(fpi_handle h, int64_t p, int64_t q, const int6
   op.st_ptr = at_ptr;
   op.st_idx = at_idx;
   op.st_val = at_val;
+  op.s_nnz = p ? fpi::host_read(a_ptr + p, h->stream) : 0;
   fpi::randomized_svd(h, op, rank, seed, d_U, d_sigma, d_Vt, &h->diag);
   FPI_API_END(h)
 }
