@@ -1,6 +1,7 @@
 // Shared plumbing for the FastPI B200 core: status codes, the handle, a
 // stream-ordered scratch allocator and small device helpers.
 #pragma once
+#include <cstring>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -100,9 +101,14 @@ inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
 
 template <typename T>
 inline T host_read(const T* d, cudaStream_t s) {
-  T v;
-  FPI_CUDA(cudaMemcpyAsync(&v, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  // through a pinned per-thread slot: a pageable destination makes the driver stage the copy
+  static thread_local void* slot = nullptr;
+  if (!slot) FPI_CUDA(cudaMallocHost(&slot, 256));
+  static_assert(sizeof(T) <= 256, "host_read of a large object");
+  FPI_CUDA(cudaMemcpyAsync(slot, d, sizeof(T), cudaMemcpyDeviceToHost, s));
   FPI_CUDA(cudaStreamSynchronize(s));
+  T v;
+  memcpy(&v, slot, sizeof(T));
   return v;
 }
 

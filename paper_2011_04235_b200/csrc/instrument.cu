@@ -13,6 +13,15 @@
 namespace fpi {
 void trace_point(fpi_context* h, const char* label) {
   static const bool on = getenv("FPI_TRACE") != nullptr;
+  static const bool host = getenv("FPI_TRACE_HOST") != nullptr;
+  if (host) {  // host wall time between points, no synchronisation: where does the host block?
+    static auto lasth = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - lasth).count();
+    if (ms > 5.0) fprintf(stderr, "[trace-host] %-28s %9.3f ms\n", label, ms);
+    lasth = now;
+    return;
+  }
   if (!on) return;
   static auto last = std::chrono::steady_clock::now();
   cudaStreamSynchronize(h->stream);

@@ -271,19 +271,6 @@ __global__ void k_pick_gcc_dev(const int32_t* __restrict__ act, const int* __res
   }
 }
 
-// Hubs: the first min(q, #positive) entries of the degree-descending (stable) active list.
-__global__ void k_assign_hubs_dev(const int32_t* __restrict__ sorted_ids, const uint32_t* __restrict__ sorted_deg,
-                                  int64_t q, int64_t hi, int32_t base, int64_t* __restrict__ fwd,
-                                  uint8_t* __restrict__ state, int* __restrict__ nhubs) {
-  FPI_GRID_STRIDE(i, q) {
-    if (sorted_deg[i] == 0) continue;
-    int32_t v = sorted_ids[i];
-    fwd[v - base] = hi - i;
-    state[v] = 0;
-    atomicAdd(nhubs, 1);
-  }
-}
-
 struct IterScalars {
   unsigned long long best;
   int32_t nroots, h_t, h_f, acnt, ne, gcc_rows, pad0, pad1;

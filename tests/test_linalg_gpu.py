@@ -90,3 +90,38 @@ def test_sym_eig(n):
     # the optional FP32-preconditioned mode (FPI_JACOBI_MIXED=1) reports 100*fp32 + fp64 sweeps
     fp32_sweeps, fp64_sweeps = divmod(sw.value, 100)
     assert 0 < fp64_sweeps < 60 and fp32_sweeps <= 40
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 200, 1000, 2048])
+def test_orth_factor_cholesky_inverse(n):
+    """fpi_orth_factor (one cooperative Cholesky + triangular inverse): Linv G Linv^T = I, Linv lower."""
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import d2h, empty
+    rng = np.random.default_rng(n)
+    B = rng.standard_normal((n + 5, n)) * np.logspace(0, -3, n)
+    G = B.T @ B
+    Li = empty((n, n))
+    cond = C.c_double(0.0)
+    _lib.call("fpi_orth_factor", n, _lib.ptr(_t(G)), _lib.ptr(Li), C.byref(cond))
+    Lh = d2h(Li)
+    assert np.abs(np.triu(Lh, 1)).max() == 0.0
+    np.testing.assert_allclose(Lh @ G @ Lh.T, np.eye(n), atol=1e-9)
+    L = np.linalg.cholesky(G)
+    np.testing.assert_allclose(Lh, np.linalg.inv(L), rtol=1e-7, atol=1e-9 * np.abs(np.linalg.inv(L)).max())
+    assert cond.value == pytest.approx(np.abs(np.diag(L)).max() / np.abs(np.diag(L)).min(), rel=1e-9)
+
+
+def test_orth_factor_rank_deficient_falls_back():
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import d2h, empty
+    rng = np.random.default_rng(3)
+    B = rng.standard_normal((50, 20))
+    B[:, 7] = B[:, 3]  # exactly rank deficient
+    G = B.T @ B
+    Li = empty((20, 20))
+    cond = C.c_double(0.0)
+    _lib.call("fpi_orth_factor", 20, _lib.ptr(_t(G)), _lib.ptr(Li), C.byref(cond))
+    Q = B @ d2h(Li).T
+    P = Q.T @ Q
+    assert np.isinf(cond.value) or cond.value > 1e7
+    np.testing.assert_allclose(P @ P, P, atol=1e-8)  # Q's columns orthonormal or zero
