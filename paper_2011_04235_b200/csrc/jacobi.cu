@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -697,7 +698,11 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
         if (pr_.done) continue;
         const double cur = __longlong_as_double((long long)pr_.offmax[sweep]);
         const double prev = sweep ? __longlong_as_double((long long)pr_.offmax[sweep - 1]) : 1e300;
-        if (cur <= tol || (cur < stagnate_below && cur > 0.25 * prev) || sweep + 1 == max_sweeps) {
+        // quadratic regime: this sweep leaves ~ C cur^2 with C = cur / prev^2 from the last step;
+        // stop when that is far below the tolerance (saves the confirming sweep)
+        const bool quad = sweep > 0 && cur < 1e-8 && prev > 0.0 && prev < 1e-3 &&
+                          (cur / (prev * prev)) * cur * cur <= 1e-2 * tol;
+        if (cur <= tol || quad || (cur < stagnate_below && cur > 0.25 * prev) || sweep + 1 == max_sweeps) {
           pr_.done = 1;
           pr_.sweeps = sweep + 1;
         }
@@ -746,12 +751,14 @@ __global__ void k_diag_keys(int64_t n, const double* G, int64_t npad, double* ke
   }
 }
 
+// V[:, k] = eigenvector order[k]; perm (optional): row a of Vp belongs to original index perm[a]
 __global__ void k_gather_eig(int64_t n, const double* Vp, int64_t npad, const int32_t* order, const double* wsorted,
-                             double* w, double* V, int64_t ldv) {
+                             const int32_t* perm, double* w, double* V, int64_t ldv) {
   FPI_GRID_STRIDE(e, n * n) {
-    int64_t i = e / n, k = e - i * n;
-    V[i * ldv + k] = Vp[i * npad + order[k]];
-    if (i == 0 && w) w[k] = wsorted[k];
+    int64_t a = e / n, k = e - a * n;
+    const int64_t i = perm ? perm[a] : a;
+    V[i * ldv + k] = Vp[a * npad + order[k]];
+    if (a == 0 && w) w[k] = wsorted[k];
   }
 }
 
@@ -862,6 +869,15 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     FPI_CUDA(cudaStreamSynchronize(s));
     fprintf(stderr, "[jacobi nprob=%d n0=%lld grid=%d gchunk=%d vchunk=%d] section %.3f (subsolve %.3f)  sync %.3f ms\n",
             nprob, (long long)n[0], grid, gchunk, vchunk, hq[0] * 1e-6, hq[4] * 1e-6, hq[1] * 1e-6);
+    std::vector<unsigned long long> om((size_t)max_sweeps + 1);
+    FPI_CUDA(cudaMemcpy(om.data(), offm.get(), sizeof(unsigned long long) * om.size(), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "[jacobi] problem 0 off-diagonal measure per sweep (tol %.1e):", tol);
+    for (int i = 0; i < hp[0].sweeps; ++i) {
+      double v;
+      memcpy(&v, &om[(size_t)i], sizeof(double));
+      fprintf(stderr, " %.2e", v);
+    }
+    fprintf(stderr, "\n");
   }
   // eigenvalues (descending diagonal) and the matching columns of V
   CubTemp tmp(s);
@@ -871,7 +887,8 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     k_diag_keys<<<grid_for(n[i], 256, h->num_sms * 4), 256, 0, s>>>(n[i], hp[i].G[hp[i].gfinal], npad[i], keys,
                                                                        idx);
     sort_pairs(tmp, keys.get(), keys2.get(), idx.get(), idx2.get(), n[i], true, 0, 64, s);
-    k_gather_eig<<<grid_for(n[i] * n[i], 256, G16), 256, 0, s>>>(n[i], Vall.get() + goff[i], npad[i], idx2, keys2, w[i],
+    k_gather_eig<<<grid_for(n[i] * n[i], 256, G16), 256, 0, s>>>(n[i], Vall.get() + goff[i], npad[i], idx2, keys2,
+                                                                  nullptr, w[i],
                                                                   V[i], ldv[i]);
     note_launch(h, 3);
   }
