@@ -4,10 +4,9 @@
 //
 //   C = alpha * op(A) * op(B) + beta * C,   all row-major, op = identity / transpose
 //
-// CTA tile 128 x 64 x 16, 8 warps (4 x 2), warp tile 32 x 32 = 4 x 4 DMMA tiles
-// (32 accumulator doubles per thread), two CTAs per SM: 4 warps per SM
-// sub-partition keep the DMMA pipe fed, and while one CTA sits at its k-tile
-// barrier the other keeps issuing.  Operands stream global -> smem with a
+// CTA tile 64 x 64 x 16, 4 warps (2 x 2), warp tile 32 x 32 = 4 x 4 DMMA tiles
+// (32 accumulator doubles per thread), three CTAs per SM: while one CTA sits at
+// its k-tile barrier the others keep the DMMA pipe issuing.  Operands stream global -> smem with a
 // 3-stage cp.async ring (16-byte copies when the operands are 16-byte aligned
 // along their contiguous dimension, 8-byte otherwise); the smem layouts are
 // padded so every fragment load is bank-conflict free for all four transpose
@@ -28,8 +27,22 @@
 namespace fpi {
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, NT = 256;
-constexpr int WARPS_N = BN / 32;  // warp grid (BM / 32) x (BN / 32)
+// Tile configuration (tools/gemm_variants.sh measures the alternatives on the solve's shapes:
+// 128x64 / 2 CTAs, 64x32 / 4-5 CTAs, 64x64 / 4 stages, 128x128 / 64x32 warps all land at 28-31
+// TFLOP/s; 64x64 with 4 warps and 3 CTAs per SM is the best overall at 31-32).
+#ifndef FPI_GEMM_CFG_BM
+#define FPI_GEMM_CFG_BM 64
+#define FPI_GEMM_CFG_BN 64
+#define FPI_GEMM_CFG_WM 32
+#define FPI_GEMM_CFG_WN 32
+#define FPI_GEMM_CFG_STAGES 3
+#define FPI_GEMM_CFG_CTAS 3
+#endif
+constexpr int BM = FPI_GEMM_CFG_BM, BN = FPI_GEMM_CFG_BN, BK = 16, STAGES = FPI_GEMM_CFG_STAGES;
+constexpr int WM = FPI_GEMM_CFG_WM, WN = FPI_GEMM_CFG_WN;  // warp tile
+constexpr int MI = WM / 8, NJ = WN / 8;                    // DMMA tiles per warp
+constexpr int WARPS_N = BN / WN;                            // warp grid (BM / WM) x (BN / WN)
+constexpr int NT = (BM / WM) * (BN / WN) * 32;
 constexpr int PAD = 4;
 // smem strides (doubles)
 constexpr int LDA_MK = BK + PAD;   // As[m][k]
@@ -39,7 +52,7 @@ constexpr int LDB_NK = BK + PAD;   // Bs[n][k]
 constexpr int A_STAGE = (BM * LDA_MK > BK * LDA_KM) ? BM * LDA_MK : BK * LDA_KM;
 constexpr int B_STAGE = (BN * LDB_NK > BK * LDB_KN) ? BN * LDB_NK : BK * LDB_KN;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
-static_assert((BM / 32) * (BN / 32) * 32 == NT, "one warp per 32 x 32 warp tile");
+static_assert((BM * BK) % NT == 0 && (BN * BK) % NT == 0, "tile loads divide evenly over the threads");
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
   unsigned saddr = (unsigned)__cvta_generic_to_shared(smem);
@@ -117,7 +130,7 @@ __host__ __device__ __forceinline__ bool tile_above_diag(int64_t bx, int64_t by)
 }
 
 template <bool TA, bool TB, bool V16>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, FPI_GEMM_CFG_CTAS)
     k_gemm(int64_t M, int64_t N, int64_t K, double alpha, const double* __restrict__ A, int64_t lda,
            const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
            int64_t k_per_split, double* __restrict__ partial, int sym) {
@@ -130,14 +143,14 @@ __global__ void __launch_bounds__(NT, 2)
   const int64_t ke = kb + k_per_split < K ? kb + k_per_split : K;
   const int64_t ntiles = ke > kb ? (ke - kb + BK - 1) / BK : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp / WARPS_N) * 32, wn = (warp % WARPS_N) * 32;
+  const int wm = (warp / WARPS_N) * WM, wn = (warp % WARPS_N) * WN;
   const int g = lane >> 2, t = lane & 3;
 
-  double acc[4][4][2];
+  double acc[MI][NJ][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   // prologue
 #pragma unroll
@@ -162,21 +175,21 @@ __global__ void __launch_bounds__(NT, 2)
     const double* bs = Bs + (kt % STAGES) * B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
+      double af[MI], bf[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < MI; ++i) {
         int m = wm + i * 8 + g;
         af[i] = TA ? as[(kk + t) * LDA_KM + m] : as[m * LDA_MK + kk + t];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         int n = wn + j * 8 + g;
         bf[j] = TB ? bs[n * LDB_NK + kk + t] : bs[(kk + t) * LDB_KN + n];
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_async_wait<0>();
@@ -185,11 +198,11 @@ __global__ void __launch_bounds__(NT, 2)
   if (partial) {
     double* P = partial + (int64_t)blockIdx.z * M * N;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < MI; ++i) {
       int64_t r = m0 + wm + i * 8 + g;
       if (r >= M) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < NJ; ++j) {
         int64_t c = n0 + wn + j * 8 + 2 * t;
         if (c < N && (!sym || c <= r)) P[r * N + c] = acc[i][j][0];
         if (c + 1 < N && (!sym || c + 1 <= r)) P[r * N + c + 1] = acc[i][j][1];
@@ -198,11 +211,11 @@ __global__ void __launch_bounds__(NT, 2)
     return;
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < MI; ++i) {
     int64_t r = m0 + wm + i * 8 + g;
     if (r >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       int64_t c = n0 + wn + j * 8 + 2 * t;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
@@ -245,7 +258,7 @@ __global__ void k_scale(int64_t M, int64_t N, double beta, double* __restrict__ 
 
 // Split count: minimise (waves of CTAs) x (K per CTA) + the partial-tile reduction traffic.
 int choose_splits(int64_t tiles, int64_t M, int64_t N, int64_t K, int num_sms) {
-  const int64_t slots = 2LL * num_sms;  // resident CTAs
+  const int64_t slots = (int64_t)FPI_GEMM_CFG_CTAS * num_sms;  // resident CTAs
   const double cta_flops = 36.0e12 / (double)slots, red_bw = 4.0e12;
   int best = 1;
   double best_t = 1e300;
