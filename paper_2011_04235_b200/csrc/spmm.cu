@@ -3,9 +3,10 @@
 // which covers inner @ X (svd.py:133 via sparse.py:28) and, applied to the
 // transposed CSR, inner^T @ Q (svd.py:135 via sparse.py:39) and Y^T U (pinv.py:75).
 //
-// Short rows: one warp owns one output row and a 128-column slice (4 doubles
-// per lane, 16-byte loads), nnz fetched 32 at a time and broadcast with
-// shuffles, four X rows in flight per lane.  grid.y walks the column slices so
+// Short rows: one warp owns one output row and a 64-column slice (2 doubles
+// per lane; one 16-byte load per lane covers 512 contiguous bytes of an X row),
+// nnz fetched 32 at a time and broadcast with shuffles, eight X rows in flight
+// per lane.  grid.y walks the column slices so
 // a slice of X stays L2-resident while every row streams past it.
 // Long rows (hub rows of T^T, popular labels of Y^T, ...): split into segments
 // of SEG nonzeros, one warp per (segment, slice) writing a partial row, then
@@ -21,17 +22,46 @@ namespace fpi {
 namespace {
 
 constexpr int WARPS = 8;       // warps per CTA
-constexpr int SLICE = 128;     // output columns per warp pass (4 per lane)
+constexpr int SLICE = 64;      // output columns per warp pass (2 per lane)
+#ifndef FPI_SPMM_UNROLL
+#define FPI_SPMM_UNROLL 8
+#endif
+#ifndef FPI_SPMM_MINB
+#define FPI_SPMM_MINB 3
+#endif
+constexpr int UNROLL = FPI_SPMM_UNROLL;  // gathered X rows in flight per lane
 constexpr int64_t SEG = 512;   // nonzeros per long-row segment (rows longer than this are split)
 
-struct Acc4 {
-  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+// Column ownership inside a 64-column slice starting at c0:
+//   VEC   : lane owns c0 + 2 lane, c0 + 2 lane + 1   (one 16-byte load, 512 contiguous bytes per warp)
+//   scalar: lane owns c0 + lane,   c0 + 32 + lane    (two 8-byte loads, 256 contiguous bytes each)
+// Lanes past column k load column 0 (always valid) and never store, so the gathers carry no
+// predicates.  In VEC mode an odd k leaves the last lane's pair half outside the row: the 16-byte
+// load stays inside the aligned 16-byte block that holds column k - 1 (ldx is even).
+template <bool VEC>
+struct Cols {
+  int64_t a, b;      // owned columns
+  int32_t la, lb;    // load offsets
+  __device__ __forceinline__ Cols(int64_t c0, int lane, int64_t k)
+      : a(VEC ? c0 + 2 * lane : c0 + lane), b(VEC ? c0 + 2 * lane + 1 : c0 + 32 + lane) {
+    la = a < k ? (int32_t)a : 0;
+    lb = b < k ? (int32_t)b : 0;
+  }
 };
 
 template <bool VEC>
+__device__ __forceinline__ double2 load2(const double* __restrict__ xr, const Cols<VEC>& c) {
+  if (VEC) return __ldg(reinterpret_cast<const double2*>(xr + c.la));
+  return make_double2(__ldg(xr + c.la), __ldg(xr + c.lb));
+}
+
+// acc += sum_{j in [b, e)} values[j] * X[indices[j], cols]; nonzeros fetched 32 at a time and
+// broadcast with shuffles, UNROLL gathered rows in flight per lane.
+template <bool VEC>
 __device__ __forceinline__ void accumulate_range(int64_t b, int64_t e, const int32_t* __restrict__ indices,
                                                  const double* __restrict__ values, const double* __restrict__ X,
-                                                 int64_t ldx, int64_t k, int64_t c0, int lane, Acc4& acc) {
+                                                 int64_t ldx, int64_t k, const Cols<VEC>& c, int lane,
+                                                 double2& acc) {
   for (int64_t base = b; base < e; base += 32) {
     const int64_t my = base + lane;
     int32_t col = 0;
@@ -42,70 +72,61 @@ __device__ __forceinline__ void accumulate_range(int64_t b, int64_t e, const int
     }
     const int cnt = (int)((e - base) < 32 ? (e - base) : 32);
     int j = 0;
-    if (VEC && c0 + 3 < k) {
-      for (; j + 4 <= cnt; j += 4) {
-        double2 xa[4], xb[4];
-        double v[4];
+    for (; j + UNROLL <= cnt; j += UNROLL) {
+      double2 x[UNROLL];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int32_t cj = __shfl_sync(0xffffffffu, col, j + u);
-          v[u] = __shfl_sync(0xffffffffu, val, j + u);
-          const double* xr = X + (int64_t)cj * ldx + c0;
-          xa[u] = __ldg(reinterpret_cast<const double2*>(xr));
-          xb[u] = __ldg(reinterpret_cast<const double2*>(xr + 2));
-        }
+      for (int u = 0; u < UNROLL; ++u) {
+        const int32_t cj = __shfl_sync(0xffffffffu, col, j + u);
+        x[u] = load2<VEC>(X + (int64_t)cj * ldx, c);
+      }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          acc.a0 = fma(v[u], xa[u].x, acc.a0);
-          acc.a1 = fma(v[u], xa[u].y, acc.a1);
-          acc.a2 = fma(v[u], xb[u].x, acc.a2);
-          acc.a3 = fma(v[u], xb[u].y, acc.a3);
-        }
+      for (int u = 0; u < UNROLL; ++u) {
+        const double v = __shfl_sync(0xffffffffu, val, j + u);
+        acc.x = fma(v, x[u].x, acc.x);
+        acc.y = fma(v, x[u].y, acc.y);
       }
     }
-    for (; j < cnt; ++j) {
-      const int32_t cj = __shfl_sync(0xffffffffu, col, j);
-      const double vj = __shfl_sync(0xffffffffu, val, j);
-      const double* xr = X + (int64_t)cj * ldx;
-      if (VEC && c0 + 3 < k) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(xr + c0));
-        const double2 bb = __ldg(reinterpret_cast<const double2*>(xr + c0 + 2));
-        acc.a0 = fma(vj, a.x, acc.a0);
-        acc.a1 = fma(vj, a.y, acc.a1);
-        acc.a2 = fma(vj, bb.x, acc.a2);
-        acc.a3 = fma(vj, bb.y, acc.a3);
-      } else {
-        if (c0 < k) acc.a0 = fma(vj, xr[c0], acc.a0);
-        if (c0 + 1 < k) acc.a1 = fma(vj, xr[c0 + 1], acc.a1);
-        if (c0 + 2 < k) acc.a2 = fma(vj, xr[c0 + 2], acc.a2);
-        if (c0 + 3 < k) acc.a3 = fma(vj, xr[c0 + 3], acc.a3);
+    if (j < cnt) {  // tail: up to UNROLL - 1 rows, still issued together
+      double2 x[UNROLL - 1];
+#pragma unroll
+      for (int u = 0; u < UNROLL - 1; ++u) {
+        const int32_t cj = __shfl_sync(0xffffffffu, col, (j + u) & 31);
+        x[u] = j + u < cnt ? load2<VEC>(X + (int64_t)cj * ldx, c) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL - 1; ++u) {
+        const double v = __shfl_sync(0xffffffffu, val, (j + u) & 31);
+        if (j + u < cnt) {
+          acc.x = fma(v, x[u].x, acc.x);
+          acc.y = fma(v, x[u].y, acc.y);
+        }
       }
     }
   }
 }
 
-__device__ __forceinline__ void store4(double* yr, int64_t c0, int64_t k, double s, double beta, const Acc4& a) {
-  const double acc[4] = {a.a0, a.a1, a.a2, a.a3};
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (c0 + q < k) yr[c0 + q] = beta == 0.0 ? s * acc[q] : s * acc[q] + beta * yr[c0 + q];
+template <bool VEC>
+__device__ __forceinline__ void store2(double* yr, const Cols<VEC>& c, int64_t k, double s, double beta,
+                                       const double2& a) {
+  if (c.a < k) yr[c.a] = beta == 0.0 ? s * a.x : s * a.x + beta * yr[c.a];
+  if (c.b < k) yr[c.b] = beta == 0.0 ? s * a.y : s * a.y + beta * yr[c.b];
 }
 
 template <bool VEC>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 2)
     k_spmm(int64_t p, int64_t k, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
            const double* __restrict__ values, const double* __restrict__ row_scale, double alpha,
            const double* __restrict__ X, int64_t ldx, double beta, double* __restrict__ Y, int64_t ldy,
            int64_t long_thresh) {
   const int lane = threadIdx.x & 31;
-  const int64_t c0 = (int64_t)blockIdx.y * SLICE + lane * 4;
+  const Cols<VEC> c((int64_t)blockIdx.y * SLICE, lane, k);
   for (int64_t row = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); row < p; row += (int64_t)gridDim.x * WARPS) {
     const int64_t b = indptr[row], e = indptr[row + 1];
     if (e - b > long_thresh) continue;  // handled by the segmented path
-    Acc4 acc;
-    accumulate_range<VEC>(b, e, indices, values, X, ldx, k, c0, lane, acc);
+    double2 acc = make_double2(0.0, 0.0);
+    accumulate_range<VEC>(b, e, indices, values, X, ldx, k, c, lane, acc);
     const double s = row_scale ? alpha * row_scale[row] : alpha;
-    store4(Y + row * ldy, c0, k, s, beta, acc);
+    store2<VEC>(Y + row * ldy, c, k, s, beta, acc);
   }
 }
 
@@ -129,13 +150,13 @@ __global__ void k_seg_counts(const int64_t* __restrict__ rows, int64_t nl, const
 
 // one warp per (segment, slice): partial row into P[seg][k]
 template <bool VEC>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 2)
     k_spmm_segments(const int64_t* __restrict__ rows, const int64_t* __restrict__ seg_off, int64_t nl,
                     int64_t nseg_total, int64_t k, const int64_t* __restrict__ indptr,
                     const int32_t* __restrict__ indices, const double* __restrict__ values,
                     const double* __restrict__ X, int64_t ldx, double* __restrict__ P) {
   const int lane = threadIdx.x & 31;
-  const int64_t c0 = (int64_t)blockIdx.y * SLICE + lane * 4;
+  const Cols<VEC> c((int64_t)blockIdx.y * SLICE, lane, k);
   for (int64_t sg = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); sg < nseg_total;
        sg += (int64_t)gridDim.x * WARPS) {
     // owning long row: last i with seg_off[i] <= sg
@@ -148,9 +169,9 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int64_t b = indptr[r] + (sg - seg_off[lo]) * SEG;
     const int64_t e0 = indptr[r + 1];
     const int64_t e = b + SEG < e0 ? b + SEG : e0;
-    Acc4 acc;
-    accumulate_range<VEC>(b, e, indices, values, X, ldx, k, c0, lane, acc);
-    store4(P + sg * k, c0, k, 1.0, 0.0, acc);
+    double2 acc = make_double2(0.0, 0.0);
+    accumulate_range<VEC>(b, e, indices, values, X, ldx, k, c, lane, acc);
+    store2<VEC>(P + sg * k, c, k, 1.0, 0.0, acc);
   }
 }
 
