@@ -29,6 +29,7 @@
 #include "capi_guard.cuh"
 #include "cub_util.cuh"
 #include "instrument.cuh"
+#include "reorder.cuh"
 #include <cmath>
 
 namespace fpi {
@@ -309,10 +310,6 @@ __global__ void k_reset_nodes_dev(const int32_t* __restrict__ act, int64_t cnt, 
 
 }  // namespace
 
-struct ReorderOut {
-  int64_t m1, n1, m2, n2, T;
-};
-
 // One host synchronisation per iteration: every count the host needs (hubs taken, active
 // nodes left, component count, giant component) is gathered into one pinned readback; edge
 // and node kernels take their lengths from device memory.
@@ -373,7 +370,9 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
   const int deg_bits = bits_for((uint64_t)(m > n ? m : n));
   const int rank_bits = bits_for((uint64_t)V);
 
-  const bool trace = getenv("FPI_TRACE_REORDER") != nullptr;
+  const char* trace_env = getenv("FPI_TRACE_REORDER");
+  const bool trace = trace_env != nullptr;
+  const double trace_min_ms = trace ? atof(trace_env) : 0.0;  // print iterations at least this long
   auto titer = std::chrono::steady_clock::now();
   if (trace) fprintf(stderr, "[reorder] setup %.2f ms\n", std::chrono::duration<double, std::milli>(titer - t_enter).count());
   while (true) {
@@ -413,7 +412,7 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
       const auto now = std::chrono::steady_clock::now();
       const double it_ms = std::chrono::duration<double, std::milli>(now - titer).count();
       const double sy_ms = std::chrono::duration<double, std::milli>(now - tsync0).count();
-      if (it_ms > 2.0) fprintf(stderr, "[reorder] iteration %lld: %.2f ms (sync wait %.2f ms)\n", (long long)iters, it_ms, sy_ms);
+      if (it_ms >= trace_min_ms) fprintf(stderr, "[reorder] iteration %lld: %.2f ms (sync wait %.2f ms)\n", (long long)iters, it_ms, sy_ms);
       titer = now;
     }
     FPI_LAUNCH_CHECK();
@@ -498,7 +497,10 @@ extern "C" int fpi_reorder(fpi_handle h, int64_t m, int64_t n, int64_t nnz, cons
   FPI_API_BEGIN(h)
   fpi::ReorderOut o{};
   fpi::KTimer kt(h, "reorder_loop(all kernels)", 0.0, 0.0);
-  fpi::run_reorder(h, m, n, nnz, d_indptr, d_indices, k, d_row_fwd, d_col_fwd, o);
+  // the persistent device loop unless it is outside its static limits (or the host loop is forced)
+  const bool hostloop = getenv("FPI_REORDER_HOSTLOOP") != nullptr;
+  if (hostloop || !fpi::run_reorder_persistent(h, m, n, nnz, d_indptr, d_indices, k, d_row_fwd, d_col_fwd, o))
+    fpi::run_reorder(h, m, n, nnz, d_indptr, d_indices, k, d_row_fwd, d_col_fwd, o);
   if (info) {
     info->m1 = o.m1;
     info->n1 = o.n1;

@@ -75,3 +75,29 @@ def test_reorder_domain_errors():
         _gpu_reorder(A, 0.0)
     with pytest.raises(ValueError):
         _gpu_reorder(A, 1.0)
+
+
+def _skewed(m, n, nnz, seed, row_const=None):
+    """Power-law bipartite graph (many isolated / small spoke components in early iterations)."""
+    rng = np.random.default_rng(seed)
+    if row_const:
+        rows = np.repeat(np.arange(m), row_const)
+    else:
+        rows = np.minimum((rng.pareto(1.2, nnz) * 3).astype(np.int64), m - 1)
+        rows = rng.permutation(m)[rows]
+    cols = np.minimum((rng.pareto(1.0, rows.size) * 2).astype(np.int64), n - 1)
+    cols = rng.permutation(n)[cols]
+    return sp.csr_matrix((np.ones(rows.size), (rows, cols)), shape=(m, n))
+
+
+@pytest.mark.parametrize("host_loop", [False, True])
+@pytest.mark.parametrize("case", [(60000, 20000, 150000, 0.01, 0), (40000, 30000, 60000, 0.005, 1),
+                                  (30000, 8000, 0, 0.05, 2), (100000, 5000, 300000, 0.02, 3)])
+def test_reorder_large_paths(case, host_loop, monkeypatch):
+    """Large spoke stages (grid-wide radix passes, > 8192 nodes / components per iteration), tie
+    splitting at the hub threshold (constant row degrees), both device drivers."""
+    m, n, nnz, k, seed = case
+    if host_loop:
+        monkeypatch.setenv("FPI_REORDER_HOSTLOOP", "1")
+    A = _skewed(m, n, nnz, seed, row_const=3 if nnz == 0 else None)
+    _check_against_oracle(A, k)
