@@ -5,6 +5,9 @@
 namespace fpi {
 void cholesky_lower(fpi_context* h, int64_t n, double* A, int64_t lda, int* h_info);
 void trsm_lower_left(fpi_context* h, int64_t n, const double* L, int64_t ldl, double* X, int64_t ldx, int64_t nrhs);
+// L (lower, upper zeroed) and L^-1 of an SPD matrix in one dataflow kernel; false if disabled
+bool chol_inverse_dataflow(fpi_context* h, int64_t n, const double* G, int64_t ldg, double* L, int64_t ldl,
+                           double* Linv, int64_t ldi, int* h_info);
 void lower_inverse(fpi_context* h, int64_t n, const double* L, int64_t ldl, double* Linv, int64_t ldi);
 // eigenvalues descending in w (n), eigenvectors as columns of V (n x n); returns Jacobi sweeps used
 // Converged when every |a_pq| <= tol * sqrt(|a_pp a_qq|) (relative), or, with `absolute`,

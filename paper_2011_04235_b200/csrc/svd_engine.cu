@@ -564,9 +564,13 @@ void orth_factor(fpi_context* h, int64_t k, const double* Gm, double* Linv, fpi_
   // (A one-kernel cooperative Cholesky + inverse was measured at 1.6 vs 2.5 ms for k = 1000 but
   // stalled the stream for 0.1-0.6 s on some launches; the launch-per-panel path below is kept.)
   Scratch<double> Gc(k * k, s);
-  FPI_CUDA(cudaMemcpyAsync(Gc.get(), Gm, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, s));
   int info = 0;
-  cholesky_lower(h, k, Gc, k, &info);
+  // L and L^-1 in one tile-dataflow kernel (chol_dataflow.cu); the blocked panel path otherwise
+  const bool fused = chol_inverse_dataflow(h, k, Gm, k, Gc, k, Linv, k, &info);
+  if (!fused) {
+    FPI_CUDA(cudaMemcpyAsync(Gc.get(), Gm, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, s));
+    cholesky_lower(h, k, Gc, k, &info);
+  }
   if (info == 0) {
     if (diag) {
       Scratch<double> ratio(1, s);
@@ -574,7 +578,7 @@ void orth_factor(fpi_context* h, int64_t k, const double* Gm, double* Linv, fpi_
       diag->cond_estimate = host_read(ratio.get(), s);
       diag->cholqr_passes = 1;
     }
-    lower_inverse(h, k, Gc, k, Linv, k);
+    if (!fused) lower_inverse(h, k, Gc, k, Linv, k);
     return;
   }
   // not numerically PD (B rank deficient): orthonormalise through the eigendecomposition
