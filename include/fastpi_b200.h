@@ -254,6 +254,13 @@ int fpi_pinv_apply_csr(fpi_handle h, int64_t m, int64_t n, int64_t r, const doub
                        const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
                        const int64_t* d_col_fwd, int64_t L, int64_t nnz, const int64_t* y_ptr,
                        const int32_t* y_idx, const double* y_val, double* d_Z);
+/* fpi_pinv_apply_csr with Z written to HOST memory h_Z (n x L, page-locked for overlap): the lift
+ * runs in row chunks whose device->host copies overlap the next chunk's GEMM; returns when h_Z is
+ * complete.  Replaces the pinv.py:72-81 apply + the host copy of its result. */
+int fpi_pinv_apply_csr_host(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U,
+                            const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
+                            const int64_t* d_col_fwd, int64_t L, int64_t nnz, const int64_t* y_ptr,
+                            const int32_t* y_idx, const double* y_val, double* h_Z);
 /* One row shard of pinv.py:75's U^T Y: W (L x r) = sum over the rows of Y whose reordered index lies
  * in [r0, r0 + m_loc) of Y[i, :]^T U_loc[row_fwd[i] - r0, :]; the shards' W sum to the full product
  * (the multi-GPU all-reduce operand).  Y is CSR (m x L) in original row order. */

@@ -97,6 +97,7 @@ SIGNATURES = {
     "fpi_pinv_assemble": (C.c_int, [vp, i64, vp, i64, i64, f64, vp, C.POINTER(f64), C.POINTER(i32)]),
     "fpi_unfold": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
     "fpi_pinv_apply_csr": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp]),
+    "fpi_pinv_apply_csr_host": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp, vp]),
     "fpi_pinv_project_csr": (C.c_int, [vp, i64, i64, i64, vp, vp, i64, i64, i64, vp, vp, vp, vp]),
     "fpi_pinv_lift": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, vp]),
     "fpi_pinv_apply_dense": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp]),

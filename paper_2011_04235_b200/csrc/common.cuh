@@ -51,6 +51,8 @@ struct fpi_context {
   int64_t n_spans = 0;
   int64_t spans_cap = 0;
   void* host_scalars = nullptr;  // pinned scratch for per-iteration device scalars (reorder)
+  cudaStream_t copy_stream = nullptr;  // device->host copies overlapped with the compute stream
+  cudaEvent_t copy_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // numerics diagnostics of the last randomized / dense SVD
   fpi_svd_diag diag{};
   // counters

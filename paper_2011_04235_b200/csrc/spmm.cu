@@ -49,10 +49,34 @@ struct Cols {
   }
 };
 
+#ifndef FPI_SPMM_LOAD
+#define FPI_SPMM_LOAD 0
+#endif
+// gather of one X row slice: 0 = ld.global.nc (L1-allocating), 1 = ld.global.cg (L2 only),
+// 2 = ld.global.nc.L1::no_allocate
+__device__ __forceinline__ double2 ldx2(const double* p) {
+#if FPI_SPMM_LOAD == 1
+  return __ldcg(reinterpret_cast<const double2*>(p));
+#elif FPI_SPMM_LOAD == 2
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#else
+  return __ldg(reinterpret_cast<const double2*>(p));
+#endif
+}
+__device__ __forceinline__ double ldx1(const double* p) {
+#if FPI_SPMM_LOAD == 1
+  return __ldcg(p);
+#else
+  return __ldg(p);
+#endif
+}
+
 template <bool VEC>
 __device__ __forceinline__ double2 load2(const double* __restrict__ xr, const Cols<VEC>& c) {
-  if (VEC) return __ldg(reinterpret_cast<const double2*>(xr + c.la));
-  return make_double2(__ldg(xr + c.la), __ldg(xr + c.lb));
+  if (VEC) return ldx2(xr + c.la);
+  return make_double2(ldx1(xr + c.la), ldx1(xr + c.lb));
 }
 
 // acc += sum_{j in [b, e)} values[j] * X[indices[j], cols]; nonzeros fetched 32 at a time and

@@ -906,6 +906,62 @@ void pinv_apply_csr(fpi_context* h, int64_t m, int64_t n, int64_t r, const doubl
   pinv_lift(h, n, r, sdag, Vt, col_fwd, L, W, Z);
 }
 
+// Columns of Vt in original order: Vg[:, i] = Vt[:, col_fwd[i]] (the unfold of pinv.py:271-275 for V).
+__global__ void k_gather_cols(int64_t r, int64_t n, const double* __restrict__ Vt, const int64_t* __restrict__ col_fwd,
+                              double* __restrict__ Vg) {
+  FPI_GRID_STRIDE(e, r * n) {
+    const int64_t k = e / n, i = e - k * n;
+    Vg[e] = Vt[k * n + col_fwd[i]];
+  }
+}
+
+// pinv_apply_csr straight into host memory: the lift Z = V diag(sigma+) W^T runs in row chunks of
+// the original order, each chunk's device->host copy (copy stream) overlapping the next chunk's
+// GEMM.  h_Z must be page-locked for the copies to be asynchronous.
+void pinv_apply_csr_host(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* sdag,
+                         const double* Vt, const int64_t* row_fwd, const int64_t* col_fwd, int64_t L, int64_t nnz,
+                         const int64_t* y_ptr, const int32_t* y_idx, const double* y_val, double* h_Z) {
+  cudaStream_t s = h->stream;
+  if (n == 0 || L == 0) return;
+  if (r == 0) {
+    memset(h_Z, 0, sizeof(double) * n * L);
+    return;
+  }
+  if (!h->copy_stream) FPI_CUDA(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  for (auto& e : h->copy_ev)
+    if (!e) FPI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  Scratch<double> W(L * r, s), Vg(r * n, s);
+  pinv_project_csr(h, 0, m, r, U, row_fwd, m, L, nnz, y_ptr, y_idx, y_val, W);
+  scale_cols(h, L, r, W, r, sdag, false);
+  k_gather_cols<<<grid_for(r * n, 256, (int64_t)h->num_sms * 16), 256, 0, s>>>(r, n, Vt, col_fwd, Vg);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+  // ~64 MB chunks, at least 256 rows, double-buffered on the device
+  int64_t rows = (int64_t)((64ll << 20) / (8 * L));
+  if (rows < 256) rows = 256;
+  if (rows > n) rows = n;
+  Scratch<double> buf(2 * rows * L, s);
+  cudaStream_t cs = h->copy_stream;
+  cudaEvent_t* ready = h->copy_ev;      // [0], [1]: chunk computed
+  cudaEvent_t* drained = h->copy_ev + 2;  // [2], [3]: buffer copied out
+  int64_t c = 0;
+  for (int64_t a = 0; a < n; a += rows, ++c) {
+    const int64_t nr = (n - a < rows) ? n - a : rows;
+    const int sl = (int)(c & 1);
+    double* d = buf.get() + sl * rows * L;
+    if (c >= 2) FPI_CUDA(cudaStreamWaitEvent(s, drained[sl], 0));
+    gemm(h, true, true, nr, L, r, 1.0, Vg.get() + a, n, W, r, 0.0, d, L);
+    FPI_CUDA(cudaEventRecord(ready[sl], s));
+    FPI_CUDA(cudaStreamWaitEvent(cs, ready[sl], 0));
+    FPI_CUDA(cudaMemcpyAsync(h_Z + a * L, d, sizeof(double) * nr * L, cudaMemcpyDeviceToHost, cs));
+    FPI_CUDA(cudaEventRecord(drained[sl], cs));
+  }
+  // the compute stream owns the scratch: it must not be freed before the last copy
+  FPI_CUDA(cudaStreamWaitEvent(s, drained[0], 0));
+  FPI_CUDA(cudaStreamWaitEvent(s, drained[1], 0));
+  FPI_CUDA(cudaStreamSynchronize(s));
+}
+
 void pinv_apply_dense(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* sdag,
                       const double* Vt, const int64_t* row_fwd, const int64_t* col_fwd, int64_t L, const double* Y,
                       int64_t ldy, double* Z) {
@@ -1055,6 +1111,16 @@ extern "C" int fpi_pinv_apply_csr(fpi_handle h, int64_t m, int64_t n, int64_t r,
                                   const int32_t* y_idx, const double* y_val, double* d_Z) {
   FPI_API_BEGIN(h)
   fpi::pinv_apply_csr(h, m, n, r, d_U, d_sigma_dagger, d_Vt, d_row_fwd, d_col_fwd, L, nnz, y_ptr, y_idx, y_val, d_Z);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_pinv_apply_csr_host(fpi_handle h, int64_t m, int64_t n, int64_t r, const double* d_U,
+                                       const double* d_sigma_dagger, const double* d_Vt, const int64_t* d_row_fwd,
+                                       const int64_t* d_col_fwd, int64_t L, int64_t nnz, const int64_t* y_ptr,
+                                       const int32_t* y_idx, const double* y_val, double* h_Z) {
+  FPI_API_BEGIN(h)
+  fpi::pinv_apply_csr_host(h, m, n, r, d_U, d_sigma_dagger, d_Vt, d_row_fwd, d_col_fwd, L, nnz, y_ptr, y_idx, y_val,
+                           h_Z);
   FPI_API_END(h)
 }
 

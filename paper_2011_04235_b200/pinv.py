@@ -137,12 +137,26 @@ class Pseudoinverse:
     def apply(self, B) -> np.ndarray:
         """pinv.py:72-81: ``pinv @ B`` right-to-left without materialising pinv."""
         if sp.issparse(B):
-            Z = self.apply_device(DeviceCSR.from_host(B))
+            return self._apply_csr_to_host(DeviceCSR.from_host(B))
         elif isinstance(B, DeviceCSR) or type(B).__module__.startswith("torch"):
             Z = self.apply_device(B)
         else:
             Z = self.apply_device(h2d(np.asarray(B, dtype=np.float64)))
         return d2h(Z)
+
+    def _apply_csr_to_host(self, Bd: DeviceCSR) -> np.ndarray:
+        """Sparse ``pinv @ B`` returned in host memory: the lift's row chunks are copied out while the
+        next chunk computes (fpi_pinv_apply_csr_host), into page-locked memory."""
+        d = self._device()
+        if Bd.shape[0] != d.m:
+            raise ValueError(f"dimension mismatch: pseudoinverse expects {d.m} rows, got {Bd.shape[0]}")
+        t = torch()
+        L = Bd.shape[1]
+        Zh = t.empty((d.n, L), dtype=t.float64, pin_memory=True)
+        _lib.call("fpi_pinv_apply_csr_host", d.m, d.n, d.r, _lib.ptr(d.U), _lib.ptr(d.sdag), _lib.ptr(d.Vt),
+                  _lib.ptr(d.row_fwd), _lib.ptr(d.col_fwd), L, Bd.nnz, _lib.ptr(Bd.indptr), _lib.ptr(Bd.indices),
+                  _lib.ptr(Bd.values), Zh.data_ptr())
+        return Zh.numpy()
 
     def validate(self, tol: float = 1e-8):
         r = len(self.sigma_dagger)

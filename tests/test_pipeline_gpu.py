@@ -179,3 +179,17 @@ def test_stagewise_parity_c4():
     ff = res.factors
     assert np.abs(ff.sigma - fo_full.sigma).max() <= SIG_TOL * fo_full.sigma[0]
     assert _lowrank_rel_factored(ff, fo_full) <= REC_TOL
+
+
+def test_apply_to_host_matches_device_apply():
+    """Pseudoinverse.apply on a sparse operand (chunked lift with overlapped device->host copies)
+    agrees with the device-resident apply."""
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200._device import DeviceCSR, d2h
+    p = problem("c2")
+    w = p.workload
+    res = fp.fastpi(p.A, fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed))
+    Zh = res.pseudoinverse.apply(p.Y)
+    Zd = d2h(res.pseudoinverse.apply_device(DeviceCSR.from_host(p.Y)))
+    assert Zh.shape == Zd.shape and Zh.dtype == np.float64
+    np.testing.assert_allclose(Zh, Zd, rtol=0, atol=1e-13 * np.abs(Zd).max())
