@@ -12,7 +12,9 @@
 // tile products run on the FP64 tensor path (mma.sync m8n8k4 -> DMMA); every tile sums its
 // terms in a fixed order, so the result is deterministic.  The critical path is ~nt diagonal
 // steps instead of the ~5 nt kernel launches of the blocked panel algorithm.
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "instrument.cuh"
@@ -29,6 +31,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -99,6 +107,27 @@ __device__ __forceinline__ void load_tile(double (*S)[LD], const double* T, int6
   }
 }
 
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// asynchronous tile copy (one commit group per call)
+__device__ __forceinline__ void load_tiles_async(double (*S0)[LD], const double* T0, int64_t ld0, double (*S1)[LD],
+                                                 const double* T1, int64_t ld1) {
+  for (int e = threadIdx.x; e < TS * TS / 2; e += CT) {
+    const int r = e >> 4, c = (e & 15) * 2;
+    cp_async16(&S0[r][c], T0 + r * ld0 + c);
+    cp_async16(&S1[r][c], T1 + r * ld1 + c);
+  }
+  cp_commit();
+}
+
 __device__ __forceinline__ void acc_to_smem(double (*S)[LD], const double acc[4]) {
   const Frag f;
   S[f.r][f.c0] = acc[0];
@@ -113,16 +142,83 @@ __device__ __forceinline__ void acc_to_global(double* T, int64_t ld, const doubl
   *reinterpret_cast<double2*>(T + f.r * ld + f.c1) = make_double2(acc[2], acc[3]);
 }
 
-__global__ void __launch_bounds__(CT, 2)
+// Step K of the register Cholesky (template recursion keeps every register index static).
+template <int K>
+__device__ __forceinline__ void chol_step(double (&a)[TS], int lane, double& myinv, int& badk) {
+  if constexpr (K < TS) {
+    double d = __shfl_sync(0xffffffffu, a[K], K);
+    badk = (badk < 0 && !(d > 0.0)) ? K : badk;  // branch-free: the step chain stays one basic block
+    d = (d > 0.0) ? d : 1e-300;
+    // 1/sqrt(d) from the MUFU estimate plus one Newton step (a few ulp; the factor only has to
+    // reproduce B^T B to rounding), sqrt(d) = d / sqrt(d)
+    double inv;
+    asm("rsqrt.approx.f64 %0, %1;" : "=d"(inv) : "d"(d));
+    inv = inv * fma(-0.5 * d * inv, inv, 1.5);
+    const double lkk = d * inv;
+    const double scaled = a[K] * inv;
+    a[K] = (lane == K) ? lkk : ((lane > K) ? scaled : a[K]);
+    myinv = (lane == K) ? inv : myinv;
+#pragma unroll
+    for (int jj = K + 1; jj < TS; ++jj) {
+      const double ljk = __shfl_sync(0xffffffffu, a[K], jj);
+      const double upd = fma(-a[K], ljk, a[jj]);
+      a[jj] = (jj <= lane) ? upd : a[jj];
+    }
+    chol_step<K + 1>(a, lane, myinv, badk);
+  }
+}
+
+// Row R of the forward substitution x = L^-1 e_lane (template recursion: static register indices).
+template <int R>
+__device__ __forceinline__ void inv_step(double (&x)[TS], const double (*SC)[LD], const double* sdinv, int lane) {
+  if constexpr (R < TS) {
+    double s = (R == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) s = fma(-SC[R][q], x[q], s);
+    x[R] = s * sdinv[R];
+    inv_step<R + 1>(x, SC, sdinv, lane);
+  }
+}
+
+// Warp 0: Cholesky of the 32 x 32 tile in SC (lower part valid) in registers (lane = row, the
+// column-k multipliers broadcast by shuffles), L written back to SC with the upper part zeroed;
+// then D = L^-1 by forward substitution (lane = column), written to SD.
+__device__ __forceinline__ void chol_inv_warp(double (*SC)[LD], double (*SD)[LD], double* sdinv, int* info,
+                                           int64_t base, unsigned long long* dbg) {
+  const int lane = threadIdx.x & 31;
+  double a[TS];
+#pragma unroll
+  for (int c = 0; c < TS; ++c) a[c] = SC[lane][c];
+  if (dbg && lane == 0) dbg[0] = gtimer_ns();
+  double myinv = 0.0;
+  int badk = -1;
+  chol_step<0>(a, lane, myinv, badk);
+  sdinv[lane] = myinv;
+  if (badk >= 0 && lane == 0) atomicCAS(info, 0, (int)(base + badk + 1));
+  if (dbg && lane == 0) dbg[1] = gtimer_ns();
+#pragma unroll
+  for (int c = 0; c < TS; ++c) SC[lane][c] = c <= lane ? a[c] : 0.0;
+  __syncwarp();
+  // forward substitution, lane = column of D (x in registers; rows above the diagonal come out 0)
+  double x[TS];
+  inv_step<0>(x, SC, sdinv, lane);
+  if (dbg && lane == 0) dbg[2] = gtimer_ns();
+#pragma unroll
+  for (int r = 0; r < TS; ++r) SD[r][lane] = x[r];
+}
+
+__global__ void __launch_bounds__(CT, 1)
     k_chol_inv_dataflow(int64_t n, int nt, const double* __restrict__ G, int64_t ldg, double* Lp, double* Xp,
-                        double* Dv, int* flagL, int* flagX, int* counter, int* info) {
-  __shared__ __align__(16) double SA[TS][LD];
-  __shared__ __align__(16) double SB[TS][LD];
+                        double* Dv, int* flagL, int* flagX, int* counter, int* info,
+                        unsigned long long* prof) {
+  __shared__ __align__(16) double SAB[2][2][TS][LD];  // double-buffered operand tiles
   __shared__ __align__(16) double SC[TS][LD];
+  double(*SA)[LD] = SAB[0][0];
+  double(*SB)[LD] = SAB[0][1];
   __shared__ int s_task;
+  __shared__ double sdinv[TS];
   const int64_t N = (int64_t)nt * TS;
   const int ntri = nt * (nt + 1) / 2;
-  const int lane = threadIdx.x & 31;
   const Frag f;
   for (;;) {
     if (threadIdx.x == 0) s_task = atomicAdd(counter, 1);
@@ -138,6 +234,7 @@ __global__ void __launch_bounds__(CT, 2)
     }
     const int i = j + tt;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (prof && threadIdx.x == 0) prof[3 * t] = gtimer_ns();
     if (!ph2) {
       // A_ij with the identity padding beyond n
       {
@@ -148,46 +245,31 @@ __global__ void __launch_bounds__(CT, 2)
         for (int e = 0; e < 4; ++e)
           acc[e] = (R < n && C4[e] < n) ? G[R * ldg + C4[e]] : (R == C4[e] ? 1.0 : 0.0);
       }
-      for (int k = 0; k < j; ++k) {
+      // sum_{k<j} L_ik L_jk^T, the next pair of tiles in flight while this one multiplies
+      auto issue1 = [&](int k) {
         wait_flag(flagL + i * nt + k);
         wait_flag(flagL + j * nt + k);
-        load_tile(SA, Lp + (int64_t)i * TS * N + (int64_t)k * TS, N);
-        load_tile(SB, Lp + (int64_t)j * TS * N + (int64_t)k * TS, N);
+        load_tiles_async(SAB[k & 1][0], Lp + (int64_t)i * TS * N + (int64_t)k * TS, N, SAB[k & 1][1],
+                         Lp + (int64_t)j * TS * N + (int64_t)k * TS, N);
+      };
+      if (j > 0) issue1(0);
+      for (int k = 0; k < j; ++k) {
+        if (k + 1 < j) {
+          issue1(k + 1);
+          cp_wait<1>();
+        } else {
+          cp_wait<0>();
+        }
         __syncthreads();
-        mma_xyt(acc, SA, SB, -1.0);
+        mma_xyt(acc, SAB[k & 1][0], SAB[k & 1][1], -1.0);
         __syncthreads();
       }
+      if (prof && threadIdx.x == 0) prof[3 * t + 1] = gtimer_ns();
       if (i == j) {
         acc_to_smem(SC, acc);
         __syncthreads();
-        if (threadIdx.x < 32) {
-          // Cholesky of the 32 x 32 tile, lane = row
-          for (int k = 0; k < TS; ++k) {
-            double d = SC[k][k];
-            if (!(d > 0.0)) {
-              if (lane == 0) atomicCAS(info, 0, (int)((int64_t)j * TS + k + 1));
-              d = 1e-300;
-            }
-            const double lkk = sqrt(d);
-            __syncwarp();
-            if (lane > k) SC[lane][k] /= lkk;
-            __syncwarp();
-            if (lane == k) SC[k][k] = lkk;
-            if (lane > k) {
-              const double lik = SC[lane][k];
-              for (int jj = k + 1; jj <= lane; ++jj) SC[lane][jj] -= lik * SC[jj][k];
-            }
-            __syncwarp();
-          }
-          for (int c = lane + 1; c < TS; ++c) SC[lane][c] = 0.0;
-          __syncwarp();
-          // D = L^-1 by forward substitution, lane = column (entries above the diagonal come out 0)
-          for (int r = 0; r < TS; ++r) {
-            double s = (r == lane) ? 1.0 : 0.0;
-            for (int q = 0; q < r; ++q) s -= SC[r][q] * SA[q][lane];
-            SA[r][lane] = s / SC[r][r];
-          }
-        }
+        unsigned long long* dbg = prof ? prof + 3 * 2 * ntri + 4 * j : nullptr;
+        if (threadIdx.x < 32) chol_inv_warp(SC, SA, sdinv, info, (int64_t)j * TS, dbg);
         __syncthreads();
         double* Lt = Lp + (int64_t)j * TS * N + (int64_t)j * TS;
         double* Dt = Dv + (int64_t)j * TS * TS;
@@ -196,7 +278,9 @@ __global__ void __launch_bounds__(CT, 2)
           Lt[r * N + c] = SC[r][c];
           Dt[e] = SA[r][c];
         }
+        if (dbg && threadIdx.x == 0) dbg[3] = gtimer_ns();
         set_flag(flagL + j * nt + j);
+        if (prof && threadIdx.x == 0) prof[3 * t + 2] = gtimer_ns();
       } else {
         wait_flag(flagL + j * nt + j);
         load_tile(SB, Dv + (int64_t)j * TS * TS, TS);
@@ -206,6 +290,7 @@ __global__ void __launch_bounds__(CT, 2)
         mma_xyt(out, SC, SB, 1.0);  // L_ij = A_ij D_j^T
         acc_to_global(Lp + (int64_t)i * TS * N + (int64_t)j * TS, N, out);
         set_flag(flagL + i * nt + j);
+        if (prof && threadIdx.x == 0) prof[3 * t + 2] = gtimer_ns();
       }
     } else {
       double* Xt = Xp + (int64_t)i * TS * N + (int64_t)j * TS;
@@ -215,13 +300,22 @@ __global__ void __launch_bounds__(CT, 2)
         for (int e = threadIdx.x; e < TS * TS; e += CT) Xt[(e >> 5) * N + (e & 31)] = __ldcg(Dt + e);
         set_flag(flagX + j * nt + j);
       } else {
-        for (int k = j; k < i; ++k) {
+        auto issue2 = [&](int k) {
           wait_flag(flagL + i * nt + k);
           wait_flag(flagX + k * nt + j);
-          load_tile(SA, Lp + (int64_t)i * TS * N + (int64_t)k * TS, N);
-          load_tile(SB, Xp + (int64_t)k * TS * N + (int64_t)j * TS, N);
+          load_tiles_async(SAB[k & 1][0], Lp + (int64_t)i * TS * N + (int64_t)k * TS, N, SAB[k & 1][1],
+                           Xp + (int64_t)k * TS * N + (int64_t)j * TS, N);
+        };
+        issue2(j);
+        for (int k = j; k < i; ++k) {
+          if (k + 1 < i) {
+            issue2(k + 1);
+            cp_wait<1>();
+          } else {
+            cp_wait<0>();
+          }
           __syncthreads();
-          mma_xy(acc, SA, SB, 1.0);
+          mma_xy(acc, SAB[k & 1][0], SAB[k & 1][1], 1.0);
           __syncthreads();
         }
         wait_flag(flagL + i * nt + i);
@@ -233,6 +327,7 @@ __global__ void __launch_bounds__(CT, 2)
         acc_to_global(Xt, N, out);
         set_flag(flagX + i * nt + j);
       }
+      if (prof && threadIdx.x == 0) prof[3 * t + 2] = gtimer_ns();
     }
   }
 }
@@ -263,10 +358,40 @@ bool chol_inverse_dataflow(fpi_context* h, int64_t n, const double* G, int64_t l
   int* counter = flags.get() + 2 * nt * nt;
   int* info = counter + 1;
   KTimer kt(h, "cholesky_inverse_dataflow", (double)n * n * n, 0.0);
-  int grid = h->num_sms * 2;
+  int grid = h->num_sms;
   if (grid > 2 * ntri) grid = 2 * ntri;
+  const bool prof_on = getenv("FPI_CHOL_PROFILE") != nullptr;
+  Scratch<unsigned long long> prof(prof_on ? 3 * 2 * ntri + 4 * nt : 1, s);
+  if (prof_on) FPI_CUDA(cudaMemsetAsync(prof.get(), 0, sizeof(unsigned long long) * (3 * 2 * ntri + 4 * nt), s));
   k_chol_inv_dataflow<<<grid, CT, 0, s>>>(n, nt, G, ldg, Lp, Xp, Dv, flags.get(), flags.get() + nt * nt, counter,
-                                          info);
+                                          info, prof_on ? prof.get() : nullptr);
+  if (prof_on) {
+    std::vector<unsigned long long> hp(3 * 2 * ntri + 4 * nt);
+    FPI_CUDA(cudaMemcpyAsync(hp.data(), prof.get(), sizeof(unsigned long long) * hp.size(), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int t = 0; t < 2 * ntri; ++t) {
+      if (hp[3 * t] && hp[3 * t] < t0) t0 = hp[3 * t];
+      if (hp[3 * t + 2] > t1) t1 = hp[3 * t + 2];
+    }
+    fprintf(stderr, "[chol n=%lld nt=%d] total %.1f us; diagonal tasks (grab / deps ready / done, us):\n", (long long)n,
+            nt, (t1 - t0) * 1e-3);
+    int t = 0;
+    for (int j = 0; j < nt; ++j) {
+      fprintf(stderr, "  d%02d %7.1f %7.1f %7.1f |", j, (hp[3 * t] - t0) * 1e-3, (hp[3 * t + 1] - t0) * 1e-3,
+              (hp[3 * t + 2] - t0) * 1e-3);
+      if (j + 1 < nt)
+        fprintf(stderr, " L%02d,%02d done %7.1f", j + 1, j, (hp[3 * (t + 1) + 2] - t0) * 1e-3);
+      const unsigned long long* dg = hp.data() + 3 * 2 * ntri + 4 * j;
+      fprintf(stderr, " [chol %.1f inv %.1f store %.1f]", (dg[1] - dg[0]) * 1e-3, (dg[2] - dg[1]) * 1e-3,
+              (dg[3] - dg[2]) * 1e-3);
+      const int tx = ntri + t;  // X_jj
+      fprintf(stderr, " | X%02d,%02d done %7.1f\n", j, j, (hp[3 * tx + 2] - t0) * 1e-3);
+      t += nt - j;
+    }
+    // last X of column 0
+    fprintf(stderr, "  X%02d,00 done %7.1f\n", nt - 1, (hp[3 * (ntri + nt - 1) + 2] - t0) * 1e-3);
+  }
   const unsigned g2 = grid_for(n * n, 256, (int64_t)h->num_sms * 16);
   k_copy_lower<<<g2, 256, 0, s>>>(n, Lp, N, L, ldl, 1);
   k_copy_lower<<<g2, 256, 0, s>>>(n, Xp, N, Linv, ldi, 1);
