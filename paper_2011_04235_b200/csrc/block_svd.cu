@@ -330,6 +330,24 @@ struct BlockSvdState {
   int64_t rank11 = 0, nnz_u = 0, nnz_v = 0, n_small = 0, n_large = 0;
 };
 
+__global__ void k_large_meta(int64_t nl, const int64_t* __restrict__ large, const int64_t* __restrict__ spans,
+                             const int64_t* __restrict__ keep, const int64_t* __restrict__ roff,
+                             const int64_t* __restrict__ uoff, const int64_t* __restrict__ voff,
+                             int64_t* __restrict__ meta) {
+  FPI_GRID_STRIDE(i, nl) {
+    const int64_t b = large[i];
+    int64_t* m = meta + 8 * i;
+    m[0] = spans[4 * b];
+    m[1] = spans[4 * b + 1];
+    m[2] = spans[4 * b + 2];
+    m[3] = spans[4 * b + 3];
+    m[4] = keep[b];
+    m[5] = roff[b];
+    m[6] = uoff[b];
+    m[7] = voff[b];
+  }
+}
+
 static int64_t smem_limit_doubles(fpi_context* h) { return (int64_t)(h->smem_optin - 1024) / 8; }
 
 static void plan(fpi_context* h, int64_t nspans, const int64_t* spans, double alpha, BlockSvdState& st) {
@@ -403,6 +421,18 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
   FPI_CUDA(cudaStreamSynchronize(s));
   st.n_small = hc[0] + hc[1];
   st.n_large = hc[2];
+  // metadata of the (few) large blocks only, fetched before the small-block kernels are queued so
+  // the host builds the large batch while the device works
+  std::vector<int64_t> meta(8 * (size_t)st.n_large);
+  if (st.n_large) {
+    Scratch<int64_t> dmeta(8 * st.n_large, s);
+    k_large_meta<<<grid_for(st.n_large, T, G), T, 0, s>>>(st.n_large, large, spans, st.keep, st.rank_off, st.u_off,
+                                                            st.v_off, dmeta);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+    FPI_CUDA(cudaMemcpyAsync(meta.data(), dmeta.get(), sizeof(int64_t) * meta.size(), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+  }
   {
     static bool attr = false;
     const size_t full = h->smem_optin - 1024;
@@ -427,29 +457,22 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
     }
   }
   if (st.n_large) {
-    std::vector<int64_t> lg(st.n_large);
-    FPI_CUDA(cudaMemcpyAsync(lg.data(), large.get(), sizeof(int64_t) * st.n_large, cudaMemcpyDeviceToHost, s));
-    std::vector<int64_t> hspans(4 * nspans), hkeep(nspans), hroff(nspans), huoff(nspans), hvoff(nspans);
-    FPI_CUDA(cudaMemcpyAsync(hspans.data(), spans, sizeof(int64_t) * 4 * nspans, cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaMemcpyAsync(hkeep.data(), st.keep.get(), sizeof(int64_t) * nspans, cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaMemcpyAsync(hroff.data(), st.rank_off.get(), sizeof(int64_t) * nspans, cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaMemcpyAsync(huoff.data(), st.u_off.get(), sizeof(int64_t) * nspans, cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaMemcpyAsync(hvoff.data(), st.v_off.get(), sizeof(int64_t) * nspans, cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaStreamSynchronize(s));
+    // meta row i: rs, hh, cs, ww, keep, rank_off, u_off, v_off of the i-th large block
     // dense, oriented (rows >= cols) copies of every large block, one batched SVD for all of them
-    const int nl = (int)lg.size();
+    const int nl = (int)st.n_large;
     std::vector<int64_t> pp(nl), qq(nl), kk(nl), ldm(nl);
     std::vector<int> tr(nl);
     int64_t tot = 0;
     for (int i = 0; i < nl; ++i) {
-      const int64_t b = lg[i], hh = hspans[4 * b + 1], ww = hspans[4 * b + 3];
+      const int64_t* mt = meta.data() + 8 * i;
+      const int64_t hh = mt[1], ww = mt[3];
       FPI_REQUIRE(hh * ww <= 4000000, FPI_ECAPACITY,
                   "diagonal block of " + std::to_string(hh) + "x" + std::to_string(ww) +
                       " entries exceeds the 4000000-entry guard; reordering produced a pathological block");
       tr[i] = hh < ww;
       pp[i] = tr[i] ? ww : hh;
       qq[i] = tr[i] ? hh : ww;
-      kk[i] = hkeep[b];
+      kk[i] = mt[4];
       ldm[i] = qq[i];
       tot += hh * ww;
     }
@@ -465,14 +488,14 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
     Scratch<double> Uall(tu, s), Vall(tv, s);
     int64_t od = 0, ou = 0, ov = 0;
     for (int i = 0; i < nl; ++i) {
-      const int64_t b = lg[i], rs = hspans[4 * b], hh = hspans[4 * b + 1], cs = hspans[4 * b + 2],
-                    ww = hspans[4 * b + 3];
+      const int64_t* mt = meta.data() + 8 * i;
+      const int64_t rs = mt[0], hh = mt[1], cs = mt[2], ww = mt[3];
       double* D = Dall.get() + od;
       k_scatter_block<<<grid_for(hh * 32, T, G), T, 0, s>>>(rs, hh, cs, ww, a_ptr, a_idx, a_val, D, tr[i]);
       Mp[i] = D;
       Up[i] = Uall.get() + ou;
       Vp[i] = Vall.get() + ov;
-      Sp[i] = sigma + hroff[b];
+      Sp[i] = sigma + mt[5];
       od += hh * ww;
       ou += pp[i] * kk[i];
       ov += kk[i] * qq[i];
@@ -481,10 +504,11 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
     dense_svd_batched(h, nl, pp.data(), qq.data(), Mp.data(), ldm.data(), kk.data(), Up.data(), Sp.data(),
                       Vp.data());
     for (int i = 0; i < nl; ++i) {
-      const int64_t b = lg[i], hh = hspans[4 * b + 1], ww = hspans[4 * b + 3];
+      const int64_t* mt = meta.data() + 8 * i;
+      const int64_t hh = mt[1], ww = mt[3];
       // oriented M = U' S V'^T; for a transposed block A = V' S U'^T
       k_store_large<<<grid_for(hh * kk[i] + kk[i] * ww, T, G), T, 0, s>>>(hh, ww, kk[i], Up[i], Vp[i], tr[i],
-                                                                           u_val + huoff[b], vt_val + hvoff[b]);
+                                                                           u_val + mt[6], vt_val + mt[7]);
       note_launch(h, 2);
     }
     FPI_LAUNCH_CHECK();

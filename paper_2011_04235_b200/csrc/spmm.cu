@@ -12,6 +12,8 @@
 // of SEG nonzeros, one warp per (segment, slice) writing a partial row, then
 // an ordered per-row reduction of the segments -- balanced and deterministic
 // (every output element is summed in a fixed order).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "capi_guard.cuh"
 #include "cub_util.cuh"
@@ -42,6 +44,7 @@ template <bool VEC>
 struct Cols {
   int64_t a, b;      // owned columns
   int32_t la, lb;    // load offsets
+  Cols() = default;
   __device__ __forceinline__ Cols(int64_t c0, int lane, int64_t k)
       : a(VEC ? c0 + 2 * lane : c0 + lane), b(VEC ? c0 + 2 * lane + 1 : c0 + 32 + lane) {
     la = a < k ? (int32_t)a : 0;
@@ -129,6 +132,46 @@ __device__ __forceinline__ void accumulate_range(int64_t b, int64_t e, const int
   }
 }
 
+// NSL consecutive 64-column slices per warp (VEC layout): the nonzeros are fetched and shuffled
+// once for all NSL slices, NSL 512-byte gathers per nonzero in flight.
+template <int NSL>
+__device__ __forceinline__ void accumulate_range_multi(int64_t b, int64_t e, const int32_t* __restrict__ indices,
+                                                       const double* __restrict__ values, const double* __restrict__ X,
+                                                       int64_t ldx, const Cols<true> (&c)[NSL], int lane,
+                                                       double2 (&acc)[NSL]) {
+  constexpr int U = (UNROLL / NSL) > 1 ? (UNROLL / NSL) : 1;
+  for (int64_t base = b; base < e; base += 32) {
+    const int64_t my = base + lane;
+    int32_t col = 0;
+    double val = 0.0;
+    if (my < e) {
+      col = __ldg(indices + my);
+      val = __ldg(values + my);
+    }
+    const int cnt = (int)((e - base) < 32 ? (e - base) : 32);
+    for (int j = 0; j < cnt; j += U) {
+      double2 x[U][NSL];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int32_t cj = __shfl_sync(0xffffffffu, col, (j + u) & 31);
+        const double* xr = X + (int64_t)cj * ldx;
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl)
+          x[u][sl] = (j + u < cnt) ? ldx2(xr + c[sl].la) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double v = __shfl_sync(0xffffffffu, val, (j + u) & 31);
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl) {
+          acc[sl].x = fma(v, x[u][sl].x, acc[sl].x);
+          acc[sl].y = fma(v, x[u][sl].y, acc[sl].y);
+        }
+      }
+    }
+  }
+}
+
 template <bool VEC>
 __device__ __forceinline__ void store2(double* yr, const Cols<VEC>& c, int64_t k, double s, double beta,
                                        const double2& a) {
@@ -151,6 +194,29 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
     accumulate_range<VEC>(b, e, indices, values, X, ldx, k, c, lane, acc);
     const double s = row_scale ? alpha * row_scale[row] : alpha;
     store2<VEC>(Y + row * ldy, c, k, s, beta, acc);
+  }
+}
+
+template <int NSL>
+__global__ void __launch_bounds__(WARPS * 32, 2)
+    k_spmm_multi(int64_t p, int64_t k, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+                 const double* __restrict__ values, const double* __restrict__ row_scale, double alpha,
+                 const double* __restrict__ X, int64_t ldx, double beta, double* __restrict__ Y, int64_t ldy,
+                 int64_t long_thresh) {
+  const int lane = threadIdx.x & 31;
+  Cols<true> c[NSL];
+#pragma unroll
+  for (int sl = 0; sl < NSL; ++sl) c[sl] = Cols<true>(((int64_t)blockIdx.y * NSL + sl) * SLICE, lane, k);
+  for (int64_t row = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); row < p; row += (int64_t)gridDim.x * WARPS) {
+    const int64_t b = indptr[row], e = indptr[row + 1];
+    if (e - b > long_thresh) continue;  // handled by the segmented path
+    double2 acc[NSL];
+#pragma unroll
+    for (int sl = 0; sl < NSL; ++sl) acc[sl] = make_double2(0.0, 0.0);
+    accumulate_range_multi<NSL>(b, e, indices, values, X, ldx, c, lane, acc);
+    const double s = row_scale ? alpha * row_scale[row] : alpha;
+#pragma unroll
+    for (int sl = 0; sl < NSL; ++sl) store2<true>(Y + row * ldy, c[sl], k, s, beta, acc[sl]);
   }
 }
 
@@ -199,6 +265,36 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
   }
 }
 
+template <int NSL>
+__global__ void __launch_bounds__(WARPS * 32, 2)
+    k_spmm_segments_multi(const int64_t* __restrict__ rows, const int64_t* __restrict__ seg_off, int64_t nl,
+                          int64_t nseg_total, int64_t k, const int64_t* __restrict__ indptr,
+                          const int32_t* __restrict__ indices, const double* __restrict__ values,
+                          const double* __restrict__ X, int64_t ldx, double* __restrict__ P) {
+  const int lane = threadIdx.x & 31;
+  Cols<true> c[NSL];
+#pragma unroll
+  for (int sl = 0; sl < NSL; ++sl) c[sl] = Cols<true>(((int64_t)blockIdx.y * NSL + sl) * SLICE, lane, k);
+  for (int64_t sg = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); sg < nseg_total;
+       sg += (int64_t)gridDim.x * WARPS) {
+    int64_t lo = 0, hi = nl - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (seg_off[mid] <= sg) lo = mid; else hi = mid - 1;
+    }
+    const int64_t r = rows[lo];
+    const int64_t b = indptr[r] + (sg - seg_off[lo]) * SEG;
+    const int64_t e0 = indptr[r + 1];
+    const int64_t e = b + SEG < e0 ? b + SEG : e0;
+    double2 acc[NSL];
+#pragma unroll
+    for (int sl = 0; sl < NSL; ++sl) acc[sl] = make_double2(0.0, 0.0);
+    accumulate_range_multi<NSL>(b, e, indices, values, X, ldx, c, lane, acc);
+#pragma unroll
+    for (int sl = 0; sl < NSL; ++sl) store2<true>(P + sg * k, c[sl], k, 1.0, 0.0, acc[sl]);
+  }
+}
+
 __global__ void k_seg_reduce(const int64_t* __restrict__ rows, const int64_t* __restrict__ seg_off, int64_t nl,
                              int64_t k, const double* __restrict__ P, const double* __restrict__ row_scale,
                              double alpha, double beta, double* __restrict__ Y, int64_t ldy) {
@@ -240,7 +336,18 @@ void spmm(fpi_context* h, int64_t p, int64_t q, int64_t k, const int64_t* indptr
   const int64_t cap = (int64_t)h->num_sms * 16;
   if (gx > cap) gx = cap;
   dim3 grid((unsigned)gx, (unsigned)slices);
-  if (vec)
+  // two 64-column slices per warp (measured: tools/spmm_variants3.sh), FPI_SPMM_NSL overrides
+  static const int nsl_env = getenv("FPI_SPMM_NSL") ? atoi(getenv("FPI_SPMM_NSL")) : 2;
+  if (vec && nsl_env > 1) {
+    const int nsl = nsl_env >= 4 ? 4 : 2;
+    dim3 gm((unsigned)gx, (unsigned)((slices + nsl - 1) / nsl));
+    if (nsl == 4)
+      k_spmm_multi<4><<<gm, WARPS * 32, 0, s>>>(p, k, indptr, indices, values, row_scale, alpha, X, ldx, beta, Y, ldy,
+                                               SEG);
+    else
+      k_spmm_multi<2><<<gm, WARPS * 32, 0, s>>>(p, k, indptr, indices, values, row_scale, alpha, X, ldx, beta, Y, ldy,
+                                               SEG);
+  } else if (vec)
     k_spmm<true><<<grid, WARPS * 32, 0, s>>>(p, k, indptr, indices, values, row_scale, alpha, X, ldx, beta, Y, ldy,
                                              SEG);
   else
@@ -258,7 +365,11 @@ void spmm(fpi_context* h, int64_t p, int64_t q, int64_t k, const int64_t* indptr
   int64_t gs = (total + WARPS - 1) / WARPS;
   if (gs > cap) gs = cap;
   dim3 g2((unsigned)gs, (unsigned)slices);
-  if (vec)
+  if (vec && nsl_env > 1) {
+    dim3 g3((unsigned)gs, (unsigned)((slices + 1) / 2));
+    k_spmm_segments_multi<2><<<g3, WARPS * 32, 0, s>>>(lrows, seg_off, nl, total, k, indptr, indices, values, X, ldx,
+                                                       P);
+  } else if (vec)
     k_spmm_segments<true><<<g2, WARPS * 32, 0, s>>>(lrows, seg_off, nl, total, k, indptr, indices, values, X, ldx, P);
   else
     k_spmm_segments<false><<<g2, WARPS * 32, 0, s>>>(lrows, seg_off, nl, total, k, indptr, indices, values, X, ldx,
