@@ -139,6 +139,35 @@ __global__ void k_col_sumsq(int64_t M, int64_t N, const double* __restrict__ A, 
   }
 }
 
+// rows [chunk * M / chunks, (chunk + 1) * M / chunks) of 32 columns -> part[chunk][col]
+__global__ void k_col_sumsq_part(int64_t M, int64_t N, const double* __restrict__ A, int64_t lda, int64_t chunks,
+                                 double* __restrict__ part) {
+  __shared__ double ps[8][33];
+  const int64_t c = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  const int64_t r0 = M * blockIdx.y / chunks, r1 = M * (blockIdx.y + 1) / chunks;
+  double sacc = 0.0;
+  if (c < N)
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
+      const double v = A[r * lda + c];
+      sacc = fma(v, v, sacc);
+    }
+  ps[threadIdx.y][threadIdx.x] = sacc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < N) {
+    double t = 0.0;
+    for (int y = 0; y < 8; ++y) t += ps[y][threadIdx.x];
+    part[blockIdx.y * N + c] = t;
+  }
+}
+
+__global__ void k_sum_parts(int64_t N, int64_t chunks, const double* __restrict__ part, double* __restrict__ out) {
+  FPI_GRID_STRIDE(c, N) {
+    double t = 0.0;
+    for (int64_t k = 0; k < chunks; ++k) t += part[k * N + c];
+    out[c] = t;
+  }
+}
+
 __global__ void k_scale_cols(int64_t M, int64_t N, double* A, int64_t lda, const double* s, int mode) {
   // mode 0: multiply by s[j]; 1: divide by s[j] (0 where s == 0)
   FPI_GRID_STRIDE(e, M * N) {
@@ -250,7 +279,21 @@ void transpose(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t ld
 
 void col_sumsq(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* out) {
   if (N <= 0) return;
-  k_col_sumsq<<<(unsigned)((N + 31) / 32), dim3(32, 8), 0, h->stream>>>(M, N, A, lda, out);
+  const int64_t groups = (N + 31) / 32;
+  // enough row chunks to fill the GPU (one CTA per (column group, chunk)); partial sums are
+  // reduced in chunk order, so the result does not depend on scheduling
+  int64_t chunks = ((int64_t)h->num_sms * 4 + groups - 1) / groups;
+  const int64_t max_chunks = (M + 255) / 256;
+  if (chunks > max_chunks) chunks = max_chunks;
+  if (chunks <= 1) {
+    k_col_sumsq<<<(unsigned)groups, dim3(32, 8), 0, h->stream>>>(M, N, A, lda, out);
+  } else {
+    Scratch<double> part(chunks * N, h->stream);
+    k_col_sumsq_part<<<dim3((unsigned)groups, (unsigned)chunks), dim3(32, 8), 0, h->stream>>>(M, N, A, lda, chunks,
+                                                                                              part);
+    k_sum_parts<<<grid_for(N, 256, (int64_t)h->num_sms * 4), 256, 0, h->stream>>>(N, chunks, part, out);
+    note_launch(h);
+  }
   FPI_LAUNCH_CHECK();
   note_launch(h);
 }

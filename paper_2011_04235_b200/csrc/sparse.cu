@@ -29,9 +29,12 @@ __global__ void k_make_keys(int64_t cnt, const int32_t* __restrict__ major, cons
                             int minor_bits, uint64_t* __restrict__ keys, int32_t* __restrict__ pos,
                             int32_t* __restrict__ counts) {
   FPI_GRID_STRIDE(i, cnt) {
-    keys[i] = ((uint64_t)(uint32_t)major[i] << minor_bits) | (uint32_t)minor[i];
+    const int32_t mj = major[i];
+    keys[i] = ((uint64_t)(uint32_t)mj << minor_bits) | (uint32_t)minor[i];
     pos[i] = (int32_t)i;
-    atomicAdd(counts + major[i], 1);
+    const unsigned mask = __activemask();
+    const unsigned peers = __match_any_sync(mask, mj);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + mj, (int32_t)__popc(peers));
   }
 }
 
@@ -114,15 +117,37 @@ struct PartBufs {
   unsigned long long* counters;  // [0] a11, [1] t, [2] a21, [3] structural violations, [4] a12
 };
 
-__device__ __forceinline__ unsigned long long warp_slot(unsigned long long* ctr, bool want) {
-  unsigned mask = __ballot_sync(__activemask(), want);
-  if (!want) return 0;
-  int lane = threadIdx.x & 31;
-  int leader = __ffs(mask) - 1;
-  unsigned long long base = 0;
-  if (lane == leader) base = atomicAdd(ctr, (unsigned long long)__popc(mask));
-  base = __shfl_sync(mask, base, leader);
-  return base + __popc(mask & ((1u << lane) - 1));
+// Slots for up to 5 per-thread flags: one global atomic per CTA and counter (a per-warp atomic on
+// five shared addresses serialised at L2); slots are unordered, build_csr sorts afterwards.
+template <int NC>
+__device__ __forceinline__ void block_slots(unsigned long long* ctr, const bool (&want)[NC],
+                                            unsigned long long (&slot)[NC]) {
+  __shared__ unsigned int wc[NC][32];
+  __shared__ unsigned long long bb[NC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  unsigned lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  unsigned masks[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    masks[c] = __ballot_sync(0xffffffffu, want[c]);
+    if (lane == 0) wc[c][warp] = __popc(masks[c]);
+  }
+  __syncthreads();
+  if (threadIdx.x < NC) {
+    const int c = threadIdx.x;
+    unsigned int run = 0;
+    for (int w = 0; w < nw; ++w) {
+      const unsigned int x = wc[c][w];
+      wc[c][w] = run;
+      run += x;
+    }
+    bb[c] = run ? atomicAdd(ctr + c, (unsigned long long)run) : 0ull;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < NC; ++c) slot[c] = bb[c] + wc[c][warp] + __popc(masks[c] & lt);
+  __syncthreads();
 }
 
 __global__ void k_partition(int64_t nnz, const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
@@ -151,14 +176,11 @@ __global__ void k_partition(int64_t nnz, const int32_t* __restrict__ rows, const
         viol = (c < cs) || (c >= cs + cl);
       }
     }
-    unsigned long long s11 = warp_slot(b.counters + 0, in11);
-    unsigned long long sT = warp_slot(b.counters + 1, inT);
-    unsigned long long s21 = warp_slot(b.counters + 2, in21);
-    warp_slot(b.counters + 3, viol);
-    if (!emit) {
-      warp_slot(b.counters + 4, inT && r < m1);
-      continue;
-    }
+    const bool want[5] = {in11, inT, in21, viol, inT && r < m1};
+    unsigned long long slot[5];
+    block_slots<5>(b.counters, want, slot);
+    if (!emit) continue;
+    const unsigned long long s11 = slot[0], sT = slot[1], s21 = slot[2];
     double v = valid && vals ? vals[e] : 0.0;
     if (in11 && b.a11_r) {
       b.a11_r[s11] = (int32_t)r;

@@ -824,6 +824,15 @@ void unfold_transpose(fpi_context* h, int64_t m, int64_t n, int64_t r, const dou
   note_launch(h, 2);
 }
 
+// Columns of Vt in original order: Vg[:, i] = Vt[:, col_fwd[i]] (the unfold of pinv.py:271-275 for V).
+__global__ void k_gather_cols(int64_t r, int64_t n, const double* __restrict__ Vt, const int64_t* __restrict__ col_fwd,
+                              double* __restrict__ Vg) {
+  FPI_GRID_STRIDE(e, r * n) {
+    const int64_t k = e / n, i = e - k * n;
+    Vg[e] = Vt[k * n + col_fwd[i]];
+  }
+}
+
 // Z (n x L) = V diag(sdag) U^T Y  with U, Vt in reordered coordinates and Y (m x L) CSR in original rows
 // W (L x r) = Y'^T U_loc for the reordered rows [r0, r0 + m_loc) that U_loc holds (pinv.py:75's U^T Y,
 // one row shard of it; the shards' W sum to the full product).  Y is CSR in original row order.
@@ -885,11 +894,12 @@ void pinv_lift(fpi_context* h, int64_t n, int64_t r, const double* sdag, const d
     return;
   }
   scale_cols(h, L, r, W, r, sdag, false);
-  Scratch<double> Zr(n * L, s);
-  gemm(h, true, true, n, L, r, 1.0, Vt, n, W, r, 0.0, Zr, L);
-  k_gather_rows<<<grid_for(n * L, 256, G), 256, 0, s>>>(n, L, Zr, L, col_fwd, Z, L);
+  // Vt's columns in original order first (r x n), so the GEMM writes Z's rows in place
+  Scratch<double> Vg(r * n, s);
+  k_gather_cols<<<grid_for(r * n, 256, G), 256, 0, s>>>(r, n, Vt, col_fwd, Vg);
   FPI_LAUNCH_CHECK();
   note_launch(h);
+  gemm(h, true, true, n, L, r, 1.0, Vg, n, W, r, 0.0, Z, L);
 }
 
 void pinv_apply_csr(fpi_context* h, int64_t m, int64_t n, int64_t r, const double* U, const double* sdag,
@@ -904,15 +914,6 @@ void pinv_apply_csr(fpi_context* h, int64_t m, int64_t n, int64_t r, const doubl
   Scratch<double> W(L * r, s);
   pinv_project_csr(h, 0, m, r, U, row_fwd, m, L, nnz, y_ptr, y_idx, y_val, W);
   pinv_lift(h, n, r, sdag, Vt, col_fwd, L, W, Z);
-}
-
-// Columns of Vt in original order: Vg[:, i] = Vt[:, col_fwd[i]] (the unfold of pinv.py:271-275 for V).
-__global__ void k_gather_cols(int64_t r, int64_t n, const double* __restrict__ Vt, const int64_t* __restrict__ col_fwd,
-                              double* __restrict__ Vg) {
-  FPI_GRID_STRIDE(e, r * n) {
-    const int64_t k = e / n, i = e - k * n;
-    Vg[e] = Vt[k * n + col_fwd[i]];
-  }
 }
 
 // pinv_apply_csr straight into host memory: the lift Z = V diag(sigma+) W^T runs in row chunks of
@@ -972,12 +973,12 @@ void pinv_apply_dense(fpi_context* h, int64_t m, int64_t n, int64_t r, const dou
     FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * n * L, s));
     return;
   }
-  Scratch<double> Yr(m * L, s), W(r * L, s), Zr(n * L, s);
+  Scratch<double> Yr(m * L, s), W(r * L, s), Vg(r * n, s);
   k_scatter_rows<<<grid_for(m * L, 256, G), 256, 0, s>>>(m, L, Y, ldy, row_fwd, Yr, L);
   gemm(h, true, false, r, L, m, 1.0, U, r, Yr, L, 0.0, W, L);
   scale_rows(h, r, L, W, L, sdag);
-  gemm(h, true, false, n, L, r, 1.0, Vt, n, W, L, 0.0, Zr, L);
-  k_gather_rows<<<grid_for(n * L, 256, G), 256, 0, s>>>(n, L, Zr, L, col_fwd, Z, L);
+  k_gather_cols<<<grid_for(r * n, 256, G), 256, 0, s>>>(r, n, Vt, col_fwd, Vg);
+  gemm(h, true, false, n, L, r, 1.0, Vg, n, W, L, 0.0, Z, L);
   FPI_LAUNCH_CHECK();
   note_launch(h, 2);
 }
