@@ -97,6 +97,10 @@ __device__ void build_tables(StepTables& tb) {
   }
 }
 
+#ifndef JACOBI_ROT32
+#define JACOBI_ROT32 1
+#endif
+
 // MUFU approximations for the rotation (measured on B200: rsqrt.approx.f64 ~2^-52.4 -- ptxas
 // refines MUFU.RSQ64H -- and rcp.approx.ftz.f64 ~2^-20).
 __device__ __forceinline__ double rcp_apx(double x) { double r; asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
@@ -119,10 +123,27 @@ __device__ __forceinline__ void rotation(double app, double aqq, double apq, dou
     d *= sc;
     f2 *= sc;
   }
+#if JACOBI_ROT32
+  // The angle in FP32 (MUFU.RSQ / MUFU.RCP, ~2^-22 relative -- better than the 2^-20 the FP64
+  // path's raw reciprocal gives), after scaling d and f2 by 2^-e (e = exponent of their larger
+  // magnitude) into FP32's range; orthogonality comes from c and s below, computed in FP64.
+  const int ex = (int)((__double_as_longlong(mx) >> 52) & 0x7ff) - 1023;
+  const int ef = 1023 - ex < 1 ? 1 : (1023 - ex > 2046 ? 2046 : 1023 - ex);
+  const double sc2 = __longlong_as_double((long long)ef << 52);
+  const float df = (float)(d * sc2), ff = (float)(f2 * sc2);
+  const float vf = fmaf(df, df, ff * ff);
+  float rs, rc;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(vf));
+  const float hypf = vf * rs;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fabsf(df) + hypf));
+  const float tf = ff * rc;
+  const double tt = (double)(df < 0.0f ? -tf : tf);
+#else
   const double v = fma(d, d, f2 * f2);
   const double hyp = v * rsqrt_apx(v);
   const double t0 = f2 * rcp_apx(fabs(d) + hyp);
   const double tt = d < 0.0 ? -t0 : t0;
+#endif
   const double cy = rsqrt_apx(fma(tt, tt, 1.0));
   c = rot ? cy : 1.0;
   sn = rot ? cy * tt : 0.0;
