@@ -155,6 +155,15 @@ int fpi_block_svd(fpi_handle h, int64_t m1, int64_t n1, const int64_t* a11_ptr, 
                   const double* a11_val, int64_t n_spans, const int64_t* d_spans, double alpha, double* d_sigma,
                   int64_t* u_ptr, int32_t* u_idx, double* u_val, int64_t* vt_ptr, int32_t* vt_idx, double* vt_val,
                   fpi_block_plan* h_plan);
+/* One rank's share of fpi_block_svd for a sharded solve (A11 blocks are independent
+ * units): small blocks dealt round-robin (block b -> rank b % world), the large ones by LPT over
+ * h w min(h, w); the structure (u_ptr/u_idx, vt_ptr/vt_idx) is complete on every rank and the
+ * values of other ranks' blocks are zero, so summing sigma, u_val and vt_val over the ranks (one
+ * all-reduce) gives fpi_block_svd's result.  Replaces svd.py:141-193's per-block loop. */
+int fpi_block_svd_shard(fpi_handle h, int64_t m1, int64_t n1, const int64_t* a11_ptr, const int32_t* a11_idx,
+                        const double* a11_val, int64_t n_spans, const int64_t* d_spans, double alpha,
+                        int64_t shard_rank, int64_t shard_world, double* d_sigma, int64_t* u_ptr, int32_t* u_idx,
+                        double* u_val, int64_t* vt_ptr, int32_t* vt_idx, double* vt_val, fpi_block_plan* h_plan);
 /* svd.py:86-117 dense_svd + truncate: rank leading triplets of a dense p x q matrix (sorted). */
 int fpi_dense_svd(fpi_handle h, int64_t p, int64_t q, const double* d_M, int64_t ldm, int64_t rank,
                   double* d_U, double* d_sigma, double* d_Vt);

@@ -79,6 +79,8 @@ SIGNATURES = {
     "fpi_block_svd_plan": (C.c_int, [vp, i64, vp, f64, C.POINTER(BlockPlan)]),
     "fpi_block_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, f64, vp, vp, vp, vp, vp, vp, vp,
                                 C.POINTER(BlockPlan)]),
+    "fpi_block_svd_shard": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, f64, i64, i64, vp, vp, vp, vp, vp, vp,
+                                      vp, C.POINTER(BlockPlan)]),
     "fpi_dense_svd": (C.c_int, [vp, i64, i64, vp, i64, i64, vp, vp, vp]),
     "fpi_randomized_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp]),
     "fpi_dataset_parse": (C.c_int, [C.c_char_p, i64, C.POINTER(vp), C.POINTER(DatasetInfo)]),

@@ -19,6 +19,8 @@
 //     (svd_engine.cu), one block at a time.
 // Each triplet gets the canonical sign (largest |.| entry of the right vector
 // positive) and zero singular values get an orthonormal completion.
+#include <algorithm>
+
 #include "common.cuh"
 #include "capi_guard.cuh"
 #include "cub_util.cuh"
@@ -282,11 +284,14 @@ struct IsFlag {
   int64_t want;
   __device__ bool operator()(int64_t b) const { return flag[b] == want; }
 };
+// non-degenerate block of size class cls owned by this rank (blocks are dealt round-robin over the
+// ranks of a sharded solve; world = 1 owns everything)
 struct IsNonDeg {
   const int64_t* keep;
   const int64_t* large;
   int64_t cls;
-  __device__ bool operator()(int64_t b) const { return keep[b] > 0 && large[b] == cls; }
+  int64_t rank, world;
+  __device__ bool operator()(int64_t b) const { return keep[b] > 0 && large[b] == cls && b % world == rank; }
 };
 
 __global__ void k_iota64(int64_t* a, int64_t n) {
@@ -382,7 +387,7 @@ static void plan(fpi_context* h, int64_t nspans, const int64_t* spans, double al
 void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, const int32_t* a_idx,
                const double* a_val, int64_t nspans, const int64_t* spans, double alpha, double* sigma,
                int64_t* u_ptr, int32_t* u_idx, double* u_val, int64_t* vt_ptr, int32_t* vt_idx, double* vt_val,
-               fpi_block_plan* out_plan) {
+               fpi_block_plan* out_plan, int64_t shard_rank, int64_t shard_world) {
   FPI_REQUIRE(alpha > 0.0 && alpha <= 1.0, FPI_EDOMAIN, "target rank ratio alpha must be in (0, 1]");
   cudaStream_t s = h->stream;
   BlockSvdState st;
@@ -413,9 +418,18 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
   Scratch<int64_t> ids(nspans, s), small(nspans, s), mid(nspans, s), large(nspans, s);
   Scratch<int> cnt(3, s);
   k_iota64<<<grid_for(nspans, T, G), T, 0, s>>>(ids, nspans);
-  select_if(tmp, ids.get(), small.get(), cnt.get(), nspans, IsNonDeg{st.keep.get(), st.large.get(), 0}, s);
-  select_if(tmp, ids.get(), mid.get(), cnt.get() + 1, nspans, IsNonDeg{st.keep.get(), st.large.get(), 2}, s);
+  select_if(tmp, ids.get(), small.get(), cnt.get(), nspans,
+            IsNonDeg{st.keep.get(), st.large.get(), 0, shard_rank, shard_world}, s);
+  select_if(tmp, ids.get(), mid.get(), cnt.get() + 1, nspans,
+            IsNonDeg{st.keep.get(), st.large.get(), 2, shard_rank, shard_world}, s);
   select_if(tmp, ids.get(), large.get(), cnt.get() + 2, nspans, IsFlag{st.large.get(), 1}, s);
+  if (shard_world > 1) {
+    // only this rank's blocks are written: the others' values stay zero, so a sum over the ranks
+    // (the all-reduce of the sharded solve) assembles the full factors
+    if (st.rank11) FPI_CUDA(cudaMemsetAsync(sigma, 0, sizeof(double) * st.rank11, s));
+    if (u_val && st.nnz_u) FPI_CUDA(cudaMemsetAsync(u_val, 0, sizeof(double) * st.nnz_u, s));
+    if (vt_val && st.nnz_v) FPI_CUDA(cudaMemsetAsync(vt_val, 0, sizeof(double) * st.nnz_v, s));
+  }
   int hc[3];
   FPI_CUDA(cudaMemcpyAsync(hc, cnt.get(), sizeof(hc), cudaMemcpyDeviceToHost, s));
   FPI_CUDA(cudaStreamSynchronize(s));
@@ -455,6 +469,32 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
       FPI_LAUNCH_CHECK();
       note_launch(h, 2);
     }
+  }
+  if (st.n_large && shard_world > 1) {
+    // sharded solve: the (few, expensive) large blocks by LPT over their cost h w min(h, w), in
+    // block order with ties to the lowest rank -- the same deal on every rank; keep this rank's
+    std::vector<int64_t> order(st.n_large);
+    for (int64_t i = 0; i < st.n_large; ++i) order[i] = i;
+    auto cost = [&](int64_t i) {
+      const int64_t hh = meta[8 * i + 1], ww = meta[8 * i + 3];
+      return (double)hh * (double)ww * (double)(hh < ww ? hh : ww);
+    };
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return cost(a) > cost(b); });
+    std::vector<double> load(shard_world, 0.0);
+    std::vector<int64_t> mine;
+    for (int64_t i : order) {
+      int64_t best = 0;
+      for (int64_t r = 1; r < shard_world; ++r)
+        if (load[r] < load[best]) best = r;
+      load[best] += cost(i);
+      if (best == shard_rank) mine.push_back(i);
+    }
+    std::sort(mine.begin(), mine.end());
+    std::vector<int64_t> kept(8 * mine.size());
+    for (size_t j = 0; j < mine.size(); ++j)
+      for (int f = 0; f < 8; ++f) kept[8 * j + f] = meta[8 * mine[j] + f];
+    meta.swap(kept);
+    st.n_large = (int64_t)mine.size();
   }
   if (st.n_large) {
     // meta row i: rs, hh, cs, ww, keep, rank_off, u_off, v_off of the i-th large block
@@ -542,6 +582,18 @@ extern "C" int fpi_block_svd(fpi_handle h, int64_t m1, int64_t n1, const int64_t
                              int32_t* vt_idx, double* vt_val, fpi_block_plan* h_plan) {
   FPI_API_BEGIN(h)
   fpi::block_svd(h, m1, n1, a11_ptr, a11_idx, a11_val, n_spans, d_spans, alpha, d_sigma, u_ptr, u_idx, u_val,
-                 vt_ptr, vt_idx, vt_val, h_plan);
+                 vt_ptr, vt_idx, vt_val, h_plan, 0, 1);
+  FPI_API_END(h)
+}
+
+extern "C" int fpi_block_svd_shard(fpi_handle h, int64_t m1, int64_t n1, const int64_t* a11_ptr,
+                                   const int32_t* a11_idx, const double* a11_val, int64_t n_spans,
+                                   const int64_t* d_spans, double alpha, int64_t shard_rank, int64_t shard_world,
+                                   double* d_sigma, int64_t* u_ptr, int32_t* u_idx, double* u_val, int64_t* vt_ptr,
+                                   int32_t* vt_idx, double* vt_val, fpi_block_plan* h_plan) {
+  FPI_API_BEGIN(h)
+  FPI_REQUIRE(shard_world >= 1 && shard_rank >= 0 && shard_rank < shard_world, FPI_EDOMAIN, "bad shard rank / world");
+  fpi::block_svd(h, m1, n1, a11_ptr, a11_idx, a11_val, n_spans, d_spans, alpha, d_sigma, u_ptr, u_idx, u_val,
+                 vt_ptr, vt_idx, vt_val, h_plan, shard_rank, shard_world);
   FPI_API_END(h)
 }

@@ -3,9 +3,13 @@ NVSwitch) for the exchanges.
 
 What shards and what is replicated:
 
-* reorder, partition, block SVD, row update: replicated.  Every rank holds A
-  and computes them itself (deterministic kernels, so the ranks agree bit for
-  bit); none of them is worth an exchange at the BASELINE sizes.
+* reorder, partition, row update: replicated.  Every rank holds A and computes
+  them itself (deterministic kernels, so the ranks agree bit for bit).
+* block SVD (svd.py:141-193): the diagonal blocks are independent units -- each
+  rank factors its share (round-robin for the many small blocks, LPT by
+  h w min(h, w) for the large ones, fpi_block_svd_shard) and one all-reduce of
+  sigma / U11 / Vt11 values (disjoint supports, so the sum is the union)
+  gives every rank the full block factors for the replicated row update.
 * column update (pinv.py:174-208, the FP64 GEMM-bound stage): the m rows of
   [U Sigma | T] are split into contiguous shards.  Every rank regenerates the
   full sketch X (svd.py:131-132), forms its B_i = M_i X, and the two
@@ -269,7 +273,7 @@ def fastpi_sharded(dev: DeviceCSR, cfg: FastpiConfig, comm: Comm | None = None, 
         part = partition_original(dev, ordering, transposes=False)
     timings.append(StageTime("reorder", tm.seconds, comm.rank))
     with _Timer() as tm:
-        f11 = block_diagonal_svd_device(part.a11, ordering.spans_device(), cfg.alpha)
+        f11 = block_diagonal_svd_device(part.a11, ordering.spans_device(), cfg.alpha, comm)
     timings.append(StageTime("block_svd", tm.seconds, comm.rank))
     n1, m2, n2 = ordering.n_spoke_cols, ordering.n_hub_rows, ordering.n_hub_cols
     with _Timer() as tm:
