@@ -18,12 +18,14 @@
 //   P8  giant component = max (size, -min id) (reorder.py:228-234)
 //   P9/P10 ordered three-way partition of the active list: giant component (next `act`) |
 //       spoke roots | other spoke nodes, all ascending
-//   P11-P14 spoke components ordered (size desc, min id asc), spans laid out by an ordered scan,
-//       spoke nodes stably grouped by component rank (members ascending) and emitted
-//       (reorder.py:236-257).  Lists up to SMALL_LIST nodes are done by CTA 0 alone (no grid
-//       barrier) while the other CTAs compact the edge list.
+//       Spoke roots / nodes are only logged here: their blocks and ids depend on nothing later
+//       iterations change, so they are laid out once after the loop (below).
 //   P15 edge list compacted to the new giant component (unordered: neither degrees nor the
-//       union-find result depend on edge order).
+//       union-find result depend on edge order); the next iteration's degrees counted on the way.
+// After the loop, all spoke components of all iterations are ordered by (iteration, size desc,
+// min id asc) with two grid-wide stable radix sorts; one exclusive scan of their (rows, cols) gives
+// the spans (the scan across iterations is exactly each iteration's lo_t / lo_f), and one more
+// stable sort groups the logged spoke nodes by component (reorder.py:236-257).
 #include <cooperative_groups.h>
 #include <cub/block/block_scan.cuh>
 #include <cmath>
@@ -45,7 +47,6 @@ constexpr int NW = NT / 32;
 constexpr int HBITS = 11;
 constexpr int HB = 1 << HBITS;
 constexpr int HUB_CAP = 1 << 15;      // hubs per side per iteration (ranked by brute force)
-constexpr int64_t SMALL_LIST = 8192;  // spoke stages up to this many nodes run on CTA 0 alone
 
 struct Ctl {
   int nhub[2];
@@ -77,6 +78,8 @@ struct Params {
   int32_t* v0;
   int32_t* v1;
   int32_t* rank_of_root;
+  int32_t* rlog;   // spoke roots of every iteration (ascending within an iteration)
+  int32_t* riter;  // their iteration
   uint64_t* tri;   // per spoke component (rank order): rows << 32 | cols
   uint64_t* toff;  // exclusive prefix of tri
   int64_t* row_fwd;
@@ -311,22 +314,6 @@ __device__ int radix_sort(cg::grid_group& grid, const Params& P, int64_t n, int 
   return cur;
 }
 
-// Spoke component table over the rank-ordered roots [c0, c1): rank_of_root, (rows, cols) per
-// component.  Returns this range's packed (rows, cols) sum.
-__device__ unsigned long long comp_table(const Params& P, const int32_t* roots, int64_t c0, int64_t c1) {
-  unsigned long long s = 0;
-  for (int64_t i = c0 + threadIdx.x; i < c1; i += NT) {
-    const int32_t r = ld_(roots + i);
-    P.rank_of_root[r] = (int32_t)i;
-    const uint64_t rows = (uint64_t)ld_(P.crows + r);
-    const uint64_t cols = (uint64_t)ld_(P.csize + r) - rows;
-    const uint64_t tr = (rows << 32) | cols;
-    P.tri[i] = tr;
-    s += tr;
-  }
-  return s;
-}
-
 // Ordered exclusive scan of tri over [c0, c1) from `carry`; writes toff and the spans.
 __device__ void comp_offsets(const Params& P, int64_t c0, int64_t c1, unsigned long long carry, int64_t lo_t,
                              int64_t lo_f, int64_t span0, Smem& sm) {
@@ -430,6 +417,8 @@ __global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
   uint64_t* E = P.e0;
   uint64_t* E_nx = P.e1;
   int hl = 0;  // hub histogram buffer rotation
+  int64_t nroots_log = 0, nnodes_log = 0, maxsz_all = 0;  // spoke log (laid out after the loop)
+  int64_t dprev[2] = {0, 0};                                // previous hub thresholds (0: none)
   unsigned long long tlast = (P.prof && gtid == 0) ? gtimer() : 0ull;
 #define RP_PROF(i)                                     \
   if (P.prof && gtid == 0) {                           \
@@ -469,7 +458,73 @@ __global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
     need[1] = (cnt_f > 0 && q_f > 0) ? (q_f < cnt_f ? q_f : cnt_f) : 0;
     htot[0] = need[0];
     htot[1] = need[1];
-    if (need[0] > 0 || need[1] > 0) {
+    // Window pass: degrees only fall from one iteration to the next and every node left active had
+    // degree <= the previous threshold, so the new threshold usually lies in the 2048 degrees
+    // (dprev - 2048, dprev]: one histogram level instead of P.levels.
+    bool gen[2] = {need[0] > 0, need[1] > 0};
+    if ((need[0] > 0 && dprev[0] > 0) || (need[1] > 0 && dprev[1] > 0)) {
+      int64_t wbase[2];
+      bool win[2];
+      for (int sd = 0; sd < 2; ++sd) {
+        win[sd] = need[sd] > 0 && dprev[sd] > 0;
+        wbase[sd] = dprev[sd] - (HB - 1) > 1 ? dprev[sd] - (HB - 1) : 1;
+      }
+      int32_t* buf = P.hist + (hl % 3) * 2 * HB;
+      int32_t* zbuf = P.hist + ((hl + 1) % 3) * 2 * HB;
+      for (int64_t i = gtid; i < 2 * HB; i += gsz) zbuf[i] = 0;
+      for (int i = t; i < 2 * HB; i += NT) (&sm.hist[0][0])[i] = 0;
+      __syncthreads();
+      for (int64_t i = gtid; i < L; i += gsz) {
+        const int32_t v = ld_(act + i);
+        const int side = v >= m;
+        if (!win[side]) continue;
+        const int64_t d = ld_(P.deg + v);
+        if (d < wbase[side]) continue;
+        atomicAdd(&sm.hist[side][d - wbase[side]], 1);
+      }
+      __syncthreads();
+      for (int i = t; i < 2 * HB; i += NT) {
+        const int c = (&sm.hist[0][0])[i];
+        if (c) atomicAdd(buf + i, c);
+      }
+      grid.sync();
+      ++hl;
+      for (int side = 0; side < 2; ++side) {
+        if (!win[side]) continue;
+        int c4[4];
+        unsigned long long mine = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          c4[j] = ld_(buf + side * HB + (HB - 1 - 4 * t - j));
+          mine += (unsigned long long)c4[j];
+        }
+        unsigned long long ex, tot;
+        BlockScanU64(sm.scan.u64).ExclusiveSum(mine, ex, tot);
+        const int64_t nd = need[side];
+        if ((int64_t)tot >= nd && (int64_t)ex < nd && nd <= (int64_t)(ex + mine)) {
+          int64_t run = (int64_t)ex;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (run + c4[j] >= nd) {
+              sm.bc[0] = HB - 1 - 4 * t - j;
+              sm.bc[1] = run;
+              sm.bc[2] = c4[j];
+              break;
+            }
+            run += c4[j];
+          }
+        }
+        __syncthreads();
+        if ((int64_t)tot >= nd) {  // found in the window (otherwise the general select below)
+          pre[side] = wbase[side] + sm.bc[0];
+          need[side] = nd - sm.bc[1];
+          eqcnt[side] = sm.bc[2];
+          gen[side] = false;
+        }
+        __syncthreads();
+      }
+    }
+    if (gen[0] || gen[1]) {
       for (int lev = P.levels - 1; lev >= 0; --lev) {
         const int shift = lev * HBITS;
         int32_t* buf = P.hist + (hl % 3) * 2 * HB;
@@ -480,7 +535,7 @@ __global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
         for (int64_t i = gtid; i < L; i += gsz) {
           const int32_t v = ld_(act + i);
           const int side = v >= m;
-          if (need[side] == 0) continue;
+          if (!gen[side] || need[side] == 0) continue;
           const int32_t d = ld_(P.deg + v);
           if (d <= 0) continue;
           if (lev < P.levels - 1 && ((int64_t)d >> (shift + HBITS)) != pre[side]) continue;
@@ -495,7 +550,7 @@ __global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
         ++hl;
         // decision, identical in every CTA: the bin holding the need-th largest degree
         for (int side = 0; side < 2; ++side) {
-          if (need[side] == 0) continue;
+          if (!gen[side] || need[side] == 0) continue;
           int c4[4];
           unsigned long long mine = 0;
 #pragma unroll
@@ -533,6 +588,8 @@ __global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
         }
       }
     }
+    dprev[0] = htot[0] > 0 ? pre[0] : 0;
+    dprev[1] = htot[1] > 0 ? pre[1] : 0;
     RP_PROF(1)
     // hubs of side s: degree > pre[s], plus the first need[s] (ascending id) of degree == pre[s]
     const bool split_ties = (htot[0] > 0 && need[0] < eqcnt[0]) || (htot[1] > 0 && need[1] < eqcnt[1]);
@@ -733,13 +790,15 @@ __global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
           P.csize[v] = 0;
           P.crows[v] = 0;
         } else if (cls == 1) {
+          // spoke roots and spoke nodes are logged; their blocks and ids are laid out once, after
+          // the loop (a spoke's parent / size / row count are never touched again)
           const int64_t p = b1 + field21(ex, 1);
-          P.cand[p] = v;
-          P.k0[p] = (uint32_t)(maxsz - ld_(P.csize + v));
-          P.v0[p] = v;
+          P.rlog[nroots_log + p] = v;
+          P.riter[nroots_log + p] = (int32_t)iters;
+          P.cand[nnodes_log + p] = v;
           P.state[v] = 0;
         } else if (cls == 2) {
-          P.cand[b2 + field21(ex, 2)] = v;
+          P.cand[nnodes_log + b2 + field21(ex, 2)] = v;
           P.state[v] = 0;
         }
         b0 += field21(tot, 0);
@@ -751,47 +810,10 @@ __global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
     grid.sync();
     RP_PROF(8)
 
-    // ---- P11-P14: spoke components -> blocks (size desc, min id asc), members ascending
     const bool stop = g_t < q_t || g_f < q_f;  // reorder.py:268-269
-    const int cbits = maxsz > 1 ? key_bits(maxsz - 1) : 0;
-    const int nbits = nsc > 1 ? key_bits(nsc - 1) : 0;
-    if (nsc > 0 && nsp <= SMALL_LIST) {
-      // small spoke stage: CTA 0 alone (block barriers only) while the others compact the edges
-      if (b == 0) {
-        const int cur = radix_sort<false>(grid, P, nsc, cbits, sm);
-        comp_table(P, cur ? P.v1 : P.v0, 0, nsc);
-        __threadfence();
-        __syncthreads();
-        comp_offsets(P, 0, nsc, 0ull, lo_t, lo_f, nspans, sm);
-        node_keys(P, t, nsp, NT);
-        __threadfence();
-        __syncthreads();
-        const int cur2 = radix_sort<false>(grid, P, nsp, nbits, sm);
-        emit_nodes(P, cur2 ? P.k1 : P.k0, cur2 ? P.v1 : P.v0, t, nsp, NT, lo_t, lo_f);
-      }
-    } else if (nsc > 0) {
-      if (nsc <= SMALL_LIST) {
-        if (b == 0) radix_sort<false>(grid, P, nsc, cbits, sm);
-        grid.sync();
-      } else {
-        radix_sort<true>(grid, P, nsc, cbits, sm);
-      }
-      const int32_t* roots = (((cbits + 7) / 8) & 1) ? P.v1 : P.v0;  // buffer after ceil(cbits / 8) passes
-      const int64_t r0 = nsc * b / G, r1 = nsc * (b + 1) / G;
-      const unsigned long long s = block_sum(comp_table(P, roots, r0, r1), sm);
-      if (t == 0) P.blk[4 * b + 3] = (int64_t)s;
-      grid.sync();
-      {
-        unsigned long long carry = 0;
-        for (int c = t; c < b; c += NT) carry += (unsigned long long)ld_(P.blk + 4 * c + 3);
-        carry = block_sum(carry, sm);
-        comp_offsets(P, r0, r1, carry, lo_t, lo_f, nspans, sm);
-      }
-      node_keys(P, gtid, nsp, gsz);
-      grid.sync();
-      const int cur2 = radix_sort<true>(grid, P, nsp, nbits, sm);
-      emit_nodes(P, cur2 ? P.k1 : P.k0, cur2 ? P.v1 : P.v0, gtid, nsp, gsz, lo_t, lo_f);
-    }
+    maxsz_all = maxsz > maxsz_all ? maxsz : maxsz_all;
+    nroots_log += nsc;
+    nnodes_log += nsp;
     if (gtid == 0) P.gcc_sizes[ngcc] = gsize;
     ++ngcc;
     nspans += nsc;
@@ -834,6 +856,58 @@ __global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
       E_nx = tmp;
     }
   }
+  // ---- spoke blocks of all iterations at once (reorder.py:236-257): components ordered by
+  // (iteration, size desc, min id asc) -- two stable LSD sorts of the root log (size key, then
+  // iteration key) -- and the global exclusive scan of their (rows, cols) IS lo_t / lo_f of their
+  // iteration plus the offset inside it; then the logged spoke nodes are stably grouped by their
+  // component's rank (roots first within an iteration's log, so members stay ascending).
+  RP_PROF(9)
+  if (nroots_log > 0) {
+    const int64_t R = nroots_log, Nn = nnodes_log;
+    for (int64_t i = gtid; i < R; i += gsz) {
+      P.k0[i] = (uint32_t)(maxsz_all - ld_(P.csize + ld_(P.rlog + i)));
+      P.v0[i] = (int32_t)i;
+    }
+    grid.sync();
+    int cur = radix_sort<true>(grid, P, R, maxsz_all > 1 ? key_bits(maxsz_all - 1) : 0, sm);
+    {
+      const int32_t* vs = cur ? P.v1 : P.v0;
+      for (int64_t i = gtid; i < R; i += gsz) {
+        const int32_t li = ld_(vs + i);
+        P.k0[i] = (uint32_t)ld_(P.riter + li);
+        P.v0[i] = li;
+      }
+    }
+    grid.sync();
+    cur = radix_sort<true>(grid, P, R, key_bits(iters), sm);
+    const int32_t* order = cur ? P.v1 : P.v0;  // log indices in rank order
+    {
+      const int64_t r0 = R * b / G, r1 = R * (b + 1) / G;
+      unsigned long long sacc = 0;
+      for (int64_t i = r0 + t; i < r1; i += NT) {
+        const int32_t r = ld_(P.rlog + ld_(order + i));
+        P.rank_of_root[r] = (int32_t)i;
+        const uint64_t rows = (uint64_t)ld_(P.crows + r);
+        const uint64_t cols = (uint64_t)ld_(P.csize + r) - rows;
+        const uint64_t tr = (rows << 32) | cols;
+        P.tri[i] = tr;
+        sacc += tr;
+      }
+      sacc = block_sum(sacc, sm);
+      if (t == 0) P.blk[4 * b + 3] = (int64_t)sacc;
+      grid.sync();
+      unsigned long long carry = 0;
+      for (int c = t; c < b; c += NT) carry += (unsigned long long)ld_(P.blk + 4 * c + 3);
+      carry = block_sum(carry, sm);
+      comp_offsets(P, r0, r1, carry, 0, 0, 0, sm);  // the global scan already includes lo_t / lo_f
+    }
+    node_keys(P, gtid, Nn, gsz);
+    grid.sync();
+    const int cur2 = radix_sort<true>(grid, P, Nn, R > 1 ? key_bits(R - 1) : 0, sm);
+    emit_nodes(P, cur2 ? P.k1 : P.k0, cur2 ? P.v1 : P.v0, gtid, Nn, gsz, 0, 0);
+    nspans = R;
+  }
+  if (P.prof && gtid == 0) P.prof[10] += gtimer() - tlast;
   // terminal giant component: the middle ids, ascending (reorder.py:271-275)
   const int64_t rem = cnt_t + cnt_f;
   for (int64_t i = gtid; i < rem; i += gsz) {
@@ -906,7 +980,7 @@ bool run_reorder_persistent(fpi_context* h, int64_t m, int64_t n, int64_t nnz, c
   Scratch<uint64_t> e0(nnz > 0 ? nnz : 1, s), e1(nnz > 0 ? nnz : 1, s);
   Scratch<uint8_t> state(V, s);
   Scratch<int32_t> deg(V, s), parent(V, s), csize(V, s), crows(V, s), act0(V, s), act1(V, s), cand(V, s),
-      rank_of_root(V, s), v0(V, s), v1(V, s);
+      rank_of_root(V, s), v0(V, s), v1(V, s), rlog(V, s), riter(V, s);
   Scratch<uint32_t> k0(V, s), k1(V, s);
   Scratch<uint64_t> tri(V, s), toff(V, s), hubkeys(2 * HUB_CAP, s);
   Scratch<int64_t> gcc(V + 2, s), blk(4 * G, s);
@@ -943,6 +1017,8 @@ bool run_reorder_persistent(fpi_context* h, int64_t m, int64_t n, int64_t nnz, c
   P.v0 = v0;
   P.v1 = v1;
   P.rank_of_root = rank_of_root;
+  P.rlog = rlog;
+  P.riter = riter;
   P.tri = tri;
   P.toff = toff;
   P.row_fwd = d_row_fwd;
@@ -974,9 +1050,10 @@ bool run_reorder_persistent(fpi_context* h, int64_t m, int64_t n, int64_t nnz, c
     unsigned long long hp[16];
     FPI_CUDA(cudaMemcpy(hp, prof.get(), sizeof(hp), cudaMemcpyDeviceToHost));
     static const char* names[] = {"degree", "hub-select", "hub-collect", "hub-rank", "hook", "label", "pick",
-                                  "part-count", "part-write", "spokes+compact"};
+                                  "part-count", "part-write", "compact"};
     fprintf(stderr, "[reorder persistent G=%d T=%lld]", G, (long long)c.out[2]);
     for (int i = 0; i < 10; ++i) fprintf(stderr, " %s %.3f", names[i], hp[i] * 1e-6);
+    fprintf(stderr, " | spoke layout (after the loop) %.3f", hp[10] * 1e-6);
     fprintf(stderr, " ms\n");
   }
   out.m1 = lo_t;
