@@ -186,55 +186,86 @@ __global__ void k_chunk_maps(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, ui
   }
 }
 
-// pass 2a: per block of CPB chunks, the composed map for each entry offset.
+// The composition passes below are pointer chases (entry -> exit offset, chunk after chunk).  One
+// warp per chain with lane = entry offset: the E = 32 maps of the next WB chunks / blocks are loaded
+// as independent coalesced loads, then the chain advances through them by shuffles.
+constexpr int WB = 16;
+
+// pass 2a: per block of CPB chunks, the composed map for each entry offset (warp per block).
 __global__ void k_block_maps(const uint32_t* __restrict__ maps, int64_t nchunks, int64_t nblocks,
                              uint64_t* __restrict__ bmaps) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nblocks * E) return;
-  int64_t b = t / E;
-  int e = (int)(t % E);
-  int64_t c0 = b * CPB, c1 = c0 + CPB < nchunks ? c0 + CPB : nchunks;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (b >= nblocks) return;
+  const int64_t c0 = b * CPB, c1 = c0 + CPB < nchunks ? c0 + CPB : nchunks;
   uint64_t cnt = 0;
-  int cur = e;
-  for (int64_t c = c0; c < c1; ++c) {
-    uint32_t mm = maps[c * E + cur];
-    cnt += mm >> 8;
-    cur = (int)(mm & 0xff);
+  int cur = lane;  // this lane follows entry offset `lane`
+  for (int64_t cb = c0; cb < c1; cb += WB) {
+    uint32_t mm[WB];
+#pragma unroll
+    for (int j = 0; j < WB; ++j) mm[j] = cb + j < c1 ? maps[(cb + j) * E + lane] : 0u;
+#pragma unroll
+    for (int j = 0; j < WB; ++j) {
+      if (cb + j >= c1) break;
+      const uint32_t m = __shfl_sync(0xffffffffu, mm[j], cur);
+      cnt += m >> 8;
+      cur = (int)(m & 0xff);
+    }
   }
-  bmaps[b * E + e] = (cnt << 8) | (uint64_t)cur;
+  bmaps[b * E + lane] = (cnt << 8) | (uint64_t)cur;
 }
 
-// pass 2b: one thread walks the blocks from entry 0.
+// pass 2b: one warp walks the blocks from entry 0.
 __global__ void k_walk_blocks(const uint64_t* __restrict__ bmaps, int64_t nblocks, int32_t* __restrict__ bentry,
                               int64_t* __restrict__ bbase, int64_t* __restrict__ total) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
   int cur = 0;
   int64_t acc = 0;
-  for (int64_t b = 0; b < nblocks; ++b) {
-    bentry[b] = cur;
-    bbase[b] = acc;
-    uint64_t mm = bmaps[b * E + cur];
-    acc += (int64_t)(mm >> 8);
-    cur = (int)(mm & 0xff);
+  for (int64_t bb = 0; bb < nblocks; bb += WB) {
+    uint64_t mm[WB];
+#pragma unroll
+    for (int j = 0; j < WB; ++j) mm[j] = bb + j < nblocks ? bmaps[(bb + j) * E + lane] : 0ull;
+#pragma unroll
+    for (int j = 0; j < WB; ++j) {
+      if (bb + j >= nblocks) break;
+      if (lane == 0) {
+        bentry[bb + j] = cur;
+        bbase[bb + j] = acc;
+      }
+      const uint64_t m = __shfl_sync(0xffffffffu, mm[j], cur);
+      acc += (int64_t)(m >> 8);
+      cur = (int)(m & 0xff);
+    }
   }
-  *total = acc;
+  if (lane == 0) *total = acc;
 }
 
-// pass 2c: per block, walk its chunks from the block entry.
+// pass 2c: per block (one warp), walk its chunks from the block entry.
 __global__ void k_walk_chunks(const uint32_t* __restrict__ maps, int64_t nchunks, int64_t nblocks,
                               const int32_t* __restrict__ bentry, const int64_t* __restrict__ bbase,
                               uint8_t* __restrict__ centry, int64_t* __restrict__ cbase) {
-  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= nblocks) return;
   int cur = bentry[b];
   int64_t acc = bbase[b];
-  int64_t c0 = b * CPB, c1 = c0 + CPB < nchunks ? c0 + CPB : nchunks;
-  for (int64_t c = c0; c < c1; ++c) {
-    centry[c] = (uint8_t)cur;
-    cbase[c] = acc;
-    uint32_t mm = maps[c * E + cur];
-    acc += mm >> 8;
-    cur = (int)(mm & 0xff);
+  const int64_t c0 = b * CPB, c1 = c0 + CPB < nchunks ? c0 + CPB : nchunks;
+  for (int64_t cb = c0; cb < c1; cb += WB) {
+    uint32_t mm[WB];
+#pragma unroll
+    for (int j = 0; j < WB; ++j) mm[j] = cb + j < c1 ? maps[(cb + j) * E + lane] : 0u;
+#pragma unroll
+    for (int j = 0; j < WB; ++j) {
+      if (cb + j >= c1) break;
+      if (lane == j) {
+        centry[cb + j] = (uint8_t)cur;
+        cbase[cb + j] = acc;
+      }
+      const uint32_t m = __shfl_sync(0xffffffffu, mm[j], cur);
+      acc += m >> 8;
+      cur = (int)(m & 0xff);
+    }
   }
 }
 
@@ -380,10 +411,10 @@ void sketch_normal(fpi_context* h, int64_t seed, int64_t rows, int64_t cols, dou
     const int T = 128;
     unsigned g1 = grid_for(nchunks, T, (int64_t)h->num_sms * 64);
     k_chunk_maps<<<g1, T, 0, s>>>(st[0], st[1], st[2], st[3], nchunks, maps, overflow);
-    k_block_maps<<<grid_for(nblocks * E, 256, 1 << 30), 256, 0, s>>>(maps, nchunks, nblocks, bmaps);
+    k_block_maps<<<grid_for(nblocks * 32, 256, 1 << 30), 256, 0, s>>>(maps, nchunks, nblocks, bmaps);
     k_walk_blocks<<<1, 32, 0, s>>>(bmaps, nblocks, bentry, bbase, total);
-    k_walk_chunks<<<grid_for(nblocks, 128, 1 << 30), 128, 0, s>>>(maps, nchunks, nblocks, bentry, bbase, centry,
-                                                                  cbase);
+    k_walk_chunks<<<grid_for(nblocks * 32, 256, 1 << 30), 256, 0, s>>>(maps, nchunks, nblocks, bentry, bbase, centry,
+                                                                       cbase);
     FPI_LAUNCH_CHECK();
     note_launch(h, 4);
     int64_t have = host_read(total.get(), s);
