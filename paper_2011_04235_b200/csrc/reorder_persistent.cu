@@ -402,7 +402,10 @@ __device__ __forceinline__ void hook_edges(const Params& P, const uint64_t* E, i
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_reorder_persistent(Params P) {
+#ifndef RP_CTAS_PER_SM
+#define RP_CTAS_PER_SM 1
+#endif
+__global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Params P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Smem sm;
   const int t = threadIdx.x, b = blockIdx.x, G = gridDim.x, lane = t & 31;
@@ -965,7 +968,7 @@ bool run_reorder_persistent(fpi_context* h, int64_t m, int64_t n, int64_t nnz, c
   int occ = 0;
   FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reorder_persistent, NT, 0));
   if (occ < 1) return false;
-  const int G = h->num_sms * (occ > 1 ? 1 : occ);
+  const int G = h->num_sms * (occ > RP_CTAS_PER_SM ? RP_CTAS_PER_SM : occ);
   if (V / G >= (1 << 20)) return false;  // per-tile counters are packed in 21-bit fields (tile <= NT anyway)
 
   cudaStream_t s = h->stream;

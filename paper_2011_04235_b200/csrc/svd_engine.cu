@@ -34,6 +34,17 @@ void sketch_normal(fpi_context* h, int64_t seed, int64_t rows, int64_t cols, dou
 
 namespace {
 
+// A <- (A + A^T) / 2 (upper and lower from the same pair of reads)
+__global__ void k_symmetrize(int64_t n, double* A, int64_t lda) {
+  FPI_GRID_STRIDE(e, n * n) {
+    const int64_t i = e / n, j = e - i * n;
+    if (j <= i) continue;
+    const double v = 0.5 * (A[i * lda + j] + A[j * lda + i]);
+    A[i * lda + j] = v;
+    A[j * lda + i] = v;
+  }
+}
+
 __global__ void k_sqrt_clamp(int64_t n, double* v) {
   FPI_GRID_STRIDE(i, n) v[i] = v[i] > 0.0 ? sqrt(v[i]) : 0.0;
 }
@@ -274,12 +285,23 @@ __global__ void k_eig_orth(int64_t k, const double* __restrict__ w, const double
 
 // ---------------------------------------------------------------------------
 // dense SVD of a tall panel (p >= q): the top `rank` triplets.
+// With R (q x q) the panel is the implicit product M R^T: its Gram is R (M^T M) R^T and every
+// product with it goes through the small R first, so the p x q product is never formed (the
+// randomized SVD's Y^T = Z L^-T, svd.py:135).
 static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M, int64_t ldm, int64_t rank,
-                           double* U, double* sigma, double* Vt, fpi_svd_diag* diag) {
+                           double* U, double* sigma, double* Vt, fpi_svd_diag* diag, const double* R = nullptr) {
   cudaStream_t s = h->stream;
   const unsigned G = (unsigned)(h->num_sms * 16);
   Scratch<double> Gm(q * q, s), W0(q * q, s), w0(q, s);
   gemm(h, true, false, q, q, p, 1.0, M, ldm, M, ldm, 0.0, Gm, q, /*sym=*/true);
+  if (R) {
+    Scratch<double> T1(q * q, s);
+    gemm(h, false, false, q, q, q, 1.0, R, q, Gm, q, 0.0, T1, q);   // R C
+    gemm(h, false, true, q, q, q, 1.0, T1, q, R, q, 0.0, Gm, q);    // (R C) R^T
+    k_symmetrize<<<grid_for(q * q, 256, G), 256, 0, s>>>(q, Gm, q);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+  }
   // Gram entries are accurate to eps * ||G|| in absolute terms: converge to that (absolute criterion)
   int sw0 = sym_eig(h, q, Gm, q, w0, W0, q, 60, 1e-15, true);
   int sw1 = 0;
@@ -301,7 +323,13 @@ static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M
     W1.alloc(q * q, s);
     w1.alloc(q, s);
     V.alloc(q * q, s);
-    gemm(h, false, false, p, q, q, 1.0, M, ldm, W0, q, 0.0, M1, q);
+    if (R) {
+      Scratch<double> T0(q * q, s);
+      gemm(h, true, false, q, q, q, 1.0, R, q, W0, q, 0.0, T0, q);  // R^T W0
+      gemm(h, false, false, p, q, q, 1.0, M, ldm, T0, q, 0.0, M1, q);
+    } else {
+      gemm(h, false, false, p, q, q, 1.0, M, ldm, W0, q, 0.0, M1, q);
+    }
     gemm(h, true, false, q, q, p, 1.0, M1, q, M1, q, 0.0, Gm, q, /*sym=*/true);
     sw1 = sym_eig(h, q, Gm, q, w1, W1, q, 60, 1e-14, false);
     gemm(h, false, false, q, q, q, 1.0, W0, q, W1, q, 0.0, V, q);
@@ -313,7 +341,13 @@ static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M
   // candidate left vectors for the top `rank` and their norms (= sigma)
   Scratch<double> Uraw(p * rank, s), ss(rank, s), ss2(rank, s);
   Scratch<int32_t> ord(rank, s), ord2(rank, s);
-  gemm(h, false, false, p, rank, q, 1.0, Mr, ldr, Wsel, q, 0.0, Uraw, rank);
+  if (R && !refine) {
+    Scratch<double> Wt2(q * rank, s);
+    gemm(h, true, false, q, rank, q, 1.0, R, q, Wsel, q, 0.0, Wt2, rank);  // R^T W[:, :rank]
+    gemm(h, false, false, p, rank, q, 1.0, M, ldm, Wt2, rank, 0.0, Uraw, rank);
+  } else {
+    gemm(h, false, false, p, rank, q, 1.0, Mr, ldr, Wsel, q, 0.0, Uraw, rank);
+  }
   col_sumsq(h, p, rank, Uraw, rank, ss);
   k_sqrt_clamp<<<grid_for(rank, 256, G), 256, 0, s>>>(rank, ss);
   // sort the kept sigma descending (ties keep order) so factors are flagged sorted
@@ -622,17 +656,23 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   Gm.release();
   trace_point(h, "rsvd:cholesky/inverse");
   // Y^T = (inner^T B) L^-T   (svd.py:135: Y = Q^T inner)
-  Scratch<double> Z(q * k, s), Yt(q * k, s);
+  Scratch<double> Z(q * k, s);
   op.applyT(h, B, k, Z);
   trace_point(h, "rsvd:Z = M^T B");
-  gemm(h, false, true, q, k, k, 1.0, Z, k, Linv, k, 0.0, Yt, k);
-  Z.release();
-  trace_point(h, "rsvd:Yt = Z L^-T");
-  // SVD of Y (k x q) through its transpose Y^T = Vy S Uy^T   (svd.py:136)
+  // SVD of Y (k x q) through its transpose Y^T = Z L^-T = Vy S Uy^T   (svd.py:135-136); for a tall
+  // Y^T the product is left implicit (Gram L^-1 (Z^T Z) L^-T)
   Scratch<double> Vy(q * rank, s), Uyt(rank * k, s);
-  dense_svd(h, q, k, Yt, k, rank, Vy, sigma, Uyt, diag);
+  // implicit only when L is well conditioned: the Gram of Z carries cond(L)^2 more rounding than
+  // the Gram of Y^T (the CholeskyQR sketches here measure cond 1.2 - 2.7)
+  if (q >= k && diag && diag->cond_estimate > 0.0 && diag->cond_estimate < 8.0) {
+    dense_svd_tall(h, q, k, Z, k, rank, Vy, sigma, Uyt, diag, Linv);
+  } else {
+    Scratch<double> Yt(q * k, s);
+    gemm(h, false, true, q, k, k, 1.0, Z, k, Linv, k, 0.0, Yt, k);
+    dense_svd(h, q, k, Yt, k, rank, Vy, sigma, Uyt, diag);
+  }
+  Z.release();
   trace_point(h, "rsvd:dense_svd(Yt)");
-  Yt.release();
   transpose(h, q, rank, Vy, rank, Vt, q);                   // Vt = Vy^T
   trace_point(h, "rsvd:transpose Vy");
   // U = Q U~ = B L^-T U~ ,  U~ = Uyt^T   (svd.py:137)
