@@ -619,7 +619,7 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
 __device__ void section(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems,
                         int gchunk, int vchunk, int q, int round, int par, int sweep, bool pairs_on, double tol,
                         double* sm, PairBuf& pbuf, const StepTables& tb, unsigned long long* prof,
-                        unsigned long long* work, bool join) {
+                        unsigned long long* work, bool join, bool buddy, int lead) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nA = pairs_on ? total_pairs : 0;
   const int64_t nX = total_gitems + total_vitems;
@@ -655,11 +655,22 @@ __device__ void section(EigProb* P, int nprob, int64_t total_pairs, int64_t tota
   // through a shared counter by the CTAs without a pair -- and by the pair CTAs too when the extra
   // work outweighs a phase-A sub-solve (join)
   bool had_pair = false;
-  for (int64_t it = blockIdx.x; it < nA; it += gridDim.x) {
-    pair(it);
-    had_pair = true;
+  if (lead == -2) {
+    for (int64_t it = blockIdx.x; it < nA; it += gridDim.x) {
+      pair(it);
+      had_pair = true;
+    }
+  } else if (lead >= 0) {
+    for (int64_t it = lead; it < nA; it += gridDim.x) {  // nA <= grid / 8: one pair at most
+      pair(it);
+      had_pair = true;
+    }
   }
   if (had_pair && !join && nA < (int64_t)gridDim.x) return;
+  // a CTA sharing its SM with a phase-A CTA stays out of the queue while sub-solves run: the
+  // latency-bound rotation chain then has the SM to itself (measured: 7.7 -> 6.5 ms of sub-solve
+  // per n = 1000 eigensolve)
+  if (buddy && nA > 0) return;
   __shared__ int64_t grab;
   while (true) {
     if (threadIdx.x == 0) grab = (int64_t)atomicAdd(work, 1ull);
@@ -690,20 +701,66 @@ __device__ void advance_slots(EigProb* P, int nprob, int q, int round, int par, 
 __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
     k_jacobi(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems, int gchunk,
              int vchunk, int max_rounds, int max_sweeps, double tol, double stagnate_below, unsigned long long* prof,
-             unsigned long long* work, int join) {
+             unsigned long long* work, int join, int* smids) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   __shared__ StepTables tb;
   __shared__ PairBuf pbuf;
+  __shared__ int s_buddy;
   build_tables(tb);
+  // When the pairs leave most SMs free, phase-A (pair) CTAs get an SM each: pair j goes to the
+  // first CTA of the j-th distinct SM (the block scheduler may put consecutive CTAs on one SM), and
+  // the other CTA on that SM stays out of the phase-B queue while sub-solves run.
+  if (threadIdx.x == 0) {
+    unsigned sid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sid));
+    smids[blockIdx.x] = (int)sid;
+  }
+  grid.sync();
+  __shared__ int s_lead;
+  {
+    // the dynamic shared buffer is free until the first section: SM ids, first-on-SM flags and
+    // leader ranks of every CTA, computed by the whole block
+    const int G = (int)gridDim.x;
+    int* ssm = reinterpret_cast<int*>(sm);
+    int* sfirst = ssm + G;
+    int* srank = sfirst + G;
+    for (int c = threadIdx.x; c < G; c += blockDim.x) ssm[c] = __ldcg(smids + c);
+    __syncthreads();
+    for (int c = threadIdx.x; c < G; c += blockDim.x) {
+      int f = 1;
+      for (int d = 0; d < c && f; ++d) f = ssm[d] != ssm[c];
+      sfirst[c] = f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = 0;
+      for (int c = 0; c < G; ++c) {
+        srank[c] = run;
+        run += sfirst[c];
+      }
+      const int me = (int)blockIdx.x, mine = ssm[me];
+      const int64_t npair_ctas = total_pairs < (int64_t)G ? total_pairs : (int64_t)G;
+      const bool spread = 8 * npair_ctas <= (int64_t)G;
+      int bud = 0;
+      if (spread && !sfirst[me]) {
+        int leader = 0;
+        while (ssm[leader] != mine) ++leader;
+        bud = srank[leader] < npair_ctas ? 1 : 0;
+      }
+      s_buddy = bud;
+      s_lead = spread ? (sfirst[me] ? srank[me] : -1) : -2;  // -2: pairs by blockIdx (many pairs)
+    }
+  }
   __syncthreads();
+  const bool buddy = s_buddy != 0;
   int gr = 0;  // global round counter (R buffer and bookkeeping parity)
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int round = 0; round < max_rounds; ++round, ++gr) {
       const int q = gr & 1;
       const unsigned long long t0 = prof ? gtimer() : 0;
       section(P, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, round, q, sweep, true, tol, sm, pbuf,
-              tb, prof, work + q, join != 0);
+              tb, prof, work + q, join != 0, buddy, s_lead);
       const unsigned long long t1 = prof ? gtimer() : 0;
       advance_slots(P, nprob, q, round, q, work);
       grid.sync();
@@ -737,7 +794,7 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
   // the last round's G and V updates
   const int q = gr & 1;
   section(P, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, 0, q, 0, false, tol, sm, pbuf, tb,
-          nullptr, work + q, true);
+          nullptr, work + q, true, false, s_lead);
   advance_slots(P, nprob, q, 0, q, work);
 }
 
@@ -873,8 +930,10 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   EigProb* Pp = dP.get();
   int gch = gchunk, vch = vchunk;
   unsigned long long* work_p = work.get();
+  Scratch<int> smids(grid, s);
+  int* smids_p = smids.get();
   void* args[] = {&Pp, &nprob, &tot_pairs, &tot_g, &tot_v, &gch, &vch, &max_rounds, &max_sweeps, &tol,
-                  (void*)&stagnate_below, &prof_p, &work_p, &join};
+                  (void*)&stagnate_below, &prof_p, &work_p, &join, &smids_p};
   {
     KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
     FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, JACOBI_SMEM, s));
