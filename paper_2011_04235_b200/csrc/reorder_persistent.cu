@@ -689,6 +689,7 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
     else
       hook_edges<1>(P, E, ne, gtid, gsz);
     grid.sync();
+    if (P.prof && gtid == 0 && iters <= 5) P.prof[10 + iters] = gtimer() - tlast;
     RP_PROF(4)
     // ---- P7: labels, sizes, row counts
     for (int64_t i = gtid; i < L; i += gsz) {
@@ -1056,7 +1057,8 @@ bool run_reorder_persistent(fpi_context* h, int64_t m, int64_t n, int64_t nnz, c
                                   "part-count", "part-write", "compact"};
     fprintf(stderr, "[reorder persistent G=%d T=%lld]", G, (long long)c.out[2]);
     for (int i = 0; i < 10; ++i) fprintf(stderr, " %s %.3f", names[i], hp[i] * 1e-6);
-    fprintf(stderr, " | spoke layout (after the loop) %.3f", hp[10] * 1e-6);
+    fprintf(stderr, " | spoke layout (after the loop) %.3f | hook it1-5: %.3f %.3f %.3f %.3f %.3f", hp[10] * 1e-6,
+            hp[11] * 1e-6, hp[12] * 1e-6, hp[13] * 1e-6, hp[14] * 1e-6, hp[15] * 1e-6);
     fprintf(stderr, " ms\n");
   }
   out.m1 = lo_t;
