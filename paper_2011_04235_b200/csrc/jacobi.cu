@@ -701,7 +701,7 @@ __device__ void advance_slots(EigProb* P, int nprob, int q, int round, int par, 
 __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
     k_jacobi(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems, int gchunk,
              int vchunk, int max_rounds, int max_sweeps, double tol, double stagnate_below, unsigned long long* prof,
-             unsigned long long* work, int join, int* smids) {
+             unsigned long long* work, int join, int* smids, int spread_factor) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   __shared__ StepTables tb;
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
       }
       const int me = (int)blockIdx.x, mine = ssm[me];
       const int64_t npair_ctas = total_pairs < (int64_t)G ? total_pairs : (int64_t)G;
-      const bool spread = 8 * npair_ctas <= (int64_t)G;
+      const bool spread = (int64_t)spread_factor * npair_ctas <= (int64_t)G;
       int bud = 0;
       if (spread && !sfirst[me]) {
         int leader = 0;
@@ -932,8 +932,11 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   unsigned long long* work_p = work.get();
   Scratch<int> smids(grid, s);
   int* smids_p = smids.get();
+  // pair CTAs get SMs of their own while the pairs need at most 1 / spread of the grid
+  int spread = 8;
+  if (const char* e = getenv("FPI_JACOBI_SPREAD")) spread = atoi(e) > 0 ? atoi(e) : 1 << 20;
   void* args[] = {&Pp, &nprob, &tot_pairs, &tot_g, &tot_v, &gch, &vch, &max_rounds, &max_sweeps, &tol,
-                  (void*)&stagnate_below, &prof_p, &work_p, &join, &smids_p};
+                  (void*)&stagnate_below, &prof_p, &work_p, &join, &smids_p, &spread};
   {
     KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
     FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, JACOBI_SMEM, s));

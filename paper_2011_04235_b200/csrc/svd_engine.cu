@@ -755,7 +755,15 @@ void row_update(fpi_context* h, int64_t m1, int64_t n1, int64_t rank11, const do
   inner_svd(h, op, s_rank, n1, thr, seed, Ui, sigma, Vt, engine, &h->diag);
   // lift: U = [U11 Ui[:rank11] ; Ui[rank11:]]   (pinv.py:168-170)
   if (m1) {
-    if (rank11)
+    if (rank11 && (s_rank & 1)) {
+      // odd width: the gathered rows go through a copy with an even stride so the SpMM can use
+      // its 16-byte gathers (spmm.cu)
+      const int64_t ldp = s_rank + 1;
+      Scratch<double> Up(rank11 * ldp, s);
+      FPI_CUDA(cudaMemcpy2DAsync(Up.get(), ldp * sizeof(double), Ui.get(), s_rank * sizeof(double),
+                                 s_rank * sizeof(double), rank11, cudaMemcpyDeviceToDevice, s));
+      spmm(h, m1, rank11, s_rank, u_ptr, u_idx, u_val, nullptr, 1.0, Up, ldp, 0.0, U, s_rank);
+    } else if (rank11)
       spmm(h, m1, rank11, s_rank, u_ptr, u_idx, u_val, nullptr, 1.0, Ui, s_rank, 0.0, U, s_rank);
     else
       FPI_CUDA(cudaMemsetAsync(U, 0, sizeof(double) * m1 * s_rank, s));
