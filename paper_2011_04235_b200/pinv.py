@@ -152,7 +152,10 @@ class Pseudoinverse:
             raise ValueError(f"dimension mismatch: pseudoinverse expects {d.m} rows, got {Bd.shape[0]}")
         t = torch()
         L = Bd.shape[1]
-        Zh = t.empty((d.n, L), dtype=t.float64, pin_memory=True)
+        try:
+            Zh = t.empty((d.n, L), dtype=t.float64, pin_memory=True)
+        except RuntimeError:  # page-locked memory exhausted: pageable copies are still correct
+            Zh = t.empty((d.n, L), dtype=t.float64)
         _lib.call("fpi_pinv_apply_csr_host", d.m, d.n, d.r, _lib.ptr(d.U), _lib.ptr(d.sdag), _lib.ptr(d.Vt),
                   _lib.ptr(d.row_fwd), _lib.ptr(d.col_fwd), L, Bd.nnz, _lib.ptr(Bd.indptr), _lib.ptr(Bd.indices),
                   _lib.ptr(Bd.values), Zh.data_ptr())
