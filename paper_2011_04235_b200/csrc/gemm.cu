@@ -38,7 +38,10 @@ namespace {
 #define FPI_GEMM_CFG_STAGES 3
 #define FPI_GEMM_CFG_CTAS 3
 #endif
-constexpr int BM = FPI_GEMM_CFG_BM, BN = FPI_GEMM_CFG_BN, BK = 16, STAGES = FPI_GEMM_CFG_STAGES;
+#ifndef FPI_GEMM_CFG_BK
+#define FPI_GEMM_CFG_BK 16
+#endif
+constexpr int BM = FPI_GEMM_CFG_BM, BN = FPI_GEMM_CFG_BN, BK = FPI_GEMM_CFG_BK, STAGES = FPI_GEMM_CFG_STAGES;
 constexpr int WM = FPI_GEMM_CFG_WM, WN = FPI_GEMM_CFG_WN;  // warp tile
 constexpr int MI = WM / 8, NJ = WN / 8;                    // DMMA tiles per warp
 constexpr int WARPS_N = BN / WN;                            // warp grid (BM / WM) x (BN / WN)
