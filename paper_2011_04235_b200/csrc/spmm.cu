@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 }
 
 template <int NSL>
-__global__ void __launch_bounds__(WARPS * 32, 2)
+__global__ void __launch_bounds__(WARPS * 32, FPI_SPMM_MINB)
     k_spmm_multi(int64_t p, int64_t k, const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                  const double* __restrict__ values, const double* __restrict__ row_scale, double alpha,
                  const double* __restrict__ X, int64_t ldx, double beta, double* __restrict__ Y, int64_t ldy,
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2)
 }
 
 template <int NSL>
-__global__ void __launch_bounds__(WARPS * 32, 2)
+__global__ void __launch_bounds__(WARPS * 32, FPI_SPMM_MINB)
     k_spmm_segments_multi(const int64_t* __restrict__ rows, const int64_t* __restrict__ seg_off, int64_t nl,
                           int64_t nseg_total, int64_t k, const int64_t* __restrict__ indptr,
                           const int32_t* __restrict__ indices, const double* __restrict__ values,
