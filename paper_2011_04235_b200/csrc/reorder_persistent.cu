@@ -42,6 +42,9 @@ namespace cg = cooperative_groups;
 namespace fpi {
 namespace {
 
+#ifndef RP_HALVING
+#define RP_HALVING 1
+#endif
 constexpr int NT = 512;
 constexpr int NW = NT / 32;
 constexpr int HBITS = 11;
@@ -142,7 +145,7 @@ __device__ __forceinline__ int32_t find_root_cg(int32_t x, int32_t* parent) {
   if (cur != x) {
     int32_t prev = x, nxt;
     while (cur > (nxt = ld_(parent + cur))) {
-      parent[prev] = nxt;  // path halving (benign race: values only move toward the root)
+      if (RP_HALVING) parent[prev] = nxt;  // path halving (benign race: values only move toward the root)
       prev = cur;
       cur = nxt;
     }
@@ -155,7 +158,7 @@ __device__ __forceinline__ int32_t find_root_from(int32_t x, int32_t cur, int32_
   if (cur != x) {
     int32_t prev = x, nxt;
     while (cur > (nxt = ld_(parent + cur))) {
-      parent[prev] = nxt;
+      if (RP_HALVING) parent[prev] = nxt;
       prev = cur;
       cur = nxt;
     }
