@@ -358,6 +358,19 @@ def ours_arm(args):
                         "avg_launch_ms": round(avg_ms, 4), "launches": dom["launches"],
                         "share_of_step": round(dom["ms"] / ms, 4), "peak_source": peak_src}
 
+    # the largest kernel class by time when it is not the roofline one (the latency-bound eigensolver
+    # carries no algorithmic flop count of its own)
+    largest = None
+    if rep:
+        big_name, big = max(rep.items(), key=lambda kv: kv[1]["ms"])
+        if big_name != dom_name:
+            largest = {"kernel": big_name, "share_of_step": round(big["ms"] / ms, 4), "launches": big["launches"],
+                       "bound": "latency",
+                       "note": "two-sided block Jacobi: sequential rotation chains + one grid barrier per round; "
+                               "ncu shows the DMMA pipe ~1.5% active (profiles/r01_ncu_full_summary_v13.json)"}
+        if roofline is not None:
+            roofline["largest_kernel"] = largest
+
     # ---- e2e through the public API with host inputs
     e2e = None
     if not args.no_e2e:
