@@ -395,6 +395,7 @@ struct EigProb {
   double* G[2];        // npad x npad each
   double* V;           // npad x npad
   double* Jbuf;        // 2 x np x JS x JS (by round parity)
+  double* Sbuf;        // 2 x np x JS x JS: each pair's rotated sub-problem J^T S J (by round parity)
   int* jflag;          // 2 x np: rotation of the pair is not the identity
   unsigned long long* offmax;  // per sweep
   const double* abs_scale;     // null: relative criterion
@@ -543,29 +544,26 @@ __device__ void build_subproblem(const EigProb& pr_, int q, int pr, int rho, dou
   double* Jy = sm + 3 * TILE;
   double* T = sm + 4 * TILE;    // tiles 4, 5, 6: G[P(X), P(X)], G[P(X), P(Y)], G[P(Y), P(Y)]
   double* W = sm + 7 * TILE;    // tile 7: three 32 x 16 products, stride 48
-  const int combos[3][2] = {{0, 0}, {0, 1}, {1, 1}};
+  // S[X, X] and S[Y, Y] are 16 x 16 diagonal blocks of the previous round's rotated sub-problems
+  // (J^T S J of pairs P(X), P(Y), published by their CTAs); only S[X, Y] mixes two pairs and is
+  // formed from the pre-update G tile G[P(X), P(Y)] and both rotations.
+  const double* S0 = pr_.Sbuf + (int64_t)par * np * JS * JS;
   j_async(Jx, J0 + (int64_t)pp[0] * JS * JS);
   j_async(Jy, J0 + (int64_t)pp[1] * JS * JS);
-  for (int c = 0; c < 3; ++c) {
-    const int pa = pp[combos[c][0]], pb = pp[combos[c][1]];
-    tile_async(T + c * TILE, Gs, ld, -1, rr_block(pa, prho, nb), rr_block(nb - 1 - pa, prho, nb),
-               rr_block(pb, prho, nb), rr_block(nb - 1 - pb, prho, nb));
-  }
+  tile_async(T, Gs, ld, -1, rr_block(pp[0], prho, nb), rr_block(nb - 1 - pp[0], prho, nb), rr_block(pp[1], prho, nb),
+             rr_block(nb - 1 - pp[1], prho, nb));
   cp_commit();
+  for (int e = threadIdx.x; e < 2 * 256; e += JT) {
+    const int a = e >> 8, i = (e >> 4) & 15, j = e & 15;
+    const double* Sprev = S0 + (int64_t)pp[a] * JS * JS;
+    S[(16 * a + i) * LDS_ + 16 * a + j] = __ldcg(Sprev + (16 * hh[a] + i) * JS + 16 * hh[a] + j);
+  }
   cp_wait<0>();
   __syncthreads();
-  // W_c = T_c J_b[:, 16 h_b : +16]   (32 x 16)
-  for (int c = 0; c < 3; ++c) {
-    const int b = combos[c][1];
-    mm_k32(T + c * TILE, LDS_, false, (b ? Jy : Jx) + 16 * hh[b], LDS_, W + 16 * c, 48, 32, 16, 8 * c, warp, lane);
-  }
+  // W = G[P(X), P(Y)] J_Y[:, 16 h_Y : +16]   (32 x 16), S[X, Y] = J_X[:, 16 h_X : +16]^T W   (16 x 16)
+  mm_k32(T, LDS_, false, Jy + 16 * hh[1], LDS_, W, 48, 32, 16, 0, warp, lane);
   __syncthreads();
-  // S[a, b] = J_a[:, 16 h_a : +16]^T W_c   (16 x 16)
-  for (int c = 0; c < 3; ++c) {
-    const int a = combos[c][0], b = combos[c][1];
-    mm_k32((a ? Jy : Jx) + 16 * hh[a], LDS_, true, W + 16 * c, 48, S + (16 * a) * LDS_ + 16 * b, LDS_, 16, 16,
-           4 * c, warp, lane);
-  }
+  mm_k32(Jx + 16 * hh[0], LDS_, true, W, 48, S + 16, LDS_, 16, 16, 0, warp, lane);
   __syncthreads();
   for (int e = threadIdx.x; e < 256; e += JT) {  // S[Y, X] = S[X, Y]^T
     const int i = e >> 4, j = e & 15;
@@ -599,10 +597,12 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
   double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
   if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
   double* Jp = pr_.Jbuf + ((int64_t)par * np + pr) * JS * JS;
+  double* Sp = pr_.Sbuf + ((int64_t)par * np + pr) * JS * JS;
   int rot = 0;
   for (int e = threadIdx.x; e < JS * JS; e += JT) {
     const double v = Ra[(e & 31) * LDS_ + (e >> 5)];  // Rt -> row-major J
     Jp[e] = v;
+    Sp[e] = Sa[(e >> 5) * LDS_ + (e & 31)];  // the rotated sub-problem: next round's diagonal blocks
     rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
   }
   rot = __syncthreads_or(rot);
@@ -897,7 +897,7 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     tot_g += g_runs_before(np, gchunk);
     tot_v += np * ((np + vchunk - 1) / vchunk);
   }
-  Scratch<double> Gall(gsz, s), Gall2(gsz, s), Vall(gsz, s), Jall(jsz, s), scales(nprob, s);
+  Scratch<double> Gall(gsz, s), Gall2(gsz, s), Vall(gsz, s), Jall(jsz, s), Sall(jsz, s), scales(nprob, s);
   Scratch<int> fall(fsz, s);
   Scratch<unsigned long long> offm((int64_t)nprob * (max_sweeps + 1), s);
   Scratch<EigProb> dP(nprob, s);
@@ -910,6 +910,7 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     hp[i].G[1] = Gall2.get() + goff[i];
     hp[i].V = Vall.get() + goff[i];
     hp[i].Jbuf = Jall.get() + jo;
+    hp[i].Sbuf = Sall.get() + jo;
     hp[i].jflag = fall.get() + fo;
     hp[i].offmax = offm.get() + (int64_t)i * (max_sweeps + 1);
     hp[i].abs_scale = absolute ? scales.get() + i : nullptr;
