@@ -26,15 +26,25 @@ __global__ void k_expand_rows(int64_t m, const int64_t* __restrict__ indptr, int
 }
 
 __global__ void k_make_keys(int64_t cnt, const int32_t* __restrict__ major, const int32_t* __restrict__ minor,
-                            int minor_bits, uint64_t* __restrict__ keys, int32_t* __restrict__ pos,
-                            int32_t* __restrict__ counts) {
+                            int minor_bits, uint64_t* __restrict__ keys, int32_t* __restrict__ pos) {
   FPI_GRID_STRIDE(i, cnt) {
-    const int32_t mj = major[i];
-    keys[i] = ((uint64_t)(uint32_t)mj << minor_bits) | (uint32_t)minor[i];
+    keys[i] = ((uint64_t)(uint32_t)major[i] << minor_bits) | (uint32_t)minor[i];
     pos[i] = (int32_t)i;
-    const unsigned mask = __activemask();
-    const unsigned peers = __match_any_sync(mask, mj);
-    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + mj, (int32_t)__popc(peers));
+  }
+}
+
+// Row pointers from the sorted keys: ptr[r] = first position whose major is >= r, by a binary search
+// per row (no per-entry atomics -- a transpose's popular columns made those serialise).
+__global__ void k_ptr_from_sorted(int64_t cnt, const uint64_t* __restrict__ keys, int minor_bits, int64_t nmajor,
+                                  int64_t* __restrict__ ptr) {
+  FPI_GRID_STRIDE(r, nmajor + 1) {
+    const uint64_t target = (uint64_t)r << minor_bits;
+    int64_t lo = 0, hi = cnt;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    ptr[r] = lo;
   }
 }
 
@@ -239,25 +249,22 @@ void build_csr(fpi_context* h, CubTemp& tmp, int64_t cnt, const int32_t* major, 
   cudaStream_t s = h->stream;
   const int T = 256;
   const int64_t G = (int64_t)h->num_sms * 16;
-  Scratch<int32_t> counts(nmajor + 1, s);
-  FPI_CUDA(cudaMemsetAsync(counts.get(), 0, sizeof(int32_t) * (nmajor + 1), s));
   if (cnt > 0) {
     const int minor_bits = bits_for((uint64_t)(nminor > 0 ? nminor : 1));
     const int major_bits = bits_for((uint64_t)(nmajor > 0 ? nmajor : 1));
     FPI_REQUIRE(minor_bits + major_bits <= 64, FPI_ECAPACITY, "sort key exceeds 64 bits");
     Scratch<uint64_t> keys(cnt, s), keys2(cnt, s);
     Scratch<int32_t> pos(cnt, s), pos2(cnt, s);
-    k_make_keys<<<grid_for(cnt, T, G), T, 0, s>>>(cnt, major, minor, minor_bits, keys, pos, counts);
+    k_make_keys<<<grid_for(cnt, T, G), T, 0, s>>>(cnt, major, minor, minor_bits, keys, pos);
     sort_pairs(tmp, keys.get(), keys2.get(), pos.get(), pos2.get(), cnt, false, 0, minor_bits + major_bits, s);
     k_scatter_sorted<<<grid_for(cnt, T, G), T, 0, s>>>(cnt, keys2, pos2, vals, (1ull << minor_bits) - 1, out_idx,
                                                       out_val);
+    k_ptr_from_sorted<<<grid_for(nmajor + 1, T, G), T, 0, s>>>(cnt, keys2, minor_bits, nmajor, out_ptr);
     FPI_LAUNCH_CHECK();
-    note_launch(h, 3);
+    note_launch(h, 4);
+  } else {
+    FPI_CUDA(cudaMemsetAsync(out_ptr, 0, sizeof(int64_t) * (nmajor + 1), s));
   }
-  k_counts_to_ptr_first<<<1, 1, 0, s>>>(out_ptr);
-  if (nmajor > 0) inclusive_sum(tmp, counts.get(), out_ptr + 1, nmajor, s);
-  FPI_LAUNCH_CHECK();
-  note_launch(h, 2);
 }
 
 void csr_transpose(fpi_context* h, int64_t p, int64_t q, int64_t nnz, const int64_t* indptr, const int32_t* indices,
