@@ -189,7 +189,7 @@ __global__ void k_chunk_maps(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, ui
 // The composition passes below are pointer chases (entry -> exit offset, chunk after chunk).  One
 // warp per chain with lane = entry offset: the E = 32 maps of the next WB chunks / blocks are loaded
 // as independent coalesced loads, then the chain advances through them by shuffles.
-constexpr int WB = 16;
+constexpr int WB = 32;
 
 // pass 2a: per block of CPB chunks, the composed map for each entry offset (warp per block).
 __global__ void k_block_maps(const uint32_t* __restrict__ maps, int64_t nchunks, int64_t nblocks,
