@@ -32,6 +32,10 @@ namespace {
 
 constexpr int BT = 256;  // threads per block-SVD CTA
 constexpr int64_t TINY_DOUBLES = 3000;  // blocks needing <= 24 KB smem run many CTAs per SM
+#ifndef FPI_GRAM_MIN_DIM
+#define FPI_GRAM_MIN_DIM 48
+#endif
+constexpr int64_t GRAM_MIN_DIM = FPI_GRAM_MIN_DIM;
 
 struct BlockMeta {
   int64_t* keep;      // per span
@@ -51,7 +55,10 @@ __global__ void k_plan(int64_t nspans, const int64_t* __restrict__ spans, double
       kp = (int64_t)ceil(alpha * (double)c);  // int(np.ceil(alpha * min(h, w))), svd.py:167
       int64_t cpad = c + (c & 1);
       const int64_t need = r * cpad + cpad * cpad + 4 * cpad;
-      lg = need > smem_doubles ? 1 : (need > TINY_DOUBLES ? 2 : 0);
+      // blocks whose one-sided Jacobi chain would be long (min dimension >= GRAM_MIN_DIM: the chain
+      // grows with c^2 sweeps-rounds and the kernel ends with its slowest CTA) join the batched Gram
+      // path with the blocks that do not fit in shared memory
+      lg = (need > smem_doubles || c >= GRAM_MIN_DIM) ? 1 : (need > TINY_DOUBLES ? 2 : 0);
     }
     keep[b] = kp;
     uk[b] = h * kp;
