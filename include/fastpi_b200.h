@@ -172,6 +172,30 @@ int fpi_randomized_svd(fpi_handle h, int64_t p, int64_t q, const int64_t* a_ptr,
                        const double* a_val, const int64_t* at_ptr, const int32_t* at_idx, const double* at_val,
                        int64_t rank, int64_t seed, double* d_U, double* d_sigma, double* d_Vt);
 
+/* ---- pinv.py:278-347 fastpi(): the whole factorization in one call -------------------------- */
+typedef struct {
+  int64_t m, n, rank;             /* rank r of the final factors */
+  int64_t m1, n1, m2, n2, n_iterations, n_spans;
+  int64_t rank11, s;              /* block-SVD rank and row-update rank */
+  int32_t row_engine, col_engine; /* 1 randomized, 2 dense, 0 none */
+  int32_t rank_clamped;           /* s < ceil(alpha n1): the pinv.py:324-328 warning */
+  int32_t all_filtered;           /* every sigma below the cutoff: the pinv.py:222-224 warning */
+  double tolerance_used;
+} fpi_fastpi_info;
+/* check_csr + reorder + partition + block SVD + row/column updates + pinv assembly on a CSR A (m >= n;
+ * for m < n factor A^T and swap the factors, pinv.py:291-303) with FastpiConfig's fields; seed is the
+ * config seed (the updates use seed + 1 and seed + 2).  The factors stay on the device, owned by the
+ * handle until fpi_fastpi_release or the next fpi_fastpi: U (m x r, reordered rows), sigma (r),
+ * Vt (r x n, reordered columns), sigma_dagger (r), row_fwd (m), col_fwd (n) -- the inputs of
+ * fpi_pinv_apply_csr / fpi_unfold.  Errors map like every entry point (ValueError / CapacityError /
+ * StructuralViolationError). */
+int fpi_fastpi(fpi_handle h, int64_t m, int64_t n, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
+               const double* d_values, double alpha, double k, int64_t seed, double low_rank_threshold,
+               double pinv_cutoff, fpi_fastpi_info* h_info);
+int fpi_fastpi_get(fpi_handle h, const double** d_U, const double** d_sigma, const double** d_Vt,
+                   const double** d_sigma_dagger, const int64_t** d_row_fwd, const int64_t** d_col_fwd);
+int fpi_fastpi_release(fpi_handle h);
+
 /* ---- dataset text format (datasets.py:81-167), host-side native parser ---------------------- */
 enum fpi_dataset_error {
   FPI_DS_OK = 0,

@@ -47,6 +47,12 @@ class DatasetInfo(C.Structure):
                 ("tok2_begin", C.c_int64), ("tok2_end", C.c_int64)]
 
 
+class FastpiInfo(C.Structure):
+    _fields_ = [("m", i64), ("n", i64), ("rank", i64), ("m1", i64), ("n1", i64), ("m2", i64), ("n2", i64),
+                ("n_iterations", i64), ("n_spans", i64), ("rank11", i64), ("s", i64), ("row_engine", i32),
+                ("col_engine", i32), ("rank_clamped", i32), ("all_filtered", i32), ("tolerance_used", f64)]
+
+
 class SvdDiag(C.Structure):
     _fields_ = [("engine", i32), ("cholqr_passes", i32), ("cond_estimate", f64),
                 ("eig_sweeps", i32 * 4), ("null_completed", i32)]
@@ -103,6 +109,9 @@ SIGNATURES = {
     "fpi_pinv_project_csr": (C.c_int, [vp, i64, i64, i64, vp, vp, i64, i64, i64, vp, vp, vp, vp]),
     "fpi_pinv_lift": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, vp]),
     "fpi_pinv_apply_dense": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, i64, vp, i64, vp]),
+    "fpi_fastpi": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, f64, f64, i64, f64, f64, C.POINTER(FastpiInfo)]),
+    "fpi_fastpi_get": (C.c_int, [vp] + [C.POINTER(vp)] * 6),
+    "fpi_fastpi_release": (C.c_int, [vp]),
     "fpi_timing_enable": (C.c_int, [vp, C.c_int]),
     "fpi_timing_report": (C.c_int, [vp, C.c_char_p, i64, C.c_int]),
     "fpi_dmma_peak": (C.c_int, [vp, C.POINTER(f64)]),

@@ -37,6 +37,11 @@ struct Error : std::runtime_error {
 
 }  // namespace fpi
 
+namespace fpi {
+struct FastpiResult;  // fastpi_capi.cu
+void fastpi_free(fpi_context* h);
+}  // namespace fpi
+
 // The handle: one stream, device properties, scratch memory and the results
 // that are fetched in a second call (variable-size outputs).
 struct fpi_context {
@@ -52,6 +57,7 @@ struct fpi_context {
   int64_t spans_cap = 0;
   void* host_scalars = nullptr;  // pinned scratch for per-iteration device scalars (reorder)
   cudaStream_t copy_stream = nullptr;  // device->host copies overlapped with the compute stream
+  fpi::FastpiResult* fastpi = nullptr;  // factors of the last fpi_fastpi call (fpi_fastpi_get)
   cudaEvent_t copy_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // numerics diagnostics of the last randomized / dense SVD
   fpi_svd_diag diag{};

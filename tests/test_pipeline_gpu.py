@@ -193,3 +193,43 @@ def test_apply_to_host_matches_device_apply():
     Zd = d2h(res.pseudoinverse.apply_device(DeviceCSR.from_host(p.Y)))
     assert Zh.shape == Zd.shape and Zh.dtype == np.float64
     np.testing.assert_allclose(Zh, Zd, rtol=0, atol=1e-13 * np.abs(Zd).max())
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_c_abi_fastpi_matches_python_pipeline(name):
+    """fpi_fastpi (Algorithm 1 in one C call) runs the same stages as the Python mirror: identical
+    sigma, sigma+, factors and permutations."""
+    import ctypes as C
+    import torch
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import DeviceCSR, d2h
+    p = problem(name)
+    w = p.workload
+    cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
+    res = fp.fastpi(p.A, cfg)
+    A = DeviceCSR.from_host(p.A)
+    info = _lib.FastpiInfo()
+    _lib.call("fpi_fastpi", A.shape[0], A.shape[1], A.nnz, _lib.ptr(A.indptr), _lib.ptr(A.indices),
+              _lib.ptr(A.values), float(w.alpha), float(w.k), int(w.seed), float(cfg.low_rank_threshold),
+              float(cfg.pinv_cutoff_factor), C.byref(info))
+    ptrs = [C.c_void_p() for _ in range(6)]
+    _lib.call("fpi_fastpi_get", *[C.byref(x) for x in ptrs])
+    m, n, r = info.m, info.n, info.rank
+    assert r == res.factors.rank
+    assert (info.m1, info.n1, info.m2, info.n2, info.n_iterations) == (
+        res.reordering.n_spoke_rows, res.reordering.n_spoke_cols, res.reordering.n_hub_rows,
+        res.reordering.n_hub_cols, res.reordering.n_iterations)
+
+    from cuda.bindings import runtime as rt
+    d = res.pseudoinverse._device()
+    fd = res.factors.device()
+    torch.cuda.synchronize()
+    for ptr, ref in ((ptrs[1], fd.sigma), (ptrs[3], d.sdag), (ptrs[0], fd.U), (ptrs[2], fd.Vt),
+                     (ptrs[4], d.row_fwd), (ptrs[5], d.col_fwd)):
+        out = torch.empty(ref.numel(), dtype=ref.dtype, device="cuda")
+        err, = rt.cudaMemcpy(out.data_ptr(), ptr.value, out.numel() * out.element_size(),
+                             rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+        assert int(err) == 0
+        np.testing.assert_array_equal(d2h(out), d2h(ref.reshape(-1)))
+    _lib.call("fpi_fastpi_release")
