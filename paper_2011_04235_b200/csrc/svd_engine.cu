@@ -211,13 +211,6 @@ __global__ void k_gather_cols_T(int64_t n, int64_t r, const double* __restrict__
 }
 
 // dst[j][:] = src[idx[j]][:]
-__global__ void k_gather_rows(int64_t n, int64_t L, const double* __restrict__ src, int64_t lds,
-                              const int64_t* __restrict__ idx, double* __restrict__ dst, int64_t ldd) {
-  FPI_GRID_STRIDE(e, n * L) {
-    int64_t j = e / L, l = e - j * L;
-    dst[j * ldd + l] = src[idx[j] * lds + l];
-  }
-}
 
 // dst[idx[i]][:] = src[i][:]
 __global__ void k_scatter_rows(int64_t m, int64_t L, const double* __restrict__ src, int64_t lds,
