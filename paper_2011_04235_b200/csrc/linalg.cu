@@ -312,6 +312,15 @@ void scale_rows(fpi_context* h, int64_t M, int64_t N, double* A, int64_t lda, co
   note_launch(h);
 }
 
+// The sign rule on the right vectors alone: Vt's rows flipped, the signs left in sign_out (r) for the
+// caller to fold into whatever produces the left vectors.
+void canonical_signs_vt(fpi_context* h, int64_t r, int64_t q, double* Vt, int64_t ldvt, double* sign_out) {
+  if (r <= 0) return;
+  k_canon_sign<<<(unsigned)(r < 4096 ? r : 4096), 256, 0, h->stream>>>(r, q, Vt, ldvt, sign_out);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+}
+
 void canonical_signs(fpi_context* h, int64_t r, int64_t p, int64_t q, double* U, int64_t ldu, double* Vt,
                      int64_t ldvt) {
   if (r <= 0) return;

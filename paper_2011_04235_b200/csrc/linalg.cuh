@@ -22,6 +22,7 @@ void transpose(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t ld
 void col_sumsq(fpi_context* h, int64_t M, int64_t N, const double* A, int64_t lda, double* out);
 void scale_cols(fpi_context* h, int64_t M, int64_t N, double* A, int64_t lda, const double* s, bool divide);
 void scale_rows(fpi_context* h, int64_t M, int64_t N, double* A, int64_t lda, const double* s);
+void canonical_signs_vt(fpi_context* h, int64_t r, int64_t q, double* Vt, int64_t ldvt, double* sign_out);
 void canonical_signs(fpi_context* h, int64_t r, int64_t p, int64_t q, double* U, int64_t ldu, double* Vt,
                      int64_t ldvt);
 }  // namespace fpi

@@ -58,13 +58,16 @@ __global__ void k_copy2d(int64_t M, int64_t N, const double* __restrict__ A, int
 }
 
 // cols of A (M x N) selected by ord[0..K) and divided by s[k]  -> B (M x K)
+// B[:, k] = sign[k] A[:, ord[k]] / s[k] (0 where s[k] == 0): sorted, normalised and sign-fixed left
+// vectors in one pass (sign may be null)
 __global__ void k_gather_cols_div(int64_t M, int64_t K, const double* __restrict__ A, int64_t lda,
                                   const int32_t* __restrict__ ord, const double* __restrict__ s,
-                                  double* __restrict__ B, int64_t ldb) {
+                                  const double* __restrict__ sign, double* __restrict__ B, int64_t ldb) {
   FPI_GRID_STRIDE(e, M * K) {
     int64_t i = e / K, k = e - i * K;
     double d = s[k];
-    B[i * ldb + k] = d > 0.0 ? A[i * lda + ord[k]] / d : 0.0;
+    const double v = d > 0.0 ? A[i * lda + ord[k]] / d : 0.0;
+    B[i * ldb + k] = sign ? sign[k] * v : v;
   }
 }
 
@@ -348,12 +351,14 @@ static void dense_svd_tall(fpi_context* h, int64_t p, int64_t q, const double* M
   CubTemp tmp(s);
   sort_pairs(tmp, ss.get(), ss2.get(), ord.get(), ord2.get(), rank, true, 0, 64, s);
   FPI_CUDA(cudaMemcpyAsync(sigma, ss2.get(), sizeof(double) * rank, cudaMemcpyDeviceToDevice, s));
-  k_gather_cols_div<<<grid_for(p * rank, 256, G), 256, 0, s>>>(p, rank, Uraw, rank, ord2, ss2, U, rank);
+  // right vectors first: their canonical signs ride along with the gather of the left ones
+  Scratch<double> sgn(rank, s);
   k_gather_vt<<<grid_for(rank * q, 256, G), 256, 0, s>>>(q, rank, Vfin, q, ord2, Vt, q);
+  canonical_signs_vt(h, rank, q, Vt, q, sgn);
+  k_gather_cols_div<<<grid_for(p * rank, 256, G), 256, 0, s>>>(p, rank, Uraw, rank, ord2, ss2, sgn, U, rank);
   FPI_LAUNCH_CHECK();
   note_launch(h, 5);
   complete_null_left(h, p, rank, U, rank, sigma, diag);
-  canonical_signs(h, rank, p, q, U, rank, Vt, q);
   if (diag) {
     // slots 0/1: the first dense SVD of a stage, slots 2/3: the next one (sweeps of pass 1 / pass 2)
     const int slot = diag->eig_sweeps[0] ? 2 : 0;
@@ -413,12 +418,13 @@ void dense_svd_batched(fpi_context* h, int nb, const int64_t* p, const int64_t* 
     k_iota32<<<grid_for(r, 256, G), 256, 0, s>>>(ord, r);
     sort_pairs(tmp, ss.get(), ss2.get(), ord.get(), ord2.get(), r, true, 0, 64, s);
     FPI_CUDA(cudaMemcpyAsync(sigma[i], ss2.get(), sizeof(double) * r, cudaMemcpyDeviceToDevice, s));
-    k_gather_cols_div<<<grid_for(p[i] * r, 256, G), 256, 0, s>>>(p[i], r, Uraw, r, ord2, ss2, U[i], r);
+    Scratch<double> sgn(r, s);
     k_gather_vt<<<grid_for(r * q[i], 256, G), 256, 0, s>>>(q[i], r, Wp[i], q[i], ord2, Vt[i], q[i]);
+    canonical_signs_vt(h, r, q[i], Vt[i], q[i], sgn);
+    k_gather_cols_div<<<grid_for(p[i] * r, 256, G), 256, 0, s>>>(p[i], r, Uraw, r, ord2, ss2, sgn, U[i], r);
     FPI_LAUNCH_CHECK();
     note_launch(h, 5);
     complete_null_left(h, p[i], r, U[i], r, sigma[i], nullptr);
-    canonical_signs(h, r, p[i], q[i], U[i], r, Vt[i], q[i]);
   }
 }
 
@@ -671,6 +677,12 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   // U = Q U~ = B L^-T U~ ,  U~ = Uyt^T   (svd.py:137)
   Scratch<double> Mx(k * rank, s);
   gemm(h, true, true, k, rank, k, 1.0, Linv, k, Uyt, k, 0.0, Mx, rank);
+  // canonical signs from Vt; U's columns follow through Mx's (no pass over the p x r U)
+  {
+    Scratch<double> sgn(rank, s);
+    canonical_signs_vt(h, rank, q, Vt, q, sgn);
+    scale_cols(h, k, rank, Mx, rank, sgn, false);
+  }
   if (op.apply_cost(rank) + 2.0 * (double)q * (double)k * (double)rank < 2.0 * (double)p * (double)k * (double)rank) {
     // = inner (X L^-T U~): the thin q x r factor first, then one pass of the inner operator -- about
     // half the flops of the p x 2r x r product with B when inner is [U Sigma | T] with a tall U
@@ -683,8 +695,6 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
     gemm(h, false, false, p, rank, k, 1.0, B, k, Mx, rank, 0.0, U, rank);
   }
   trace_point(h, "rsvd:U");
-  canonical_signs(h, rank, p, q, U, rank, Vt, q);
-  trace_point(h, "rsvd:canonical signs");
   if (diag) diag->engine = 1;
 }
 
