@@ -48,6 +48,33 @@ __global__ void k_ptr_from_sorted(int64_t cnt, const uint64_t* __restrict__ keys
   }
 }
 
+__global__ void k_iota_pos(int64_t n, int32_t* __restrict__ pos) {
+  FPI_GRID_STRIDE(i, n) pos[i] = (int32_t)i;
+}
+
+__global__ void k_gather_transposed(int64_t nnz, const int32_t* __restrict__ pos, const int32_t* __restrict__ rows,
+                                    const double* __restrict__ vals, int32_t* __restrict__ t_idx,
+                                    double* __restrict__ t_val) {
+  FPI_GRID_STRIDE(i, nnz) {
+    const int32_t p = pos[i];
+    t_idx[i] = rows[p];
+    if (t_val) t_val[i] = vals ? vals[p] : 0.0;
+  }
+}
+
+// t_ptr[c] = first position whose (sorted) column is >= c
+__global__ void k_ptr_from_sorted32(int64_t cnt, const uint32_t* __restrict__ keys, int64_t ncols,
+                                    int64_t* __restrict__ ptr) {
+  FPI_GRID_STRIDE(c, ncols + 1) {
+    int64_t lo = 0, hi = cnt;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((int64_t)keys[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    ptr[c] = lo;
+  }
+}
+
 __global__ void k_scatter_sorted(int64_t cnt, const uint64_t* __restrict__ keys, const int32_t* __restrict__ pos,
                                  const double* __restrict__ vals, uint64_t minor_mask, int32_t* __restrict__ out_idx,
                                  double* __restrict__ out_val) {
@@ -267,13 +294,29 @@ void build_csr(fpi_context* h, CubTemp& tmp, int64_t cnt, const int32_t* major, 
   }
 }
 
+// Transpose of a CSR: the entries are already in row-major order, so one STABLE radix sort on the
+// column index alone (bits_for(q) bits instead of column + row bits) leaves every column's rows
+// ascending.
 void csr_transpose(fpi_context* h, int64_t p, int64_t q, int64_t nnz, const int64_t* indptr, const int32_t* indices,
                    const double* values, int64_t* t_ptr, int32_t* t_idx, double* t_val) {
   cudaStream_t s = h->stream;
+  const int T = 256;
+  const int64_t G = (int64_t)h->num_sms * 16;
+  if (nnz == 0) {
+    FPI_CUDA(cudaMemsetAsync(t_ptr, 0, sizeof(int64_t) * (q + 1), s));
+    return;
+  }
   CubTemp tmp(s);
-  Scratch<int32_t> rows(nnz, s);
+  Scratch<int32_t> rows(nnz, s), pos(nnz, s), pos2(nnz, s);
+  Scratch<uint32_t> keys2(nnz, s);
   expand_rows(h, p, indptr, rows);
-  build_csr(h, tmp, nnz, indices, rows, values, q, p, t_ptr, t_idx, t_val);
+  k_iota_pos<<<grid_for(nnz, T, G), T, 0, s>>>(nnz, pos);
+  sort_pairs(tmp, reinterpret_cast<const uint32_t*>(indices), keys2.get(), pos.get(), pos2.get(), nnz, false, 0,
+             bits_for((uint64_t)(q > 0 ? q : 1)), s);
+  k_gather_transposed<<<grid_for(nnz, T, G), T, 0, s>>>(nnz, pos2, rows, values, t_idx, t_val);
+  k_ptr_from_sorted32<<<grid_for(q + 1, T, G), T, 0, s>>>(nnz, keys2, q, t_ptr);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 5);
 }
 
 void csr_canonicalize(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const int64_t* indptr,
@@ -382,9 +425,20 @@ void partition(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const int64_t*
   note_launch(h);
   if (out->a11_ptr) build_csr(h, tmp, n11, a11_r, a11_c, a11_v, m1, n1, out->a11_ptr, out->a11_idx, out->a11_val);
   if (out->t_ptr) build_csr(h, tmp, nT, t_r, t_c, t_v, m, n2, out->t_ptr, out->t_idx, out->t_val);
-  if (out->tt_ptr) build_csr(h, tmp, nT, t_c, t_r, t_v, n2, m, out->tt_ptr, out->tt_idx, out->tt_val);
+  if (out->tt_ptr) {
+    if (out->t_ptr)  // from the sorted T: one column-key sort
+      csr_transpose(h, m, n2, nT, out->t_ptr, out->t_idx, out->t_val, out->tt_ptr, out->tt_idx, out->tt_val);
+    else
+      build_csr(h, tmp, nT, t_c, t_r, t_v, n2, m, out->tt_ptr, out->tt_idx, out->tt_val);
+  }
   if (out->a21_ptr) build_csr(h, tmp, n21, a21_r, a21_c, a21_v, m2, n1, out->a21_ptr, out->a21_idx, out->a21_val);
-  if (out->a21t_ptr) build_csr(h, tmp, n21, a21_c, a21_r, a21_v, n1, m2, out->a21t_ptr, out->a21t_idx, out->a21t_val);
+  if (out->a21t_ptr) {
+    if (out->a21_ptr)
+      csr_transpose(h, m2, n1, n21, out->a21_ptr, out->a21_idx, out->a21_val, out->a21t_ptr, out->a21t_idx,
+                    out->a21t_val);
+    else
+      build_csr(h, tmp, n21, a21_c, a21_r, a21_v, n1, m2, out->a21t_ptr, out->a21t_idx, out->a21t_val);
+  }
 }
 
 void permute(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const int64_t* indptr, const int32_t* indices,
