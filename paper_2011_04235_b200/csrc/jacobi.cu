@@ -97,13 +97,16 @@ __device__ void build_tables(StepTables& tb) {
   }
 }
 
+#ifndef JACOBI_CS32
+#define JACOBI_CS32 1
+#endif
 #ifndef JACOBI_ROT32
 #define JACOBI_ROT32 1
 #endif
 
 // MUFU approximations for the rotation (measured on B200: rsqrt.approx.f64 ~2^-52.4 -- ptxas
 // refines MUFU.RSQ64H -- and rcp.approx.ftz.f64 ~2^-20).
-__device__ __forceinline__ double rcp_apx(double x) { double r; asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
+__device__ __forceinline__ __attribute__((unused)) double rcp_apx(double x) { double r; asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
 __device__ __forceinline__ double rsqrt_apx(double x) { double r; asm("rsqrt.approx.f64 %0, %1;" : "=d"(r) : "d"(x)); return r; }
 
 // Rotation of one pair from (app, aqq, apq), without the z = (aqq - app) / (2 apq) division:
@@ -118,12 +121,17 @@ __device__ __forceinline__ void rotation(double app, double aqq, double apq, dou
   const bool rot = apq != 0.0 && apq * apq > tol * tol * den2;
   double d = aqq - app, f2 = 2.0 * apq;
   const double mx = fmax(fabs(d), fabs(f2));
+#if !JACOBI_ROT32
   if (mx > 1e150 || mx < 1e-150) {
     const double sc = mx > 0.0 ? rcp_apx(mx) : 1.0;
     d *= sc;
     f2 *= sc;
   }
-#if JACOBI_ROT32
+  const double v = fma(d, d, f2 * f2);
+  const double hyp = v * rsqrt_apx(v);
+  const double t0 = f2 * rcp_apx(fabs(d) + hyp);
+  const double tt = d < 0.0 ? -t0 : t0;
+#else
   // The angle in FP32 (MUFU.RSQ / MUFU.RCP, ~2^-22 relative -- better than the 2^-20 the FP64
   // path's raw reciprocal gives), after scaling d and f2 by 2^-e (e = exponent of their larger
   // magnitude) into FP32's range; orthogonality comes from c and s below, computed in FP64.
@@ -137,12 +145,21 @@ __device__ __forceinline__ void rotation(double app, double aqq, double apq, dou
   const float hypf = vf * rs;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fabsf(df) + hypf));
   const float tf = ff * rc;
-  const double tt = (double)(df < 0.0f ? -tf : tf);
-#else
-  const double v = fma(d, d, f2 * f2);
-  const double hyp = v * rsqrt_apx(v);
-  const double t0 = f2 * rcp_apx(fabs(d) + hyp);
-  const double tt = d < 0.0 ? -t0 : t0;
+  const float tsf = df < 0.0f ? -tf : tf;
+#if JACOBI_CS32
+  // c, s from FP32 (c0 = 1 / sqrt(1 + t^2), s0 = c0 t, ~2^-22) made orthogonal in FP64 by the
+  // series 1 / sqrt(1 + e) = 1 - e / 2 + 3 e^2 / 8 (e = c0^2 + s0^2 - 1 ~ 1e-7: the next term is
+  // below FP64 rounding); four dependent FMAs instead of the refined MUFU.RSQ64H
+  float c0f;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(c0f) : "f"(fmaf(tsf, tsf, 1.0f)));
+  const double c0 = (double)c0f, s0 = (double)(c0f * tsf);
+  const double e = fma(c0, c0, fma(s0, s0, -1.0));
+  const double rn = fma(e, fma(e, 0.375, -0.5), 1.0);
+  c = rot ? c0 * rn : 1.0;
+  sn = rot ? s0 * rn : 0.0;
+  return;
+#endif
+  const double tt = (double)tsf;
 #endif
   const double cy = rsqrt_apx(fma(tt, tt, 1.0));
   c = rot ? cy : 1.0;
