@@ -140,25 +140,30 @@ __device__ __forceinline__ void rotation(double app, double aqq, double apq, dou
   const double sc2 = __longlong_as_double((long long)ef << 52);
   const float df = (float)(d * sc2), ff = (float)(f2 * sc2);
   const float vf = fmaf(df, df, ff * ff);
-  float rs, rc;
+  float rs;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(vf));
-  const float hypf = vf * rs;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fabsf(df) + hypf));
-  const float tf = ff * rc;
-  const float tsf = df < 0.0f ? -tf : tf;
 #if JACOBI_CS32
-  // c, s from FP32 (c0 = 1 / sqrt(1 + t^2), s0 = c0 t, ~2^-22) made orthogonal in FP64 by the
-  // series 1 / sqrt(1 + e) = 1 - e / 2 + 3 e^2 / 8 (e = c0^2 + s0^2 - 1 ~ 1e-7: the next term is
-  // below FP64 rounding); four dependent FMAs instead of the refined MUFU.RSQ64H
-  float c0f;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(c0f) : "f"(fmaf(tsf, tsf, 1.0f)));
-  const double c0 = (double)c0f, s0 = (double)(c0f * tsf);
+  // c, s straight from h = sqrt(d^2 + f^2) and w = |d| + h: 1 + t^2 = 2 h / w, so
+  // c = w / sqrt(2 h w) and s = sign(d) f / sqrt(2 h w) -- two MUFU.RSQ, no reciprocal (~2^-22);
+  // then made orthogonal in FP64 by the series 1 / sqrt(1 + e) = 1 - e / 2 + 3 e^2 / 8
+  // (e = c0^2 + s0^2 - 1 ~ 1e-7: the next term is below FP64 rounding) -- four dependent FMAs
+  // instead of a refined MUFU.RSQ64H
+  float uf;
+  const float hf = vf * rs, wf = fmaf(vf, rs, fabsf(df));
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(uf) : "f"(2.0f * hf * wf));
+  const float c0f = wf * uf, s0f = (df < 0.0f ? -ff : ff) * uf;
+  const double c0 = (double)c0f, s0 = (double)s0f;
   const double e = fma(c0, c0, fma(s0, s0, -1.0));
   const double rn = fma(e, fma(e, 0.375, -0.5), 1.0);
   c = rot ? c0 * rn : 1.0;
   sn = rot ? s0 * rn : 0.0;
   return;
 #endif
+  float rc;
+  const float hypf = vf * rs;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc) : "f"(fabsf(df) + hypf));
+  const float tf = ff * rc;
+  const float tsf = df < 0.0f ? -tf : tf;
   const double tt = (double)tsf;
 #endif
   const double cy = rsqrt_apx(fma(tt, tt, 1.0));
