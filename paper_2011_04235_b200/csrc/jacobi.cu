@@ -256,29 +256,34 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
   // cross steps: pair k = (k, 16 + (k + t) % 16).  Identity rotations (c = 1, s = 0) are applied
   // as arithmetic (exact), so every load of a step is issued up front without branches.
   const int k = tid & 15, l = (k + 1 + (tid >> 4)) & 15;
-  const int u = tid - 32;  // R updater index (warps 1..7): items u, u + 224, u + 448 of 16 x 32
+  // R (stored transposed, Rt[col][row]) lives in registers during the cross steps: thread
+  // (g, k) of warps 1..7 (g = (tid - 32) / 16) holds rows g, g + 14, g + 28 of column k and of the
+  // column currently paired with k.  Step t pairs k with 16 + (k + t) % 16, and step t + 1 pairs k
+  // with the column lane k + 1 held at step t, so the updated q values move one lane down (a
+  // shuffle inside each 16-lane group) instead of round-tripping through shared memory.
+  const int u = tid - 32, g = u >> 4, lane = tid & 31;
+  const int src = (lane & 16) | ((lane + 1) & 15);
+  double rp_[3] = {0.0, 0.0, 0.0}, rq_[3] = {0.0, 0.0, 0.0};
+  if (u >= 0) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int row = g + 14 * r;
+      if (row < JS) {
+        rp_[r] = R[k * LDS_ + row];
+        rq_[r] = R[(16 + k) * LDS_ + row];
+      }
+    }
+  }
   for (int st = 15; st < st_end; ++st) {
     const int t = st - 15, b = st & 1, nbuf = b ^ 1;
     const int pk = k, qk = 16 + ((k + t) & 15), pl = l, ql = 16 + ((l + t) & 15);
     const double ck = pb.c[b][k], sk = pb.s[b][k], cl = pb.c[b][l], sl = pb.s[b][l];
     const double a = S[pk * LDS_ + pl], bb = S[pk * LDS_ + ql], c2 = S[qk * LDS_ + pl], d = S[qk * LDS_ + ql];
     // the producer's inputs for the new diagonals, loaded before any store of the step
-    const double appk = pb.app[b][k], aqqk = pb.aqq[b][k], apqk = pb.apq[b][k];
-    const double appl = pb.app[b][l], aqql = pb.aqq[b][l], apql = pb.apq[b][l];
-    double rc_[3], rs_[3], rp_[3], rq_[3];
-    int rpi[3], rqi[3];
-    if (u >= 0) {
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int idx = u + r * (JT - 32);
-        const int kk = (idx >> 5) & 15, row = idx & 31;
-        rpi[r] = kk * LDS_ + row;
-        rqi[r] = (16 + ((kk + t) & 15)) * LDS_ + row;
-        rc_[r] = pb.c[b][kk];
-        rs_[r] = pb.s[b][kk];
-        rp_[r] = R[rpi[r]];
-        rq_[r] = R[rqi[r]];
-      }
+    double appk = 0.0, aqqk = 0.0, apqk = 0.0, appl = 0.0, aqql = 0.0, apql = 0.0;
+    if (tid < 16) {
+      appk = pb.app[b][k]; aqqk = pb.aqq[b][k]; apqk = pb.apq[b][k];
+      appl = pb.app[b][l]; aqql = pb.aqq[b][l]; apql = pb.apq[b][l];
     }
     const double ra = ck * a - sk * c2, rb = ck * bb - sk * d;
     const double rc = sk * a + ck * c2, rd = sk * bb + ck * d;
@@ -299,14 +304,27 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
     } else if (u >= 0) {
 #pragma unroll
       for (int r = 0; r < 3; ++r) {
-        if (u + r * (JT - 32) < 16 * JS) {
-          R[rpi[r]] = rc_[r] * rp_[r] - rs_[r] * rq_[r];
-          R[rqi[r]] = rs_[r] * rp_[r] + rc_[r] * rq_[r];
+        if (g + 14 * r < JS) {  // warp-uniform
+          const double p0 = rp_[r], q0 = rq_[r];
+          rp_[r] = ck * p0 - sk * q0;
+          rq_[r] = __shfl_sync(0xffffffffu, sk * p0 + ck * q0, src);
         }
       }
     }
     __syncthreads();
   }
+  // after the 16th shift thread k holds column 16 + k again
+  if (u >= 0) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int row = g + 14 * r;
+      if (row < JS) {
+        R[k * LDS_ + row] = rp_[r];
+        R[(16 + k) * LDS_ + row] = rq_[r];
+      }
+    }
+  }
+  __syncthreads();
   return om;
 }
 
