@@ -922,11 +922,11 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   if (grid < 1) grid = 1;
   // run lengths of the G (phase B) and V updates of round r - 1: a few 32 x 32 tiles per queue item,
   // enough items to balance across the grid (a G tile costs two 32^3 products, a V tile one)
-  // (measured, tools/eig_compare.py / bench_eig.py: n <= ~1000 balances best with short V runs,
-  //  n = 1628 / 2000 with longer ones)
+  // (measured, tools/eig_compare.py / bench_eig.py / jacobi_tune.py: n <= ~1000 balances best with
+  //  short V runs, n = 1628 / 2000 with longer ones; n <= ~900 with 3-tile G runs)
   int64_t np_max = 0;
   for (int i = 0; i < nprob; ++i) np_max = hp[i].nb / 2 > np_max ? hp[i].nb / 2 : np_max;
-  int gchunk = 4, vchunk = np_max <= 40 ? 3 : 8;
+  int gchunk = np_max <= 28 ? 3 : 4, vchunk = np_max <= 40 ? 3 : 8;
   if (const char* e = getenv("FPI_JACOBI_CHUNKS")) sscanf(e, "%d,%d", &gchunk, &vchunk);
   // pair CTAs join the queue when the extra work per idle CTA exceeds ~20 tile products (~ one sub-solve)
   const int64_t xcta = grid - tot_pairs > 1 ? grid - tot_pairs : 1;
