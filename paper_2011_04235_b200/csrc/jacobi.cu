@@ -620,6 +620,8 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
   const double ascale = absolute ? *pr_.abs_scale : 0.0;
   double* Sa = sm;
   double* Ra = sm + TILE;
+  const bool tprof = prof && blockIdx.x == 0 && threadIdx.x == 0;
+  const unsigned long long tb0 = tprof ? gtimer() : 0;
   if (pr_.pend[q]) {
     build_subproblem(pr_, q, pr, round, sm, threadIdx.x >> 5, threadIdx.x & 31);
   } else {
@@ -633,9 +635,11 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
     Ra[a * LDS_ + b] = a == b ? 1.0 : 0.0;
   }
   __syncthreads();
-  const unsigned long long ts0 = prof ? gtimer() : 0;
+  const unsigned long long ts0 = tprof ? gtimer() : 0;
+  if (tprof) prof[5] += ts0 - tb0;
   double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
-  if (prof && blockIdx.x == 0 && threadIdx.x == 0) prof[4] += gtimer() - ts0;
+  const unsigned long long ts1 = tprof ? gtimer() : 0;
+  if (tprof) prof[4] += ts1 - ts0;
   double* Jp = pr_.Jbuf + ((int64_t)par * np + pr) * JS * JS;
   double* Sp = pr_.Sbuf + ((int64_t)par * np + pr) * JS * JS;
   int rot = 0;
@@ -652,6 +656,7 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
     if (threadIdx.x == 0 && om > 0.0) atomicMax(pr_.offmax + sweep, (unsigned long long)__double_as_longlong(om));
   }
   __syncthreads();
+  if (tprof) prof[6] += gtimer() - ts1;
 }
 
 // One round's parallel section: phase A of every active problem's pairs, and -- on the CTAs phase A
@@ -969,8 +974,8 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   FPI_LAUNCH_CHECK();
   Scratch<unsigned long long> work(2, s);
   FPI_CUDA(cudaMemsetAsync(work.get(), 0, sizeof(unsigned long long) * 2, s));
-  Scratch<unsigned long long> prof(5, s);
-  FPI_CUDA(cudaMemsetAsync(prof.get(), 0, sizeof(unsigned long long) * 5, s));
+  Scratch<unsigned long long> prof(8, s);
+  FPI_CUDA(cudaMemsetAsync(prof.get(), 0, sizeof(unsigned long long) * 8, s));
   unsigned long long* prof_p = getenv("FPI_JACOBI_PROFILE") ? prof.get() : nullptr;
   EigProb* Pp = dP.get();
   int gch = gchunk, vch = vchunk;
@@ -992,11 +997,13 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   if (sweeps_out)
     for (int i = 0; i < nprob; ++i) sweeps_out[i] = hp[i].sweeps;
   if (prof_p) {
-    unsigned long long hq[5];
+    unsigned long long hq[8];
     FPI_CUDA(cudaMemcpyAsync(hq, prof_p, sizeof(hq), cudaMemcpyDeviceToHost, s));
     FPI_CUDA(cudaStreamSynchronize(s));
-    fprintf(stderr, "[jacobi nprob=%d n0=%lld grid=%d gchunk=%d vchunk=%d] section %.3f (subsolve %.3f)  sync %.3f ms\n",
-            nprob, (long long)n[0], grid, gchunk, vchunk, hq[0] * 1e-6, hq[4] * 1e-6, hq[1] * 1e-6);
+    fprintf(stderr, "[jacobi nprob=%d n0=%lld grid=%d gchunk=%d vchunk=%d] section %.3f (build %.3f subsolve %.3f "
+            "epilogue %.3f)  sync %.3f ms\n",
+            nprob, (long long)n[0], grid, gchunk, vchunk, hq[0] * 1e-6, hq[5] * 1e-6, hq[4] * 1e-6, hq[6] * 1e-6,
+            hq[1] * 1e-6);
     std::vector<unsigned long long> om((size_t)max_sweeps + 1);
     FPI_CUDA(cudaMemcpy(om.data(), offm.get(), sizeof(unsigned long long) * om.size(), cudaMemcpyDeviceToHost));
     fprintf(stderr, "[jacobi] problem 0 off-diagonal measure per sweep (tol %.1e):", tol);
