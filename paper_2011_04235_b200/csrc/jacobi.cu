@@ -187,8 +187,10 @@ __device__ __forceinline__ double new_diag(bool isp, double c, double sn, double
 // round, the hot loop): thread tid = 16 d + k owns block (k, k + 1 + d); the producers of the
 // next rotations are exactly d = 0, i.e. lanes 0..15 of warp 0, so the rotation chain (the
 // critical path) runs on one warp while warps 1..7 apply the previous rotations to R.
+// With Jout, the final rotation is written there as row-major J (straight from the registers of the
+// cross steps) and *rot says whether this thread saw a non-identity entry; R is then left stale.
 __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& pb, bool round0, double tol,
-                           double ascale, bool absolute) {
+                           double ascale, bool absolute, double* Jout = nullptr, int* rot = nullptr) {
   const int st0 = round0 ? 0 : 15, st_end = 31;
   const int tid = threadIdx.x;
   // convergence measure of this sub-problem before rotating
@@ -314,6 +316,22 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
     __syncthreads();
   }
   // after the 16th shift thread k holds column 16 + k again
+  if (Jout) {
+    int nz = 0;
+    if (u >= 0) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int row = g + 14 * r;
+        if (row < JS) {
+          Jout[row * JS + k] = rp_[r];
+          Jout[row * JS + 16 + k] = rq_[r];
+          nz |= (rp_[r] != (row == k ? 1.0 : 0.0)) | (rq_[r] != (row == 16 + k ? 1.0 : 0.0));
+        }
+      }
+    }
+    *rot = nz;
+    return om;
+  }
   if (u >= 0) {
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
@@ -637,18 +655,14 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
   __syncthreads();
   const unsigned long long ts0 = tprof ? gtimer() : 0;
   if (tprof) prof[5] += ts0 - tb0;
-  double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute);
-  const unsigned long long ts1 = tprof ? gtimer() : 0;
-  if (tprof) prof[4] += ts1 - ts0;
   double* Jp = pr_.Jbuf + ((int64_t)par * np + pr) * JS * JS;
   double* Sp = pr_.Sbuf + ((int64_t)par * np + pr) * JS * JS;
   int rot = 0;
-  for (int e = threadIdx.x; e < JS * JS; e += JT) {
-    const double v = Ra[(e & 31) * LDS_ + (e >> 5)];  // Rt -> row-major J
-    Jp[e] = v;
+  double om = subsolve(Sa, Ra, tb, pbuf, round == 0, tol, ascale, absolute, Jp, &rot);
+  const unsigned long long ts1 = tprof ? gtimer() : 0;
+  if (tprof) prof[4] += ts1 - ts0;
+  for (int e = threadIdx.x; e < JS * JS; e += JT)
     Sp[e] = Sa[(e >> 5) * LDS_ + (e & 31)];  // the rotated sub-problem: next round's diagonal blocks
-    rot |= (v != (((e >> 5) == (e & 31)) ? 1.0 : 0.0));
-  }
   rot = __syncthreads_or(rot);
   if (threadIdx.x == 0) pr_.jflag[par * np + pr] = rot;
   if (threadIdx.x < 32) {
