@@ -351,6 +351,7 @@ constexpr int TILE = JS * LDS_;
 constexpr int NST = 4;              // cp.async pipeline depth of the phase B / V runs
 constexpr int NTILE = 2 + 2 * NST;  // G run: Jb, U, NST x {G tile, Ja}; V run: Jb, NST x V tile
 constexpr size_t JACOBI_SMEM = (size_t)NTILE * TILE * sizeof(double);
+constexpr int JMAXP = 8;  // batches up to this size keep their descriptors in shared memory
 #ifndef JACOBI_CTAS_PER_SM
 #define JACOBI_CTAS_PER_SM 2
 #endif
@@ -457,6 +458,7 @@ struct EigProb {
   int* jflag;          // 2 x np: rotation of the pair is not the identity
   unsigned long long* offmax;  // per sweep
   const double* abs_scale;     // null: relative criterion
+  double ascale;               // *abs_scale, fetched once at kernel start
   int64_t pair_off, gitem_off, vitem_off;  // prefix sums over the batch (phase A pairs, G runs, V runs)
 };
 
@@ -635,7 +637,7 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
                           PairBuf& pbuf, const StepTables& tb, unsigned long long* prof) {
   const int nb = pr_.nb, np = nb / 2;
   const bool absolute = pr_.abs_scale != nullptr;
-  const double ascale = absolute ? *pr_.abs_scale : 0.0;
+  const double ascale = absolute ? pr_.ascale : 0.0;
   double* Sa = sm;
   double* Ra = sm + TILE;
   const bool tprof = prof && blockIdx.x == 0 && threadIdx.x == 0;
@@ -741,20 +743,28 @@ __device__ void section(EigProb* P, int nprob, int64_t total_pairs, int64_t tota
   }
 }
 
-// Block 0, after its own section work: the next round's bookkeeping slot (q ^ 1) and work counter.
-__device__ void advance_slots(EigProb* P, int nprob, int q, int round, int par, unsigned long long* work) {
+// The next round's bookkeeping slot (q ^ 1) of one problem.
+__device__ __forceinline__ void advance_one(EigProb& pr_, int q, int round, int par) {
+  const int cur = pr_.pend[q] ? pr_.gcur[q] ^ 1 : pr_.gcur[q];
+  const bool active = !pr_.done && round < pr_.nb - 1;
+  pr_.gcur[q ^ 1] = cur;
+  pr_.pend[q ^ 1] = active ? 1 : 0;
+  pr_.pround[q ^ 1] = round;
+  pr_.ppar[q ^ 1] = par;
+  pr_.gfinal = cur;
+}
+
+// After a CTA's section work: the next round's slot in its shared copy of the descriptors (every
+// CTA replays the same deterministic update, so no CTA reads bookkeeping from global memory on the
+// per-round critical path) and, on block 0, in the global copy (the host reads gfinal) plus the
+// work counter.
+__device__ void advance_slots(EigProb* P, EigProb* PL, int nprob, int q, int round, int par,
+                              unsigned long long* work) {
+  if (PL != P)
+    for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) advance_one(PL[pi], q, round, par);
   if (blockIdx.x != 0) return;
   if (threadIdx.x == 0) work[q ^ 1] = 0ull;
-  for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) {
-    EigProb& pr_ = P[pi];
-    const int cur = pr_.pend[q] ? pr_.gcur[q] ^ 1 : pr_.gcur[q];
-    const bool active = !pr_.done && round < pr_.nb - 1;
-    pr_.gcur[q ^ 1] = cur;
-    pr_.pend[q ^ 1] = active ? 1 : 0;
-    pr_.pround[q ^ 1] = round;
-    pr_.ppar[q ^ 1] = par;
-    pr_.gfinal = cur;
-  }
+  for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) advance_one(P[pi], q, round, par);
 }
 
 __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
@@ -813,15 +823,25 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
   }
   __syncthreads();
   const bool buddy = s_buddy != 0;
+  // descriptors: a shared copy when the batch is small (JMAXP), else the global array
+  __shared__ EigProb sP[JMAXP];
+  if (blockIdx.x == 0)
+    for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x)
+      P[pi].ascale = P[pi].abs_scale ? *P[pi].abs_scale : 0.0;
+  grid.sync();
+  EigProb* PL = nprob <= JMAXP ? sP : P;
+  if (PL != P)
+    for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) sP[pi] = P[pi];
+  __syncthreads();
   int gr = 0;  // global round counter (R buffer and bookkeeping parity)
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int round = 0; round < max_rounds; ++round, ++gr) {
       const int q = gr & 1;
       const unsigned long long t0 = prof ? gtimer() : 0;
-      section(P, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, round, q, sweep, true, tol, sm, pbuf,
-              tb, prof, work + q, join != 0, buddy, s_lead);
+      section(PL, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, round, q, sweep, true, tol, sm,
+              pbuf, tb, prof, work + q, join != 0, buddy, s_lead);
       const unsigned long long t1 = prof ? gtimer() : 0;
-      advance_slots(P, nprob, q, round, q, work);
+      advance_slots(P, PL, nprob, q, round, q, work);
       grid.sync();
       if (prof && blockIdx.x == 0 && threadIdx.x == 0) {
         prof[0] += t1 - t0;
@@ -846,15 +866,22 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
       }
     }
     grid.sync();
+    if (PL != P) {
+      for (int pi = threadIdx.x; pi < nprob; pi += blockDim.x) {
+        sP[pi].done = P[pi].done;
+        sP[pi].sweeps = P[pi].sweeps;
+      }
+      __syncthreads();
+    }
     bool all = true;
-    for (int pi = 0; pi < nprob; ++pi) all &= (P[pi].done != 0);
+    for (int pi = 0; pi < nprob; ++pi) all &= (PL[pi].done != 0);
     if (all) break;
   }
   // the last round's G and V updates
   const int q = gr & 1;
-  section(P, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, 0, q, 0, false, tol, sm, pbuf, tb,
+  section(PL, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, 0, q, 0, false, tol, sm, pbuf, tb,
           nullptr, work + q, true, false, s_lead);
-  advance_slots(P, nprob, q, 0, q, work);
+  advance_slots(P, PL, nprob, q, 0, q, work);
 }
 
 __global__ void k_max_diag(int64_t n, const double* A, int64_t lda, double* out) {
