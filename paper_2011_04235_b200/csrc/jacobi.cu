@@ -680,7 +680,7 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
 __device__ void section(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems,
                         int gchunk, int vchunk, int q, int round, int par, int sweep, bool pairs_on, double tol,
                         double* sm, PairBuf& pbuf, const StepTables& tb, unsigned long long* prof,
-                        unsigned long long* work, bool join, bool buddy, int lead) {
+                        unsigned long long* work, bool join, bool buddy, int lead, int qrank, int nq) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nA = pairs_on ? total_pairs : 0;
   const int64_t nX = total_gitems + total_vitems;
@@ -732,9 +732,12 @@ __device__ void section(EigProb* P, int nprob, int64_t total_pairs, int64_t tota
   // latency-bound rotation chain then has the SM to itself (measured: 7.7 -> 6.5 ms of sub-solve
   // per n = 1000 eigensolve)
   if (buddy && nA > 0) return;
+  // rounds with pairs: items [0, nq) go to the queue CTAs by rank, the rest through the counter
+  const int64_t x0 = nA > 0 ? nq : 0;
+  if (nA > 0 && qrank >= 0 && qrank < nX) extra(qrank);
   __shared__ int64_t grab;
   while (true) {
-    if (threadIdx.x == 0) grab = (int64_t)atomicAdd(work, 1ull);
+    if (threadIdx.x == 0) grab = x0 + (int64_t)atomicAdd(work, 1ull);
     __syncthreads();
     const int64_t x = grab;
     __syncthreads();
@@ -786,7 +789,7 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
     smids[blockIdx.x] = (int)sid;
   }
   grid.sync();
-  __shared__ int s_lead;
+  __shared__ int s_lead, s_qrank, s_nq, s_spread;
   {
     // the dynamic shared buffer is free until the first section: SM ids, first-on-SM flags and
     // leader ranks of every CTA, computed by the whole block
@@ -819,6 +822,35 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
       }
       s_buddy = bud;
       s_lead = spread ? (sfirst[me] ? srank[me] : -1) : -2;  // -2: pairs by blockIdx (many pairs)
+      s_spread = spread ? 1 : 0;
+    }
+    __syncthreads();
+    // rank among the CTAs that go straight to the G / V queue in a round with pairs (no pair of
+    // their own, not a buddy): their first item is theirs by rank, without an atomic
+    int* spart = srank + G;
+    const int64_t npair_ctas = total_pairs < (int64_t)G ? total_pairs : (int64_t)G;
+    for (int c = threadIdx.x; c < G; c += blockDim.x) {
+      bool part;
+      if (!s_spread) {
+        part = (int64_t)c >= total_pairs;
+      } else if (sfirst[c]) {
+        part = (int64_t)srank[c] >= total_pairs;
+      } else {
+        int leader = 0;
+        while (ssm[leader] != ssm[c]) ++leader;
+        part = !((int64_t)srank[leader] < npair_ctas);
+      }
+      spart[c] = part ? 1 : 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int nq = 0, qr = -1;
+      for (int c = 0; c < G; ++c) {
+        if (c == (int)blockIdx.x && spart[c]) qr = nq;
+        nq += spart[c];
+      }
+      s_qrank = qr;
+      s_nq = nq;
     }
   }
   __syncthreads();
@@ -839,7 +871,7 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
       const int q = gr & 1;
       const unsigned long long t0 = prof ? gtimer() : 0;
       section(PL, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, round, q, sweep, true, tol, sm,
-              pbuf, tb, prof, work + q, join != 0, buddy, s_lead);
+              pbuf, tb, prof, work + q, join != 0, buddy, s_lead, s_qrank, s_nq);
       const unsigned long long t1 = prof ? gtimer() : 0;
       advance_slots(P, PL, nprob, q, round, q, work);
       grid.sync();
@@ -880,7 +912,7 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
   // the last round's G and V updates
   const int q = gr & 1;
   section(PL, nprob, total_pairs, total_gitems, total_vitems, gchunk, vchunk, q, 0, q, 0, false, tol, sm, pbuf, tb,
-          nullptr, work + q, true, false, s_lead);
+          nullptr, work + q, true, false, s_lead, -1, 0);
   advance_slots(P, PL, nprob, q, 0, q, work);
 }
 
