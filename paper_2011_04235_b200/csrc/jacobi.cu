@@ -270,9 +270,9 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       const int row = g + 14 * r;
-      if (row < JS) {
-        rp_[r] = R[k * LDS_ + row];
-        rq_[r] = R[(16 + k) * LDS_ + row];
+      if (row < JS) {  // R = I unless round 0's within-block steps ran
+        rp_[r] = round0 ? R[k * LDS_ + row] : (row == k ? 1.0 : 0.0);
+        rq_[r] = round0 ? R[(16 + k) * LDS_ + row] : (row == 16 + k ? 1.0 : 0.0);
       }
     }
   }
@@ -567,7 +567,7 @@ __device__ __forceinline__ int rr_pos(int x, int rho, int nb) {
 // C (M x N) = op(A) (M x 32) B (32 x N), all in shared memory with explicit strides; M, N multiples
 // of 8.  8 x 8 output tiles are dealt round-robin to the warps (DMMA m8n8k4, K = 32).
 __device__ __forceinline__ void mm_k32(const double* A, int lda, bool ta, const double* B, int ldb, double* C, int ldc,
-                                       int M, int N, int tile0, int warp, int lane) {
+                                       int M, int N, int tile0, int warp, int lane, double* CT = nullptr) {
   const int g = lane >> 2, t = lane & 3;
   const int tn = N / 8, nt = (M / 8) * tn;
   for (int tl = (warp + 8 - tile0 % 8) % 8; tl < nt; tl += 8) {
@@ -581,6 +581,10 @@ __device__ __forceinline__ void mm_k32(const double* A, int lda, bool ta, const 
     }
     C[(m0 + g) * ldc + n0 + 2 * t] = d0;
     C[(m0 + g) * ldc + n0 + 2 * t + 1] = d1;
+    if (CT) {  // and C^T (same stride)
+      CT[(n0 + 2 * t) * ldc + m0 + g] = d0;
+      CT[(n0 + 2 * t + 1) * ldc + m0 + g] = d1;
+    }
   }
 }
 
@@ -623,12 +627,7 @@ __device__ void build_subproblem(const EigProb& pr_, int q, int pr, int rho, dou
   // W = G[P(X), P(Y)] J_Y[:, 16 h_Y : +16]   (32 x 16), S[X, Y] = J_X[:, 16 h_X : +16]^T W   (16 x 16)
   mm_k32(T, LDS_, false, Jy + 16 * hh[1], LDS_, W, 48, 32, 16, 0, warp, lane);
   __syncthreads();
-  mm_k32(Jx + 16 * hh[0], LDS_, true, W, 48, S + 16, LDS_, 16, 16, 0, warp, lane);
-  __syncthreads();
-  for (int e = threadIdx.x; e < 256; e += JT) {  // S[Y, X] = S[X, Y]^T
-    const int i = e >> 4, j = e & 15;
-    S[(16 + i) * LDS_ + j] = S[j * LDS_ + 16 + i];
-  }
+  mm_k32(Jx + 16 * hh[0], LDS_, true, W, 48, S + 16, LDS_, 16, 16, 0, warp, lane, S + 16 * LDS_);  // + S[Y, X]
   __syncthreads();
 }
 
@@ -650,10 +649,11 @@ __device__ void pair_exec(const EigProb& pr_, int q, int pr, int round, int par,
     cp_commit();
     cp_wait<0>();
   }
-  for (int e = threadIdx.x; e < JS * JS; e += JT) {
-    const int a = e >> 5, b = e & 31;
-    Ra[a * LDS_ + b] = a == b ? 1.0 : 0.0;
-  }
+  if (round == 0)  // R in shared memory only for round 0's within-block steps
+    for (int e = threadIdx.x; e < JS * JS; e += JT) {
+      const int a = e >> 5, b = e & 31;
+      Ra[a * LDS_ + b] = a == b ? 1.0 : 0.0;
+    }
   __syncthreads();
   const unsigned long long ts0 = tprof ? gtimer() : 0;
   if (tprof) prof[5] += ts0 - tb0;
