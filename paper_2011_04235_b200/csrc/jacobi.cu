@@ -193,15 +193,20 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
                            double ascale, bool absolute, double* Jout = nullptr, int* rot = nullptr) {
   const int st0 = round0 ? 0 : 15, st_end = 31;
   const int tid = threadIdx.x;
-  // convergence measure of this sub-problem before rotating
+  // convergence measure of this sub-problem before rotating -- on warps 1..7, so warp 0 starts the
+  // prologue rotations (the critical path) at once
   double om = 0.0;
-  for (int e = tid; e < JS * JS; e += JT) {
+  for (int e = tid - 32; e >= 0 && e < JS * JS; e += JT - 32) {
     const int x = e >> 5, y = e & 31;
     if (x == y) continue;
     const double sxy = S[x * LDS_ + y];
     const double den2 = absolute ? ascale * ascale : fabs(S[x * LDS_ + x]) * fabs(S[y * LDS_ + y]);
     if (sxy != 0.0) om = fmax(om, den2 > 0.0 ? fabs(sxy) * rsqrt_apx(den2) : 1.0);
   }
+  // block maximum: warp partials now, thread 0 combines them after the steps' barriers
+  __shared__ double s_om[JT / 32];
+  for (int o = 16; o; o >>= 1) om = fmax(om, __shfl_xor_sync(0xffffffffu, om, o));
+  if ((tid & 31) == 0) s_om[tid >> 5] = om;
   // prologue: rotations of the first step
   if (tid < 16) {
     const int k = tid, p = tb.P[st0][k], q = tb.Q[st0][k];
@@ -330,7 +335,9 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
       }
     }
     *rot = nz;
-    return om;
+    if (tid == 0)
+      for (int w = 1; w < JT / 32; ++w) om = fmax(om, s_om[w]);
+    return om;  // the sub-problem's measure in thread 0
   }
   if (u >= 0) {
 #pragma unroll
@@ -343,6 +350,8 @@ __device__ double subsolve(double* S, double* R, const StepTables& tb, PairBuf& 
     }
   }
   __syncthreads();
+  if (tid == 0)
+    for (int w = 1; w < JT / 32; ++w) om = fmax(om, s_om[w]);
   return om;
 }
 
