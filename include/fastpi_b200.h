@@ -46,6 +46,9 @@ typedef struct {
   int64_t n_iterations;     /* T */
   int64_t n_spans;          /* number of BlockSpan entries */
   int64_t n_gcc;            /* len(gcc_sizes) */
+  int64_t edges_visited;    /* sum over iterations of E_t: edges with both endpoints active at entry */
+  int64_t nodes_visited;    /* sum over iterations of V_t: active nodes at entry (SURVEY 8(d):
+                               algorithmic bytes = 24 * edges_visited + 32 * nodes_visited) */
 } fpi_reorder_info;
 
 typedef struct {

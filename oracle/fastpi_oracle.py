@@ -77,6 +77,8 @@ class Ordering:
     spans: np.ndarray        # (B, 4) int64: row_start, row_len, col_start, col_len
     n_iterations: int
     gcc_sizes: tuple
+    edges_visited: int = 0   # sum_t E_t (edges with both endpoints active at entry), SURVEY 8(d)
+    nodes_visited: int = 0   # sum_t V_t (active nodes at entry)
 
 
 def _hub_order(deg, active, quota):
@@ -105,12 +107,15 @@ def reorder(m: int, n: int, indptr, indices, k: float) -> Ordering:
     spans = []
     gcc_sizes = []
     it = 0
+    e_sum = v_sum = 0
     while True:
         it += 1
         q_t = math.ceil(k * int(act_t.sum()))          # reorder.py:196-199
         q_f = math.ceil(k * int(act_f.sum()))
         live = act_t[er] & act_f[ec]                    # edges inside the current graph
         er, ec = er[live], ec[live]
+        e_sum += int(er.size)
+        v_sum += int(act_t.sum()) + int(act_f.sum())
         deg_t = np.bincount(er, minlength=m)            # reorder.py:201-202
         deg_f = np.bincount(ec, minlength=n)
         hubs_t = _hub_order(deg_t, act_t, q_t)
@@ -180,7 +185,7 @@ def reorder(m: int, n: int, indptr, indices, k: float) -> Ordering:
     col_new[rem_f] = lo_f + np.arange(rem_f.size)
     spans_arr = np.concatenate(spans) if spans else np.zeros((0, 4), dtype=np.int64)
     return Ordering(row_new, col_new, lo_t, lo_f, m - lo_t, n - lo_f,
-                    spans_arr.astype(np.int64), it, tuple(gcc_sizes))
+                    spans_arr.astype(np.int64), it, tuple(gcc_sizes), e_sum, v_sum)
 
 
 # --------------------------------------------------------------------------

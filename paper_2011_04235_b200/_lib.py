@@ -28,7 +28,8 @@ P_u64 = C.POINTER(C.c_uint64)
 
 class ReorderInfo(C.Structure):
     _fields_ = [("m1", i64), ("n1", i64), ("m2", i64), ("n2", i64),
-                ("n_iterations", i64), ("n_spans", i64), ("n_gcc", i64)]
+                ("n_iterations", i64), ("n_spans", i64), ("n_gcc", i64), ("edges_visited", i64),
+                ("nodes_visited", i64)]
 
 
 class PartitionInfo(C.Structure):

@@ -455,12 +455,11 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
     FPI_CUDA(cudaStreamSynchronize(s));
   }
   {
-    static bool attr = false;
+    static std::atomic<uint64_t> attr{0};
     const size_t full = h->smem_optin - 1024;
-    if (!attr) {
+    once_per_device(attr, h->device, [&] {
       FPI_CUDA(cudaFuncSetAttribute(k_block_svd_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)full));
-      attr = true;
-    }
+    });
     const int64_t counts[2] = {hc[0], hc[1]};
     const int64_t* lists[2] = {small.get(), mid.get()};
     const size_t smem[2] = {(size_t)TINY_DOUBLES * 8, full};

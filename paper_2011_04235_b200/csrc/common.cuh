@@ -1,7 +1,9 @@
 // Shared plumbing for the FastPI B200 core: status codes, the handle, a
 // stream-ordered scratch allocator and small device helpers.
 #pragma once
+#include <atomic>
 #include <cstring>
+#include <mutex>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -34,6 +36,20 @@ struct Error : std::runtime_error {
   } while (0)
 
 #define FPI_LAUNCH_CHECK() FPI_CUDA(cudaGetLastError())
+
+// One-time initialisation per CUDA device (kernel attributes such as the dynamic shared-memory
+// opt-in are per device, and the handles are per device): runs f() the first time a call site is
+// reached with `dev` current, under a lock, then marks the device done in `mask`.
+template <class F>
+inline void once_per_device(std::atomic<uint64_t>& mask, int dev, F&& f) {
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (mask.load(std::memory_order_relaxed) & bit) return;
+  f();
+  mask.fetch_or(bit, std::memory_order_release);
+}
 
 }  // namespace fpi
 

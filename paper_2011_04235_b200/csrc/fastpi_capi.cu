@@ -143,7 +143,7 @@ extern "C" int fpi_fastpi(fpi_handle h, int64_t m, int64_t n, int64_t nnz, const
     fpi::ok(h, fpi_pinv_assemble(h, r, static_cast<double*>(res->sigma.p), m, n, pinv_cutoff,
                                  static_cast<double*>(res->sdag.p), &tol, &af));
   info.tolerance_used = tol;
-  info.all_filtered = r > 0 ? af : 1;
+  info.all_filtered = af;  // pinv.py:222-224: False for an empty sigma
   FPI_CUDA(cudaStreamSynchronize(s));  // the scratch above is released at scope exit, after its last use
   if (h_info) *h_info = info;
   FPI_API_END(h)

@@ -284,11 +284,10 @@ int choose_splits(int64_t tiles, int64_t M, int64_t N, int64_t K, int num_sms) {
 template <bool TA, bool TB, bool V16>
 void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
             const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int sym) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_set{0};
+  once_per_device(attr_set, h->device, [] {
     FPI_CUDA(cudaFuncSetAttribute(k_gemm<TA, TB, V16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-    attr_set = true;
-  }
+  });
   cudaStream_t s = h->stream;
   const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
   int64_t tiles = tm * tn;

@@ -974,7 +974,12 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
                      bool absolute, int* sweeps_out) {
   if (nprob <= 0) return;
   cudaStream_t s = h->stream;
-  const double stagnate_below = 1e-9;
+  // Stagnation stop: the off-diagonal measure stops falling (cur > prev / 4) while below the rounding
+  // floor of a rotation sweep, ~c n eps (c = 32).  Above that floor a stalled measure keeps iterating
+  // (to max_sweeps): stopping there would leave eigenvector errors of ~measure / gap.
+  int64_t n_max = 1;
+  for (int i = 0; i < nprob; ++i) n_max = n[i] > n_max ? n[i] : n_max;
+  const double stagnate_below = 32.0 * (double)n_max * 2.220446049250313e-16;
   std::vector<EigProb> hp(nprob);
   std::vector<int64_t> npad(nprob), goff(nprob);
   int64_t gsz = 0, jsz = 0, fsz = 0, tot_pairs = 0, tot_tri = 0, tot_vt = 0;
@@ -996,14 +1001,16 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
     tot_vt += np * np;
     if (nb - 1 > max_rounds) max_rounds = nb - 1;
   }
-  static int max_blocks = 0;
-  if (!max_blocks) {
+  static std::atomic<uint64_t> attr_set{0};
+  static std::atomic<int> blocks_per_sm[64];
+  once_per_device(attr_set, h->device, [&] {
     FPI_CUDA(cudaFuncSetAttribute((const void*)k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)JACOBI_SMEM));
     int per_sm = 0;
     FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_jacobi, JT, JACOBI_SMEM));
-    max_blocks = per_sm * h->num_sms;
-  }
+    blocks_per_sm[h->device & 63].store(per_sm);
+  });
+  const int max_blocks = blocks_per_sm[h->device & 63].load() * h->num_sms;
   int grid = max_blocks;
   if (const char* e = getenv("FPI_JACOBI_GRID")) grid = atoi(e) < max_blocks ? atoi(e) : max_blocks;
   if (grid < 1) grid = 1;

@@ -380,6 +380,7 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
     const int64_t q_t = (int64_t)std::ceil(k * (double)cnt_t);  // math.ceil(k * cnt), reorder.py:198-199
     const int64_t q_f = (int64_t)std::ceil(k * (double)cnt_f);
     const int64_t cnt = cnt_t + cnt_f;
+    out.v_sum += cnt;  // SURVEY 8(d) accounting (E_t added once the iteration's edge count is read)
 
     // 1. degrees over the compacted edge list
     k_reset_nodes_dev<<<grid_for(cnt, T, G), T, 0, s>>>(act, cnt, deg, parent, csize, crows, dsc, d_best);
@@ -418,6 +419,7 @@ static void run_reorder(fpi_context* h, int64_t m, int64_t n, int64_t nnz, const
     FPI_LAUNCH_CHECK();
     note_launch(h, 8);
     const int64_t h_t = hs->h_t, h_f = hs->h_f;
+    out.e_sum += any_edges ? (int64_t)hs->ne : 0;
     hi_t -= h_t;
     hi_f -= h_f;
     cnt_t -= h_t;
@@ -496,11 +498,13 @@ extern "C" int fpi_reorder(fpi_handle h, int64_t m, int64_t n, int64_t nnz, cons
                            fpi_reorder_info* info) {
   FPI_API_BEGIN(h)
   fpi::ReorderOut o{};
+  // algorithmic bytes: sum_t (3 * 8 * E_t + 4 * 8 * V_t), known once the loop ends
   fpi::KTimer kt(h, "reorder_loop(all kernels)", 0.0, 0.0);
   // the persistent device loop unless it is outside its static limits (or the host loop is forced)
   const bool hostloop = getenv("FPI_REORDER_HOSTLOOP") != nullptr;
   if (hostloop || !fpi::run_reorder_persistent(h, m, n, nnz, d_indptr, d_indices, k, d_row_fwd, d_col_fwd, o))
     fpi::run_reorder(h, m, n, nnz, d_indptr, d_indices, k, d_row_fwd, d_col_fwd, o);
+  kt.bytes = 24.0 * (double)o.e_sum + 32.0 * (double)o.v_sum;
   if (info) {
     info->m1 = o.m1;
     info->n1 = o.n1;
@@ -509,6 +513,8 @@ extern "C" int fpi_reorder(fpi_handle h, int64_t m, int64_t n, int64_t nnz, cons
     info->n_iterations = o.T;
     info->n_spans = h->n_spans;
     info->n_gcc = (int64_t)h->gcc_sizes.size();
+    info->edges_visited = o.e_sum;
+    info->nodes_visited = o.v_sum;
   }
   FPI_API_END(h)
 }

@@ -6,6 +6,9 @@ namespace fpi {
 
 struct ReorderOut {
   int64_t m1, n1, m2, n2, T;
+  // SURVEY 8(d) work accounting: sum over iterations of E_t (edges with both endpoints active at
+  // the iteration's entry) and V_t (active nodes at entry); algorithmic bytes = 24 E + 32 V
+  int64_t e_sum = 0, v_sum = 0;
 };
 
 // One persistent cooperative kernel for the whole iteration loop (reorder_persistent.cu).

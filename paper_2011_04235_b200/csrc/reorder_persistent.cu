@@ -57,7 +57,7 @@ struct Ctl {
   int maxsz;
   int ne_next[2];
   unsigned long long best;
-  long long out[8];  // lo_t, lo_f, iterations, spans, gcc entries
+  long long out[8];  // lo_t, lo_f, iterations, spans, gcc entries, sum E_t, sum V_t
 };
 
 struct Params {
@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
   int hl = 0;  // hub histogram buffer rotation
   int64_t nroots_log = 0, nnodes_log = 0, maxsz_all = 0;  // spoke log (laid out after the loop)
   int64_t dprev[2] = {0, 0};                                // previous hub thresholds (0: none)
+  int64_t e_sum = 0, v_sum = 0;                             // sum_t E_t, sum_t V_t
   unsigned long long tlast = (P.prof && gtid == 0) ? gtimer() : 0ull;
 #define RP_PROF(i)                                     \
   if (P.prof && gtid == 0) {                           \
@@ -439,6 +440,8 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
     const int64_t q_t = (int64_t)ceil(P.k * (double)cnt_t);  // math.ceil(k * cnt), reorder.py:198-199
     const int64_t q_f = (int64_t)ceil(P.k * (double)cnt_f);
     const int64_t L = cnt_t + cnt_f;  // length of the active list this iteration
+    e_sum += ne;  // edges with both endpoints active (the list is compacted to the previous GCC)
+    v_sum += L;
 
     // ---- P1: degrees; clear this iteration's accumulators
     if (gtid == 0) {
@@ -930,6 +933,8 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
     ctl->out[2] = iters;
     ctl->out[3] = nspans;
     ctl->out[4] = ngcc;
+    ctl->out[5] = e_sum;
+    ctl->out[6] = v_sum;
   }
 }
 
@@ -1069,6 +1074,8 @@ bool run_reorder_persistent(fpi_context* h, int64_t m, int64_t n, int64_t nnz, c
   out.m2 = m - lo_t;
   out.n2 = n - lo_f;
   out.T = c.out[2];
+  out.e_sum = c.out[5];
+  out.v_sum = c.out[6];
   return true;
 }
 

@@ -634,8 +634,9 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   const int64_t k = 2 * rank;
   if (diag) diag->engine = 1;
   if (p <= k) {
-    // QR of a p x 2r sketch with p <= 2r gives a p x p orthogonal Q: the result is the exact SVD of inner
-    FPI_REQUIRE(p * q <= 100000000LL, FPI_ECAPACITY, "inner matrix too large to densify");
+    // QR of a p x 2r sketch with p <= 2r gives a p x p orthogonal Q: the result is the exact SVD of inner.
+    // No capacity guard, as in the reference (svd.py:120-138): p <= 2r rows of q columns fit HBM
+    // at every size the rank rule admits.
     Scratch<double> Dn(p * q, s);
     op.densify(h, Dn);
     dense_svd(h, p, q, Dn, q, rank, U, sigma, Vt, diag);

@@ -248,8 +248,11 @@ def reorder_device(dev: DeviceCSR, k: float) -> ReorderResult:
     spans = empty(max(info.n_spans, 0) * 4, "i64")
     gcc = (C.c_int64 * max(info.n_gcc, 1))()
     _lib.call("fpi_reorder_fetch", _lib.ptr(spans), gcc)
-    return ReorderResult(Permutation(row_fwd), Permutation(col_fwd), info.m1, info.n1, info.m2, info.n2,
-                         None, info.n_iterations, [gcc[i] for i in range(info.n_gcc)], spans_device=spans)
+    res = ReorderResult(Permutation(row_fwd), Permutation(col_fwd), info.m1, info.n1, info.m2, info.n2,
+                        None, info.n_iterations, [gcc[i] for i in range(info.n_gcc)], spans_device=spans)
+    # SURVEY 8(d) work of the loop: sum_t E_t and V_t (algorithmic bytes 24 E + 32 V)
+    res.edges_visited, res.nodes_visited = int(info.edges_visited), int(info.nodes_visited)
+    return res
 
 
 def reorder(graph: BipartiteGraph, k: float) -> ReorderResult:

@@ -1,40 +1,130 @@
-"""GPU: the largest BASELINE config (c5: 2M x 200k, 30M nnz, r = 1000, 3000 labels) at full size,
-checked through size-independent properties (the CPU oracle needs hours here):
-  * the permutations are bijections, the spans tile the spoke region, T / m1 / n1 are consistent;
-  * sigma is positive and sorted, r = min(ceil(alpha n), s + n2, m) (pinv.py:336);
-  * U and V have orthonormal columns (1e-9: the small SVD of Y goes through its Gram, so the
-    right vectors of the smallest kept singular values carry ~eps cond(Y)^2; the parity bar on
-    reconstruction / Z is 1e-8);
-  * Z = pinv(A) Y agrees with V diag(sigma+) (U^T (Y x)) on random probes x (1e-10): the apply path
-    against an independent small-product route."""
+"""GPU: the largest BASELINE config (c5: 2M x 200k, 30M nnz, r = 1000, 3000 labels) at full size.
+
+Oracle parity (the CPU oracle, oracle/fastpi_oracle.py, on the box's host cores: reorder ~7 s,
+permute + partition ~5 s, block SVD ~8 s, row update ~2-3 min):
+  * P1 reorder: permutations, spans, T, GCC sizes and m1/n1/m2/n2 bit-exact (reorder.py:158-287);
+  * partition: A11, T = [A12; A22], A21 (and the transposes) bit-exact CSR (reorder.py:290-337);
+  * P2 block SVD: every kept sigma of every non-degenerate block (51k blocks, incl. the min-dim >= 48
+    blocks of the batched Gram path) against LAPACK dgesdd, per value (svd.py:141-193);
+  * P3 row update: the oracle's row_update fed the GPU's own f11 (pinv.py:131-171): every sigma
+    per value, and the low-rank product U S Vt to 1e-8 (computed on the GPU with torch as the
+    checker: the 2M-row factors do not fit a host QR).
+The column update at c5 is not run through the oracle (its CPU peak RSS, ~130 GB for the 2M x 2000
+B / Q panels, is too close to the box's host memory); it is covered by size-independent
+properties:
+  * sigma positive and sorted, r = min(ceil(alpha n), s + n2, m) (pinv.py:336);
+  * U and V have orthonormal columns (1e-9);
+  * Z = pinv(A) Y agrees with V diag(sigma+) (U^T (Y x)) on random probes x (1e-10)."""
 import math
 
 import numpy as np
 import pytest
+import scipy.sparse as sp
 
 from conftest import problem
+from oracle import fastpi_oracle as orc
+from parity import REC_TOL, assert_block_sigma, assert_sigma, lowrank_rel_factored_gpu
 
 pytestmark = pytest.mark.gpu
 
 
-def test_c5_fullsize_properties():
-    import torch
+@pytest.fixture(scope="module")
+def c5():
     import paper_2011_04235_b200 as fp
-    from paper_2011_04235_b200._device import DeviceCSR, d2h
+    from paper_2011_04235_b200._device import DeviceCSR
     from paper_2011_04235_b200.pinv import fastpi_device
     p = problem("c5")
     w = p.workload
     cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
-    A = DeviceCSR.from_host(p.A)
     stats = {}
-    res = fastpi_device(A, cfg, stats=stats)
+    res = fastpi_device(DeviceCSR.from_host(p.A), cfg, stats=stats)
+    yield p, res, stats
+    stats.clear()
+
+
+@pytest.fixture(scope="module")
+def c5_oracle(c5):
+    p, _, _ = c5
+    A = orc.canonical_csr(p.A)
+    o = orc.reorder(A.shape[0], A.shape[1], A.indptr, A.indices, p.workload.k)
+    return A, o
+
+
+def _same_csr(a, b):
+    a, b = sp.csr_matrix(a), sp.csr_matrix(b)
+    assert a.shape == b.shape
+    np.testing.assert_array_equal(a.indptr, b.indptr)
+    np.testing.assert_array_equal(a.indices, b.indices)
+    np.testing.assert_array_equal(a.data, b.data)
+
+
+def test_c5_reorder_bit_exact(c5, c5_oracle):
+    _, res, st = c5
+    _, o = c5_oracle
+    r = res.reordering
+    np.testing.assert_array_equal(r.row_perm.forward, o.row_fwd)
+    np.testing.assert_array_equal(r.col_perm.forward, o.col_fwd)
+    np.testing.assert_array_equal(r.spans, o.spans)
+    assert (st["m1"], st["n1"], st["m2"], st["n2"], st["T"]) == (o.m1, o.n1, o.m2, o.n2, o.n_iterations)
+    assert r.gcc_sizes == tuple(o.gcc_sizes)
+    print(f"c5 reorder: T={o.n_iterations} m1/n1/m2/n2={o.m1}/{o.n1}/{o.m2}/{o.n2} spans={len(o.spans)}")
+
+
+def test_c5_partition_bit_exact(c5, c5_oracle):
+    _, _, st = c5
+    A, o = c5_oracle
+    Ap = orc.permute(A, o.row_fwd, o.col_fwd)
+    spoke, A12, A21, A22 = orc.partition(Ap, o)
+    part = st["part"]
+    _same_csr(part.a11.to_host(), spoke)
+    T = sp.vstack([A12, A22]).tocsr()
+    _same_csr(part.T.to_host(), T)
+    _same_csr(part.Tt.to_host(), T.T.tocsr())
+    _same_csr(part.a21.to_host(), A21)
+    _same_csr(part.a21t.to_host(), A21.T.tocsr())
+
+
+def test_c5_block_sigma_against_lapack(c5):
+    p, res, st = c5
+    spans = res.reordering.spans
+    fo = orc.block_svd(st["part"].a11.to_host(), spans, p.workload.alpha)
+    assert st["f11"].rank == fo.rank == st["rank11"]
+    assert_block_sigma(st["f11"].sigma, fo.sigma, spans, p.workload.alpha, label="c5 f11")
+
+
+def test_c5_row_update_stagewise(c5):
+    """P3 at c5: the oracle's row_update (pinv.py:131-171) fed the GPU's block factors."""
+    p, _, st = c5
+    w = p.workload
+    f11 = st["f11"]
+    fo, eng = orc.row_update(orc.Factors(f11.U, f11.sigma.copy(), f11.Vt, False), st["part"].a21.to_host(),
+                             st["s"], 0.3, w.seed + 1)
+    fr = st["f_rows"]
+    assert eng == ("randomized" if st["engines"][0] == 1 else "dense")
+    assert_sigma(fr.sigma, fo.sigma, label="c5 row update")
+    d = fr.device()
+    rel = lowrank_rel_factored_gpu(d.U, d2h_sigma(d.sigma), d.Vt, fo.U, fo.sigma, fo.Vt)
+    print(f"c5 row update: low-rank rel diff {rel:.3e} (s={st['s']}, engine {eng})")
+    assert rel <= REC_TOL
+
+
+def d2h_sigma(t):
+    from paper_2011_04235_b200._device import d2h
+    return d2h(t)
+
+
+def test_c5_fullsize_properties(c5):
+    import torch
+    from paper_2011_04235_b200._device import DeviceCSR, d2h
+    p, res, stats = c5
+    w = p.workload
     m, n = p.A.shape
     o = res.reordering
     rf, cf = o.row_perm.forward, o.col_perm.forward
     assert np.array_equal(np.sort(rf), np.arange(m)) and np.array_equal(np.sort(cf), np.arange(n))
-    sp = np.asarray(o.spans)
-    assert sp[:, 1].sum() == o.n_spoke_rows and sp[:, 3].sum() == o.n_spoke_cols
-    assert np.all(sp[1:, 0] == sp[:-1, 0] + sp[:-1, 1]) and np.all(sp[1:, 2] == sp[:-1, 2] + sp[:-1, 3])
+    spn = np.asarray(o.spans)
+    assert spn[:, 1].sum() == o.n_spoke_rows and spn[:, 3].sum() == o.n_spoke_cols
+    assert np.all(spn[1:, 0] == spn[:-1, 0] + spn[:-1, 1]) and np.all(spn[1:, 2] == spn[:-1, 2] + spn[:-1, 3])
     assert o.n_spoke_rows + o.n_hub_rows == m and o.n_spoke_cols + o.n_hub_cols == n
 
     d = res.factors.device()

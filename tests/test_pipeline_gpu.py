@@ -2,8 +2,8 @@
 
 P3 stage-wise: the oracle's row_update / column_update are fed the GPU's own
 upstream factors (removing LAPACK's arbitrary singular-vector signs) and must
-agree with the GPU stage: sigma <= 1e-9 relative, reconstruction and
-U S Vt <= 1e-8 relative.
+agree with the GPU stage: every singular value to <= 1e-9 relative to itself
+(tests/parity.py), reconstruction and U S Vt <= 1e-8 relative.
 P4 end-to-end on the dense-column-update configs (c1, c3r200): sigma <= 1e-9,
 Z <= 1e-8 against the golden fixtures written from the reference.
 P5 randomized-column configs: end-to-end quality is reported, not bit-level.
@@ -14,11 +14,9 @@ import scipy.sparse as sp
 
 from conftest import golden, problem
 from oracle import fastpi_oracle as orc
+from parity import REC_TOL, assert_block_sigma, assert_sigma, lowrank_rel_factored
 
 pytestmark = pytest.mark.gpu
-
-SIG_TOL = 1e-9
-REC_TOL = 1e-8
 
 
 def _run(name):
@@ -51,20 +49,20 @@ def test_stagewise_parity(name):
     assert (st["m1"], st["n1"], st["m2"], st["n2"], st["T"]) == tuple(g["sizes"])
     assert (st["s"], st["r"]) == tuple(g["s_r"])
     assert list(st["engines"]) == [1 if e == "randomized" else 2 for e in g["engines"]]
-    # block stage vs reference fixture
-    assert np.abs(st["f11"].sigma - g["f11_sigma"]).max() <= SIG_TOL * g["f11_sigma"].max()
+    # block stage vs reference fixture: every kept sigma of every block
+    assert_block_sigma(st["f11"].sigma, g["f11_sigma"], g["spans"], w.alpha, label=f"{name} f11")
     part = st["part"]
     A21 = part.a21.to_host()
     T = part.T.to_host()
     # row update fed with the GPU's f11
     fo_rows, _ = orc.row_update(_host_factors(st["f11"]), A21, st["s"], 0.3, w.seed + 1)
     fr = st["f_rows"]
-    assert np.abs(fr.sigma - fo_rows.sigma).max() <= SIG_TOL * fo_rows.sigma[0]
+    assert_sigma(fr.sigma, fo_rows.sigma, label=f"{name} row update")
     assert _lowrank_rel(fr, fo_rows) <= REC_TOL
     # column update fed with the GPU's row-update factors
     fo_full, _ = orc.column_update(_host_factors(fr), T, st["r"], 0.3, w.seed + 2)
     ff = res.factors
-    assert np.abs(ff.sigma - fo_full.sigma).max() <= SIG_TOL * fo_full.sigma[0]
+    assert_sigma(ff.sigma, fo_full.sigma, label=f"{name} column update")
     assert _lowrank_rel(ff, fo_full) <= REC_TOL
     assert ff.orthonormality_defect() < 1e-8
     # sign-invariant reconstruction of the reordered matrix
@@ -85,7 +83,7 @@ def test_stagewise_parity(name):
 def test_end_to_end_dense_column_configs(name):
     p, res, st = _run(name)
     g = golden(name)
-    assert np.abs(res.factors.sigma - g["sigma"]).max() <= SIG_TOL * g["sigma"][0]
+    assert_sigma(res.factors.sigma, g["sigma"], label=f"{name} end to end")
     Z = res.pseudoinverse.apply(p.Y)
     if "Z" in g:
         assert np.linalg.norm(Z - g["Z"]) <= REC_TOL * np.linalg.norm(g["Z"])
@@ -133,12 +131,7 @@ def test_public_api_fit_and_spec_examples():
     sd = np.linalg.svd(Ad, compute_uv=False)
     k = min(len(sd), res.factors.rank)
     assert np.abs(res.factors.sigma[:k] - sd[:k]).max() <= 1e-7 * sd[0]
-    # wide input runs on the transpose
-    R2 = sp.random(60, 150, density=0.08, random_state=rng, format="csr")
-    g = golden("spec_examples")
-    res2 = fp.fastpi(R2, fp.FastpiConfig(alpha=0.5, k=0.05, seed=5))
-    assert np.abs(res2.factors.sigma - g["spec_wide_sigma"]).max() <= 1e-9 * g["spec_wide_sigma"][0] or True
-    assert res2.pseudoinverse.shape == (150, 60)
+    # wide input runs on the transpose: tested stage by stage in test_wide_input_transpose_branch
     # regression fit through the public API
     p = problem("c1")
     w = p.workload
@@ -152,13 +145,7 @@ def test_public_api_fit_and_spec_examples():
 
 
 def _lowrank_rel_factored(fa, fb):
-    """||A - B||_F / ||B||_F for A = Ua Sa Vta, B = Ub Sb Vtb without forming them and without the
-    cancellation of ||A||^2 + ||B||^2 - 2<A, B>: A - B = [Ua Sa, -Ub Sb] [Vta; Vtb] = Q (R N)."""
-    Ua, Vta, Ub, Vtb = (np.asarray(x) for x in (fa.U, fa.Vt, fb.U, fb.Vt))
-    M = np.hstack([Ua * fa.sigma, -(Ub * fb.sigma)])
-    _, R = np.linalg.qr(M)
-    D = R @ np.vstack([Vta, Vtb])
-    return np.linalg.norm(D) / np.linalg.norm(fb.sigma)  # B's factors are orthonormal
+    return lowrank_rel_factored(fa.U, fa.sigma, fa.Vt, fb.U, fb.sigma, fb.Vt)
 
 
 def test_stagewise_parity_c4():
@@ -173,11 +160,11 @@ def test_stagewise_parity_c4():
     part = st["part"]
     fo_rows, _ = orc.row_update(_host_factors(st["f11"]), part.a21.to_host(), st["s"], 0.3, w.seed + 1)
     fr = st["f_rows"]
-    assert np.abs(fr.sigma - fo_rows.sigma).max() <= SIG_TOL * fo_rows.sigma[0]
+    assert_sigma(fr.sigma, fo_rows.sigma, label="c4 row update")
     assert _lowrank_rel_factored(fr, fo_rows) <= REC_TOL
     fo_full, _ = orc.column_update(_host_factors(fr), part.T.to_host(), st["r"], 0.3, w.seed + 2)
     ff = res.factors
-    assert np.abs(ff.sigma - fo_full.sigma).max() <= SIG_TOL * fo_full.sigma[0]
+    assert_sigma(ff.sigma, fo_full.sigma, label="c4 column update")
     assert _lowrank_rel_factored(ff, fo_full) <= REC_TOL
 
 
@@ -233,3 +220,73 @@ def test_c_abi_fastpi_matches_python_pipeline(name):
         assert int(err) == 0
         np.testing.assert_array_equal(d2h(out), d2h(ref.reshape(-1)))
     _lib.call("fpi_fastpi_release")
+
+
+def test_wide_input_transpose_branch():
+    """pinv.py:291-303: an m < n input is solved as fastpi(A^T) and the results are swapped.
+    The SPEC wide example (60 x 150, alpha 0.5, k 0.05, seed 5; the generator sequence of
+    oracle/pin_against_reference.py) is checked stage by stage against the oracle's own transposed
+    run -- reorder of A^T bit-exact, block sigma per value, row / column updates fed the GPU's
+    upstream factors -- and the swap itself: factors transposed, the pseudoinverse of A equal to
+    the transpose of the pseudoinverse of A^T.  End to end the column update of this example takes
+    the randomized engine, so its sigma depend on LAPACK's singular-vector signs; the
+    golden end-to-end sigma are reported, not asserted."""
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200._device import DeviceCSR
+    from paper_2011_04235_b200.pinv import fastpi_device
+    rng = np.random.default_rng(7)
+    sp.random(400, 100, density=0.05, random_state=rng, format="csr")
+    R2 = sp.random(60, 150, density=0.08, random_state=rng, format="csr")
+    alpha, k, seed = 0.5, 0.05, 5
+    cfg = fp.FastpiConfig(alpha=alpha, k=k, seed=seed)
+    res = fp.fastpi(R2, cfg)
+    st = {}
+    res_t = fastpi_device(DeviceCSR.from_host(R2).transpose(), cfg, stats=st)
+    ref = orc.fastpi(R2, alpha, k, seed)
+    assert ref["transposed"]
+    # the swap (pinv.py:297-303)
+    assert res.factors.shape == (60, 150) and res.pseudoinverse.shape == (150, 60)
+    np.testing.assert_array_equal(res.factors.sigma, res_t.factors.sigma)
+    np.testing.assert_array_equal(res.factors.U, res_t.factors.Vt.T)
+    np.testing.assert_array_equal(res.factors.Vt, res_t.factors.U.T)
+    P, Pt = fp.materialize(res.pseudoinverse), fp.materialize(res_t.pseudoinverse)
+    # same factors; only the side diag(sigma+) is multiplied onto differs (rounding)
+    np.testing.assert_allclose(P, Pt.T, rtol=0, atol=1e-13 * np.abs(P).max())
+    # reorder of A^T: bit-exact against the oracle's transposed run
+    o = ref["ordering"]
+    np.testing.assert_array_equal(res_t.reordering.row_perm.forward, o.row_fwd)
+    np.testing.assert_array_equal(res_t.reordering.col_perm.forward, o.col_fwd)
+    np.testing.assert_array_equal(res_t.reordering.spans, o.spans)
+    assert (st["m1"], st["n1"], st["m2"], st["n2"], st["T"]) == (o.m1, o.n1, o.m2, o.n2, o.n_iterations)
+    assert (st["s"], st["r"]) == (ref["s"], ref["r"])
+    # block stage (sign-free): per block, per value
+    assert_block_sigma(st["f11"].sigma, ref["f11"].sigma, o.spans, alpha, label="wide f11")
+    # updates fed the GPU's own upstream factors
+    fo_rows, _ = orc.row_update(_host_factors(st["f11"]), ref["A21"], st["s"], 0.3, seed + 1)
+    assert_sigma(st["f_rows"].sigma, fo_rows.sigma, label="wide row update")
+    assert _lowrank_rel(st["f_rows"], fo_rows) <= REC_TOL
+    fo_full, eng = orc.column_update(_host_factors(st["f_rows"]), ref["T"], st["r"], 0.3, seed + 2)
+    assert_sigma(res.factors.sigma, fo_full.sigma, label="wide column update")
+    assert _lowrank_rel(res_t.factors, fo_full) <= REC_TOL
+    # pseudoinverse of A from the GPU-fed oracle factors, swapped back as pinv.py:297-301 does
+    pv_t = orc.pinv_from_svd(orc.unfold(fo_full, o))
+    P_o = (pv_t.Ut.T * pv_t.sigma_dagger) @ pv_t.V.T
+    assert np.linalg.norm(P - P_o) <= REC_TOL * np.linalg.norm(P_o)
+    g = golden("spec_examples")
+    gap = np.abs(res.factors.sigma - g["spec_wide_sigma"]).max() / g["spec_wide_sigma"][0]
+    print(f"wide example: end-to-end sigma gap vs the reference {gap:.3e} (column engine {eng})")
+
+
+def test_block_sigma_c4_against_lapack():
+    """P2 at the benchmark size: every non-degenerate c4 block (incl. the min-dim >= 48 blocks of the
+    batched Gram path, block_svd.cu) against LAPACK dgesdd, per value (svd.py:154-178)."""
+    p, res, st = _run("c4")
+    part = st["part"]
+    spans = res.reordering.spans
+    fo = orc.block_svd(part.a11.to_host(), spans, p.workload.alpha)
+    assert st["f11"].rank == fo.rank
+    assert_block_sigma(st["f11"].sigma, fo.sigma, spans, p.workload.alpha, label="c4 f11")
+    fo1 = orc.block_svd(part.a11.to_host(), spans, 1.0)
+    from paper_2011_04235_b200.svd import block_diagonal_svd_device
+    f1 = block_diagonal_svd_device(part.a11, res.reordering.spans_device(), 1.0)
+    assert_block_sigma(f1.sigma, fo1.sigma, spans, 1.0, label="c4 f11 alpha=1")

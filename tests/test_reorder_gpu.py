@@ -24,6 +24,8 @@ def _check_against_oracle(A, k):
     assert (r.n_spoke_rows, r.n_spoke_cols, r.n_hub_rows, r.n_hub_cols, r.n_iterations) == \
         (o.m1, o.n1, o.m2, o.n2, o.n_iterations)
     assert r.gcc_sizes == tuple(o.gcc_sizes)
+    # SURVEY 8(d) work accounting of the loop (sum_t E_t, sum_t V_t) equals the oracle's
+    assert (r.edges_visited, r.nodes_visited) == (o.edges_visited, o.nodes_visited)
     return r
 
 

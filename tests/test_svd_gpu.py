@@ -5,6 +5,7 @@ import scipy.sparse as sp
 
 from conftest import problem
 from oracle import fastpi_oracle as orc
+from parity import assert_block_sigma, assert_sigma
 
 pytestmark = pytest.mark.gpu
 
@@ -23,6 +24,7 @@ def test_dense_svd(p, q):
     f = fp.dense_svd(M)
     s = np.linalg.svd(M, compute_uv=False)
     assert _rel_sigma(f.sigma, s) < 1e-12
+    assert_sigma(f.sigma, s, label=f"dense {p}x{q}")
     assert np.abs((f.U * f.sigma) @ f.Vt - M).max() < 1e-12 * s[0]
     assert f.orthonormality_defect() < 1e-10
 
@@ -52,16 +54,8 @@ def test_block_svd_matches_oracle(name):
         f = block_diagonal_svd_device(part.a11, r.spans_device(), a)
         fo = orc.block_svd(part.a11.to_host(), r.spans, a)
         assert f.rank == fo.rank
-        # per block: sigma relative to the block sigma_max
-        spans = r.spans
-        off = 0
-        for rs, h, cs, w in spans.tolist():
-            if not h or not w:
-                continue
-            kp = int(np.ceil(a * min(h, w)))
-            sg, so = f.sigma[off:off + kp], fo.sigma[off:off + kp]
-            assert np.abs(sg - so).max() <= 1e-9 * max(so[0], 1e-300), (rs, h, cs, w)
-            off += kp
+        # per block, per value (tests/parity.py)
+        assert_block_sigma(f.sigma, fo.sigma, r.spans, a, label=f"{name} alpha={a}")
         # block-sparse structure identical, reconstruction of the kept part identical up to signs
         Ug, Vg = f.U.toarray(), f.Vt.toarray()
         Uo, Vo = fo.U.toarray(), fo.Vt.toarray()
@@ -87,6 +81,7 @@ def test_randomized_svd_matches_oracle(seed, rank):
     f = fp.randomized_svd(A, rank, seed)
     fo = orc.randomized_svd(A, rank, seed)
     assert _rel_sigma(f.sigma, fo.sigma) < 1e-10
+    assert_sigma(f.sigma, fo.sigma, label=f"randomized seed {seed} rank {rank}")
     Bg = (f.U * f.sigma) @ f.Vt
     Bo = (fo.U * fo.sigma) @ fo.Vt
     assert np.linalg.norm(Bg - Bo) <= 1e-9 * np.linalg.norm(Bo)
@@ -111,12 +106,7 @@ def test_block_svd_large_tier_batched():
             co += b.shape[1]
         fo = orc.block_svd(spoke, np.array(spans), alpha)
         assert f.rank == fo.rank
-        off = 0
-        for b in blocks:
-            kp = int(np.ceil(alpha * min(b.shape)))
-            so = fo.sigma[off:off + kp]
-            assert np.abs(f.sigma[off:off + kp] - so).max() <= 1e-9 * so[0]
-            off += kp
+        assert_block_sigma(f.sigma, fo.sigma, np.array(spans), alpha, label=f"large tier alpha={alpha}")
         Ug, Vg = f.U.toarray(), f.Vt.toarray()
         Uo, Vo = fo.U.toarray(), fo.Vt.toarray()
         assert np.abs((Ug * f.sigma) @ Vg - (Uo * fo.sigma) @ Vo).max() < 1e-9 * fo.sigma.max()
