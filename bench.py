@@ -447,7 +447,26 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     return ours_arm(args)
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: launch the N ranks ourselves (one process per GPU,
+    torch.distributed.run on 127.0.0.1) with this command line; rank 0 prints the JSON line.
+    NCCL's communicator log (NCCL_DEBUG=INFO unless set) stays on stderr."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    log(f"[bench] spawning {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.run(cmd, env=env).returncode
 
 
 if __name__ == "__main__":

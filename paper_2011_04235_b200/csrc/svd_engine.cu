@@ -649,16 +649,32 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   trace_point(h, "rsvd:sketch");
   op.apply(h, X, k, B);                 // svd.py:133
   trace_point(h, "rsvd:B = M X");
-  // CholeskyQR: B^T B = L L^T, Q = B L^-T   (svd.py:134)
-  gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k, /*sym=*/true);
-  trace_point(h, "rsvd:gram B^T B");
+  // CholeskyQR: B^T B = L L^T, Q = B L^-T   (svd.py:134), and Z = inner^T B for Y^T = Z L^-T
+  // (svd.py:135: Y = Q^T inner).  B^T B = X^T (inner^T B) = X^T Z: for a tall inner (q < p / 2,
+  // the column update's [U Sigma | T]) the Gram comes from the q x k Z at 2 q k^2 flops instead of
+  // the p x k B at p k^2 -- at c5 that is 0.1 instead of 4 TFLOP.  The product of two different
+  // factors is symmetrised; its rounding (eps ||X|| ||Z||) is of the order of the direct Gram's.
+  Scratch<double> Z(q * k, s);
+  const bool gram_from_z = 2 * q < p && getenv("FPI_RSVD_DIRECT_GRAM") == nullptr;
+  if (gram_from_z) {
+    op.applyT(h, B, k, Z);
+    trace_point(h, "rsvd:Z = M^T B");
+    gemm(h, true, false, k, k, q, 1.0, X, k, Z, k, 0.0, Gm, k);
+    k_symmetrize<<<grid_for(k * k, 256, (unsigned)(h->num_sms * 16)), 256, 0, s>>>(k, Gm, k);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+    trace_point(h, "rsvd:gram X^T Z");
+  } else {
+    gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k, /*sym=*/true);
+    trace_point(h, "rsvd:gram B^T B");
+  }
   orth_factor(h, k, Gm, Linv, diag);
   Gm.release();
   trace_point(h, "rsvd:cholesky/inverse");
-  // Y^T = (inner^T B) L^-T   (svd.py:135: Y = Q^T inner)
-  Scratch<double> Z(q * k, s);
-  op.applyT(h, B, k, Z);
-  trace_point(h, "rsvd:Z = M^T B");
+  if (!gram_from_z) {
+    op.applyT(h, B, k, Z);
+    trace_point(h, "rsvd:Z = M^T B");
+  }
   // SVD of Y (k x q) through its transpose Y^T = Z L^-T = Vy S Uy^T   (svd.py:135-136); for a tall
   // Y^T the product is left implicit (Gram L^-1 (Z^T Z) L^-T)
   Scratch<double> Vy(q * rank, s), Uyt(rank * k, s);
