@@ -40,6 +40,7 @@ int fpi_destroy(fpi_handle h) {
   if (h->d_spans) cudaFree(h->d_spans);
   if (h->host_scalars) cudaFreeHost(h->host_scalars);
   fpi::fastpi_free(h);
+  fpi::comm_free(h);
   for (auto& e : h->copy_ev)
     if (e) cudaEventDestroy(e);
   if (h->copy_stream) cudaStreamDestroy(h->copy_stream);

@@ -55,7 +55,9 @@ inline void once_per_device(std::atomic<uint64_t>& mask, int dev, F&& f) {
 
 namespace fpi {
 struct FastpiResult;  // fastpi_capi.cu
+struct Comm;          // comm.cuh
 void fastpi_free(fpi_context* h);
+void comm_free(fpi_context* h);
 }  // namespace fpi
 
 // The handle: one stream, device properties, scratch memory and the results
@@ -77,6 +79,8 @@ struct fpi_context {
   cudaEvent_t copy_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // numerics diagnostics of the last randomized / dense SVD
   fpi_svd_diag diag{};
+  // cross-rank communicator of a sharded solve (comm.cu), null for one rank
+  fpi::Comm* comm = nullptr;
   // counters
   int64_t kernel_launches = 0;
   bool timing_on = false;

@@ -1,0 +1,412 @@
+// The inner Gram H = inner^T inner of the column update's inner matrix
+// [U Sigma | T] (pinv.py:202-203), for the randomized SVD's Z = inner^T (inner X)
+// (svd.py:133-135).  When inner is tall (p rows >> q = s + n2 columns) the two passes
+// of inner over the p x 2r sketch product B cost 2 x (2 nzr s 2r) DMMA flops plus two
+// gather SpMMs of 2r columns over T's nonzeros, while H costs about nzr s^2 + a sparse
+// Gram of T, after which Z = H X is one q x q x 2r GEMM and B never exists.  At c5
+// (p = 2M, q = 13k, 2r = 2000) that is ~50 instead of ~180 ms.  The choice is made per
+// call by the cost model in plan_inner_gram.
+//
+// Blocks of H (S = T, q2 = n2 columns, D = U, sd = s):
+//   H11 = Sigma (D^T D) Sigma                   DMMA Gram over the nonzero rows of D
+//   H21 = S^T D Sigma      heavy rows of S^T:   DMMA on the densified heavy columns
+//                          light rows:          gather SpMM over the nonzero rows of D
+//   H22 = S^T S            light rows:          one CTA per (light column, segment) with a
+//                                               q2-wide shared-memory row accumulator
+//                          heavy rows:          DMMA Gram of the heavy columns + symmetry
+// "Heavy" columns are the most populated columns of S (Zipf hubs: at c5 the top 256 of
+// 12,274 hold 85% of T's nonzeros); they are densified into a p x K panel so that their
+// O(nnz^2 / p) products run on the tensor pipe instead of as scattered updates.
+//
+// Every entry is summed in a fixed order (no atomics): H is deterministic.
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "cub_util.cuh"
+#include "gemm.cuh"
+#include "gram_route.cuh"
+#include "instrument.cuh"
+#include "spmm.cuh"
+
+namespace fpi {
+namespace {
+
+constexpr int GR_WARPS = 16;       // warps per CTA of the sparse Gram rows
+constexpr int64_t GR_SEG = 4096;   // S^T row entries per work item
+
+// Sh[i][hidx[c]] = S[i][c] for heavy c (Sh pre-zeroed): one warp per row
+__global__ void k_densify_heavy(int64_t p, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                const double* __restrict__ val, const int32_t* __restrict__ hidx, int64_t K,
+                                double* __restrict__ Sh) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < p; i += nw) {
+    for (int64_t e = ptr[i] + lane; e < ptr[i + 1]; e += 32) {
+      const int32_t a = hidx[idx[e]];
+      if (a >= 0) Sh[i * K + a] = val[e];
+    }
+  }
+}
+
+// Rows of S^T S for light columns.  Work item w: S column col[w], S^T row entries [b[w], e[w]).
+// acc[x] = sum_{i in item} S[i][col] * S[i][x]  over all q2 columns x.  Warp g owns the 32-column
+// chunks x >> 5 == g (mod GR_WARPS) and walks every row of the item in order, so each acc[x] is
+// updated by one warp, in ascending i: the sum's order is fixed.  dst[w] >= 0: partial row
+// P[dst[w]]; otherwise the finished row goes to H[(sd + col) * ldh + sd + x].
+__global__ void __launch_bounds__(GR_WARPS * 32)
+    k_gram_rows(int64_t nitems, const int32_t* __restrict__ icol, const int64_t* __restrict__ ib,
+                const int64_t* __restrict__ ie, const int32_t* __restrict__ idst, int64_t q2,
+                const int64_t* __restrict__ s_ptr, const int32_t* __restrict__ s_idx,
+                const double* __restrict__ s_val, const int32_t* __restrict__ st_idx,
+                const double* __restrict__ st_val, double* __restrict__ P, double* __restrict__ H, int64_t ldh,
+                int64_t sd) {
+  extern __shared__ double acc[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t w = blockIdx.x; w < nitems; w += gridDim.x) {
+    for (int64_t x = threadIdx.x; x < q2; x += blockDim.x) acc[x] = 0.0;
+    __syncthreads();
+    const int64_t b = ib[w], e = ie[w];
+    for (int64_t base = b; base < e; base += 32) {
+      const int64_t my = base + lane;
+      int64_t rb = 0, re = 0;
+      double v = 0.0;
+      if (my < e) {
+        const int32_t i = __ldg(st_idx + my);
+        v = __ldg(st_val + my);
+        rb = __ldg(s_ptr + i);
+        re = __ldg(s_ptr + i + 1);
+      }
+      const int cnt = (int)((e - base) < 32 ? (e - base) : 32);
+      for (int t = 0; t < cnt; ++t) {
+        const int64_t r0 = __shfl_sync(0xffffffffu, rb, t);
+        const int64_t r1 = __shfl_sync(0xffffffffu, re, t);
+        const double vt = __shfl_sync(0xffffffffu, v, t);
+        for (int64_t q = r0 + lane; q < r1 + lane; q += 32) {
+          if (q < r1) {
+            const int32_t x = __ldg(s_idx + q);
+            if (((x >> 5) % GR_WARPS) == warp) acc[x] = fma(vt, __ldg(s_val + q), acc[x]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int32_t d = idst[w];
+    double* out = d >= 0 ? P + (int64_t)d * q2 : H + (sd + icol[w]) * ldh + sd;
+    for (int64_t x = threadIdx.x; x < q2; x += blockDim.x) out[x] = acc[x];
+    __syncthreads();
+  }
+}
+
+// H[(sd + col[j]) * ldh + sd + x] = sum_{g in [pb[j], pe[j])} P[g][x]   (segments in order)
+__global__ void k_gram_rows_reduce(int64_t nmulti, const int32_t* __restrict__ col, const int32_t* __restrict__ pb,
+                                   const int32_t* __restrict__ pe, int64_t q2, const double* __restrict__ P,
+                                   double* __restrict__ H, int64_t ldh, int64_t sd) {
+  FPI_GRID_STRIDE(t, nmulti * q2) {
+    const int64_t j = t / q2, x = t - j * q2;
+    double a = 0.0;
+    for (int32_t g = pb[j]; g < pe[j]; ++g) a += P[(int64_t)g * q2 + x];
+    H[(sd + col[j]) * ldh + sd + x] = a;
+  }
+}
+
+// Heavy rows of H22: H[sd + heavy[a]][sd + x] = x heavy ? HH[a][hidx[x]] : H[sd + x][sd + heavy[a]]
+__global__ void k_fill_heavy_rows(int64_t K, int64_t q2, const int32_t* __restrict__ heavy,
+                                  const int32_t* __restrict__ hidx, const double* __restrict__ HH,
+                                  double* __restrict__ H, int64_t ldh, int64_t sd) {
+  FPI_GRID_STRIDE(t, K * q2) {
+    const int64_t a = t / q2, x = t - a * q2;
+    const int32_t hx = hidx[x];
+    const int64_t c = heavy[a];
+    H[(sd + c) * ldh + sd + x] = hx >= 0 ? HH[a * K + hx] : H[(sd + x) * ldh + sd + c];
+  }
+}
+
+// H21 into both off-diagonal blocks: row c of S^T D (heavy: Rh[hidx[c]], light: Rl[lidx[c]])
+// scaled by dscale: H[sd + c][t] = H[t][sd + c] = R[c][t] * dscale[t]
+__global__ void k_fill_h21(int64_t q2, int64_t sd, const int32_t* __restrict__ hidx,
+                           const int32_t* __restrict__ lidx, const double* __restrict__ Rh,
+                           const double* __restrict__ Rl, const double* __restrict__ dscale, double* __restrict__ H,
+                           int64_t ldh) {
+  FPI_GRID_STRIDE(e, q2 * sd) {
+    const int64_t c = e / sd, t = e - c * sd;
+    const double r = hidx[c] >= 0 ? Rh[(int64_t)hidx[c] * sd + t] : Rl[(int64_t)lidx[c] * sd + t];
+    const double v = dscale ? r * dscale[t] : r;
+    H[(sd + c) * ldh + t] = v;
+    H[t * ldh + sd + c] = v;
+  }
+}
+
+// H11 = diag(ds) G diag(ds)
+__global__ void k_fill_h11(int64_t sd, const double* __restrict__ G, const double* __restrict__ ds,
+                           double* __restrict__ H, int64_t ldh) {
+  FPI_GRID_STRIDE(e, sd * sd) {
+    const int64_t a = e / sd, b = e - a * sd;
+    const double g = G[e];
+    H[a * ldh + b] = ds ? ds[a] * g * ds[b] : g;
+  }
+}
+
+// Light rows of S^T restricted to the nonzero rows of D, row ids remapped to positions in the
+// nonzero-row list (nzpos[i] >= 0): counts, then entries (order kept), one warp per row.
+__global__ void k_restrict_count(int64_t nl, const int32_t* __restrict__ light, const int64_t* __restrict__ st_ptr,
+                                 const int32_t* __restrict__ st_idx, const int32_t* __restrict__ nzpos,
+                                 int64_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nl; j += nw) {
+    const int32_t c = light[j];
+    int64_t n = 0;
+    for (int64_t e = st_ptr[c] + lane; e < st_ptr[c + 1]; e += 32) n += nzpos[st_idx[e]] >= 0;
+    for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) cnt[j] = n;
+  }
+}
+
+__global__ void k_restrict_fill(int64_t nl, const int32_t* __restrict__ light, const int64_t* __restrict__ st_ptr,
+                                const int32_t* __restrict__ st_idx, const double* __restrict__ st_val,
+                                const int32_t* __restrict__ nzpos, const int64_t* __restrict__ optr,
+                                int32_t* __restrict__ oidx, double* __restrict__ oval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nl; j += nw) {
+    const int32_t c = light[j];
+    int64_t o = optr[j];
+    const int64_t b = st_ptr[c], e = st_ptr[c + 1];
+    for (int64_t base = b; base < e; base += 32) {
+      const int64_t my = base + lane;
+      const int32_t np = my < e ? nzpos[st_idx[my]] : -1;
+      const unsigned keep = __ballot_sync(0xffffffffu, np >= 0);
+      if (np >= 0) {
+        const int64_t at = o + __popc(keep & ((1u << lane) - 1u));
+        oidx[at] = np;
+        oval[at] = st_val[my];
+      }
+      o += __popc(keep);
+    }
+  }
+}
+
+__global__ void k_fill_i32(int32_t* a, int64_t n, int32_t v) {
+  FPI_GRID_STRIDE(i, n) a[i] = v;
+}
+__global__ void k_nzpos(int64_t nzr, const int32_t* __restrict__ rows, int32_t* __restrict__ nzpos) {
+  FPI_GRID_STRIDE(t, nzr) nzpos[rows[t]] = (int32_t)t;
+}
+__global__ void k_iota_pos(int64_t p, int32_t* __restrict__ nzpos) {
+  FPI_GRID_STRIDE(t, p) nzpos[t] = (int32_t)t;
+}
+__global__ void k_gather_rows_ld(int64_t nr, int64_t k, const double* __restrict__ src, int64_t lds,
+                                 const int32_t* __restrict__ rows, double* __restrict__ dst, int64_t ldd) {
+  FPI_GRID_STRIDE(e, nr * k) {
+    const int64_t i = e / k, c = e - i * k;
+    dst[i * ldd + c] = src[(rows ? (int64_t)rows[i] : i) * lds + c];
+  }
+}
+
+double env_double(const char* name, double dflt) {
+  const char* e = getenv(name);
+  return e ? atof(e) : dflt;
+}
+
+}  // namespace
+
+GramPlan plan_inner_gram(fpi_context* h, const SparseGramIn& in, int64_t k) {
+  GramPlan pl;
+  const int64_t q = in.sd + in.q2;
+  const int force = getenv("FPI_GRAM_ROUTE") ? atoi(getenv("FPI_GRAM_ROUTE")) : -1;
+  // feasibility: one q2-wide row accumulator per CTA in shared memory; H (q x q) in HBM
+  if (force == 0 || in.q2 <= 0 || in.s_nnz <= 0 || (in.q2 * 8 + 1024) > (int64_t)h->smem_optin ||
+      q > 32768)
+    return pl;
+  std::vector<int64_t> ptr(in.q2 + 1);
+  FPI_CUDA(cudaMemcpyAsync(ptr.data(), in.st_ptr, sizeof(int64_t) * (in.q2 + 1), cudaMemcpyDeviceToHost, h->stream));
+  FPI_CUDA(cudaStreamSynchronize(h->stream));
+  std::vector<int32_t> ord(in.q2);
+  for (int64_t c = 0; c < in.q2; ++c) ord[c] = (int32_t)c;
+  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
+    return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b];
+  });
+  // heavy: columns holding at least p / 256 (and 64) entries, at most 256 of them
+  const int64_t thresh = std::max<int64_t>(64, in.p / 256);
+  int64_t K = 0;
+  const int64_t kmax = (int64_t)env_double("FPI_GRAM_HEAVY", 256);
+  while (K < in.q2 && K < kmax && ptr[ord[K] + 1] - ptr[ord[K]] >= thresh) ++K;
+  std::vector<char> isheavy(in.q2, 0);
+  for (int64_t a = 0; a < K; ++a) isheavy[ord[a]] = 1;
+  for (int64_t c = 0; c < in.q2; ++c) {
+    const int64_t n = ptr[c + 1] - ptr[c];
+    if (isheavy[c]) {
+      pl.heavy.push_back((int32_t)c);
+      pl.heavy_nnz += n;
+    } else {
+      pl.light.push_back((int32_t)c);
+      pl.light_nnz += n;
+    }
+  }
+  // cost model (seconds): DMMA ~28 TFLOP/s, gathered SpMM bytes ~8 TB/s (L2-fed), HBM ~6 TB/s
+  const double RF = 28e12, RG = 8e12, RH = 6e12;
+  const double nzr = (double)(in.nzr >= 0 ? in.nzr : (in.D ? in.p : 0));
+  const double sd = (double)in.sd, kk = (double)k, P = (double)in.p, Kd = (double)K;
+  const double avg_row = (double)in.s_nnz / std::max<double>(1.0, P);
+  pl.t_direct = 4.0 * nzr * sd * kk / RF + 2.0 * (double)in.s_nnz * kk * 8.0 / RG;
+  const double t_rows = (double)pl.light_nnz * (1.0 + avg_row / 32.0) * 45e-9 / (2.0 * h->num_sms);
+  pl.t_gram = nzr * sd * sd / RF + P * Kd * Kd / RF + 2.0 * nzr * Kd * sd / RF +
+              (double)pl.light_nnz * sd * 8.0 / RG + t_rows + 2.0 * (double)q * (double)q * kk / RF +
+              3.0 * 8.0 * (double)q * (double)q / RH + P * Kd * 8.0 * 2.0 / RH;
+  pl.use = force == 1 || pl.t_gram < 0.85 * pl.t_direct;
+  return pl;
+}
+
+void inner_gram(fpi_context* h, const SparseGramIn& in, const GramPlan& pl, double* H, int64_t ldh) {
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  const int64_t p = in.p, sd = in.sd, q2 = in.q2, q = sd + q2;
+  const int64_t K = (int64_t)pl.heavy.size(), nl = (int64_t)pl.light.size();
+  KTimer kt(h, "inner_gram_route", 0.0, 0.0);
+  Scratch<int32_t> heavy(K + 1, s), light(nl + 1, s), hidx(q2, s), lidx(q2, s);
+  if (K) FPI_CUDA(cudaMemcpyAsync(heavy.get(), pl.heavy.data(), 4 * K, cudaMemcpyHostToDevice, s));
+  if (nl) FPI_CUDA(cudaMemcpyAsync(light.get(), pl.light.data(), 4 * nl, cudaMemcpyHostToDevice, s));
+  {
+    std::vector<int32_t> hl(q2, -1), ll(q2, -1);
+    for (int64_t a = 0; a < K; ++a) hl[pl.heavy[a]] = (int32_t)a;
+    for (int64_t j = 0; j < nl; ++j) ll[pl.light[j]] = (int32_t)j;
+    FPI_CUDA(cudaMemcpyAsync(hidx.get(), hl.data(), 4 * q2, cudaMemcpyHostToDevice, s));
+    FPI_CUDA(cudaMemcpyAsync(lidx.get(), ll.data(), 4 * q2, cudaMemcpyHostToDevice, s));
+    FPI_CUDA(cudaStreamSynchronize(s));  // the host vectors go out of scope
+  }
+  // ---- heavy panel Sh (p x K) and HH = Sh^T Sh
+  Scratch<double> Sh, HH;
+  if (K) {
+    Sh.alloc(p * K, s);
+    FPI_CUDA(cudaMemsetAsync(Sh.get(), 0, sizeof(double) * p * K, s));
+    k_densify_heavy<<<grid_for(p * 32, 256, G), 256, 0, s>>>(p, in.s_ptr, in.s_idx, in.s_val, hidx, K, Sh);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+    HH.alloc(K * K, s);
+    gemm(h, true, false, K, K, p, 1.0, Sh, K, Sh, K, 0.0, HH, K, /*sym=*/true);
+  }
+  // ---- light rows of H22 (they include the light x heavy block)
+  if (nl) {
+    std::vector<int64_t> ptr(q2 + 1);
+    FPI_CUDA(cudaMemcpyAsync(ptr.data(), in.st_ptr, sizeof(int64_t) * (q2 + 1), cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+    std::vector<int32_t> icol, idst, mcol, mpb, mpe;
+    std::vector<int64_t> ib, ie;
+    int32_t npart = 0;
+    for (int64_t j = 0; j < nl; ++j) {
+      const int32_t c = pl.light[j];
+      const int64_t b = ptr[c], e = ptr[c + 1];
+      const int64_t nseg = e > b ? (e - b + GR_SEG - 1) / GR_SEG : 1;
+      if (nseg > 1) {
+        mcol.push_back(c);
+        mpb.push_back(npart);
+        mpe.push_back(npart + (int32_t)nseg);
+      }
+      for (int64_t g = 0; g < nseg; ++g) {
+        icol.push_back(c);
+        ib.push_back(b + g * GR_SEG);
+        ie.push_back(std::min(e, b + (g + 1) * GR_SEG));
+        idst.push_back(nseg > 1 ? npart++ : -1);
+      }
+    }
+    const int64_t nit = (int64_t)icol.size(), nm = (int64_t)mcol.size();
+    Scratch<int32_t> d_icol(nit, s), d_idst(nit, s), d_mcol(nm + 1, s), d_mpb(nm + 1, s), d_mpe(nm + 1, s);
+    Scratch<int64_t> d_ib(nit, s), d_ie(nit, s);
+    FPI_CUDA(cudaMemcpyAsync(d_icol.get(), icol.data(), 4 * nit, cudaMemcpyHostToDevice, s));
+    FPI_CUDA(cudaMemcpyAsync(d_idst.get(), idst.data(), 4 * nit, cudaMemcpyHostToDevice, s));
+    FPI_CUDA(cudaMemcpyAsync(d_ib.get(), ib.data(), 8 * nit, cudaMemcpyHostToDevice, s));
+    FPI_CUDA(cudaMemcpyAsync(d_ie.get(), ie.data(), 8 * nit, cudaMemcpyHostToDevice, s));
+    if (nm) {
+      FPI_CUDA(cudaMemcpyAsync(d_mcol.get(), mcol.data(), 4 * nm, cudaMemcpyHostToDevice, s));
+      FPI_CUDA(cudaMemcpyAsync(d_mpb.get(), mpb.data(), 4 * nm, cudaMemcpyHostToDevice, s));
+      FPI_CUDA(cudaMemcpyAsync(d_mpe.get(), mpe.data(), 4 * nm, cudaMemcpyHostToDevice, s));
+    }
+    Scratch<double> P((size_t)npart * q2 + 1, s);
+    const size_t smem = (size_t)q2 * 8;
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, h->device, [&] {
+      FPI_CUDA(cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(h->smem_optin - 1024)));
+    });
+    int per_sm = 0;
+    FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram_rows, GR_WARPS * 32, smem));
+    const int64_t grid = std::min<int64_t>(nit, (int64_t)h->num_sms * std::max(per_sm, 1));
+    k_gram_rows<<<(unsigned)grid, GR_WARPS * 32, smem, s>>>(nit, d_icol, d_ib, d_ie, d_idst, q2, in.s_ptr, in.s_idx,
+                                                           in.s_val, in.st_idx, in.st_val, P, H, ldh, sd);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+    if (nm) {
+      k_gram_rows_reduce<<<grid_for(nm * q2, 256, G), 256, 0, s>>>(nm, d_mcol, d_mpb, d_mpe, q2, P, H, ldh, sd);
+      FPI_LAUNCH_CHECK();
+      note_launch(h);
+    }
+    FPI_CUDA(cudaStreamSynchronize(s));  // host work lists go out of scope
+  }
+  if (K) {
+    k_fill_heavy_rows<<<grid_for(K * q2, 256, G), 256, 0, s>>>(K, q2, heavy, hidx, HH, H, ldh, sd);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+  }
+  if (sd == 0 || !in.D) return;
+  // ---- H21 = S^T D diag(dscale) and H11 = diag(dscale) D^T D diag(dscale) over the nonzero rows of D
+  const bool compact = in.nzr >= 0;
+  const int64_t nzr = compact ? in.nzr : p;
+  if (nzr == 0) {
+    // D is zero: H11 = 0, H21 = 0
+    for (int64_t r = 0; r < sd; ++r) FPI_CUDA(cudaMemsetAsync(H + r * ldh, 0, sizeof(double) * q, s));
+    FPI_CUDA(cudaMemset2DAsync(H + sd * ldh, ldh * sizeof(double), 0, sd * sizeof(double), q2, s));
+    return;
+  }
+  const double* Dz = compact ? in.Dnz : in.D;
+  const int64_t ldz = compact ? sd : in.ldd;
+  // nonzero rows in an even-stride copy (16-byte gathers in the SpMM)
+  const int64_t ldp = (sd + 1) & ~(int64_t)1;
+  Scratch<double> Dp(nzr * ldp, s);
+  k_gather_rows_ld<<<grid_for(nzr * sd, 256, G), 256, 0, s>>>(nzr, sd, Dz, ldz, nullptr, Dp, ldp);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+  Scratch<double> G11(sd * sd, s);
+  gemm(h, true, false, sd, sd, nzr, 1.0, Dp, ldp, Dp, ldp, 0.0, G11, sd, /*sym=*/true);
+  k_fill_h11<<<grid_for(sd * sd, 256, G), 256, 0, s>>>(sd, G11, in.dscale, H, ldh);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+  G11.release();
+  Scratch<double> Rh(K * sd + 1, s), Rl(nl * sd + 1, s);
+  if (K) {
+    Scratch<double> Shz(nzr * K, s);
+    k_gather_rows_ld<<<grid_for(nzr * K, 256, G), 256, 0, s>>>(nzr, K, Sh, K, compact ? in.nz_rows : nullptr, Shz,
+                                                                K);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+    Sh.release();
+    gemm(h, true, false, K, sd, nzr, 1.0, Shz, K, Dp, ldp, 0.0, Rh, sd);
+  }
+  if (nl) {
+    Scratch<int32_t> nzpos(p, s);
+    if (compact) {
+      k_fill_i32<<<grid_for(p, 256, G), 256, 0, s>>>(nzpos, p, -1);
+      k_nzpos<<<grid_for(nzr, 256, G), 256, 0, s>>>(nzr, in.nz_rows, nzpos);
+    } else {
+      k_iota_pos<<<grid_for(p, 256, G), 256, 0, s>>>(p, nzpos);
+    }
+    Scratch<int64_t> cnt(nl + 1, s), rptr(nl + 1, s);
+    FPI_CUDA(cudaMemsetAsync(cnt.get() + nl, 0, sizeof(int64_t), s));
+    k_restrict_count<<<grid_for(nl * 32, 256, G), 256, 0, s>>>(nl, light, in.st_ptr, in.st_idx, nzpos, cnt);
+    CubTemp tmp(s);
+    exclusive_sum(tmp, cnt.get(), rptr.get(), nl + 1, s);
+    const int64_t rn = host_read(rptr.get() + nl, s);
+    Scratch<int32_t> ridx(rn + 1, s);
+    Scratch<double> rval(rn + 1, s);
+    k_restrict_fill<<<grid_for(nl * 32, 256, G), 256, 0, s>>>(nl, light, in.st_ptr, in.st_idx, in.st_val, nzpos, rptr,
+                                                              ridx, rval);
+    FPI_LAUNCH_CHECK();
+    note_launch(h, 4);
+    spmm(h, nl, nzr, sd, rptr, ridx, rval, nullptr, 1.0, Dp, ldp, 0.0, Rl, sd);
+  }
+  k_fill_h21<<<grid_for(q2 * sd, 256, G), 256, 0, s>>>(q2, sd, hidx, lidx, Rh, Rl, in.dscale, H, ldh);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+}
+
+}  // namespace fpi

@@ -27,10 +27,11 @@
 #include "sparse.cuh"
 #include "spmm.cuh"
 #include "svd_engine.cuh"
+#include "gram_route.cuh"
+#include "inner_op.cuh"
 
 namespace fpi {
 
-void sketch_normal(fpi_context* h, int64_t seed, int64_t rows, int64_t cols, double* d_out, int64_t ld);
 
 namespace {
 
@@ -77,6 +78,17 @@ __global__ void k_gather_vt(int64_t q, int64_t K, const double* __restrict__ V, 
   FPI_GRID_STRIDE(e, K * q) {
     int64_t k = e / q, j = e - k * q;
     Vt[k * ldvt + j] = V[j * ldv + ord[k]];
+  }
+}
+
+// Vt[k][j] = V[j][ord[k]] / s[k]   (0 where s[k] == 0)
+__global__ void k_gather_vt_div(int64_t q, int64_t K, const double* __restrict__ V, int64_t ldv,
+                                const int32_t* __restrict__ ord, const double* __restrict__ sv,
+                                double* __restrict__ Vt, int64_t ldvt) {
+  FPI_GRID_STRIDE(e, K * q) {
+    int64_t k = e / q, j = e - k * q;
+    const double d = sv[k];
+    Vt[k * ldvt + j] = d > 0.0 ? V[j * ldv + ord[k]] / d : 0.0;
   }
 }
 
@@ -497,98 +509,79 @@ void dense_svd(fpi_context* h, int64_t p, int64_t q, const double* M, int64_t ld
 }
 
 // ---------------------------------------------------------------------------
-// inner-matrix operator: [D diag(dscale) | S] (horizontal) -- D may be null
-struct InnerOp {
-  int64_t p = 0, q = 0;
-  const double* D = nullptr;
-  int64_t ldd = 0, sd = 0;
-  const double* dscale = nullptr;
-  const int64_t* s_ptr = nullptr;
-  const int32_t* s_idx = nullptr;
-  const double* s_val = nullptr;  // p x (q - sd)
-  const int64_t* st_ptr = nullptr;
-  const int32_t* st_idx = nullptr;
-  const double* st_val = nullptr;  // (q - sd) x p
-  // optional: only nzr rows of D are nonzero (rows listed in nz_rows, gathered into Dnz)
-  int64_t nzr = -1;
-  const int32_t* nz_rows = nullptr;
-  const double* Dnz = nullptr;
-  int64_t s_nnz = 0;  // stored entries of the sparse part (cost model only)
-
-  // flop-equivalent cost of apply() with k columns (a gathered SpMM byte ~ 10 flops on B200)
-  double apply_cost(int64_t k) const {
-    const double dense_rows = (double)(nzr >= 0 ? nzr : p);
-    return (D && sd > 0 ? 2.0 * dense_rows * (double)sd * (double)k : 0.0) + 10.0 * 8.0 * (double)s_nnz * (double)k;
-  }
-
-  // B (p x k) = inner * X (q x k)
-  void apply(fpi_context* h, const double* X, int64_t k, double* B) const {
-    if (D && sd > 0 && nzr >= 0) {
-      cudaStream_t s = h->stream;
-      const unsigned G = (unsigned)(h->num_sms * 16);
-      if (q > sd)
-        spmm(h, p, q - sd, k, s_ptr, s_idx, s_val, nullptr, 1.0, X + sd * k, k, 0.0, B, k);
-      else
-        FPI_CUDA(cudaMemsetAsync(B, 0, sizeof(double) * p * k, s));
-      if (nzr > 0) {
-        Scratch<double> Xs(sd * k, s), tmp(nzr * k, s);
-        FPI_CUDA(cudaMemcpyAsync(Xs.get(), X, sizeof(double) * sd * k, cudaMemcpyDeviceToDevice, s));
-        if (dscale) scale_rows(h, sd, k, Xs, k, dscale);
-        gemm(h, false, false, nzr, k, sd, 1.0, Dnz, sd, Xs, k, 0.0, tmp, k);
-        k_scatter_add_rows32<<<grid_for(nzr * k, 256, G), 256, 0, s>>>(nzr, k, tmp, k, nz_rows, B, k);
-        FPI_LAUNCH_CHECK();
-      }
-      return;
-    }
-    if (D && sd > 0) {
-      Scratch<double> Xs(sd * k, h->stream);
-      FPI_CUDA(cudaMemcpyAsync(Xs.get(), X, sizeof(double) * sd * k, cudaMemcpyDeviceToDevice, h->stream));
-      if (dscale) scale_rows(h, sd, k, Xs, k, dscale);
-      gemm(h, false, false, p, k, sd, 1.0, D, ldd, Xs, k, 0.0, B, k);
-      if (q > sd) spmm(h, p, q - sd, k, s_ptr, s_idx, s_val, nullptr, 1.0, X + sd * k, k, 1.0, B, k);
-    } else {
-      spmm(h, p, q, k, s_ptr, s_idx, s_val, nullptr, 1.0, X, k, 0.0, B, k);
-    }
-  }
-  // Z (q x k) = inner^T * B (p x k)
-  void applyT(fpi_context* h, const double* B, int64_t k, double* Z) const {
-    if (D && sd > 0 && nzr >= 0) {
-      cudaStream_t s = h->stream;
-      const unsigned G = (unsigned)(h->num_sms * 16);
-      if (nzr > 0) {
-        Scratch<double> Bg(nzr * k, s);
-        k_gather_rows32<<<grid_for(nzr * k, 256, G), 256, 0, s>>>(nzr, k, B, k, nz_rows, Bg, k);
-        FPI_LAUNCH_CHECK();
-        gemm(h, true, false, sd, k, nzr, 1.0, Dnz, sd, Bg, k, 0.0, Z, k);
-        if (dscale) scale_rows(h, sd, k, Z, k, dscale);
-      } else {
-        FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * sd * k, s));
-      }
-      if (q > sd) spmm(h, q - sd, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z + sd * k, k);
-      return;
-    }
-    if (D && sd > 0) {
-      gemm(h, true, false, sd, k, p, 1.0, D, ldd, B, k, 0.0, Z, k);
-      if (dscale) scale_rows(h, sd, k, Z, k, dscale);
-      if (q > sd) spmm(h, q - sd, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z + sd * k, k);
-    } else {
-      spmm(h, q, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z, k);
-    }
-  }
-  // dense copy (p x q)
-  void densify(fpi_context* h, double* out) const {
+// inner-matrix operator (inner_op.cuh): B (p x k) = inner * X (q x k)
+void InnerOp::apply(fpi_context* h, const double* X, int64_t k, double* B) const {
+  if (D && sd > 0 && nzr >= 0) {
     cudaStream_t s = h->stream;
     const unsigned G = (unsigned)(h->num_sms * 16);
-    k_fill<<<grid_for(p * q, 256, G), 256, 0, s>>>(p * q, out, 0.0);
-    if (D && sd > 0) {
-      k_copy2d<<<grid_for(p * sd, 256, G), 256, 0, s>>>(p, sd, D, ldd, out, q);
-      if (dscale) scale_cols(h, p, sd, out, q, dscale, false);
+    if (q > sd)
+      spmm(h, p, q - sd, k, s_ptr, s_idx, s_val, nullptr, 1.0, X + sd * k, k, 0.0, B, k);
+    else
+      FPI_CUDA(cudaMemsetAsync(B, 0, sizeof(double) * p * k, s));
+    if (nzr > 0) {
+      Scratch<double> Xs(sd * k, s), tmp(nzr * k, s);
+      FPI_CUDA(cudaMemcpyAsync(Xs.get(), X, sizeof(double) * sd * k, cudaMemcpyDeviceToDevice, s));
+      if (dscale) scale_rows(h, sd, k, Xs, k, dscale);
+      gemm(h, false, false, nzr, k, sd, 1.0, Dnz, sd, Xs, k, 0.0, tmp, k);
+      k_scatter_add_rows32<<<grid_for(nzr * k, 256, G), 256, 0, s>>>(nzr, k, tmp, k, nz_rows, B, k);
+      FPI_LAUNCH_CHECK();
     }
-    if (q > sd) k_csr_to_dense<<<grid_for(p * 32, 256, G), 256, 0, s>>>(p, s_ptr, s_idx, s_val, out, q, sd);
-    FPI_LAUNCH_CHECK();
-    note_launch(h, 3);
+    return;
   }
-};
+  if (D && sd > 0) {
+    Scratch<double> Xs(sd * k, h->stream);
+    FPI_CUDA(cudaMemcpyAsync(Xs.get(), X, sizeof(double) * sd * k, cudaMemcpyDeviceToDevice, h->stream));
+    if (dscale) scale_rows(h, sd, k, Xs, k, dscale);
+    gemm(h, false, false, p, k, sd, 1.0, D, ldd, Xs, k, 0.0, B, k);
+    if (q > sd) spmm(h, p, q - sd, k, s_ptr, s_idx, s_val, nullptr, 1.0, X + sd * k, k, 1.0, B, k);
+  } else {
+    spmm(h, p, q, k, s_ptr, s_idx, s_val, nullptr, 1.0, X, k, 0.0, B, k);
+  }
+}
+// Z (q x k) = inner^T * B (p x k)
+void InnerOp::applyT(fpi_context* h, const double* B, int64_t k, double* Z) const {
+  if (D && sd > 0 && nzr >= 0) {
+    cudaStream_t s = h->stream;
+    const unsigned G = (unsigned)(h->num_sms * 16);
+    if (nzr > 0) {
+      Scratch<double> Bg(nzr * k, s);
+      k_gather_rows32<<<grid_for(nzr * k, 256, G), 256, 0, s>>>(nzr, k, B, k, nz_rows, Bg, k);
+      FPI_LAUNCH_CHECK();
+      gemm(h, true, false, sd, k, nzr, 1.0, Dnz, sd, Bg, k, 0.0, Z, k);
+      if (dscale) scale_rows(h, sd, k, Z, k, dscale);
+    } else {
+      FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * sd * k, s));
+    }
+    if (q > sd) spmm(h, q - sd, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z + sd * k, k);
+    return;
+  }
+  if (D && sd > 0) {
+    gemm(h, true, false, sd, k, p, 1.0, D, ldd, B, k, 0.0, Z, k);
+    if (dscale) scale_rows(h, sd, k, Z, k, dscale);
+    if (q > sd) spmm(h, q - sd, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z + sd * k, k);
+  } else {
+    spmm(h, q, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z, k);
+  }
+}
+// dense copy (p x q)
+void InnerOp::densify(fpi_context* h, double* out) const {
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  k_fill<<<grid_for(p * q, 256, G), 256, 0, s>>>(p * q, out, 0.0);
+  if (D && sd > 0) {
+    k_copy2d<<<grid_for(p * sd, 256, G), 256, 0, s>>>(p, sd, D, ldd, out, q);
+    if (dscale) scale_cols(h, p, sd, out, q, dscale, false);
+  }
+  if (q > sd) k_csr_to_dense<<<grid_for(p * 32, 256, G), 256, 0, s>>>(p, s_ptr, s_idx, s_val, out, q, sd);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 3);
+}
+
+void symmetrize(fpi_context* h, int64_t n, double* A, int64_t lda) {
+  k_symmetrize<<<grid_for(n * n, 256, (unsigned)(h->num_sms * 16)), 256, 0, h->stream>>>(n, A, lda);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+}
 
 // Q = B L^-T orthonormal from the Gram G = B^T B (k x k, preserved): CholeskyQR (svd.py:134's QR
 // without forming Q), or, when G is not numerically positive definite, an eigen-based factor.
@@ -625,6 +618,68 @@ void orth_factor(fpi_context* h, int64_t k, const double* Gm, double* Linv, fpi_
   }
 }
 
+// The finish of the randomized SVD from the right side (svd.py:135-137): with W the top eigenvectors
+// of Y Y^T = L^-1 (Z^T Z) L^-T, the left vectors are U = Q W = B (L^-T W) and the right ones
+// V = Y^T W / sigma = inner^T U / sigma.  For a wide sparse inner (the row update's
+// [Sigma Vt11 ; A21], q = n1 >> p) that is one SpMM of inner^T with r columns instead of the
+// q x 2r x r product Z (L^-T W) of the left-side finish.  sigma_i = ||inner^T u_i|| as in the
+// left-side finish (column norms).  Returns false (nothing written) when the kept spectrum is wide
+// enough to need the refined path.
+static bool rsvd_finish_right(fpi_context* h, const InnerOp& op, int64_t rank, const double* X, const double* B,
+                              const double* Z, const double* Linv, double* U, double* sigma, double* Vt,
+                              fpi_svd_diag* diag) {
+  cudaStream_t s = h->stream;
+  const int64_t p = op.p, q = op.q, k = 2 * rank;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  Scratch<double> Gm(k * k, s), T1(k * k, s), W0(k * k, s), w0(k, s);
+  gemm(h, true, false, k, k, q, 1.0, Z, k, Z, k, 0.0, Gm, k, /*sym=*/true);
+  gemm(h, false, false, k, k, k, 1.0, Linv, k, Gm, k, 0.0, T1, k);   // L^-1 (Z^T Z)
+  gemm(h, false, true, k, k, k, 1.0, T1, k, Linv, k, 0.0, Gm, k);    // ... L^-T
+  k_symmetrize<<<grid_for(k * k, 256, G), 256, 0, s>>>(k, Gm, k);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+  T1.release();
+  const int sw0 = sym_eig(h, k, Gm, k, w0, W0, k, 60, 1e-15, true);
+  double lam[2];
+  FPI_CUDA(cudaMemcpyAsync(&lam[0], w0.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  FPI_CUDA(cudaMemcpyAsync(&lam[1], w0.get() + (rank - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+  FPI_CUDA(cudaStreamSynchronize(s));
+  if (!(lam[0] > 0.0) || lam[1] < 1e-6 * lam[0]) return false;  // wide spectrum: refined left-side path
+  Gm.release();
+  // U0 = Q W[:, :r] = B (L^-T W) or inner (X (L^-T W))
+  Scratch<double> Mx(k * rank, s), U0(p * rank, s);
+  gemm(h, true, false, k, rank, k, 1.0, Linv, k, W0, k, 0.0, Mx, rank);
+  if (!B || op.apply_cost(rank) + 2.0 * (double)q * (double)k * (double)rank < 2.0 * (double)p * (double)k * (double)rank) {
+    Scratch<double> XM(q * rank, s);
+    gemm(h, false, false, q, rank, k, 1.0, X, k, Mx, rank, 0.0, XM, rank);
+    op.apply(h, XM, rank, U0);
+  } else {
+    gemm(h, false, false, p, rank, k, 1.0, B, k, Mx, rank, 0.0, U0, rank);
+  }
+  // V sigma = inner^T U0
+  Scratch<double> Vs(q * rank, s), ss(rank, s), ss2(rank, s), ones(rank, s), sgn(rank, s);
+  op.applyT(h, U0, rank, Vs);
+  col_sumsq(h, q, rank, Vs, rank, ss);
+  k_sqrt_clamp<<<grid_for(rank, 256, G), 256, 0, s>>>(rank, ss);
+  Scratch<int32_t> ord(rank, s), ord2(rank, s);
+  k_iota32<<<grid_for(rank, 256, G), 256, 0, s>>>(ord, rank);
+  CubTemp tmp(s);
+  sort_pairs(tmp, ss.get(), ss2.get(), ord.get(), ord2.get(), rank, true, 0, 64, s);
+  FPI_CUDA(cudaMemcpyAsync(sigma, ss2.get(), sizeof(double) * rank, cudaMemcpyDeviceToDevice, s));
+  k_gather_vt_div<<<grid_for(rank * q, 256, G), 256, 0, s>>>(q, rank, Vs, rank, ord2, ss2, Vt, q);
+  canonical_signs_vt(h, rank, q, Vt, q, sgn);
+  k_fill<<<grid_for(rank, 256, G), 256, 0, s>>>(rank, ones, 1.0);
+  k_gather_cols_div<<<grid_for(p * rank, 256, G), 256, 0, s>>>(p, rank, U0, rank, ord2, ones, sgn, U, rank);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 5);
+  if (diag) {
+    const int slot = diag->eig_sweeps[0] ? 2 : 0;
+    diag->eig_sweeps[slot] = sw0;
+    diag->eig_sweeps[slot + 1] = 0;
+  }
+  return true;
+}
+
 static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int64_t seed, double* U, double* sigma,
                            double* Vt, fpi_svd_diag* diag) {
   const int64_t p = op.p, q = op.q;
@@ -643,22 +698,42 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
     return;
   }
   trace_point(h, "rsvd:start");
-  Scratch<double> X(q * k, s), B(p * k, s), Gm(k * k, s), Linv(k * k, s);
-  trace_point(h, "rsvd:alloc X,B");
+  Scratch<double> X(q * k, s), B, Gm(k * k, s), Linv(k * k, s);
   sketch_normal(h, seed, q, k, X, k);   // svd.py:131-132
   trace_point(h, "rsvd:sketch");
-  op.apply(h, X, k, B);                 // svd.py:133
-  trace_point(h, "rsvd:B = M X");
-  // CholeskyQR: B^T B = L L^T, Q = B L^-T   (svd.py:134), and Z = inner^T B for Y^T = Z L^-T
-  // (svd.py:135: Y = Q^T inner).  B^T B = X^T (inner^T B) = X^T Z: for a tall inner (q < p / 2,
-  // the column update's [U Sigma | T]) the Gram comes from the q x k Z at 2 q k^2 flops instead of
-  // the p x k B at p k^2 -- at c5 that is 0.1 instead of 4 TFLOP.  The product of two different
-  // factors is symmetrised; its rounding (eps ||X|| ||Z||) is of the order of the direct Gram's.
+  // Z = inner^T B = inner^T inner X, with B = inner X (svd.py:133) and Y^T = Z L^-T (svd.py:135:
+  // Y = Q^T inner).  Two ways: through B (two passes of inner over k columns), or, for a tall
+  // inner with few columns, through the q x q Gram H = inner^T inner (gram_route.cu): Z = H X and
+  // B never exists.  Both are the same product; the cost model picks the cheaper.
   Scratch<double> Z(q * k, s);
-  const bool gram_from_z = 2 * q < p && getenv("FPI_RSVD_DIRECT_GRAM") == nullptr;
+  GramPlan gp;
+  SparseGramIn gin;
+  if (op.s_ptr && op.st_ptr && q > op.sd && 2 * q < p) {
+    gin = op.gram_in();
+    gp = plan_inner_gram(h, gin, k);
+  }
+  bool gram_from_z = gp.use;
+  if (gp.use) {
+    Scratch<double> H(q * q, s);
+    inner_gram(h, gin, gp, H, q);
+    trace_point(h, "rsvd:H = M^T M");
+    gemm(h, false, false, q, k, q, 1.0, H, q, X, k, 0.0, Z, k);
+    trace_point(h, "rsvd:Z = H X");
+  } else {
+    B.alloc(p * k, s);
+    op.apply(h, X, k, B);
+    trace_point(h, "rsvd:B = M X");
+    // CholeskyQR: B^T B = L L^T, Q = B L^-T  (svd.py:134).  B^T B = X^T (inner^T B) = X^T Z: for a
+    // tall inner (q < p / 2) the Gram comes from the q x k Z at 2 q k^2 flops instead of the p x k
+    // B at p k^2 -- at c5 that is 0.1 instead of 4 TFLOP.  The product of two different factors
+    // is symmetrised; its rounding (eps ||X|| ||Z||) is of the order of the direct Gram's.
+    gram_from_z = 2 * q < p && getenv("FPI_RSVD_DIRECT_GRAM") == nullptr;
+    if (gram_from_z) {
+      op.applyT(h, B, k, Z);
+      trace_point(h, "rsvd:Z = M^T B");
+    }
+  }
   if (gram_from_z) {
-    op.applyT(h, B, k, Z);
-    trace_point(h, "rsvd:Z = M^T B");
     gemm(h, true, false, k, k, q, 1.0, X, k, Z, k, 0.0, Gm, k);
     k_symmetrize<<<grid_for(k * k, 256, (unsigned)(h->num_sms * 16)), 256, 0, s>>>(k, Gm, k);
     FPI_LAUNCH_CHECK();
@@ -677,10 +752,19 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   }
   // SVD of Y (k x q) through its transpose Y^T = Z L^-T = Vy S Uy^T   (svd.py:135-136); for a tall
   // Y^T the product is left implicit (Gram L^-1 (Z^T Z) L^-T)
-  Scratch<double> Vy(q * rank, s), Uyt(rank * k, s);
   // implicit only when L is well conditioned: the Gram of Z carries cond(L)^2 more rounding than
   // the Gram of Y^T (the CholeskyQR sketches here measure cond 1.2 - 2.7)
-  if (q >= k && diag && diag->cond_estimate > 0.0 && diag->cond_estimate < 8.0) {
+  const bool implicit_ok = q >= k && diag && diag->cond_estimate > 0.0 && diag->cond_estimate < 8.0;
+  // right-side finish when one pass of inner^T over r columns undercuts the q x 2r x r product
+  if (implicit_ok && getenv("FPI_RSVD_LEFT_FINISH") == nullptr &&
+      op.apply_cost(rank) < 0.5 * 2.0 * (double)q * (double)k * (double)rank &&
+      rsvd_finish_right(h, op, rank, X, B.get(), Z, Linv, U, sigma, Vt, diag)) {
+    trace_point(h, "rsvd:right-side finish");
+    if (diag) diag->engine = 1;
+    return;
+  }
+  Scratch<double> Vy(q * rank, s), Uyt(rank * k, s);
+  if (implicit_ok) {
     dense_svd_tall(h, q, k, Z, k, rank, Vy, sigma, Uyt, diag, Linv);
   } else {
     Scratch<double> Yt(q * k, s);
@@ -700,7 +784,8 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
     canonical_signs_vt(h, rank, q, Vt, q, sgn);
     scale_cols(h, k, rank, Mx, rank, sgn, false);
   }
-  if (op.apply_cost(rank) + 2.0 * (double)q * (double)k * (double)rank < 2.0 * (double)p * (double)k * (double)rank) {
+  if (!B.get() ||
+      op.apply_cost(rank) + 2.0 * (double)q * (double)k * (double)rank < 2.0 * (double)p * (double)k * (double)rank) {
     // = inner (X L^-T U~): the thin q x r factor first, then one pass of the inner operator -- about
     // half the flops of the p x 2r x r product with B when inner is [U Sigma | T] with a tall U
     B.release();

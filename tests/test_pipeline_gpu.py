@@ -42,6 +42,20 @@ def _lowrank_rel(fa, fb):
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3r50", "c3r100", "c3r200"])
 def test_stagewise_parity(name):
+    _check_stagewise(name)
+
+
+@pytest.mark.parametrize("heavy", ["0", "16", "256"])
+@pytest.mark.parametrize("name", ["c2", "c3r50", "c3r100"])
+def test_stagewise_parity_gram_route(name, heavy, monkeypatch):
+    """The column update's Z = H X route (gram_route.cu) forced on the small randomized-column
+    configs, with no / some / all-qualifying heavy (densified) columns of T."""
+    monkeypatch.setenv("FPI_GRAM_ROUTE", "1")
+    monkeypatch.setenv("FPI_GRAM_HEAVY", heavy)
+    _check_stagewise(name)
+
+
+def _check_stagewise(name):
     p, res, st = _run(name)
     g = golden(name)
     w = p.workload
@@ -148,9 +162,13 @@ def _lowrank_rel_factored(fa, fb):
     return lowrank_rel_factored(fa.U, fa.sigma, fa.Vt, fb.U, fb.sigma, fb.Vt)
 
 
-def test_stagewise_parity_c4():
+@pytest.mark.parametrize("route", ["auto", "gram"])
+def test_stagewise_parity_c4(route, monkeypatch):
     """P3 at the benchmark size (c4, 200k x 50k): oracle row / column updates fed the GPU's own
-    upstream factors; the reorder sizes against the live oracle."""
+    upstream factors; the reorder sizes against the live oracle.  route=gram forces the column
+    update's Z = H X route (gram_route.cu), which the cost model leaves off at c4."""
+    if route == "gram":
+        monkeypatch.setenv("FPI_GRAM_ROUTE", "1")
     p, res, st = _run("c4")
     w = p.workload
     Ac = orc.canonical_csr(p.A)
