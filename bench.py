@@ -21,10 +21,11 @@ regression.py:50-70).  The metric is seconds per solve (lower is better).
 * ``--impl reference`` -- the reference's CPU path (the oracle port; the
   Python reference itself cannot travel to the GPU box) on the same workload.
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): the same problem is solved by all
-ranks together (strong scaling) -- reorder, block SVD and row update
-replicated, column update and apply row-sharded with NCCL all-reduces
-(paper_2011_04235_b200/sharded.py).
+Multi-GPU (torchrun, or `--gpus N` which spawns the ranks itself; one rank per
+GPU, NCCL inside the library): the same problem is solved by all ranks together
+(strong scaling) -- A11 blocks, U rows and Vt / Z columns owned per rank, NCCL
+reductions of the small Grams and projections (csrc/sharded.cu, SURVEY.md
+section 8(e)); the reorder and the 2r x 2r eigensolves are replicated.
 """
 
 from __future__ import annotations
@@ -230,8 +231,9 @@ def workload_config(p, world=1):
             "nnz_Y": int(p.Y.nnz), "rank": w.rank, "alpha": w.alpha, "k": w.k, "seed": w.seed,
             "l2_flush": "512MB write before every timed step",
             "parallelism": "1 GPU" if world == 1 else
-            f"{world} ranks: column update + apply row-sharded (NCCL all-reduce of the 2r x 2r Gram, "
-            "of M^T B and of U^T Y); reorder, block SVD, row update replicated"}
+            f"{world} ranks (csrc/sharded.cu): A11 blocks, U rows and Vt / Z columns owned per rank; "
+            "NCCL all-reduce of the k x k Grams, of the column update's M^T B and of U^T Y, ncclReduce of "
+            "the row update's inner^T B onto column owners; reorder and the small eigensolves replicated"}
 
 
 def _ncu_traffic():
@@ -264,16 +266,17 @@ def ours_arm(args):
     stats = {}
 
     if world > 1:
-        from paper_2011_04235_b200.sharded import Comm, apply_distributed, fastpi_distributed, fastpi_sharded
+        from paper_2011_04235_b200.sharded import Comm, apply_local, fastpi_distributed, fastpi_sharded
         comm = Comm()
+        comm.bind()
+        log(f"[bench] rank {rank}/{world}: communicator {comm.kind}")
 
     def step():
         if world > 1:
             res = fastpi_sharded(A_dev, cfg, comm, stats=stats)
-        else:
-            res = fastpi_device(A_dev, cfg, stats=stats)
-        Z = res.pseudoinverse.apply_device(Y_dev)
-        return res, Z
+            return res, res.pseudoinverse.apply_local(Y_dev)[1]   # this rank's rows of Z
+        res = fastpi_device(A_dev, cfg, stats=stats)
+        return res, res.pseudoinverse.apply_device(Y_dev)
 
     for i in range(args.warmup):
         t0 = time.perf_counter()
@@ -380,8 +383,10 @@ def ours_arm(args):
         d2h_bytes = 0
         def e2e_step():
             if world > 1:
+                # every rank uploads A and Y and copies ITS rows of Z back (the per-GPU copies run in
+                # parallel); the job's Z is the union of the ranks' slices
                 res = fastpi_distributed(p.A, cfg, comm)
-                return res, apply_distributed(res.pseudoinverse, p.Y), int(res.sigma.shape[0])
+                return res, apply_local(res.pseudoinverse, p.Y)[1], int(res.sigma.shape[0])
             res = fp.fastpi(p.A, cfg)
             return res, res.pseudoinverse.apply(p.Y), res.factors.rank
 

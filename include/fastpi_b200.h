@@ -158,15 +158,6 @@ int fpi_block_svd(fpi_handle h, int64_t m1, int64_t n1, const int64_t* a11_ptr, 
                   const double* a11_val, int64_t n_spans, const int64_t* d_spans, double alpha, double* d_sigma,
                   int64_t* u_ptr, int32_t* u_idx, double* u_val, int64_t* vt_ptr, int32_t* vt_idx, double* vt_val,
                   fpi_block_plan* h_plan);
-/* One rank's share of fpi_block_svd for a sharded solve (A11 blocks are independent
- * units): small blocks dealt round-robin (block b -> rank b % world), the large ones by LPT over
- * h w min(h, w); the structure (u_ptr/u_idx, vt_ptr/vt_idx) is complete on every rank and the
- * values of other ranks' blocks are zero, so summing sigma, u_val and vt_val over the ranks (one
- * all-reduce) gives fpi_block_svd's result.  Replaces svd.py:141-193's per-block loop. */
-int fpi_block_svd_shard(fpi_handle h, int64_t m1, int64_t n1, const int64_t* a11_ptr, const int32_t* a11_idx,
-                        const double* a11_val, int64_t n_spans, const int64_t* d_spans, double alpha,
-                        int64_t shard_rank, int64_t shard_world, double* d_sigma, int64_t* u_ptr, int32_t* u_idx,
-                        double* u_val, int64_t* vt_ptr, int32_t* vt_idx, double* vt_val, fpi_block_plan* h_plan);
 /* svd.py:86-117 dense_svd + truncate: rank leading triplets of a dense p x q matrix (sorted). */
 int fpi_dense_svd(fpi_handle h, int64_t p, int64_t q, const double* d_M, int64_t ldm, int64_t rank,
                   double* d_U, double* d_sigma, double* d_Vt);
@@ -318,6 +309,64 @@ int fpi_timing_enable(fpi_handle h, int on);
 int fpi_timing_report(fpi_handle h, char* h_buf, int64_t cap, int reset);
 /* FP64 tensor-pipe (DMMA) issue-rate peak of this GPU, TFLOP/s. */
 int fpi_dmma_peak(fpi_handle h, double* h_tflops);
+
+/* ---- sharded solve over several GPUs; csrc/comm.cu, csrc/sharded.cu --------------
+ * One process (and handle) per GPU.  The handle owns the communicator; the exchanges are
+ * stream-ordered NCCL calls (NVLink / NVSwitch) on the handle's stream. */
+/* Exchange callback (host): op 0 all-reduce sum in place (send == recv), 1 all-reduce max,
+ * 2 all-gather (recv holds world * count), 3 reduce to root.  Device pointers; the library has
+ * synchronised its stream; return 0 once recv is written. */
+typedef int (*fpi_comm_fn)(void* user, int op, const void* d_send, void* d_recv, int64_t count, int root);
+/* A fresh NCCL unique id (128 bytes) for rank 0 to share with the other ranks out of band. */
+int fpi_comm_nccl_id(char* h_out128, char* h_err, int64_t err_cap);
+/* NCCL communicator of `world` ranks on this handle (libnccl.so.2 loaded at run time). */
+int fpi_comm_init_nccl(fpi_handle h, const char* h_id128, int rank, int world);
+/* Host-callback communicator (e.g. torch.distributed over gloo: several ranks on one GPU). */
+int fpi_comm_init_callback(fpi_handle h, int rank, int world, fpi_comm_fn fn, void* user);
+/* World of one (every exchange is the identity). */
+int fpi_comm_init_self(fpi_handle h);
+int fpi_comm_free(fpi_handle h);
+int fpi_comm_info(fpi_handle h, int* h_rank, int* h_world);
+/* In-place sum of n doubles over the ranks. */
+int fpi_comm_allreduce(fpi_handle h, double* d_buf, int64_t n);
+/* Ownership table h_out[world][10]: b_lo, b_hi (A11 block range), r_lo, r_hi (spoke rows), c_lo,
+ * c_hi (spoke columns), h_lo, h_hi (hub rows within [0, m2)), hc_lo, hc_hi (hub columns within
+ * [0, n2)); block ranges balanced by rows' work (8 + T row nnz), columns and h w min(h, w). */
+int fpi_shard_plan(fpi_handle h, int64_t m, int64_t m1, int64_t n1, int64_t n2, int64_t n_spans,
+                   const int64_t* d_spans, const int64_t* d_t_ptr, int world, int64_t* h_out);
+/* svd.py:141-193 for the blocks [b_lo, b_hi) only (structure complete, other values zero);
+ * h_keep_range[2] = the kept-rank range [k_lo, k_hi) of those blocks. */
+int fpi_block_svd_range(fpi_handle h, int64_t m1, int64_t n1, const int64_t* a11_ptr, const int32_t* a11_idx,
+                        const double* a11_val, int64_t n_spans, const int64_t* d_spans, double alpha, int64_t b_lo,
+                        int64_t b_hi, double* d_sigma, int64_t* u_ptr, int32_t* u_idx, double* u_val,
+                        int64_t* vt_ptr, int32_t* vt_idx, double* vt_val, fpi_block_plan* h_plan,
+                        int64_t* h_keep_range);
+/* pinv.py:131-171 on this rank's rows of [Sigma Vt11 ; A21] (kept rows [k_lo, k_lo + k_loc), U11 rows
+ * [r_lo, r_lo + r_rows), A21 rows [h_lo, h_lo + m2_loc); global CSRs).  Z = inner^T B is reduced onto
+ * the owners of the column ranges h_zoff[world + 1].  Out: U_loc ((r_rows + m2_loc) x s), sigma (s),
+ * Vt_loc (s x own columns).  Randomized engine only. */
+int fpi_row_update_shard(fpi_handle h, int64_t n1, const double* d_sigma11, const int64_t* vt_ptr,
+                         const int32_t* vt_idx, const double* vt_val, int64_t k_lo, int64_t k_loc,
+                         const int64_t* u_ptr, const int32_t* u_idx, const double* u_val, int64_t r_lo, int64_t r_rows,
+                         const int64_t* a_ptr, const int32_t* a_idx, const double* a_val, int64_t h_lo,
+                         int64_t m2_loc, int64_t p_global, int64_t s_rank, double thr, int64_t seed,
+                         const int64_t* h_zoff, double* d_U, double* d_sigma, double* d_Vt);
+/* pinv.py:174-208 on this rank's m_loc rows of [U Sigma | T] (T_loc and its transpose), its columns
+ * of the previous Vt (s_prev x nc_loc) and its hub columns [hc_lo, hc_hi).  Out: U (m_loc x r),
+ * sigma (r), Vt_loc (r x (nc_loc + hc_hi - hc_lo)).  Randomized engine only. */
+int fpi_column_update_shard(fpi_handle h, int64_t m_loc, int64_t s_prev, const double* d_U_prev,
+                            const double* d_sigma_prev, const double* d_Vt_prev, int64_t nc_loc, int64_t n2,
+                            const int64_t* t_ptr, const int32_t* t_idx, const double* t_val, const int64_t* tt_ptr,
+                            const int32_t* tt_idx, const double* tt_val, int64_t m_global, int64_t hc_lo,
+                            int64_t hc_hi, int64_t r, double thr, int64_t seed, double* d_U, double* d_sigma,
+                            double* d_Vt);
+/* pinv.py:72-81 on this rank: W = sum over ranks of Y_i^T U_loc (all-reduce), then the rows of Z of
+ * its columns, Z_loc (n_loc x L) = Vt_loc^T diag(sigma+) W^T.  Its rows are [r_lo, r_hi) then
+ * [m1 + h_lo, m1 + h_hi) in reordered coordinates. */
+int fpi_pinv_apply_shard(fpi_handle h, int64_t m, int64_t m1, int64_t r_lo, int64_t r_hi, int64_t h_lo,
+                         int64_t h_hi, int64_t r, const double* d_U_loc, const double* d_sdag, const double* d_Vt_loc,
+                         int64_t n_loc, const int64_t* d_row_fwd, int64_t L, int64_t nnz, const int64_t* y_ptr,
+                         const int32_t* y_idx, const double* y_val, double* d_Z_loc);
 
 #ifdef __cplusplus
 }

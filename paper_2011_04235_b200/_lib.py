@@ -59,6 +59,9 @@ class SvdDiag(C.Structure):
                 ("eig_sweeps", i32 * 4), ("null_completed", i32)]
 
 
+# exchange callback of a sharded solve (fpi_comm_fn): (user, op, send, recv, count, root) -> status
+COMM_FN = C.CFUNCTYPE(C.c_int, vp, C.c_int, vp, vp, i64, C.c_int)
+
 # name -> (restype, argtypes); mirrors include/fastpi_b200.h
 SIGNATURES = {
     "fpi_abi_version": (C.c_int, []),
@@ -86,8 +89,6 @@ SIGNATURES = {
     "fpi_block_svd_plan": (C.c_int, [vp, i64, vp, f64, C.POINTER(BlockPlan)]),
     "fpi_block_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, f64, vp, vp, vp, vp, vp, vp, vp,
                                 C.POINTER(BlockPlan)]),
-    "fpi_block_svd_shard": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, f64, i64, i64, vp, vp, vp, vp, vp, vp,
-                                      vp, C.POINTER(BlockPlan)]),
     "fpi_dense_svd": (C.c_int, [vp, i64, i64, vp, i64, i64, vp, vp, vp]),
     "fpi_randomized_svd": (C.c_int, [vp, i64, i64, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp, vp]),
     "fpi_dataset_parse": (C.c_int, [C.c_char_p, i64, C.POINTER(vp), C.POINTER(DatasetInfo)]),
@@ -116,6 +117,23 @@ SIGNATURES = {
     "fpi_timing_enable": (C.c_int, [vp, C.c_int]),
     "fpi_timing_report": (C.c_int, [vp, C.c_char_p, i64, C.c_int]),
     "fpi_dmma_peak": (C.c_int, [vp, C.POINTER(f64)]),
+    # sharded solve (csrc/comm.cu, csrc/sharded.cu)
+    "fpi_comm_nccl_id": (C.c_int, [C.c_char_p, C.c_char_p, i64]),
+    "fpi_comm_init_nccl": (C.c_int, [vp, C.c_char_p, C.c_int, C.c_int]),
+    "fpi_comm_init_callback": (C.c_int, [vp, C.c_int, C.c_int, COMM_FN, vp]),
+    "fpi_comm_init_self": (C.c_int, [vp]),
+    "fpi_comm_free": (C.c_int, [vp]),
+    "fpi_comm_info": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "fpi_comm_allreduce": (C.c_int, [vp, vp, i64]),
+    "fpi_shard_plan": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, vp, C.c_int, vp]),
+    "fpi_block_svd_range": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, vp, f64, i64, i64, vp, vp, vp, vp, vp, vp, vp,
+                                      C.POINTER(BlockPlan), C.POINTER(i64)]),
+    "fpi_row_update_shard": (C.c_int, [vp, i64, vp, vp, vp, vp, i64, i64, vp, vp, vp, i64, i64, vp, vp, vp, i64, i64,
+                                       i64, i64, f64, i64, vp, vp, vp, vp]),
+    "fpi_column_update_shard": (C.c_int, [vp, i64, i64, vp, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, i64, i64, i64,
+                                          i64, f64, i64, vp, vp, vp]),
+    "fpi_pinv_apply_shard": (C.c_int, [vp, i64, i64, i64, i64, i64, i64, i64, vp, vp, vp, i64, vp, i64, i64, vp, vp,
+                                       vp, vp]),
 }
 
 _lib = None

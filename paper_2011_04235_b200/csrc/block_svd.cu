@@ -291,17 +291,14 @@ struct IsFlag {
   int64_t want;
   __device__ bool operator()(int64_t b) const { return flag[b] == want; }
 };
-// non-degenerate block of size class cls owned by this rank (blocks are dealt round-robin over the
-// ranks of a sharded solve; world = 1 owns everything) and inside the owned block range [lo, hi)
+// non-degenerate block of size class cls inside the owned block range [lo, hi) (a sharded solve's
+// rank owns a contiguous range of blocks, sharded.cu; one rank owns them all)
 struct IsNonDeg {
   const int64_t* keep;
   const int64_t* large;
   int64_t cls;
-  int64_t rank, world;
   int64_t lo, hi;
-  __device__ bool operator()(int64_t b) const {
-    return keep[b] > 0 && large[b] == cls && b % world == rank && b >= lo && b < hi;
-  }
+  __device__ bool operator()(int64_t b) const { return keep[b] > 0 && large[b] == cls && b >= lo && b < hi; }
 };
 
 __global__ void k_iota64(int64_t* a, int64_t n) {
@@ -397,8 +394,7 @@ static void plan(fpi_context* h, int64_t nspans, const int64_t* spans, double al
 void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, const int32_t* a_idx,
                const double* a_val, int64_t nspans, const int64_t* spans, double alpha, double* sigma,
                int64_t* u_ptr, int32_t* u_idx, double* u_val, int64_t* vt_ptr, int32_t* vt_idx, double* vt_val,
-               fpi_block_plan* out_plan, int64_t shard_rank, int64_t shard_world, int64_t b_lo, int64_t b_hi,
-               int64_t* keep_range) {
+               fpi_block_plan* out_plan, int64_t b_lo, int64_t b_hi, int64_t* keep_range) {
   FPI_REQUIRE(alpha > 0.0 && alpha <= 1.0, FPI_EDOMAIN, "target rank ratio alpha must be in (0, 1]");
   cudaStream_t s = h->stream;
   BlockSvdState st;
@@ -430,11 +426,11 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
   Scratch<int> cnt(3, s);
   k_iota64<<<grid_for(nspans, T, G), T, 0, s>>>(ids, nspans);
   select_if(tmp, ids.get(), small.get(), cnt.get(), nspans,
-            IsNonDeg{st.keep.get(), st.large.get(), 0, shard_rank, shard_world, b_lo, b_hi}, s);
+            IsNonDeg{st.keep.get(), st.large.get(), 0, b_lo, b_hi}, s);
   select_if(tmp, ids.get(), mid.get(), cnt.get() + 1, nspans,
-            IsNonDeg{st.keep.get(), st.large.get(), 2, shard_rank, shard_world, b_lo, b_hi}, s);
+            IsNonDeg{st.keep.get(), st.large.get(), 2, b_lo, b_hi}, s);
   select_if(tmp, ids.get(), large.get(), cnt.get() + 2, nspans, IsFlag{st.large.get(), 1}, s);
-  const bool partial = shard_world > 1 || b_lo > 0 || b_hi < nspans;
+  const bool partial = b_lo > 0 || b_hi < nspans;
   if (keep_range) {
     // keep offsets [k_lo, k_hi) of the owned block range (rank_off is the exclusive keep prefix)
     keep_range[0] = b_lo >= nspans ? st.rank11 : (b_lo <= 0 ? 0 : host_read(st.rank_off.get() + b_lo, s));
@@ -496,32 +492,6 @@ void block_svd(fpi_context* h, int64_t m1, int64_t n1, const int64_t* a_ptr, con
         for (int f = 0; f < 8; ++f) kept.push_back(meta[8 * i + f]);
     meta.swap(kept);
     st.n_large = (int64_t)(meta.size() / 8);
-  }
-  if (st.n_large && shard_world > 1) {
-    // sharded solve: the (few, expensive) large blocks by LPT over their cost h w min(h, w), in
-    // block order with ties to the lowest rank -- the same deal on every rank; keep this rank's
-    std::vector<int64_t> order(st.n_large);
-    for (int64_t i = 0; i < st.n_large; ++i) order[i] = i;
-    auto cost = [&](int64_t i) {
-      const int64_t hh = meta[8 * i + 1], ww = meta[8 * i + 3];
-      return (double)hh * (double)ww * (double)(hh < ww ? hh : ww);
-    };
-    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return cost(a) > cost(b); });
-    std::vector<double> load(shard_world, 0.0);
-    std::vector<int64_t> mine;
-    for (int64_t i : order) {
-      int64_t best = 0;
-      for (int64_t r = 1; r < shard_world; ++r)
-        if (load[r] < load[best]) best = r;
-      load[best] += cost(i);
-      if (best == shard_rank) mine.push_back(i);
-    }
-    std::sort(mine.begin(), mine.end());
-    std::vector<int64_t> kept(8 * mine.size());
-    for (size_t j = 0; j < mine.size(); ++j)
-      for (int f = 0; f < 8; ++f) kept[8 * j + f] = meta[8 * mine[j] + f];
-    meta.swap(kept);
-    st.n_large = (int64_t)mine.size();
   }
   if (st.n_large) {
     // meta row i: rs, hh, cs, ww, keep, rank_off, u_off, v_off of the i-th large block
@@ -609,19 +579,7 @@ extern "C" int fpi_block_svd(fpi_handle h, int64_t m1, int64_t n1, const int64_t
                              int32_t* vt_idx, double* vt_val, fpi_block_plan* h_plan) {
   FPI_API_BEGIN(h)
   fpi::block_svd(h, m1, n1, a11_ptr, a11_idx, a11_val, n_spans, d_spans, alpha, d_sigma, u_ptr, u_idx, u_val,
-                 vt_ptr, vt_idx, vt_val, h_plan, 0, 1, 0, n_spans, nullptr);
-  FPI_API_END(h)
-}
-
-extern "C" int fpi_block_svd_shard(fpi_handle h, int64_t m1, int64_t n1, const int64_t* a11_ptr,
-                                   const int32_t* a11_idx, const double* a11_val, int64_t n_spans,
-                                   const int64_t* d_spans, double alpha, int64_t shard_rank, int64_t shard_world,
-                                   double* d_sigma, int64_t* u_ptr, int32_t* u_idx, double* u_val, int64_t* vt_ptr,
-                                   int32_t* vt_idx, double* vt_val, fpi_block_plan* h_plan) {
-  FPI_API_BEGIN(h)
-  FPI_REQUIRE(shard_world >= 1 && shard_rank >= 0 && shard_rank < shard_world, FPI_EDOMAIN, "bad shard rank / world");
-  fpi::block_svd(h, m1, n1, a11_ptr, a11_idx, a11_val, n_spans, d_spans, alpha, d_sigma, u_ptr, u_idx, u_val,
-                 vt_ptr, vt_idx, vt_val, h_plan, shard_rank, shard_world, 0, n_spans, nullptr);
+                 vt_ptr, vt_idx, vt_val, h_plan, 0, n_spans, nullptr);
   FPI_API_END(h)
 }
 
@@ -633,6 +591,6 @@ extern "C" int fpi_block_svd_range(fpi_handle h, int64_t m1, int64_t n1, const i
   FPI_API_BEGIN(h)
   FPI_REQUIRE(0 <= b_lo && b_lo <= b_hi && b_hi <= n_spans, FPI_EDOMAIN, "bad block range");
   fpi::block_svd(h, m1, n1, a11_ptr, a11_idx, a11_val, n_spans, d_spans, alpha, d_sigma, u_ptr, u_idx, u_val,
-                 vt_ptr, vt_idx, vt_val, h_plan, 0, 1, b_lo, b_hi, h_keep_range);
+                 vt_ptr, vt_idx, vt_val, h_plan, b_lo, b_hi, h_keep_range);
   FPI_API_END(h)
 }

@@ -77,11 +77,8 @@ struct NcclComm final : Comm {
   void group_end() override { FPI_NCCL(nccl().group_end()); }
 };
 
-// op: 0 all-reduce sum (in place, send == recv), 1 all-reduce max, 2 all-gather, 3 reduce to root.
-// Device pointers; the library has synchronised its stream before the call and the callback must
-// have completed the exchange (device memory written) when it returns 0.
-typedef int (*fpi_comm_fn)(void* user, int op, const void* send, void* recv, int64_t count, int root);
-
+// fpi_comm_fn (fastpi_b200.h): op 0 all-reduce sum (in place), 1 all-reduce max, 2 all-gather,
+// 3 reduce to root; the library has synchronised its stream before the call.
 struct CallbackComm final : Comm {
   fpi_comm_fn fn = nullptr;
   void* user = nullptr;
@@ -156,7 +153,7 @@ int fpi_comm_init_nccl(fpi_handle h, const char* h_id128, int rank, int world) {
   FPI_API_END(h)
 }
 
-int fpi_comm_init_callback(fpi_handle h, int rank, int world, fpi::fpi_comm_fn fn, void* user) {
+int fpi_comm_init_callback(fpi_handle h, int rank, int world, fpi_comm_fn fn, void* user) {
   FPI_API_BEGIN(h)
   FPI_REQUIRE(world >= 1 && rank >= 0 && rank < world && fn, FPI_EDOMAIN, "bad rank / world / callback");
   fpi::comm_free(h);

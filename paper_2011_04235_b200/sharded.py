@@ -1,36 +1,49 @@
-"""Multi-GPU FastPI: one process per GPU, torch.distributed (NCCL over NVLink /
-NVSwitch) for the exchanges.
+"""Multi-GPU FastPI: one process per GPU; the exchanges run inside the library
+(csrc/sharded.cu) on the handle's communicator (csrc/comm.cu: NCCL over
+NVLink / NVSwitch, loaded from the libnccl.so.2 torch ships).
+section 8(e).
 
-What shards and what is replicated:
+Ownership (``fpi_shard_plan``): rank i owns a contiguous range of the A11
+diagonal blocks (balanced by the rows' work, the blocks' columns and their
+h w min(h, w) SVD cost) -- hence spoke rows [r_lo, r_hi) and spoke columns
+[c_lo, c_hi) -- plus a chunk [h_lo, h_hi) of the m2 hub rows and a chunk
+[hc_lo, hc_hi) of the n2 hub columns.  Its rows of U, T, A21, Y are its spoke
+rows then its hub rows; its columns of Vt and its rows of Z are its spoke
+columns then its hub columns.
 
-* reorder, partition, row update: replicated.  Every rank holds A and computes
-  them itself (deterministic kernels, so the ranks agree bit for bit).
-* block SVD (svd.py:141-193): the diagonal blocks are independent units -- each
-  rank factors its share (round-robin for the many small blocks, LPT by
-  h w min(h, w) for the large ones, fpi_block_svd_shard) and one all-reduce of
-  sigma / U11 / Vt11 values (disjoint supports, so the sum is the union)
-  gives every rank the full block factors for the replicated row update.
-* column update (pinv.py:174-208, the FP64 GEMM-bound stage): the m rows of
-  [U Sigma | T] are split into contiguous shards.  Every rank regenerates the
-  full sketch X (svd.py:131-132), forms its B_i = M_i X, and the two
-  reductions of the randomized SVD are all-reduces:
-      G = sum_i B_i^T B_i          (2r x 2r,  svd.py:134's QR Gram)
-      Z = sum_i M_i^T B_i          ((s+n2) x 2r, svd.py:135's Q^T M)
-  The small SVD of Y^T = Z L^-T is replicated; U_i = B_i L^-T U~ stays local.
-  The dense engine (small problems) runs replicated and keeps its row shard.
-* apply (pinv.py:72-81): W = sum_i Y_i^T U_i is all-reduced (L x r); the lift
-  Z = V Sigma+ W^T is replicated.
+=============================  ==================================================================
+stage (reference)              what each rank does / what is exchanged
+=============================  ==================================================================
+reorder, partition             replicated (deterministic kernels: identical on every rank)
+block SVD (svd.py:141-193)     its own blocks only (``fpi_block_svd_range``); nothing exchanged
+row update (pinv.py:131-171)   rows of inner = its kept Sigma Vt11 rows + its A21 rows;
+                               G = sum B_i^T B_i (all-reduce 2s x 2s); Z = inner^T B reduced onto
+                               the owner of each spoke-column range (one ncclReduce per rank, the
+                               reduce-scatter of Y); Gram of Y^T all-reduced; eigensolve
+                               replicated; U rows and Vt columns local
+column update (pinv.py:174-   rows of [U Sigma | T]; Z = sum M_i^T B_i (all-reduce (s+n2) x 2r);
+208)                           G = X^T Z split over the ranks (all-reduce); small SVD replicated;
+                               U rows local; Vt columns = [Vt~[:, :s] Vt_prev_loc | own hub cols]
+apply (pinv.py:72-81)          W = sum Y_i^T U_i (all-reduce L x r); each rank the rows of Z of its
+                               own columns (its V-row slice); gathered at the host boundary
+=============================  ==================================================================
 
-The algorithm is written against two small interfaces -- ``ops`` (the
-library's kernels on device tensors, ``GpuOps``) and ``comm`` (the
-all-reduce) -- so the same code runs with world size 1, with N GPUs over
-NCCL, and in the CPU tests with a numpy stand-in for ``ops`` over gloo.
+Small problems whose updates take the dense engine run the single-GPU
+pipeline on every rank and keep their slices (the sharded engines are the
+randomized ones; the dense path is for inner matrices below the 1e8-entry
+guard).
+
+``FPI_COMM=callback`` (or a non-NCCL torch.distributed backend) routes the
+exchanges through a host callback over torch.distributed -- the functional
+test of the pattern with several ranks on one GPU.
 """
 
 from __future__ import annotations
 
 import ctypes as C
 import math
+import os
+import traceback
 import warnings
 from dataclasses import dataclass
 
@@ -38,14 +51,29 @@ import numpy as np
 
 from . import _lib
 from ._device import DeviceCSR, d2h, empty, torch
-from .pinv import (FastpiConfig, StageTime, _assemble, _Timer, column_update_device, row_update_device)
+from .pinv import FastpiConfig, StageTime, _Timer, fastpi_device
 from .reorder import partition_original, reorder_device
-from .svd import block_diagonal_svd_device
+
+PLAN_FIELDS = ("b_lo", "b_hi", "r_lo", "r_hi", "c_lo", "c_hi", "h_lo", "h_hi", "hc_lo", "hc_hi")
 
 
 # ---------------------------------------------------------------- communication
+class _DeviceView:
+    """A raw device buffer as a torch tensor (CUDA array interface), for the callback exchanges."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr or 0), False),
+                                         "version": 3}
+
+
+def _view(ptr, n):
+    return torch().as_tensor(_DeviceView(ptr, n), device="cuda")
+
+
 class Comm:
-    """Rank / world of the current torch.distributed group (world 1 when not initialised)."""
+    """Rank / world of the current torch.distributed group, and the binding of the library
+    handle's communicator: native NCCL when the group's backend is NCCL, a torch.distributed
+    callback otherwise (world 1: the identity)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -53,25 +81,85 @@ class Comm:
         self.group = group
         self.world = self._dist.get_world_size(group) if self._dist else 1
         self.rank = self._dist.get_rank(group) if self._dist else 0
+        self.backend = self._dist.get_backend(group) if self._dist else "none"
+        self._cb = None
+        self._bound = set()
+        self.kind = None
 
-    def all_reduce_(self, t):
-        """In-place sum over ranks (NCCL for device tensors, gloo for host tensors)."""
-        if self.world > 1:
-            self._dist.all_reduce(t, group=self.group)
-        return t
+    def bind(self):
+        """Attach a communicator to this thread's library handle on the current device (once)."""
+        h = _lib.handle()
+        if h.value in self._bound:
+            return
+        lib = _lib.load()
+        if self.world == 1:
+            rc = lib.fpi_comm_init_self(h)
+            self.kind = "self"
+        elif self.backend == "nccl" and os.environ.get("FPI_COMM", "nccl") != "callback":
+            uid = C.create_string_buffer(128)
+            if self.rank == 0:
+                err = C.create_string_buffer(256)
+                if lib.fpi_comm_nccl_id(uid, err, len(err)) != _lib.FPI_OK:
+                    raise RuntimeError(f"NCCL unavailable: {err.value.decode()}")
+            obj = [bytes(uid.raw)]
+            self._dist.broadcast_object_list(obj, src=0, group=self.group)
+            rc = lib.fpi_comm_init_nccl(h, obj[0], self.rank, self.world)
+            self.kind = "nccl"
+        else:
+            self._cb = _lib.COMM_FN(self._callback)
+            rc = lib.fpi_comm_init_callback(h, self.rank, self.world, self._cb, None)
+            self.kind = "callback"
+        if rc != _lib.FPI_OK:
+            raise RuntimeError(f"communicator setup failed: {lib.fpi_last_error(h).decode()}")
+        self._bound.add(h.value)
+
+    def _callback(self, user, op, send, recv, count, root):
+        """Exchanges staged through host memory (gloo); device pointers in, device memory out."""
+        try:
+            t = torch()
+            d = self._dist
+            if op in (0, 1):
+                buf = _view(recv, count)
+                hb = buf.cpu()
+                d.all_reduce(hb, op=d.ReduceOp.SUM if op == 0 else d.ReduceOp.MAX, group=self.group)
+                buf.copy_(hb)
+            elif op == 2:
+                hs = _view(send, count).cpu()
+                parts = [t.empty_like(hs) for _ in range(self.world)]
+                d.all_gather(parts, hs, group=self.group)
+                _view(recv, count * self.world).copy_(t.cat(parts))
+            elif op == 3:
+                hs = _view(send, count).cpu().clone()
+                d.reduce(hs, dst=root, group=self.group)
+                if self.rank == root:
+                    _view(recv, count).copy_(hs)
+            else:
+                return 1
+            t.cuda.synchronize()
+            return 0
+        except Exception:  # pragma: no cover - reported through the status code
+            traceback.print_exc()
+            return 1
+
+    def all_gather_object(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self._dist.all_gather_object(out, obj, group=self.group)
+        return out
 
     def max(self, x: float) -> float:
         if self.world == 1:
             return x
-        import torch as T
-        dev = "cuda" if self._dist.get_backend(self.group) == "nccl" else "cpu"
-        t = T.tensor([x], dtype=T.float64, device=dev)
-        self._dist.all_reduce(t, op=self._dist.ReduceOp.MAX, group=self.group)
-        return float(t.item())
+        t = torch()
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        v = t.tensor([x], dtype=t.float64, device=dev)
+        self._dist.all_reduce(v, op=self._dist.ReduceOp.MAX, group=self.group)
+        return float(v.item())
 
 
 def shard_bounds(m: int, world: int) -> list[tuple[int, int]]:
-    """Contiguous, balanced row ranges (the first m % world shards get one extra row)."""
+    """Contiguous, balanced ranges (the first m % world get one extra)."""
     base, extra = divmod(m, world)
     out, r0 = [], 0
     for i in range(world):
@@ -81,172 +169,74 @@ def shard_bounds(m: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
-# ---------------------------------------------------------------- kernels on the device
-class GpuOps:
-    """The library's sm_100a kernels on torch device tensors (row-major float64)."""
-
-    def empty(self, shape):
-        return empty(shape)
-
-    def zeros(self, shape):
-        t = empty(shape)
-        t.zero_()
-        return t
-
-    def sketch(self, seed, rows, cols):
-        X = empty((rows, cols))
-        if rows and cols:
-            _lib.call("fpi_sketch_normal", int(seed), rows, cols, _lib.ptr(X), cols)
-        return X
-
-    def gemm(self, A, B, ta=False, tb=False, out=None, beta=0.0):
-        M = A.shape[1] if ta else A.shape[0]
-        K = A.shape[0] if ta else A.shape[1]
-        N = B.shape[0] if tb else B.shape[1]
-        C_ = out if out is not None else empty((M, N))
-        _lib.call("fpi_gemm", int(ta), int(tb), M, N, K, 1.0, _lib.ptr(A), A.shape[1], _lib.ptr(B), B.shape[1],
-                  float(beta), _lib.ptr(C_), N)
-        return C_
-
-    def gram(self, B):
-        """B^T B for a p x k row shard (symmetric product)."""
-        p, k = B.shape
-        G = empty((k, k))
-        _lib.call("fpi_gram", 1, k, p, _lib.ptr(B), k, _lib.ptr(G), k)
-        return G
-
-    def spmm(self, A: DeviceCSR, X, out, beta=0.0):
-        p, q = A.shape
-        k = X.shape[1]
-        if p and k:
-            if A.nnz == 0 or q == 0:
-                if beta == 0.0:
-                    out.zero_()
-            else:
-                _lib.call("fpi_spmm", p, q, k, _lib.ptr(A.indptr), _lib.ptr(A.indices), _lib.ptr(A.values), 1.0,
-                          _lib.ptr(X), k, float(beta), _lib.ptr(out), k)
-        return out
-
-    def scale_rows(self, A, s):
-        _lib.call("fpi_scale_rows", A.shape[0], A.shape[1], _lib.ptr(A), A.shape[1], _lib.ptr(s))
-        return A
-
-    def orth_factor(self, G):
-        k = G.shape[0]
-        Linv = empty((k, k))
-        cond = C.c_double(0.0)
-        _lib.call("fpi_orth_factor", k, _lib.ptr(G), _lib.ptr(Linv), C.byref(cond))
-        return Linv
-
-    def dense_svd(self, M, rank):
-        p, q = M.shape
-        U, s, Vt = empty((p, rank)), empty(rank), empty((rank, q))
-        _lib.call("fpi_dense_svd", p, q, _lib.ptr(M), q, int(rank), _lib.ptr(U), _lib.ptr(s), _lib.ptr(Vt))
-        return U, s, Vt
-
-    def transpose(self, A):
-        At = empty((A.shape[1], A.shape[0]))
-        _lib.call("fpi_transpose", A.shape[0], A.shape[1], _lib.ptr(A), A.shape[1], _lib.ptr(At), A.shape[0])
-        return At
-
-    def canonical_signs(self, U, Vt):
-        r, q = Vt.shape
-        _lib.call("fpi_canonical_signs", r, U.shape[0], q, _lib.ptr(U), U.shape[1], _lib.ptr(Vt), q)
-
-    def slice_rows(self, A, r0, r1):
-        return A[r0:r1]
-
-    def csr_rows(self, A: DeviceCSR, r0, r1):
-        return A.row_slice(r0, r1)
-
-    def csr_transpose(self, A: DeviceCSR):
-        return A.transpose()
-
-    def copy(self, A):
-        return A.clone()
-
-    def hstack_lift(self, Vt, Vt_prev, s, n1, n2):
-        """[Vt[:, :s] Vt_prev | Vt[:, s:]] (pinv.py:205-207)."""
-        r = Vt.shape[0]
-        out = empty((r, n1 + n2))
-        if n1:
-            if s:
-                _lib.call("fpi_gemm", 0, 0, r, n1, s, 1.0, _lib.ptr(Vt), Vt.shape[1], _lib.ptr(Vt_prev), n1, 0.0,
-                          _lib.ptr(out), n1 + n2)
-            else:
-                out[:, :n1].zero_()
-        if n2:
-            out[:, n1:].copy_(Vt[:, s:])
-        return out
+def shard_plan(ordering, T: DeviceCSR, world: int) -> np.ndarray:
+    """(world, 10) int64 ownership table, columns PLAN_FIELDS (fpi_shard_plan)."""
+    m, n2 = T.shape
+    out = np.zeros((world, len(PLAN_FIELDS)), np.int64)
+    spans = ordering.spans_device()
+    _lib.call("fpi_shard_plan", m, ordering.n_spoke_rows, ordering.n_spoke_cols, n2, int(spans.numel() // 4),
+              _lib.ptr(spans), _lib.ptr(T.indptr), int(world), out.ctypes.data_as(C.c_void_p))
+    return out
 
 
-# ---------------------------------------------------------------- column update (row-sharded)
-def column_update_shard(ops, comm, U_i, sigma, Vt_prev, T_i, Tt_i, m: int, r: int, seed: int):
-    """Randomized engine of pinv.py:174-208 on the row shard M_i = [U_i diag(sigma) | T_i].
-
-    Returns (U_out_i, sigma_out, Vt_out) with Vt_out the lifted r x (n1 + n2) factor, identical
-    on every rank.  Mirrors svd_engine.cu's randomized_svd step by step (svd.py:120-138)."""
-    s = int(sigma.shape[0])
-    n1 = int(Vt_prev.shape[1])
-    n2 = int(T_i.shape[1])
-    q = s + n2
-    k = 2 * r
-    m_i = int(T_i.shape[0])
-    X = ops.sketch(seed, q, k)                              # svd.py:131-132 (same on every rank)
-    B = ops.zeros((m_i, k))
-    if s:
-        X1 = ops.copy(X[:s])
-        ops.scale_rows(X1, sigma)                           # diag(sigma) X1
-        ops.gemm(U_i, X1, out=B)
-    if n2:
-        ops.spmm(T_i, X[s:], out=B, beta=1.0 if s else 0.0)  # + T_i X2      (svd.py:133)
-    G = comm.all_reduce_(ops.gram(B))                       # B^T B        (svd.py:134)
-    Linv = ops.orth_factor(G)
-    Z = ops.zeros((q, k))                                   # M^T B
-    if s:
-        ops.gemm(U_i, B, ta=True, out=Z[:s])
-        ops.scale_rows(Z[:s], sigma)
-    if n2:
-        ops.spmm(Tt_i, B, out=Z[s:])
-    comm.all_reduce_(Z)
-    Yt = ops.gemm(Z, Linv, tb=True)                         # Y^T = Z L^-T (svd.py:135)
-    Vy, sig, Uyt = ops.dense_svd(Yt, r)                     # svd.py:136
-    Vt = ops.transpose(Vy)
-    Mx = ops.gemm(Linv, Uyt, ta=True, tb=True)              # L^-T U~
-    U_out = ops.gemm(B, Mx)                                 # svd.py:137, local rows
-    ops.canonical_signs(U_out, Vt)                          # sign from Vt: same on every rank
-    return U_out, sig, ops.hstack_lift(Vt, Vt_prev, s, n1, n2)
+def _rows_of(A: DeviceCSR, ranges) -> DeviceCSR:
+    """The rows of several [a, b) ranges of a CSR, stacked in order."""
+    t = torch()
+    parts = [A.row_slice(a, b) for a, b in ranges if b > a]
+    rows = sum(b - a for a, b in ranges)
+    if not parts:
+        return DeviceCSR((0, A.shape[1]), t.zeros(1, dtype=t.int64, device="cuda"), A.indices[:0], A.values[:0])
+    ptrs, off = [parts[0].indptr], int(parts[0].indptr[-1].item())
+    for p in parts[1:]:
+        ptrs.append(p.indptr[1:] + off)
+        off += p.nnz
+    return DeviceCSR((rows, A.shape[1]), t.cat(ptrs), t.cat([p.indices for p in parts]),
+                     t.cat([p.values for p in parts]))
 
 
 # ---------------------------------------------------------------- results
 class ShardedPseudoinverse:
-    """pinv(A) with U row-sharded in reordered coordinates: rank i holds rows [r0, r1)."""
+    """pinv(A) with this rank's slices: U_loc (its rows, reordered coordinates), Vt_loc (its
+    columns), sigma+ replicated."""
 
-    def __init__(self, comm, U_i, r0, m, sdag, Vt, row_fwd, col_fwd, tolerance_used, all_filtered):
-        self.comm, self.U_i, self.r0, self.m = comm, U_i, r0, m
-        self.sdag, self.Vt, self.row_fwd, self.col_fwd = sdag, Vt, row_fwd, col_fwd
+    def __init__(self, comm, plan_row, m, n, m1, n1, U_loc, sdag, Vt_loc, row_fwd, col_perm, tolerance_used,
+                 all_filtered):
+        self.comm, self.m, self.n, self.m1, self.n1 = comm, m, n, m1, n1
+        self.p = dict(zip(PLAN_FIELDS, (int(x) for x in plan_row)))
+        self.U_loc, self.sdag, self.Vt_loc, self.row_fwd = U_loc, sdag, Vt_loc, row_fwd
         self.tolerance_used, self.all_filtered = tolerance_used, all_filtered
         self.r = int(sdag.shape[0])
-        self.n = int(Vt.shape[1])
+        p = self.p
+        reord = np.concatenate([np.arange(p["c_lo"], p["c_hi"]), n1 + np.arange(p["hc_lo"], p["hc_hi"])])
+        self.cols = col_perm.backward[reord] if len(reord) else np.zeros(0, np.int64)  # original column ids
 
     @property
     def sigma_dagger(self) -> np.ndarray:
         return d2h(self.sdag)
 
-    def apply_device(self, Y: DeviceCSR):
-        """pinv @ Y (Y CSR m x L, original rows): the full n x L result on every rank."""
+    def apply_local(self, Y: DeviceCSR):
+        """(original column ids, Z rows of this rank's columns on the device) of Z = pinv @ Y."""
         if Y.shape[0] != self.m:
             raise ValueError(f"dimension mismatch: pseudoinverse expects {self.m} rows, got {Y.shape[0]}")
+        self.comm.bind()
         L = Y.shape[1]
-        W = empty((L, self.r))
-        _lib.call("fpi_pinv_project_csr", self.r0, int(self.U_i.shape[0]), self.r, _lib.ptr(self.U_i),
-                  _lib.ptr(self.row_fwd), self.m, L, Y.nnz, _lib.ptr(Y.indptr), _lib.ptr(Y.indices),
-                  _lib.ptr(Y.values), _lib.ptr(W))
-        self.comm.all_reduce_(W)
-        Z = empty((self.n, L))
-        _lib.call("fpi_pinv_lift", self.n, self.r, _lib.ptr(self.sdag), _lib.ptr(self.Vt), _lib.ptr(self.col_fwd), L,
-                  _lib.ptr(W), _lib.ptr(Z))
-        return Z
+        p = self.p
+        Z = empty((len(self.cols), L))
+        _lib.call("fpi_pinv_apply_shard", self.m, self.m1, p["r_lo"], p["r_hi"], p["h_lo"], p["h_hi"], self.r,
+                  _lib.ptr(self.U_loc), _lib.ptr(self.sdag), _lib.ptr(self.Vt_loc), len(self.cols),
+                  _lib.ptr(self.row_fwd), L, Y.nnz, _lib.ptr(Y.indptr), _lib.ptr(Y.indices), _lib.ptr(Y.values),
+                  _lib.ptr(Z))
+        return self.cols, Z
+
+    def apply(self, Y) -> np.ndarray:
+        """The full n x L Z on every rank (each rank's rows gathered on the host)."""
+        Yd = Y if isinstance(Y, DeviceCSR) else DeviceCSR.from_host(Y)
+        cols, Z = self.apply_local(Yd)
+        parts = self.comm.all_gather_object((cols, d2h(Z)))
+        out = np.zeros((self.n, Yd.shape[1]))
+        for c, z in parts:
+            out[c] = z
+        return out
 
 
 @dataclass
@@ -255,15 +245,15 @@ class ShardedResult:
     sigma: object
     reordering: object
     timings: list
-    engine: int
+    engines: tuple
+    sharded: bool
 
 
-def fastpi_sharded(dev: DeviceCSR, cfg: FastpiConfig, comm: Comm | None = None, *, stats: dict | None = None,
-                   ops=None) -> ShardedResult:
-    """Algorithm 1 (pinv.py:278-347) on every rank of ``comm``; m >= n.  The column update and
-    the apply are row-sharded; the earlier stages are replicated."""
+def fastpi_sharded(dev: DeviceCSR, cfg: FastpiConfig, comm: Comm | None = None, *,
+                   stats: dict | None = None) -> ShardedResult:
+    """Algorithm 1 (pinv.py:278-347) over the ranks of ``comm``; m >= n."""
     comm = comm or Comm()
-    ops = ops or GpuOps()
+    comm.bind()
     m, n = dev.shape
     if m < n:
         raise ValueError("fastpi_sharded expects m >= n (transpose the problem first)")
@@ -271,52 +261,107 @@ def fastpi_sharded(dev: DeviceCSR, cfg: FastpiConfig, comm: Comm | None = None, 
     with _Timer() as tm:
         ordering = reorder_device(dev, cfg.k)
         part = partition_original(dev, ordering, transposes=False)
-    timings.append(StageTime("reorder", tm.seconds, comm.rank))
-    with _Timer() as tm:
-        f11 = block_diagonal_svd_device(part.a11, ordering.spans_device(), cfg.alpha, comm)
-    timings.append(StageTime("block_svd", tm.seconds, comm.rank))
-    n1, m2, n2 = ordering.n_spoke_cols, ordering.n_hub_rows, ordering.n_hub_cols
-    with _Timer() as tm:
-        want_s = math.ceil(cfg.alpha * n1)
-        s = min(want_s, f11.rank + m2, n1)
-        if s < want_s:
-            warnings.warn(f"row-update target rank clamped from {want_s} to {s} "
-                          "(block stage produced less derivable rank)")
-        f_rows, _ = row_update_device(f11, part.a21, s, low_rank_threshold=cfg.low_rank_threshold, seed=cfg.seed + 1)
-    timings.append(StageTime("row_update", tm.seconds, comm.rank))
-
-    r = min(math.ceil(cfg.alpha * n), f_rows.rank + n2, m)
-    q = f_rows.rank + n2
-    r0, r1 = shard_bounds(m, comm.world)[comm.rank]
-    with _Timer() as tm:
-        randomized = r >= 1 and r < cfg.low_rank_threshold * q and m > 2 * r
-        if randomized:
-            d = f_rows.device()
-            T_i = ops.csr_rows(part.T, r0, r1)
-            U_i, sig, Vt = column_update_shard(ops, comm, ops.slice_rows(d.U, r0, r1), d.sigma, d.Vt, T_i,
-                                               ops.csr_transpose(T_i), m, r, cfg.seed + 2)
-            engine = 1
-        else:
-            # dense engine (or r == 0): replicated, each rank keeps its rows of U
-            f_full, engine = column_update_device(f_rows, part.T, part.T.transpose(), r,
-                                                  low_rank_threshold=cfg.low_rank_threshold, seed=cfg.seed + 2)
-            fd = f_full.device()
-            U_i, sig, Vt = fd.U[r0:r1].contiguous(), fd.sigma, fd.Vt
-    timings.append(StageTime("column_update", tm.seconds, comm.rank))
+    timings.append(StageTime("reorder", tm.seconds, 0))
+    m1, n1 = ordering.n_spoke_rows, ordering.n_spoke_cols
+    m2, n2 = ordering.n_hub_rows, ordering.n_hub_cols
+    plan = shard_plan(ordering, part.T, comm.world)
+    P = dict(zip(PLAN_FIELDS, (int(x) for x in plan[comm.rank])))
+    spans = ordering.spans_device()
+    nsp = int(spans.numel() // 4)
+    thr = cfg.low_rank_threshold
 
     with _Timer() as tm:
-        # pinv.py:211-231 on the replicated sigma: the same sigma+ on every rank
-        from .svd import SvdFactors, _Dense
-        probe = _assemble(SvdFactors(_dev=_Dense(empty((0, r)), sig, Vt), is_sorted=True, _shape=(m, n)),
-                          ordering.row_perm.device_forward(), ordering.col_perm.device_forward(),
-                          cfg.pinv_cutoff_factor)
-        pdev = probe._dev
-        pv = ShardedPseudoinverse(comm, U_i, r0, m, pdev.sdag, Vt, pdev.row_fwd, pdev.col_fwd, probe.tolerance_used,
-                                  probe.all_filtered)
-    timings.append(StageTime("pinv_assembly", tm.seconds, comm.rank))
+        bplan = _lib.BlockPlan()
+        _lib.call("fpi_block_svd_plan", nsp, _lib.ptr(spans), float(cfg.alpha), C.byref(bplan))
+        rank11 = int(bplan.rank11)
+        U11 = DeviceCSR.empty(m1, rank11, bplan.nnz_u11)
+        Vt11 = DeviceCSR.empty(rank11, n1, bplan.nnz_vt11)
+        sig11 = empty(rank11)
+        krange = (C.c_int64 * 2)()
+        _lib.call("fpi_block_svd_range", m1, n1, _lib.ptr(part.a11.indptr), _lib.ptr(part.a11.indices),
+                  _lib.ptr(part.a11.values), nsp, _lib.ptr(spans), float(cfg.alpha), P["b_lo"], P["b_hi"],
+                  _lib.ptr(sig11), _lib.ptr(U11.indptr), _lib.ptr(U11.indices), _lib.ptr(U11.values),
+                  _lib.ptr(Vt11.indptr), _lib.ptr(Vt11.indices), _lib.ptr(Vt11.values), C.byref(bplan), krange)
+        k_lo, k_hi = int(krange[0]), int(krange[1])
+    timings.append(StageTime("block_svd", tm.seconds, rank11))
+
+    want_s = math.ceil(cfg.alpha * n1)
+    s = min(want_s, rank11 + m2, n1)
+    if s < want_s:
+        warnings.warn(f"row-update target rank clamped from {want_s} to {s} (block stage produced less derivable rank)")
+    r = min(math.ceil(cfg.alpha * n), s + n2, m)
+    row_sharded = 1 <= s < thr * n1 and rank11 + m2 > 2 * s
+    col_sharded = 1 <= r < thr * (s + n2) and m > 2 * r
+    if not (row_sharded and col_sharded):
+        return _replicated(dev, cfg, comm, plan, P, ordering, stats)
+
+    r_rows, m2_loc = P["r_hi"] - P["r_lo"], P["h_hi"] - P["h_lo"]
+    nc_loc = P["c_hi"] - P["c_lo"]
+    zoff = np.ascontiguousarray(np.append(plan[:, 4], n1).astype(np.int64))  # spoke-column ranges
+    with _Timer() as tm:
+        U_rows = empty((r_rows + m2_loc, s))
+        sig_rows = empty(s)
+        Vt_rows = empty((s, nc_loc))
+        _lib.call("fpi_row_update_shard", n1, _lib.ptr(sig11), _lib.ptr(Vt11.indptr), _lib.ptr(Vt11.indices),
+                  _lib.ptr(Vt11.values), k_lo, k_hi - k_lo, _lib.ptr(U11.indptr), _lib.ptr(U11.indices),
+                  _lib.ptr(U11.values), P["r_lo"], r_rows, _lib.ptr(part.a21.indptr), _lib.ptr(part.a21.indices),
+                  _lib.ptr(part.a21.values), P["h_lo"], m2_loc, rank11 + m2, s, float(thr), cfg.seed + 1,
+                  zoff.ctypes.data_as(C.c_void_p), _lib.ptr(U_rows), _lib.ptr(sig_rows), _lib.ptr(Vt_rows))
+        diag_r = _lib.svd_diag() if stats is not None else None
+    timings.append(StageTime("row_update", tm.seconds, s))
+
+    with _Timer() as tm:
+        T_loc = _rows_of(part.T, [(P["r_lo"], P["r_hi"]), (m1 + P["h_lo"], m1 + P["h_hi"])])
+        Tt_loc = T_loc.transpose()
+        m_loc = T_loc.shape[0]
+        nh_loc = P["hc_hi"] - P["hc_lo"]
+        U_loc = empty((m_loc, r))
+        sig = empty(r)
+        Vt_loc = empty((r, nc_loc + nh_loc))
+        _lib.call("fpi_column_update_shard", m_loc, s, _lib.ptr(U_rows), _lib.ptr(sig_rows), _lib.ptr(Vt_rows),
+                  nc_loc, n2, _lib.ptr(T_loc.indptr), _lib.ptr(T_loc.indices), _lib.ptr(T_loc.values),
+                  _lib.ptr(Tt_loc.indptr), _lib.ptr(Tt_loc.indices), _lib.ptr(Tt_loc.values), m, P["hc_lo"],
+                  P["hc_hi"], r, float(thr), cfg.seed + 2, _lib.ptr(U_loc), _lib.ptr(sig), _lib.ptr(Vt_loc))
+        diag_c = _lib.svd_diag() if stats is not None else None
+    timings.append(StageTime("column_update", tm.seconds, r))
+
+    with _Timer() as tm:
+        sdag = empty(r)
+        tol = C.c_double(0.0)
+        af = C.c_int32(0)
+        _lib.call("fpi_pinv_assemble", r, _lib.ptr(sig), m, n, float(cfg.pinv_cutoff_factor), _lib.ptr(sdag),
+                  C.byref(tol), C.byref(af))
+        if af.value:
+            warnings.warn("every singular value fell below the cutoff; the pseudoinverse is zero")
+        pv = ShardedPseudoinverse(comm, plan[comm.rank], m, n, m1, n1, U_loc, sdag, Vt_loc,
+                                  ordering.row_perm.device_forward(), ordering.col_perm, float(tol.value),
+                                  bool(af.value))
+    timings.append(StageTime("pinv_assembly", tm.seconds, r))
     if stats is not None:
-        stats.update(engine=engine, r=r, q=q, shard=(r0, r1), world=comm.world)
-    return ShardedResult(pv, sig, ordering, timings, engine)
+        stats.update(engines=(1, 1), s=s, r=r, rank11=rank11, m1=m1, n1=n1, m2=m2, n2=n2,
+                     T=ordering.n_iterations, plan=plan, world=comm.world, sharded=True, svd_diag_row=diag_r,
+                     svd_diag_col=diag_c)
+    return ShardedResult(pv, sig, ordering, timings, (1, 1), True)
+
+
+def _replicated(dev, cfg, comm, plan, P, ordering, stats):
+    """Small problems (a dense-engine update): the single-GPU pipeline on every rank, each rank
+    keeping its rows of U and its columns of Vt."""
+    res = fastpi_device(dev, cfg, stats=stats)
+    fd = res.factors.device()
+    m1, n1 = ordering.n_spoke_rows, ordering.n_spoke_cols
+    t = torch()
+    U_loc = t.cat([fd.U[P["r_lo"]:P["r_hi"]], fd.U[m1 + P["h_lo"]:m1 + P["h_hi"]]]).contiguous()
+    Vt_loc = t.cat([fd.Vt[:, P["c_lo"]:P["c_hi"]], fd.Vt[:, n1 + P["hc_lo"]:n1 + P["hc_hi"]]], dim=1).contiguous()
+    pvd = res.pseudoinverse._dev
+    m, n = dev.shape
+    pv = ShardedPseudoinverse(comm, plan[comm.rank], m, n, m1, n1, U_loc, pvd.sdag, Vt_loc, pvd.row_fwd,
+                              res.reordering.col_perm, res.pseudoinverse.tolerance_used,
+                              res.pseudoinverse.all_filtered)
+    if stats is not None:
+        stats.update(plan=plan, world=comm.world, sharded=False)
+    return ShardedResult(pv, fd.sigma, res.reordering, res.timings, tuple(stats.get("engines", (0, 0)))
+                         if stats else (0, 0), False)
 
 
 def fastpi_distributed(A, config: FastpiConfig | None = None, comm: Comm | None = None) -> ShardedResult:
@@ -329,7 +374,14 @@ def fastpi_distributed(A, config: FastpiConfig | None = None, comm: Comm | None 
     return fastpi_sharded(dev, cfg, comm)
 
 
-def apply_distributed(pv: ShardedPseudoinverse, Y) -> np.ndarray:
-    """pinv @ Y for host (scipy) or device Y; the n x L result as numpy on every rank."""
+def apply_local(pv: ShardedPseudoinverse, Y):
+    """This rank's rows of Z = pinv @ Y as (original column ids, host array): the per-GPU
+    device->host copies run in parallel; the caller assembles them."""
     Yd = Y if isinstance(Y, DeviceCSR) else DeviceCSR.from_host(Y)
-    return d2h(pv.apply_device(Yd))
+    cols, Z = pv.apply_local(Yd)
+    return cols, d2h(Z)
+
+
+def apply_distributed(pv: ShardedPseudoinverse, Y) -> np.ndarray:
+    """pinv @ Y for host (scipy) or device Y; the full n x L result as numpy on every rank."""
+    return pv.apply(Y)

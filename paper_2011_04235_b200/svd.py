@@ -199,11 +199,9 @@ def randomized_svd(A, rank: int, seed: int) -> SvdFactors:
     return randomized_svd_device(dev, rank, seed)
 
 
-def block_diagonal_svd_device(a11: DeviceCSR, spans_dev, alpha: float, comm=None) -> SvdFactors:
-    """svd.py:141-193 on the spoke CSR + device span table (the hot path).
-
-    With a multi-rank ``comm`` (sharded.Comm) every rank factors its share of the blocks
-    (fpi_block_svd_shard) and one all-reduce of the values assembles the full factors."""
+def block_diagonal_svd_device(a11: DeviceCSR, spans_dev, alpha: float) -> SvdFactors:
+    """svd.py:141-193 on the spoke CSR + device span table (the hot path).  (A sharded solve
+    factors only its own block range: fpi_block_svd_range, sharded.py.)"""
     if not 0.0 < alpha <= 1.0:
         raise ValueError(f"target rank ratio alpha must be in (0, 1], got {alpha}")
     m1, n1 = a11.shape
@@ -214,18 +212,9 @@ def block_diagonal_svd_device(a11: DeviceCSR, spans_dev, alpha: float, comm=None
     U = DeviceCSR.empty(m1, r, plan.nnz_u11)
     Vt = DeviceCSR.empty(r, n1, plan.nnz_vt11)
     sig = empty(r)
-    if comm is not None and comm.world > 1:
-        _lib.call("fpi_block_svd_shard", m1, n1, _lib.ptr(a11.indptr), _lib.ptr(a11.indices), _lib.ptr(a11.values),
-                  nsp, _lib.ptr(spans_dev), float(alpha), comm.rank, comm.world, _lib.ptr(sig), _lib.ptr(U.indptr),
-                  _lib.ptr(U.indices), _lib.ptr(U.values), _lib.ptr(Vt.indptr), _lib.ptr(Vt.indices),
-                  _lib.ptr(Vt.values), C.byref(plan))
-        for t in (sig, U.values, Vt.values):
-            if t.numel():
-                comm.all_reduce_(t)
-    else:
-        _lib.call("fpi_block_svd", m1, n1, _lib.ptr(a11.indptr), _lib.ptr(a11.indices), _lib.ptr(a11.values), nsp,
-                  _lib.ptr(spans_dev), float(alpha), _lib.ptr(sig), _lib.ptr(U.indptr), _lib.ptr(U.indices),
-                  _lib.ptr(U.values), _lib.ptr(Vt.indptr), _lib.ptr(Vt.indices), _lib.ptr(Vt.values), C.byref(plan))
+    _lib.call("fpi_block_svd", m1, n1, _lib.ptr(a11.indptr), _lib.ptr(a11.indices), _lib.ptr(a11.values), nsp,
+              _lib.ptr(spans_dev), float(alpha), _lib.ptr(sig), _lib.ptr(U.indptr), _lib.ptr(U.indices),
+              _lib.ptr(U.values), _lib.ptr(Vt.indptr), _lib.ptr(Vt.indices), _lib.ptr(Vt.values), C.byref(plan))
     return SvdFactors(_dev=_Block(U, sig, Vt), is_sorted=False, _shape=(m1, n1))
 
 
