@@ -239,13 +239,14 @@ def workload_config(p, world=1):
 def _ncu_traffic():
     """DRAM bytes of one representative launch of the dominant kernel, from the committed
     `ncu --set full` capture summary (profiles/); None when absent."""
-    f = Path(__file__).resolve().parent / "profiles" / "r01_ncu_full_summary.json"
+    f = Path(__file__).resolve().parent / "profiles" / "r02_ncu_full_summary.json"
     try:
-        g = json.loads(f.read_text())["r01_gemm_gram_c4"]
+        g = json.loads(f.read_text())["r02_gemm_c4_apply_lift"]
     except (OSError, KeyError, ValueError):
         return None
     return {"source": f"profiles/{f.name}", "launch": g.get("launch"), "traffic_bytes": g.get("traffic_bytes"),
-            "algorithmic_bytes": g.get("algorithmic_bytes"), "dmma_pipe_active": g.get("dmma_pipe_active_pct")}
+            "algorithmic_bytes": g.get("algorithmic_bytes"), "dmma_pipe_active": g.get("dmma_pipe_active_pct"),
+            "ncu_duration": g.get("duration")}
 
 
 def ours_arm(args):
@@ -336,6 +337,19 @@ def ours_arm(args):
     kernels = {k: {"launches": v["launches"], "ms": round(v["ms"], 3), "share_of_step": round(v["ms"] / ms, 4),
                    "gflop": round(v["flops"] / 1e9, 3), "gbytes": round(v["bytes"] / 1e9, 4)}
                for k, v in sorted(rep.items(), key=lambda kv: -kv[1]["ms"])}
+    # every class against its own roofline: FP64 tensor for the DMMA GEMM, HBM for the
+    # byte-counted classes (SpMM, reorder, permute/partition, sketch); latency-bound classes carry none
+    peaks0, _ = measured_peaks()
+    fp64_ref = max(_lib.dmma_peak_tflops(), 1e-9)
+    for k, v in rep.items():
+        if v["ms"] <= 0:
+            continue
+        if "gemm" in k and v["flops"] > 0:
+            kernels[k]["tflops"] = round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2)
+            kernels[k]["roofline_frac"] = round(kernels[k]["tflops"] / fp64_ref, 4)
+        elif v["bytes"] > 0:
+            kernels[k]["gbs"] = round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1)
+            kernels[k]["roofline_frac"] = round(kernels[k]["gbs"] / peaks0["hbm_gbs"], 4)
     dom_name, dom = max(((k, v) for k, v in rep.items() if v["flops"] > 0 or v["bytes"] > 0),
                         key=lambda kv: kv[1]["ms"], default=(None, None))
     roofline = None
@@ -417,6 +431,15 @@ def ours_arm(args):
         cpu = {"value": dt, "unit": "s", "cores": cores, "kind": "port",
                "sample": f"one full {w.name} solve (oracle port: fastpi + apply), {cores} BLAS threads"}
 
+    # ---- the largest config (configs[4], c5) as a second record, measured in a child process
+    c5 = None
+    if rank == 0 and world == 1 and args.workload == "c4" and not args.no_c5:
+        c5 = c5_record(args)
+
+    cpu_partial = None
+    if rank == 0 and world == 1 and args.cpu_partial:
+        cpu_partial = cpu_partial_c5(p, {k: statistics.mean(v) for k, v in stage_ms.items()})
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": ms_max / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -432,11 +455,60 @@ def ours_arm(args):
                                                  "svd_diag_row", "svd_diag_col") if k in stats},
             "fp64_peaks_tflops": {"cublas_dgemm_8192": round(cublas_dgemm, 2), "dmma_microbench": round(fp64_peak, 2)},
         }
+        if c5 is not None:
+            line["c5"] = c5
+        if cpu_partial is not None:
+            line["cpu_partial"] = cpu_partial
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def c5_record(args):
+    """configs[4] (2M x 200k, 30M nnz, r = 1000, L = 3000) on this GPU: value, e2e, roofline and
+    stage times, plus the oracle port's reorder / partition / block-SVD stages on the host cores
+    (the full CPU solve of c5 takes tens of minutes; these three stages are the bounded sample)."""
+    cmd = [sys.executable, str(Path(__file__).resolve()), "--workload", "c5", "--steps", "3", "--warmup", "3",
+           "--no-cpu-baseline", "--cpu-partial"]
+    log(f"[bench] c5 record: {' '.join(cmd)}")
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=args.c5_timeout)
+    except subprocess.TimeoutExpired:
+        return {"unavailable": f"c5 run exceeded {args.c5_timeout:.0f}s"}
+    sys.stderr.write(out.stderr[-3000:])
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    if out.returncode != 0 or not lines:
+        return {"unavailable": f"c5 run failed (exit {out.returncode})"}
+    rec = json.loads(lines[-1])
+    keep = ("value", "unit", "ms_per_step", "e2e", "roofline", "stages_ms", "kernels", "structure", "clocks",
+            "gpu_launches", "config", "cpu_partial", "step_ms_all")
+    return {k: rec[k] for k in keep if k in rec}
+
+
+def cpu_partial_c5(p, gpu_stages):
+    """The oracle port's reorder (+ permute / partition) and block SVD on the host cores."""
+    from threadpoolctl import threadpool_limits
+    from oracle import fastpi_oracle as orc
+    w = p.workload
+    cores = cpu_cores()
+    with threadpool_limits(cores):
+        A = orc.canonical_csr(p.A)
+        t0 = time.perf_counter()
+        o = orc.reorder(*A.shape, A.indptr, A.indices, w.k)
+        Ap = orc.permute(A, o.row_fwd, o.col_fwd)
+        spoke, _, _, _ = orc.partition(Ap, o)
+        t1 = time.perf_counter()
+        orc.block_svd(spoke, o.spans, w.alpha)
+        t2 = time.perf_counter()
+    cpu = {"reorder": t1 - t0, "block_svd": t2 - t1}
+    return {"kind": "port", "cores": cores, "unit": "s",
+            "sample": "c5 stages reorder + permute/partition and block SVD (oracle port); the row / column "
+                      "updates are not run on the host (minutes to hours)",
+            "stages_s": {k: round(v, 3) for k, v in cpu.items()},
+            "gpu_stages_s": {k: round(gpu_stages[k] / 1e3, 5) for k in cpu if k in gpu_stages},
+            "speedup": {k: round(cpu[k] / (gpu_stages[k] / 1e3), 1) for k in cpu if gpu_stages.get(k)}}
 
 
 def main():
@@ -449,6 +521,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=240.0, help="seconds of reference steps before stopping")
+    ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (c5) record of the c4 run")
+    ap.add_argument("--c5-timeout", type=float, default=600.0)
+    ap.add_argument("--cpu-partial", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)

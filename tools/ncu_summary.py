@@ -14,7 +14,7 @@ KEYS = {
     "l1_throughput_pct": "l1tex__throughput.avg.pct_of_peak_sustained_active",
     "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
-    "dmma_pipe_active_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "dmma_pipe_active_pct": "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
     "achieved_occupancy_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
     "regs": "launch__registers_per_thread",
     "grid": "launch__grid_size",
