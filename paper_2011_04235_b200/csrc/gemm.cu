@@ -19,6 +19,9 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "capi_guard.cuh"
 #include "gemm.cuh"
@@ -237,6 +240,196 @@ __global__ void __launch_bounds__(NT, FPI_GEMM_CFG_CTAS)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// TMA-fed variant (operands 16-byte aligned along their contiguous dimension, even leading
+// dimensions): the same 64 x 64 x 16 CTA tile and DMMA warp tiles, but every stage's A and B tiles
+// arrive by cp.async.bulk.tensor (one elected thread issues them, an mbarrier counts the bytes)
+// into 128-byte-swizzled shared memory, so the fragment loads stay conflict-free without padding.
+// Tiles reaching past M / N / K are zero-filled by the TMA unit (no predicated copies).
+// Sub-tiles are 16 doubles (128 B, the swizzle span) wide: a K-contiguous operand is one
+// 16 x 64 box per stage, an M- or N-contiguous one four 16 x 16 boxes.
+constexpr int TSTAGES = 4;
+constexpr int T_STAGE = BM * BK + BN * BK;  // doubles per stage (A then B)
+constexpr size_t TMA_SMEM_BYTES = (size_t)TSTAGES * T_STAGE * sizeof(double) + 1024 + 16 * TSTAGES;
+static_assert(BM == 64 && BN == 64 && BK == 16, "the TMA box layout assumes 64 x 64 x 16 tiles");
+
+// element (r, c) of a [rows][16] sub-tile written by TMA with CU_TENSOR_MAP_SWIZZLE_128B: the
+// 16-byte chunk index is XORed with the row index mod 8
+__device__ __forceinline__ int swz(int r, int c) { return r * 16 + ((((c >> 1) ^ (r & 7)) << 1) | (c & 1)); }
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(double* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(NT + 32, FPI_GEMM_CFG_CTAS)
+    k_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
+               int64_t N, int64_t K, double alpha, double beta, double* __restrict__ C, int64_t ldc,
+               int64_t k_per_split, double* __restrict__ partial, int sym) {
+  static_assert(TA != TB, "the TMA kernel serves the conflict-free NT / TN layouts");
+  constexpr bool NT_MODE = !TA && TB;
+  constexpr int CONSUMERS = NT / 32;  // compute warps; warp CONSUMERS is the TMA producer
+  if (sym && tile_above_diag(blockIdx.x, blockIdx.y)) return;
+  extern __shared__ unsigned char smem_raw[];
+  double* st = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(st + TSTAGES * T_STAGE);
+  uint64_t* empty = full + TSTAGES;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb = (int64_t)blockIdx.z * k_per_split;
+  const int64_t ke = kb + k_per_split < K ? kb + k_per_split : K;
+  const int64_t ntiles = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == CONSUMERS) {
+    // producer warp: one elected lane refills a slot as soon as every compute warp released it
+    if (lane == 0) {
+      for (int64_t kt = 0; kt < ntiles; ++kt) {
+        const int slot = (int)(kt % TSTAGES);
+        if (kt >= TSTAGES) mbar_wait(&empty[slot], (unsigned)(((kt / TSTAGES) - 1) & 1));
+        double* As = st + slot * T_STAGE;
+        double* Bs = As + BM * BK;
+        mbar_expect_tx(&full[slot], (unsigned)(T_STAGE * sizeof(double)));
+        const int k0 = (int)(kb + kt * BK);
+        if (!TA) {
+          tma_load_2d(As, &tmA, k0, (int)m0, &full[slot]);  // A[m][k]: one 16 (k) x 64 (m) box
+        } else {
+#pragma unroll
+          for (int j = 0; j < BM / 16; ++j) tma_load_2d(As + j * 256, &tmA, (int)m0 + 16 * j, k0, &full[slot]);
+        }
+        if (TB) {
+          tma_load_2d(Bs, &tmB, k0, (int)n0, &full[slot]);  // B stored N x K: one 16 (k) x 64 (n) box
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / 16; ++j) tma_load_2d(Bs + j * 256, &tmB, (int)n0 + 16 * j, k0, &full[slot]);
+        }
+      }
+    }
+    return;
+  }
+  const int wm = (warp / WARPS_N) * WM, wn = (warp % WARPS_N) * WN;
+  const int g = lane >> 2, t = lane & 3;
+
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // Fragment placement that keeps the swizzled loads conflict-free (one 256-byte warp load = two
+  // wavefronts): the 128-byte swizzle XORs the chunk index with (row mod 8), so
+  //  * NT (both operands K-contiguous rows): fragment row g takes tile row pi(g) = 2(g mod 4) + g/4,
+  //    putting the two 16-byte chunks of consecutive k for half a warp's 4 rows on 8 distinct chunks;
+  //    C rows and columns follow pi;
+  //  * TN (both M- / N-contiguous): the four k of one DMMA step are k0 + 2t (k0 in 0, 1, 8, 9), whose
+  //    rows' XOR patterns spread a half warp's 8 chunk slots over all 8 chunks.
+  const int pg = NT_MODE ? (((g & 3) << 1) | (g >> 2)) : g;
+  for (int64_t kt = 0; kt < ntiles; ++kt) {
+    const int slot = (int)(kt % TSTAGES);
+    mbar_wait(&full[slot], (unsigned)((kt / TSTAGES) & 1));
+    const double* as = st + slot * T_STAGE;
+    const double* bs = as + BM * BK;
+#pragma unroll
+    for (int step = 0; step < BK / 4; ++step) {
+      double af[MI], bf[NJ];
+      if (NT_MODE) {
+        const int k = step * 4 + t;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) af[i] = as[swz(wm + i * 8 + pg, k)];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) bf[j] = bs[swz(wn + j * 8 + pg, k)];
+      } else {
+        const int k = ((step & 1) | ((step >> 1) << 3)) + 2 * t;
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int m = wm + i * 8 + g;
+          af[i] = as[(m >> 4) * 256 + swz(k, m & 15)];
+        }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const int n = wn + j * 8 + g;
+          bf[j] = bs[(n >> 4) * 256 + swz(k, n & 15)];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&empty[slot])) : "memory");
+  }
+
+  // accumulator (i, j, q) holds C[m0 + wm + 8i + pi(g)][n0 + wn + 8j + pi(2t + q)]  (pi = id for TN)
+  auto colmap = [](int c) { return NT_MODE ? (((c & 3) << 1) | (c >> 2)) : c; };
+  if (partial) {
+    double* P = partial + (int64_t)blockIdx.z * M * N;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int64_t r = m0 + wm + i * 8 + pg;
+      if (r >= M) continue;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int64_t c = n0 + wn + j * 8 + colmap(2 * t + q);
+          if (c < N && (!sym || c <= r)) P[r * N + c] = acc[i][j][q];
+        }
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int64_t r = m0 + wm + i * 8 + pg;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t cq = n0 + wn + j * 8 + colmap(2 * t + q);
+        if (cq < N && (!sym || cq <= r)) {
+          double v = alpha * acc[i][j][q];
+          double* dst = C + r * ldc + cq;
+          *dst = beta == 0.0 ? v : v + beta * *dst;
+          if (sym && cq < r) {
+            double* mir = C + cq * ldc + r;
+            *mir = beta == 0.0 ? v : v + beta * *mir;
+          }
+        }
+      }
+    }
+  }
+}
+
 __global__ void k_reduce_split(int64_t M, int64_t N, int splits, const double* __restrict__ P, double alpha,
                                double beta, double* __restrict__ C, int64_t ldc, int sym) {
   FPI_GRID_STRIDE(e, M * N) {
@@ -320,11 +513,92 @@ void launch(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const
   note_launch(h, 2);
 }
 
+// ---- TMA descriptors (driver entry point fetched through the runtime: no -lcuda at link time)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// row-major rows x cols (leading dimension ld) operand, boxes of 16 (contiguous) x box_rows
+bool encode_operand(CUtensorMap* tm, const double* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <bool TA, bool TB>
+bool launch_tma(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int sym) {
+  if (M >= (1LL << 31) || N >= (1LL << 31) || K >= (1LL << 31)) return false;
+  alignas(64) CUtensorMap tmA, tmB;
+  // op(A) = A (M x K, K contiguous: 16 x 64 boxes) or A^T (A stored K x M: 16 x 16 boxes)
+  if (!(TA ? encode_operand(&tmA, A, K, M, lda, 16) : encode_operand(&tmA, A, M, K, lda, 64))) return false;
+  // op(B) = B (K x N stored, N contiguous: 16 x 16 boxes) or B^T (B stored N x K: 16 x 64 boxes)
+  if (!(TB ? encode_operand(&tmB, B, N, K, ldb, 64) : encode_operand(&tmB, B, K, N, ldb, 16))) return false;
+  static std::atomic<uint64_t> attr_set{0};
+  once_per_device(attr_set, h->device, [] {
+    FPI_CUDA(cudaFuncSetAttribute(k_gemm_tma<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)TMA_SMEM_BYTES));
+  });
+  cudaStream_t s = h->stream;
+  const int64_t tm = (M + BM - 1) / BM, tn = (N + BN - 1) / BN;
+  int64_t tiles = tm * tn;
+  if (sym) {
+    tiles = 0;
+    for (int64_t by = 0; by < tm; ++by) {
+      const int64_t lim = ((by + 1) * BM + BN - 1) / BN;
+      tiles += lim < tn ? lim : tn;
+    }
+  }
+  int splits = choose_splits(tiles, M, N, K, h->num_sms);
+  if (const char* e = getenv("FPI_GEMM_SPLITS")) splits = atoi(e) > 0 ? atoi(e) : splits;
+  FPI_REQUIRE(tm < 65536 && tn < (1LL << 31), FPI_ECAPACITY, "gemm grid too large");
+  if (splits == 1) {
+    dim3 grid((unsigned)tn, (unsigned)tm, 1);
+    k_gemm_tma<TA, TB><<<grid, NT + 32, TMA_SMEM_BYTES, s>>>(tmA, tmB, M, N, K, alpha, beta, C, ldc, K, nullptr, sym);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+    return true;
+  }
+  int64_t kps = (K + splits - 1) / splits;
+  kps = (kps + BK - 1) / BK * BK;  // a k-tile never straddles two splits
+  splits = (int)((K + kps - 1) / kps);
+  Scratch<double> part((size_t)splits * M * N, s);
+  dim3 grid((unsigned)tn, (unsigned)tm, (unsigned)splits);
+  k_gemm_tma<TA, TB><<<grid, NT + 32, TMA_SMEM_BYTES, s>>>(tmA, tmB, M, N, K, alpha, beta, C, ldc, kps, part, sym);
+  k_reduce_split<<<grid_for(M * N, 256, (int64_t)h->num_sms * 16), 256, 0, s>>>(M, N, splits, part, alpha, beta, C,
+                                                                                 ldc, sym);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 2);
+  return true;
+}
+
 template <bool TA, bool TB>
 void launch_any(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                 const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int sym) {
   const bool v16 = ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) && lda % 2 == 0 && ldb % 2 == 0 &&
                    !getenv("FPI_GEMM_NO_V16");
+  // TMA needs 16-byte aligned bases and row strides (the v16 condition)
+  const bool no_tma = getenv("FPI_GEMM_NO_TMA") != nullptr;
+  // TMA for the NT / TN layouts (both operands contiguous along the same dimension: the fixed
+  // 128-byte swizzle then admits conflict-free fragment loads); NN / TT keep the padded cp.async
+  // tiles (with TMA one operand's loads would be 2-way bank-conflicted: measured 7% slower)
+  if constexpr (TA != TB) {
+    if (v16 && !no_tma && launch_tma<TA, TB>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym)) return;
+  }
   if (v16) launch<TA, TB, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym);
   else launch<TA, TB, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym);
 }

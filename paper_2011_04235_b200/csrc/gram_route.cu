@@ -32,7 +32,7 @@
 namespace fpi {
 namespace {
 
-constexpr int GR_WARPS = 16;       // warps per CTA of the sparse Gram rows
+constexpr int GR_WARPS = 8;        // warps per CTA of the sparse Gram rows
 constexpr int64_t GR_SEG = 4096;   // S^T row entries per work item
 
 // Sh[i][hidx[c]] = S[i][c] for heavy c (Sh pre-zeroed): one warp per row
@@ -49,13 +49,14 @@ __global__ void k_densify_heavy(int64_t p, const int64_t* __restrict__ ptr, cons
   }
 }
 
-// Rows of S^T S for light columns.  Work item w: S column col[w], S^T row entries [b[w], e[w]).
-// acc[x] = sum_{i in item} S[i][col] * S[i][x]  over all q2 columns x.  Warp g owns the 32-column
-// chunks x >> 5 == g (mod GR_WARPS) and walks every row of the item in order, so each acc[x] is
-// updated by one warp, in ascending i: the sum's order is fixed.  dst[w] >= 0: partial row
-// P[dst[w]]; otherwise the finished row goes to H[(sd + col) * ldh + sd + x].
+// Rows of S^T S for light columns.  Work item w: S column col[w], S^T row entries [b[w], e[w]);
+// column part `part` of NPART: output columns [x0, x1).  acc[x - x0] = sum_{i in item}
+// S[i][col] * S[i][x].  Warp g owns the 32-column chunks ((x - x0) >> 5) == g (mod warps) and
+// walks every row of the item in order, so each acc entry is updated by one warp, in ascending i:
+// the sum's order is fixed.  Two rows are in flight per warp (their entry loads are independent).
+// dst[w] >= 0: partial row P[dst[w]]; otherwise the finished row goes to H[(sd + col) * ldh + sd + x].
 __global__ void __launch_bounds__(GR_WARPS * 32)
-    k_gram_rows(int64_t nitems, const int32_t* __restrict__ icol, const int64_t* __restrict__ ib,
+    k_gram_rows(int64_t nitems, int nparts, const int32_t* __restrict__ icol, const int64_t* __restrict__ ib,
                 const int64_t* __restrict__ ie, const int32_t* __restrict__ idst, int64_t q2,
                 const int64_t* __restrict__ s_ptr, const int32_t* __restrict__ s_idx,
                 const double* __restrict__ s_val, const int32_t* __restrict__ st_idx,
@@ -63,8 +64,13 @@ __global__ void __launch_bounds__(GR_WARPS * 32)
                 int64_t sd) {
   extern __shared__ double acc[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t w = blockIdx.x; w < nitems; w += gridDim.x) {
-    for (int64_t x = threadIdx.x; x < q2; x += blockDim.x) acc[x] = 0.0;
+  const int64_t chunk = ((q2 + nparts - 1) / nparts + 31) & ~(int64_t)31;
+  for (int64_t w2 = blockIdx.x; w2 < nitems * nparts; w2 += gridDim.x) {
+    const int64_t w = w2 / nparts;
+    const int64_t x0 = (w2 - w * nparts) * chunk;
+    const int64_t x1 = x0 + chunk < q2 ? x0 + chunk : q2;
+    const int64_t nx = x1 - x0;
+    for (int64_t x = threadIdx.x; x < nx; x += blockDim.x) acc[x] = 0.0;
     __syncthreads();
     const int64_t b = ib[w], e = ie[w];
     for (int64_t base = b; base < e; base += 32) {
@@ -78,22 +84,48 @@ __global__ void __launch_bounds__(GR_WARPS * 32)
         re = __ldg(s_ptr + i + 1);
       }
       const int cnt = (int)((e - base) < 32 ? (e - base) : 32);
-      for (int t = 0; t < cnt; ++t) {
-        const int64_t r0 = __shfl_sync(0xffffffffu, rb, t);
-        const int64_t r1 = __shfl_sync(0xffffffffu, re, t);
-        const double vt = __shfl_sync(0xffffffffu, v, t);
-        for (int64_t q = r0 + lane; q < r1 + lane; q += 32) {
-          if (q < r1) {
+      for (int t = 0; t < cnt; t += 2) {
+        // two rows in flight: their first 32 entries are loaded before either is applied
+        const int t1 = t + 1 < cnt ? t + 1 : t;
+        const int64_t ra = __shfl_sync(0xffffffffu, rb, t), ea = __shfl_sync(0xffffffffu, re, t);
+        const int64_t rc = __shfl_sync(0xffffffffu, rb, t1), ec = __shfl_sync(0xffffffffu, re, t1);
+        const double va = __shfl_sync(0xffffffffu, v, t), vc = __shfl_sync(0xffffffffu, v, t1);
+        const bool two = t + 1 < cnt;
+        int32_t xa = -1, xc = -1;
+        double sa = 0.0, sc = 0.0;
+        if (ra + lane < ea) {
+          xa = __ldg(s_idx + ra + lane);
+          sa = __ldg(s_val + ra + lane);
+        }
+        if (two && rc + lane < ec) {
+          xc = __ldg(s_idx + rc + lane);
+          sc = __ldg(s_val + rc + lane);
+        }
+        if (xa >= x0 && xa < x1 && (((xa - x0) >> 5) % GR_WARPS) == warp) acc[xa - x0] = fma(va, sa, acc[xa - x0]);
+        for (int64_t q = ra + 32 + lane; q < ea + lane; q += 32) {  // rest of a long row
+          if (q < ea) {
             const int32_t x = __ldg(s_idx + q);
-            if (((x >> 5) % GR_WARPS) == warp) acc[x] = fma(vt, __ldg(s_val + q), acc[x]);
+            if (x >= x0 && x < x1 && (((x - x0) >> 5) % GR_WARPS) == warp)
+              acc[x - x0] = fma(va, __ldg(s_val + q), acc[x - x0]);
+          }
+        }
+        if (two) {
+          if (xc >= x0 && xc < x1 && (((xc - x0) >> 5) % GR_WARPS) == warp)
+            acc[xc - x0] = fma(vc, sc, acc[xc - x0]);
+          for (int64_t q = rc + 32 + lane; q < ec + lane; q += 32) {
+            if (q < ec) {
+              const int32_t x = __ldg(s_idx + q);
+              if (x >= x0 && x < x1 && (((x - x0) >> 5) % GR_WARPS) == warp)
+                acc[x - x0] = fma(vc, __ldg(s_val + q), acc[x - x0]);
+            }
           }
         }
       }
     }
     __syncthreads();
     const int32_t d = idst[w];
-    double* out = d >= 0 ? P + (int64_t)d * q2 : H + (sd + icol[w]) * ldh + sd;
-    for (int64_t x = threadIdx.x; x < q2; x += blockDim.x) out[x] = acc[x];
+    double* out = (d >= 0 ? P + (int64_t)d * q2 : H + (sd + icol[w]) * ldh + sd) + x0;
+    for (int64_t x = threadIdx.x; x < nx; x += blockDim.x) out[x] = acc[x];
     __syncthreads();
   }
 }
@@ -323,7 +355,10 @@ void inner_gram(fpi_context* h, const SparseGramIn& in, const GramPlan& pl, doub
       FPI_CUDA(cudaMemcpyAsync(d_mpe.get(), mpe.data(), 4 * nm, cudaMemcpyHostToDevice, s));
     }
     Scratch<double> P((size_t)npart * q2 + 1, s);
-    const size_t smem = (size_t)q2 * 8;
+    // column parts of <= 48 KB of accumulator: four CTAs (32 warps) per SM instead of two
+    const int nparts = (int)std::max<int64_t>(1, (q2 * 8 + 49151) / 49152);
+    const int64_t chunk = ((q2 + nparts - 1) / nparts + 31) & ~(int64_t)31;
+    const size_t smem = (size_t)chunk * 8;
     static std::atomic<uint64_t> attr{0};
     once_per_device(attr, h->device, [&] {
       FPI_CUDA(cudaFuncSetAttribute(k_gram_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -331,9 +366,9 @@ void inner_gram(fpi_context* h, const SparseGramIn& in, const GramPlan& pl, doub
     });
     int per_sm = 0;
     FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram_rows, GR_WARPS * 32, smem));
-    const int64_t grid = std::min<int64_t>(nit, (int64_t)h->num_sms * std::max(per_sm, 1));
-    k_gram_rows<<<(unsigned)grid, GR_WARPS * 32, smem, s>>>(nit, d_icol, d_ib, d_ie, d_idst, q2, in.s_ptr, in.s_idx,
-                                                           in.s_val, in.st_idx, in.st_val, P, H, ldh, sd);
+    const int64_t grid = std::min<int64_t>(nit * nparts, (int64_t)h->num_sms * std::max(per_sm, 1));
+    k_gram_rows<<<(unsigned)grid, GR_WARPS * 32, smem, s>>>(nit, nparts, d_icol, d_ib, d_ie, d_idst, q2, in.s_ptr,
+                                                           in.s_idx, in.s_val, in.st_idx, in.st_val, P, H, ldh, sd);
     FPI_LAUNCH_CHECK();
     note_launch(h);
     if (nm) {

@@ -17,6 +17,8 @@ SHAPES = [  # (name, ta, tb, M, N, K)
     ("gram_YtY_c5", 1, 0, 2000, 2000, 2000000),
     ("YtU_c5", 1, 0, 2000, 1000, 2000000),
     ("U_eq_Y_X_c5", 0, 0, 2000000, 1000, 2000),
+    ("Gram_NT_c4", 0, 1, 1000, 1000, 200000),
+    ("Z_L_NT_c4", 0, 1, 10684, 1000, 1000),
 ]
 
 
