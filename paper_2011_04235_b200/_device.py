@@ -26,12 +26,16 @@ def device():
 
 
 def h2d(arr: np.ndarray, dtype=None):
-    """Host numpy -> device tensor (through pinned memory, async on the current stream)."""
+    """Host numpy -> device tensor (through pinned memory, async on the current stream).  Large
+    arrays are staged into a page-locked block from torch's caching host allocator by a parallel
+    (intra-op threads) copy; the allocator keeps the block until the stream has consumed it."""
     t = torch()
     a = np.ascontiguousarray(arr if dtype is None else arr.astype(dtype, copy=False))
     host = t.from_numpy(a)
     if a.nbytes >= (1 << 20):
-        host = host.pin_memory()
+        staged = t.empty(host.shape, dtype=host.dtype, pin_memory=True)
+        staged.copy_(host)
+        host = staged
     return host.to(device(), non_blocking=True)
 
 
