@@ -781,7 +781,8 @@ __device__ void advance_slots(EigProb* P, EigProb* PL, int nprob, int q, int rou
 
 __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
     k_jacobi(EigProb* P, int nprob, int64_t total_pairs, int64_t total_gitems, int64_t total_vitems, int gchunk,
-             int vchunk, int max_rounds, int max_sweeps, double tol, double stagnate_below, unsigned long long* prof,
+             int vchunk, int max_rounds, int max_sweeps, double tol, double stagnate_below, double quad_margin,
+             unsigned long long* prof,
              unsigned long long* work, int join, int* smids, int spread_factor) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
@@ -899,7 +900,7 @@ __global__ void __launch_bounds__(JT, JACOBI_CTAS_PER_SM)
         // quadratic regime: this sweep leaves ~ C cur^2 with C = cur / prev^2 from the last step;
         // stop when that is far below the tolerance (saves the confirming sweep)
         const bool quad = sweep > 0 && cur < 1e-8 && prev > 0.0 && prev < 1e-3 &&
-                          (cur / (prev * prev)) * cur * cur <= 1e-2 * tol;
+                          (cur / (prev * prev)) * cur * cur <= quad_margin * tol;
         if (cur <= tol || quad || (cur < stagnate_below && cur > 0.25 * prev) || sweep + 1 == max_sweeps) {
           pr_.done = 1;
           pr_.sweeps = sweep + 1;
@@ -980,6 +981,9 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   int64_t n_max = 1;
   for (int i = 0; i < nprob; ++i) n_max = n[i] > n_max ? n[i] : n_max;
   const double stagnate_below = 32.0 * (double)n_max * 2.220446049250313e-16;
+  // the quadratic-regime stop: the sweep's predicted residual C cur^2 (C = cur / prev^2) below
+  // quad_margin * tol (FPI_JACOBI_QUAD overrides)
+  static const double quad_margin = getenv("FPI_JACOBI_QUAD") ? atof(getenv("FPI_JACOBI_QUAD")) : 1e-1;
   std::vector<EigProb> hp(nprob);
   std::vector<int64_t> npad(nprob), goff(nprob);
   int64_t gsz = 0, jsz = 0, fsz = 0, tot_pairs = 0, tot_tri = 0, tot_vt = 0;
@@ -1075,7 +1079,7 @@ void sym_eig_batched(fpi_context* h, int nprob, const int64_t* n, const double* 
   int spread = 8;
   if (const char* e = getenv("FPI_JACOBI_SPREAD")) spread = atoi(e) > 0 ? atoi(e) : 1 << 20;
   void* args[] = {&Pp, &nprob, &tot_pairs, &tot_g, &tot_v, &gch, &vch, &max_rounds, &max_sweeps, &tol,
-                  (void*)&stagnate_below, &prof_p, &work_p, &join, &smids_p, &spread};
+                  (void*)&stagnate_below, (void*)&quad_margin, &prof_p, &work_p, &join, &smids_p, &spread};
   {
     KTimer kt(h, "sym_eig_block_jacobi", 0.0, 0.0);
     FPI_CUDA(cudaLaunchCooperativeKernel((void*)k_jacobi, grid, JT, args, JACOBI_SMEM, s));

@@ -612,6 +612,7 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
           if (d > 0 && (int64_t)d >= pre[side]) {
             const int pos = atomicAdd(&ctl->nhub[side], 1);
             P.hubkeys[side * HUB_CAP + pos] = ((uint64_t)(0xffffffffu - (uint32_t)d) << 32) | (uint32_t)v;
+            P.state[v] = 0;  // retired now: the hooking below (same phase as the ranks) skips it
           }
         }
       } else {
@@ -651,6 +652,7 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
             if ((int64_t)d > pre[side] || (eq && eqrank < need[side])) {
               const int pos = atomicAdd(&ctl->nhub[side], 1);
               P.hubkeys[side * HUB_CAP + pos] = ((uint64_t)(0xffffffffu - (uint32_t)d) << 32) | (uint32_t)v;
+              P.state[v] = 0;
             }
           }
           base0 += field21(tot, 0);
@@ -676,10 +678,10 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
             P.col_fwd[v - m] = hi_f - r;
           else
             P.row_fwd[v] = hi_t - r;
-          P.state[v] = 0;
         }
       }
-      grid.sync();
+      // (no barrier: the ranks only write the permutations, the hooking below reads states that
+      // were final at the collection barrier)
       RP_PROF(3)
       hi_t -= htot[0];
       hi_f -= htot[1];
@@ -704,6 +706,7 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
       int32_t r = v, p;
       while ((p = ld_(P.parent + r)) != r) r = p;
       P.parent[v] = r;
+      P.deg[v] = 0;  // this iteration's degrees are spent; the compaction below counts the next ones
       agg_inc(P.csize, r);
       if (v < m) agg_inc(P.crows, r);
     }
@@ -771,6 +774,28 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
         if (mx) atomicMax(&ctl->maxsz, (int)mx);
       }
     }
+    // ---- P15: compact the edge list to the new giant component (unordered), counting the next
+    // iteration's degrees on the way (reorder.py:201-202).  Runs in the same phase as the partition
+    // counts: an edge stays iff both endpoints' labels are the giant root (hubs retired this
+    // iteration keep parent == self, spoke nodes carry their own roots), read before P10 resets them.
+    for (int64_t e0 = gtid - lane; e0 < ne; e0 += gsz) {
+      const int64_t e = e0 + lane;
+      bool keep = false;
+      uint64_t ed = 0;
+      if (e < ne) {
+        ed = ld_(E + e);
+        keep = ld_(P.parent + (int32_t)(ed >> 32)) == gcc && ld_(P.parent + (int32_t)(ed & 0xffffffffu) + m) == gcc;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&ctl->ne_next[par], __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (keep) {
+        E_nx[base + __popc(bal & lanemask_lt())] = ed;
+        agg_inc(P.deg, (int32_t)(ed >> 32));
+        agg_inc(P.deg, (int32_t)(ed & 0xffffffffu) + m);
+      }
+    }
     grid.sync();
     RP_PROF(7)
     // ---- P10: partition write; giant members reset for the next iteration, spokes retired
@@ -795,7 +820,6 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
         BlockScanU64(sm.scan.u64).ExclusiveSum(x, ex, tot);
         if (cls == 0) {
           act_nx[b0 + field21(ex, 0)] = v;
-          P.deg[v] = 0;
           P.parent[v] = v;
           P.csize[v] = 0;
           P.crows[v] = 0;
@@ -819,6 +843,12 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
     }
     grid.sync();
     RP_PROF(8)
+    ne = __ldcg(&ctl->ne_next[par]);
+    {
+      uint64_t* tmp = E;
+      E = E_nx;
+      E_nx = tmp;
+    }
 
     const bool stop = g_t < q_t || g_f < q_f;  // reorder.py:268-269
     maxsz_all = maxsz > maxsz_all ? maxsz : maxsz_all;
@@ -838,33 +868,6 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
     }
     if (stop) break;
 
-    // ---- P15: compact the edge list to the new giant component
-    for (int64_t e0 = gtid - lane; e0 < ne; e0 += gsz) {
-      const int64_t e = e0 + lane;
-      bool keep = false;
-      uint64_t ed = 0;
-      if (e < ne) {
-        ed = ld_(E + e);
-        keep = ld_(P.state + (int32_t)(ed >> 32)) && ld_(P.state + (int32_t)(ed & 0xffffffffu) + m);
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(&ctl->ne_next[par], __popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (keep) {
-        E_nx[base + __popc(bal & lanemask_lt())] = ed;
-        agg_inc(P.deg, (int32_t)(ed >> 32));  // next iteration's degrees (reorder.py:201-202)
-        agg_inc(P.deg, (int32_t)(ed & 0xffffffffu) + m);
-      }
-    }
-    grid.sync();
-    RP_PROF(9)
-    ne = __ldcg(&ctl->ne_next[par]);
-    {
-      uint64_t* tmp = E;
-      E = E_nx;
-      E_nx = tmp;
-    }
   }
   // ---- spoke blocks of all iterations at once (reorder.py:236-257): components ordered by
   // (iteration, size desc, min id asc) -- two stable LSD sorts of the root log (size key, then
