@@ -699,29 +699,27 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
     grid.sync();
     if (P.prof && gtid == 0 && iters <= 5) P.prof[10 + iters] = gtimer() - tlast;
     RP_PROF(4)
-    // ---- P7: labels, sizes, row counts
-    for (int64_t i = gtid; i < L; i += gsz) {
-      const int32_t v = ld_(act + i);
-      if (!ld_(P.state + v)) continue;
-      int32_t r = v, p;
-      while ((p = ld_(P.parent + r)) != r) r = p;
-      P.parent[v] = r;
-      P.deg[v] = 0;  // this iteration's degrees are spent; the compaction below counts the next ones
-      agg_inc(P.csize, r);
-      if (v < m) agg_inc(P.crows, r);
-    }
-    grid.sync();
-    RP_PROF(5)
-    // ---- P8: giant component (max size, then min id) and the component count
+    // ---- P7: labels, sizes, row counts, and the giant component (max size, then min id,
+    // reorder.py:228-234) with the component count -- in one pass: a root's final size is the value
+    // its last (aggregated) size increment produces, so the max over every increment's result is
+    // the max over the final sizes
     {
       unsigned long long best = 0, nr = 0;
       for (int64_t i = gtid; i < L; i += gsz) {
         const int32_t v = ld_(act + i);
-        if (!ld_(P.state + v) || ld_(P.parent + v) != v) continue;
-        const unsigned long long key =
-            ((unsigned long long)(uint32_t)ld_(P.csize + v) << 32) | (uint32_t)(0x7fffffff - v);
-        best = key > best ? key : best;
-        ++nr;
+        if (!ld_(P.state + v)) continue;
+        int32_t r = v, p;
+        while ((p = ld_(P.parent + r)) != r) r = p;
+        P.parent[v] = r;
+        P.deg[v] = 0;  // this iteration's degrees are spent; the compaction below counts the next ones
+        const unsigned peers = __match_any_sync(__activemask(), r);
+        if (lane == __ffs(peers) - 1) {
+          const unsigned nsz = (unsigned)atomicAdd(P.csize + r, __popc(peers)) + (unsigned)__popc(peers);
+          const unsigned long long key = ((unsigned long long)nsz << 32) | (uint32_t)(0x7fffffff - r);
+          best = key > best ? key : best;
+        }
+        if (v < m) agg_inc(P.crows, r);
+        nr += r == v;
       }
       best = block_max(best, sm);
       nr = block_sum(nr, sm);
@@ -731,7 +729,7 @@ __global__ void __launch_bounds__(NT, RP_CTAS_PER_SM) k_reorder_persistent(Param
       }
     }
     grid.sync();
-    RP_PROF(6)
+    RP_PROF(5)
     const int64_t acnt = cnt_t + cnt_f;
     if (acnt == 0) {  // reorder.py:224-226
       if (gtid == 0) P.gcc_sizes[ngcc] = 0;
