@@ -362,6 +362,19 @@ __global__ void k_large_meta(int64_t nl, const int64_t* __restrict__ large, cons
 
 static int64_t smem_limit_doubles(fpi_context* h) { return (int64_t)(h->smem_optin - 1024) / 8; }
 
+__global__ void k_plan_tails(int64_t n, const int64_t* __restrict__ a0, const int64_t* __restrict__ a1,
+                             const int64_t* __restrict__ a2, const int64_t* __restrict__ a3,
+                             const int64_t* __restrict__ a4, const int64_t* __restrict__ a5, int64_t* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    out[0] = a0[n - 1];
+    out[1] = a1[n - 1];
+    out[2] = a2[n - 1];
+    out[3] = a3[n - 1];
+    out[4] = a4[n - 1];
+    out[5] = a5[n - 1];
+  }
+}
+
 static void plan(fpi_context* h, int64_t nspans, const int64_t* spans, double alpha, BlockSvdState& st) {
   cudaStream_t s = h->stream;
   st.nspans = nspans;
@@ -378,14 +391,12 @@ static void plan(fpi_context* h, int64_t nspans, const int64_t* spans, double al
   exclusive_sum(tmp, st.vk.get(), st.v_off.get(), nspans, s);
   FPI_LAUNCH_CHECK();
   note_launch(h, 4);
-  int64_t last[7];
-  FPI_CUDA(cudaMemcpyAsync(&last[0], st.rank_off.get() + nspans - 1, 8, cudaMemcpyDeviceToHost, s));
-  FPI_CUDA(cudaMemcpyAsync(&last[1], st.keep.get() + nspans - 1, 8, cudaMemcpyDeviceToHost, s));
-  FPI_CUDA(cudaMemcpyAsync(&last[2], st.u_off.get() + nspans - 1, 8, cudaMemcpyDeviceToHost, s));
-  FPI_CUDA(cudaMemcpyAsync(&last[3], st.uk.get() + nspans - 1, 8, cudaMemcpyDeviceToHost, s));
-  FPI_CUDA(cudaMemcpyAsync(&last[4], st.v_off.get() + nspans - 1, 8, cudaMemcpyDeviceToHost, s));
-  FPI_CUDA(cudaMemcpyAsync(&last[5], st.vk.get() + nspans - 1, 8, cudaMemcpyDeviceToHost, s));
-  FPI_CUDA(cudaStreamSynchronize(s));
+  // the six scan tails in one pinned read (one synchronisation instead of six pageable copies)
+  Scratch<int64_t> tails(6, s);
+  k_plan_tails<<<1, 32, 0, s>>>(nspans, st.rank_off, st.keep, st.u_off, st.uk, st.v_off, st.vk, tails);
+  FPI_LAUNCH_CHECK();
+  int64_t last[6];
+  host_read_n(tails.get(), last, 6, s);
   st.rank11 = last[0] + last[1];
   st.nnz_u = last[2] + last[3];
   st.nnz_v = last[4] + last[5];

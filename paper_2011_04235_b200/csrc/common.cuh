@@ -140,6 +140,17 @@ inline T host_read(const T* d, cudaStream_t s) {
   return v;
 }
 
+// n (<= 256 bytes of) device values to the host through the same pinned slot, one synchronisation
+template <typename T>
+inline void host_read_n(const T* d, T* out, int n, cudaStream_t s) {
+  static thread_local void* slot = nullptr;
+  if (!slot) FPI_CUDA(cudaMallocHost(&slot, 256));
+  if ((size_t)n * sizeof(T) > 256) throw Error(FPI_ECUDA, "host_read_n: too many values");
+  FPI_CUDA(cudaMemcpyAsync(slot, d, sizeof(T) * n, cudaMemcpyDeviceToHost, s));
+  FPI_CUDA(cudaStreamSynchronize(s));
+  memcpy(out, slot, sizeof(T) * n);
+}
+
 void note_launch(fpi_context* h, int count = 1);
 
 }  // namespace fpi

@@ -254,18 +254,27 @@ GramPlan plan_inner_gram(fpi_context* h, const SparseGramIn& in, int64_t k) {
   std::vector<int64_t> ptr(in.q2 + 1);
   FPI_CUDA(cudaMemcpyAsync(ptr.data(), in.st_ptr, sizeof(int64_t) * (in.q2 + 1), cudaMemcpyDeviceToHost, h->stream));
   FPI_CUDA(cudaStreamSynchronize(h->stream));
-  std::vector<int32_t> ord(in.q2);
-  for (int64_t c = 0; c < in.q2; ++c) ord[c] = (int32_t)c;
-  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) {
-    return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b];
-  });
-  // heavy: columns holding at least p / 256 (and 64) entries, at most 256 of them
+  // heavy: columns holding at least p / 256 (and 64) entries, at most 256 of them (the most
+  // populated; ties to the lower index) -- one pass, a partial selection only when over the cap
   const int64_t thresh = std::max<int64_t>(64, in.p / 256);
-  int64_t K = 0;
   const int64_t kmax = (int64_t)env_double("FPI_GRAM_HEAVY", 256);
-  while (K < in.q2 && K < kmax && ptr[ord[K] + 1] - ptr[ord[K]] >= thresh) ++K;
+  std::vector<int32_t> cand;
+  for (int64_t c = 0; c < in.q2; ++c)
+    if (ptr[c + 1] - ptr[c] >= thresh) cand.push_back((int32_t)c);
+  if ((int64_t)cand.size() > kmax) {
+    auto more = [&](int32_t a, int32_t b) {
+      const int64_t na = ptr[a + 1] - ptr[a], nb = ptr[b + 1] - ptr[b];
+      return na != nb ? na > nb : a < b;
+    };
+    std::nth_element(cand.begin(), cand.begin() + kmax, cand.end(), more);
+    cand.resize((size_t)kmax);
+    std::sort(cand.begin(), cand.end());
+  }
+  const int64_t K = (int64_t)cand.size();
   std::vector<char> isheavy(in.q2, 0);
-  for (int64_t a = 0; a < K; ++a) isheavy[ord[a]] = 1;
+  for (int32_t c : cand) isheavy[c] = 1;
+  pl.heavy.reserve((size_t)K);
+  pl.light.reserve((size_t)(in.q2 - K));
   for (int64_t c = 0; c < in.q2; ++c) {
     const int64_t n = ptr[c + 1] - ptr[c];
     if (isheavy[c]) {

@@ -350,6 +350,33 @@ class _Timer:
         self.seconds = time.perf_counter() - self.t0
 
 
+class _StageClock:
+    """Stage boundaries as CUDA events on the current stream: no host synchronisation inside the
+    solve (a wall-clock timer would drain the GPU at every stage edge and leave it idle while Python
+    sets up the next stage).  ``resolve`` waits for the last boundary once and returns the
+    reference's StageTime list (pinv.py:95-98) with device-measured seconds."""
+
+    def __init__(self):
+        self.t = torch()
+        self.t0 = time.perf_counter()
+        self.ev = [self._event()]
+        self.stages = []
+
+    def _event(self):
+        e = self.t.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def mark(self, stage: str, rank: int):
+        self.ev.append(self._event())
+        self.stages.append((stage, int(rank)))
+
+    def resolve(self) -> list:
+        self.ev[-1].synchronize()
+        return [StageTime(name, self.ev[i].elapsed_time(self.ev[i + 1]) * 1e-3, rank)
+                for i, (name, rank) in enumerate(self.stages)]
+
+
 _TRACE = bool(__import__("os").environ.get("FPI_TRACE_REORDER"))
 
 
@@ -362,41 +389,36 @@ def _trace_mark(label, tm):
 def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = None) -> FastpiResult:
     """Algorithm 1 on a canonical device CSR (m >= n); everything stays in HBM."""
     m, n = dev.shape
-    timings = []
-    with _Timer() as tm:
-        ordering = reorder_device(dev, cfg.k)
-        if _TRACE:
-            _trace_mark("reorder_device", tm)
-        part = partition_original(dev, ordering, transposes=True)
-    timings.append(StageTime("reorder", tm.seconds, 0))
+    clock = _StageClock()
+    ordering = reorder_device(dev, cfg.k)
+    if _TRACE:
+        _trace_mark("reorder_device", clock)
+    part = partition_original(dev, ordering, transposes=True)
+    clock.mark("reorder", 0)
 
-    with _Timer() as tm:
-        f11 = block_diagonal_svd_device(part.a11, ordering.spans_device(), cfg.alpha)
-    timings.append(StageTime("block_svd", tm.seconds, f11.rank))
+    f11 = block_diagonal_svd_device(part.a11, ordering.spans_device(), cfg.alpha)
+    clock.mark("block_svd", f11.rank)
 
     n1, m2, n2 = ordering.n_spoke_cols, ordering.n_hub_rows, ordering.n_hub_cols
-    with _Timer() as tm:
-        want_s = math.ceil(cfg.alpha * n1)
-        s = min(want_s, f11.rank + m2, n1)
-        if s < want_s:
-            warnings.warn(f"row-update target rank clamped from {want_s} to {s} "
-                          "(block stage produced less derivable rank)")
-        f_rows, eng_r = row_update_device(f11, part.a21, s, low_rank_threshold=cfg.low_rank_threshold,
-                                          seed=cfg.seed + 1)
-        diag_r = _lib.svd_diag() if stats is not None else None
-    timings.append(StageTime("row_update", tm.seconds, f_rows.rank))
+    want_s = math.ceil(cfg.alpha * n1)
+    s = min(want_s, f11.rank + m2, n1)
+    if s < want_s:
+        warnings.warn(f"row-update target rank clamped from {want_s} to {s} "
+                      "(block stage produced less derivable rank)")
+    f_rows, eng_r = row_update_device(f11, part.a21, s, low_rank_threshold=cfg.low_rank_threshold, seed=cfg.seed + 1)
+    diag_r = _lib.svd_diag() if stats is not None else None
+    clock.mark("row_update", f_rows.rank)
 
-    with _Timer() as tm:
-        r = min(math.ceil(cfg.alpha * n), f_rows.rank + n2, m)
-        f_full, eng_c = column_update_device(f_rows, part.T, part.Tt, r, low_rank_threshold=cfg.low_rank_threshold,
-                                             seed=cfg.seed + 2)
-        diag_c = _lib.svd_diag() if stats is not None else None
-    timings.append(StageTime("column_update", tm.seconds, f_full.rank))
+    r = min(math.ceil(cfg.alpha * n), f_rows.rank + n2, m)
+    f_full, eng_c = column_update_device(f_rows, part.T, part.Tt, r, low_rank_threshold=cfg.low_rank_threshold,
+                                         seed=cfg.seed + 2)
+    diag_c = _lib.svd_diag() if stats is not None else None
+    clock.mark("column_update", f_full.rank)
 
-    with _Timer() as tm:
-        pv = _assemble(f_full, ordering.row_perm.device_forward(), ordering.col_perm.device_forward(),
-                       cfg.pinv_cutoff_factor)
-    timings.append(StageTime("pinv_assembly", tm.seconds, pv.retained_rank))
+    pv = _assemble(f_full, ordering.row_perm.device_forward(), ordering.col_perm.device_forward(),
+                   cfg.pinv_cutoff_factor)
+    clock.mark("pinv_assembly", pv.retained_rank)
+    timings = clock.resolve()
     if stats is not None:
         stats.update(engines=(eng_r, eng_c), s=s, r=r, rank11=f11.rank, m1=ordering.n_spoke_rows, n1=n1, m2=m2,
                      n2=n2, T=ordering.n_iterations, nnz_a12=part.info.nnz_a12, nnz_a22=part.info.nnz_a22,

@@ -51,7 +51,7 @@ import numpy as np
 
 from . import _lib
 from ._device import DeviceCSR, d2h, empty, torch
-from .pinv import FastpiConfig, StageTime, _Timer, fastpi_device
+from .pinv import FastpiConfig, StageTime, _StageClock, fastpi_device
 from .reorder import partition_original, reorder_device
 
 PLAN_FIELDS = ("b_lo", "b_hi", "r_lo", "r_hi", "c_lo", "c_hi", "h_lo", "h_hi", "hc_lo", "hc_hi")
@@ -257,11 +257,10 @@ def fastpi_sharded(dev: DeviceCSR, cfg: FastpiConfig, comm: Comm | None = None, 
     m, n = dev.shape
     if m < n:
         raise ValueError("fastpi_sharded expects m >= n (transpose the problem first)")
-    timings = []
-    with _Timer() as tm:
-        ordering = reorder_device(dev, cfg.k)
-        part = partition_original(dev, ordering, transposes=False)
-    timings.append(StageTime("reorder", tm.seconds, 0))
+    clock = _StageClock()
+    ordering = reorder_device(dev, cfg.k)
+    part = partition_original(dev, ordering, transposes=False)
+    clock.mark("reorder", 0)
     m1, n1 = ordering.n_spoke_rows, ordering.n_spoke_cols
     m2, n2 = ordering.n_hub_rows, ordering.n_hub_cols
     plan = shard_plan(ordering, part.T, comm.world)
@@ -270,20 +269,19 @@ def fastpi_sharded(dev: DeviceCSR, cfg: FastpiConfig, comm: Comm | None = None, 
     nsp = int(spans.numel() // 4)
     thr = cfg.low_rank_threshold
 
-    with _Timer() as tm:
-        bplan = _lib.BlockPlan()
-        _lib.call("fpi_block_svd_plan", nsp, _lib.ptr(spans), float(cfg.alpha), C.byref(bplan))
-        rank11 = int(bplan.rank11)
-        U11 = DeviceCSR.empty(m1, rank11, bplan.nnz_u11)
-        Vt11 = DeviceCSR.empty(rank11, n1, bplan.nnz_vt11)
-        sig11 = empty(rank11)
-        krange = (C.c_int64 * 2)()
-        _lib.call("fpi_block_svd_range", m1, n1, _lib.ptr(part.a11.indptr), _lib.ptr(part.a11.indices),
-                  _lib.ptr(part.a11.values), nsp, _lib.ptr(spans), float(cfg.alpha), P["b_lo"], P["b_hi"],
-                  _lib.ptr(sig11), _lib.ptr(U11.indptr), _lib.ptr(U11.indices), _lib.ptr(U11.values),
-                  _lib.ptr(Vt11.indptr), _lib.ptr(Vt11.indices), _lib.ptr(Vt11.values), C.byref(bplan), krange)
-        k_lo, k_hi = int(krange[0]), int(krange[1])
-    timings.append(StageTime("block_svd", tm.seconds, rank11))
+    bplan = _lib.BlockPlan()
+    _lib.call("fpi_block_svd_plan", nsp, _lib.ptr(spans), float(cfg.alpha), C.byref(bplan))
+    rank11 = int(bplan.rank11)
+    U11 = DeviceCSR.empty(m1, rank11, bplan.nnz_u11)
+    Vt11 = DeviceCSR.empty(rank11, n1, bplan.nnz_vt11)
+    sig11 = empty(rank11)
+    krange = (C.c_int64 * 2)()
+    _lib.call("fpi_block_svd_range", m1, n1, _lib.ptr(part.a11.indptr), _lib.ptr(part.a11.indices),
+              _lib.ptr(part.a11.values), nsp, _lib.ptr(spans), float(cfg.alpha), P["b_lo"], P["b_hi"],
+              _lib.ptr(sig11), _lib.ptr(U11.indptr), _lib.ptr(U11.indices), _lib.ptr(U11.values),
+              _lib.ptr(Vt11.indptr), _lib.ptr(Vt11.indices), _lib.ptr(Vt11.values), C.byref(bplan), krange)
+    k_lo, k_hi = int(krange[0]), int(krange[1])
+    clock.mark("block_svd", rank11)
 
     want_s = math.ceil(cfg.alpha * n1)
     s = min(want_s, rank11 + m2, n1)
@@ -298,45 +296,43 @@ def fastpi_sharded(dev: DeviceCSR, cfg: FastpiConfig, comm: Comm | None = None, 
     r_rows, m2_loc = P["r_hi"] - P["r_lo"], P["h_hi"] - P["h_lo"]
     nc_loc = P["c_hi"] - P["c_lo"]
     zoff = np.ascontiguousarray(np.append(plan[:, 4], n1).astype(np.int64))  # spoke-column ranges
-    with _Timer() as tm:
-        U_rows = empty((r_rows + m2_loc, s))
-        sig_rows = empty(s)
-        Vt_rows = empty((s, nc_loc))
-        _lib.call("fpi_row_update_shard", n1, _lib.ptr(sig11), _lib.ptr(Vt11.indptr), _lib.ptr(Vt11.indices),
-                  _lib.ptr(Vt11.values), k_lo, k_hi - k_lo, _lib.ptr(U11.indptr), _lib.ptr(U11.indices),
-                  _lib.ptr(U11.values), P["r_lo"], r_rows, _lib.ptr(part.a21.indptr), _lib.ptr(part.a21.indices),
-                  _lib.ptr(part.a21.values), P["h_lo"], m2_loc, rank11 + m2, s, float(thr), cfg.seed + 1,
-                  zoff.ctypes.data_as(C.c_void_p), _lib.ptr(U_rows), _lib.ptr(sig_rows), _lib.ptr(Vt_rows))
-        diag_r = _lib.svd_diag() if stats is not None else None
-    timings.append(StageTime("row_update", tm.seconds, s))
+    U_rows = empty((r_rows + m2_loc, s))
+    sig_rows = empty(s)
+    Vt_rows = empty((s, nc_loc))
+    _lib.call("fpi_row_update_shard", n1, _lib.ptr(sig11), _lib.ptr(Vt11.indptr), _lib.ptr(Vt11.indices),
+              _lib.ptr(Vt11.values), k_lo, k_hi - k_lo, _lib.ptr(U11.indptr), _lib.ptr(U11.indices),
+              _lib.ptr(U11.values), P["r_lo"], r_rows, _lib.ptr(part.a21.indptr), _lib.ptr(part.a21.indices),
+              _lib.ptr(part.a21.values), P["h_lo"], m2_loc, rank11 + m2, s, float(thr), cfg.seed + 1,
+              zoff.ctypes.data_as(C.c_void_p), _lib.ptr(U_rows), _lib.ptr(sig_rows), _lib.ptr(Vt_rows))
+    diag_r = _lib.svd_diag() if stats is not None else None
+    clock.mark("row_update", s)
 
-    with _Timer() as tm:
-        T_loc = _rows_of(part.T, [(P["r_lo"], P["r_hi"]), (m1 + P["h_lo"], m1 + P["h_hi"])])
-        Tt_loc = T_loc.transpose()
-        m_loc = T_loc.shape[0]
-        nh_loc = P["hc_hi"] - P["hc_lo"]
-        U_loc = empty((m_loc, r))
-        sig = empty(r)
-        Vt_loc = empty((r, nc_loc + nh_loc))
-        _lib.call("fpi_column_update_shard", m_loc, s, _lib.ptr(U_rows), _lib.ptr(sig_rows), _lib.ptr(Vt_rows),
-                  nc_loc, n2, _lib.ptr(T_loc.indptr), _lib.ptr(T_loc.indices), _lib.ptr(T_loc.values),
-                  _lib.ptr(Tt_loc.indptr), _lib.ptr(Tt_loc.indices), _lib.ptr(Tt_loc.values), m, P["hc_lo"],
-                  P["hc_hi"], r, float(thr), cfg.seed + 2, _lib.ptr(U_loc), _lib.ptr(sig), _lib.ptr(Vt_loc))
-        diag_c = _lib.svd_diag() if stats is not None else None
-    timings.append(StageTime("column_update", tm.seconds, r))
+    T_loc = _rows_of(part.T, [(P["r_lo"], P["r_hi"]), (m1 + P["h_lo"], m1 + P["h_hi"])])
+    Tt_loc = T_loc.transpose()
+    m_loc = T_loc.shape[0]
+    nh_loc = P["hc_hi"] - P["hc_lo"]
+    U_loc = empty((m_loc, r))
+    sig = empty(r)
+    Vt_loc = empty((r, nc_loc + nh_loc))
+    _lib.call("fpi_column_update_shard", m_loc, s, _lib.ptr(U_rows), _lib.ptr(sig_rows), _lib.ptr(Vt_rows),
+              nc_loc, n2, _lib.ptr(T_loc.indptr), _lib.ptr(T_loc.indices), _lib.ptr(T_loc.values),
+              _lib.ptr(Tt_loc.indptr), _lib.ptr(Tt_loc.indices), _lib.ptr(Tt_loc.values), m, P["hc_lo"],
+              P["hc_hi"], r, float(thr), cfg.seed + 2, _lib.ptr(U_loc), _lib.ptr(sig), _lib.ptr(Vt_loc))
+    diag_c = _lib.svd_diag() if stats is not None else None
+    clock.mark("column_update", r)
 
-    with _Timer() as tm:
-        sdag = empty(r)
-        tol = C.c_double(0.0)
-        af = C.c_int32(0)
-        _lib.call("fpi_pinv_assemble", r, _lib.ptr(sig), m, n, float(cfg.pinv_cutoff_factor), _lib.ptr(sdag),
-                  C.byref(tol), C.byref(af))
-        if af.value:
-            warnings.warn("every singular value fell below the cutoff; the pseudoinverse is zero")
-        pv = ShardedPseudoinverse(comm, plan[comm.rank], m, n, m1, n1, U_loc, sdag, Vt_loc,
-                                  ordering.row_perm.device_forward(), ordering.col_perm, float(tol.value),
-                                  bool(af.value))
-    timings.append(StageTime("pinv_assembly", tm.seconds, r))
+    sdag = empty(r)
+    tol = C.c_double(0.0)
+    af = C.c_int32(0)
+    _lib.call("fpi_pinv_assemble", r, _lib.ptr(sig), m, n, float(cfg.pinv_cutoff_factor), _lib.ptr(sdag),
+              C.byref(tol), C.byref(af))
+    if af.value:
+        warnings.warn("every singular value fell below the cutoff; the pseudoinverse is zero")
+    pv = ShardedPseudoinverse(comm, plan[comm.rank], m, n, m1, n1, U_loc, sdag, Vt_loc,
+                              ordering.row_perm.device_forward(), ordering.col_perm, float(tol.value),
+                              bool(af.value))
+    clock.mark("pinv_assembly", r)
+    timings = clock.resolve()
     if stats is not None:
         stats.update(engines=(1, 1), s=s, r=r, rank11=rank11, m1=m1, n1=n1, m2=m2, n2=n2,
                      T=ordering.n_iterations, plan=plan, world=comm.world, sharded=True, svd_diag_row=diag_r,

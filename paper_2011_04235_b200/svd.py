@@ -44,21 +44,34 @@ class SvdFactors:
         self.is_sorted = bool(is_sorted)
         self._U = U
         self._Vt = Vt
+        self._sigma = None
         if _dev is not None:
-            self.sigma = d2h(_dev.sigma).astype(np.float64).ravel()
+            # factors produced on the device: sigma is copied to the host on first access only, so a
+            # stage hands its factors to the next one without draining the stream (the kernels emit
+            # non-negative, and when flagged sorted, non-increasing sigma)
             if _shape is None:
                 _shape = (int(_dev.U.shape[0]), int(_dev.Vt.shape[1]))
             self._shape = _shape
-        else:
-            self.sigma = np.asarray(sigma, dtype=np.float64).ravel()
-            if U.shape[1] != len(self.sigma) or Vt.shape[0] != len(self.sigma):
-                raise ValueError(f"inconsistent factor shapes: U {U.shape}, sigma ({len(self.sigma)},), "
-                                 f"Vt {Vt.shape}")
-            self._shape = (U.shape[0], Vt.shape[1])
-        if len(self.sigma) and self.sigma.min() < 0:
+            return
+        self._sigma = np.asarray(sigma, dtype=np.float64).ravel()
+        if U.shape[1] != len(self._sigma) or Vt.shape[0] != len(self._sigma):
+            raise ValueError(f"inconsistent factor shapes: U {U.shape}, sigma ({len(self._sigma)},), "
+                             f"Vt {Vt.shape}")
+        self._shape = (U.shape[0], Vt.shape[1])
+        if len(self._sigma) and self._sigma.min() < 0:
             raise ValueError("singular values must be non-negative")
-        if self.is_sorted and len(self.sigma) > 1 and np.any(np.diff(self.sigma) > 0):
+        if self.is_sorted and len(self._sigma) > 1 and np.any(np.diff(self._sigma) > 0):
             raise ValueError("factors flagged sorted but sigma is not non-increasing")
+
+    @property
+    def sigma(self) -> np.ndarray:
+        if self._sigma is None:
+            self._sigma = d2h(self._dev.sigma).astype(np.float64).ravel()
+        return self._sigma
+
+    @sigma.setter
+    def sigma(self, value):
+        self._sigma = np.asarray(value, dtype=np.float64).ravel()
 
     # -- host views (lazy) --------------------------------------------------
     @property
@@ -75,7 +88,9 @@ class SvdFactors:
 
     @property
     def rank(self) -> int:
-        return len(self.sigma)
+        if self._sigma is None:
+            return int(self._dev.sigma.numel())
+        return len(self._sigma)
 
     @property
     def shape(self) -> tuple:
