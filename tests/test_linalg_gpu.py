@@ -32,7 +32,8 @@ def test_gemm(ta, tb, M, N, K):
 
 
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
-@pytest.mark.parametrize("M,N,K", [(64, 128, 32), (200, 136, 1000), (130, 258, 4096), (1000, 500, 20000)])
+@pytest.mark.parametrize("M,N,K", [(2, 2, 2), (6, 18, 4), (64, 128, 32), (200, 136, 1000), (130, 258, 4096),
+                                   (1000, 500, 20000)])
 @pytest.mark.parametrize("tma", [True, False])
 def test_gemm_tma_path(ta, tb, M, N, K, tma, monkeypatch):
     """Even leading dimensions and 16-byte aligned operands of the NT / TN layouts take the TMA-fed
