@@ -395,7 +395,8 @@ def ours_arm(args):
             largest = {"kernel": big_name, "share_of_step": round(big["ms"] / ms, 4), "launches": big["launches"],
                        "bound": "latency",
                        "note": "two-sided block Jacobi: sequential rotation chains + one grid barrier per round; "
-                               "ncu shows the DMMA pipe ~1.5% active (profiles/r01_ncu_full_summary_v13.json)"}
+                               "ncu (c4 n = 1000 launch): DMMA sub-pipe 24% active, 4.9 barrier stalls per issue "
+                               "(profiles/r02_ncu_jacobi_final.json)"}
         if roofline is not None:
             roofline["largest_kernel"] = largest
 
