@@ -96,6 +96,101 @@ __global__ void k_iota32(int32_t* a, int64_t n) {
   FPI_GRID_STRIDE(i, n) a[i] = (int32_t)i;
 }
 
+// The finish of many small dense SVDs at once (dense_svd_batched), one CTA per panel: sigma =
+// column norms of Uraw = M W[:, :r], sorted descending (stable: ties keep index order), Vt = the
+// matching eigenvector columns with the canonical sign (largest-|.| entry positive, first index on
+// ties), U = sign * Uraw[:, ord] / sigma; zero_flag[i] = 1 when a sigma is at rounding level (the
+// caller completes those left vectors).  Same results as the per-panel kernel sequence.
+struct PanelDesc {
+  int64_t p, q, r;
+  const double* Uraw;  // p x r
+  const double* W;     // q x q eigenvectors (columns)
+  double* U;           // p x r
+  double* sigma;       // r
+  double* Vt;          // r x q
+};
+
+__global__ void __launch_bounds__(256) k_panel_finish(const PanelDesc* __restrict__ desc, int nb,
+                                                      int* __restrict__ zero_flag) {
+  extern __shared__ double psm[];
+  __shared__ double rbv[8];
+  __shared__ int64_t rbi[8];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = blockIdx.x; i < nb; i += gridDim.x) {
+    const PanelDesc P = desc[i];
+    const int64_t p = P.p, q = P.q, r = P.r;
+    double* ss = psm;
+    double* ssd = psm + r;
+    double* sgn = psm + 2 * r;
+    int* ord = reinterpret_cast<int*>(psm + 3 * r);
+    for (int64_t j = tid; j < r; j += blockDim.x) {
+      double a = 0.0;
+      for (int64_t row = 0; row < p; ++row) {
+        const double v = P.Uraw[row * r + j];
+        a = fma(v, v, a);
+      }
+      ss[j] = a > 0.0 ? sqrt(a) : 0.0;
+    }
+    __syncthreads();
+    for (int64_t j = tid; j < r; j += blockDim.x) {
+      const double v = ss[j];
+      int64_t rk = 0;
+      for (int64_t l = 0; l < r; ++l) rk += (ss[l] > v) || (ss[l] == v && l < j);
+      ord[rk] = (int)j;
+      ssd[rk] = v;
+    }
+    __syncthreads();
+    for (int64_t k = tid; k < r; k += blockDim.x) P.sigma[k] = ssd[k];
+    for (int64_t k = 0; k < r; ++k) {
+      const int c = ord[k];
+      double bv = -1.0;
+      int64_t bi = 0;
+      for (int64_t jj = tid; jj < q; jj += blockDim.x) {
+        const double a = fabs(P.W[jj * q + c]);
+        if (a > bv) { bv = a; bi = jj; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) { rbv[wid] = bv; rbi[wid] = bi; }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w2 = 1; w2 < (int)(blockDim.x >> 5); ++w2)
+          if (rbv[w2] > rbv[0] || (rbv[w2] == rbv[0] && rbi[w2] < rbi[0])) { rbv[0] = rbv[w2]; rbi[0] = rbi[w2]; }
+        sgn[k] = (q > 0 && P.W[rbi[0] * q + c] < 0.0) ? -1.0 : 1.0;
+      }
+      __syncthreads();
+      const double sk = sgn[k];
+      for (int64_t jj = tid; jj < q; jj += blockDim.x) P.Vt[k * q + jj] = sk * P.W[jj * q + c];
+    }
+    __syncthreads();
+    for (int64_t e = tid; e < p * r; e += blockDim.x) {
+      const int64_t row = e / r, k = e - row * r;
+      const double d = ssd[k];
+      const double v = d > 0.0 ? P.Uraw[row * r + ord[k]] / d : 0.0;
+      P.U[row * r + k] = sgn[k] * v;
+    }
+    if (tid == 0) {
+      const double tol = 2.220446049250313e-16 * (ssd[0] > 0.0 ? ssd[0] : 1.0) * (double)(p > r ? p : r);
+      int z = 0;
+      for (int64_t k = 0; k < r; ++k) z |= !(ssd[k] > tol);
+      zero_flag[i] = z;
+    }
+    __syncthreads();
+  }
+}
+
+// lam[2 i] = w_i[0], lam[2 i + 1] = w_i[r_i - 1] (the wide-spectrum test of every panel at once)
+__global__ void k_lam_pairs(int nb, const double* const* __restrict__ w, const int64_t* __restrict__ r,
+                            double* __restrict__ lam) {
+  FPI_GRID_STRIDE(i, nb) {
+    lam[2 * i] = w[i][0];
+    lam[2 * i + 1] = w[i][r[i] - 1];
+  }
+}
+
 // rows [0, rank11) of the inner CSR: Vt11 rows scaled by sigma; rows after: A21
 __global__ void k_inner_rows(int64_t rank11, int64_t m2, const int64_t* __restrict__ vptr,
                              const int64_t* __restrict__ aptr, int64_t nnz_v, int64_t* __restrict__ iptr) {
@@ -409,35 +504,64 @@ void dense_svd_batched(fpi_context* h, int nb, const int64_t* p, const int64_t* 
   }
   std::vector<int> sw(nb);
   sym_eig_batched(h, nb, q, Gp.data(), ldq.data(), wp.data(), Wp.data(), ldq.data(), 60, 1e-15, true, sw.data());
+  // wide-spectrum test of every panel in one copy
   std::vector<double> hl(2 * nb);
-  for (int i = 0; i < nb; ++i) {
-    FPI_CUDA(cudaMemcpyAsync(&hl[2 * i], wp[i], sizeof(double), cudaMemcpyDeviceToHost, s));
-    FPI_CUDA(cudaMemcpyAsync(&hl[2 * i + 1], wp[i] + rank[i] - 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+  {
+    Scratch<const double*> dw(nb, s);
+    Scratch<int64_t> dr(nb, s);
+    Scratch<double> dl(2 * nb, s);
+    std::vector<const double*> wpc(wp.begin(), wp.end());
+    FPI_CUDA(cudaMemcpyAsync(dw.get(), wpc.data(), sizeof(double*) * nb, cudaMemcpyHostToDevice, s));
+    FPI_CUDA(cudaMemcpyAsync(dr.get(), rank, sizeof(int64_t) * nb, cudaMemcpyHostToDevice, s));
+    k_lam_pairs<<<grid_for(nb, 256, G), 256, 0, s>>>(nb, dw, dr, dl);
+    FPI_LAUNCH_CHECK();
+    FPI_CUDA(cudaMemcpyAsync(hl.data(), dl.get(), sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
   }
-  FPI_CUDA(cudaStreamSynchronize(s));
-  CubTemp tmp(s);
+  // panels with a narrow kept spectrum: Uraw GEMMs, then one batched finish; wide ones: refined path
+  std::vector<int> fin;
+  int64_t tot_u = 0, rmax = 0;
   for (int i = 0; i < nb; ++i) {
-    const int64_t r = rank[i];
     if (!(hl[2 * i] > 0.0) || hl[2 * i + 1] < 1e-6 * hl[2 * i]) {  // wide spectrum: refined path
-      dense_svd(h, p[i], q[i], M[i], ldm[i], r, U[i], sigma[i], Vt[i], nullptr);
+      dense_svd(h, p[i], q[i], M[i], ldm[i], rank[i], U[i], sigma[i], Vt[i], nullptr);
       continue;
     }
-    Scratch<double> Uraw(p[i] * r, s), ss(r, s), ss2(r, s);
-    Scratch<int32_t> ord(r, s), ord2(r, s);
-    gemm(h, false, false, p[i], r, q[i], 1.0, M[i], ldm[i], Wp[i], q[i], 0.0, Uraw, r);
-    col_sumsq(h, p[i], r, Uraw, r, ss);
-    k_sqrt_clamp<<<grid_for(r, 256, G), 256, 0, s>>>(r, ss);
-    k_iota32<<<grid_for(r, 256, G), 256, 0, s>>>(ord, r);
-    sort_pairs(tmp, ss.get(), ss2.get(), ord.get(), ord2.get(), r, true, 0, 64, s);
-    FPI_CUDA(cudaMemcpyAsync(sigma[i], ss2.get(), sizeof(double) * r, cudaMemcpyDeviceToDevice, s));
-    Scratch<double> sgn(r, s);
-    k_gather_vt<<<grid_for(r * q[i], 256, G), 256, 0, s>>>(q[i], r, Wp[i], q[i], ord2, Vt[i], q[i]);
-    canonical_signs_vt(h, r, q[i], Vt[i], q[i], sgn);
-    k_gather_cols_div<<<grid_for(p[i] * r, 256, G), 256, 0, s>>>(p[i], r, Uraw, r, ord2, ss2, sgn, U[i], r);
-    FPI_LAUNCH_CHECK();
-    note_launch(h, 5);
-    complete_null_left(h, p[i], r, U[i], r, sigma[i], nullptr);
+    fin.push_back(i);
+    tot_u += p[i] * rank[i];
+    rmax = std::max(rmax, rank[i]);
   }
+  if (fin.empty()) return;
+  const int nf = (int)fin.size();
+  Scratch<double> Uraw_all(tot_u + 1, s);
+  std::vector<PanelDesc> pd(nf);
+  int64_t ou = 0;
+  for (int f = 0; f < nf; ++f) {
+    const int i = fin[f];
+    double* Uraw = Uraw_all.get() + ou;
+    gemm(h, false, false, p[i], rank[i], q[i], 1.0, M[i], ldm[i], Wp[i], q[i], 0.0, Uraw, rank[i]);
+    pd[f] = PanelDesc{p[i], q[i], rank[i], Uraw, Wp[i], U[i], sigma[i], Vt[i]};
+    ou += p[i] * rank[i];
+  }
+  Scratch<PanelDesc> dpd(nf, s);
+  Scratch<int> zf(nf, s);
+  FPI_CUDA(cudaMemcpyAsync(dpd.get(), pd.data(), sizeof(PanelDesc) * nf, cudaMemcpyHostToDevice, s));
+  const size_t psmem = (size_t)rmax * (3 * sizeof(double) + sizeof(int)) + 16;
+  FPI_REQUIRE(psmem <= h->smem_optin, FPI_ECAPACITY, "batched SVD finish: kept rank too large for shared memory");
+  if (psmem > 48 * 1024) {
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, h->device, [&] {
+      FPI_CUDA(cudaFuncSetAttribute(k_panel_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(h->smem_optin - 1024)));
+    });
+  }
+  k_panel_finish<<<(unsigned)std::min<int64_t>(nf, (int64_t)h->num_sms * 4), 256, psmem, s>>>(dpd, nf, zf);
+  FPI_LAUNCH_CHECK();
+  note_launch(h);
+  std::vector<int> hz(nf);
+  FPI_CUDA(cudaMemcpyAsync(hz.data(), zf.get(), sizeof(int) * nf, cudaMemcpyDeviceToHost, s));
+  FPI_CUDA(cudaStreamSynchronize(s));
+  for (int f = 0; f < nf; ++f)
+    if (hz[f]) complete_null_left(h, p[fin[f]], rank[fin[f]], U[fin[f]], rank[fin[f]], sigma[fin[f]], nullptr);
 }
 
 // Orthonormal completion of left vectors whose sigma is numerically zero
