@@ -596,8 +596,10 @@ void launch_any(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, c
   // TMA for the NT / TN layouts (both operands contiguous along the same dimension: the fixed
   // 128-byte swizzle then admits conflict-free fragment loads); NN / TT keep the padded cp.async
   // tiles (with TMA one operand's loads would be 2-way bank-conflicted: measured 7% slower)
+  // (symmetric Gram products stay on cp.async: with TMA their lower-tile / long split-K grids measured
+  // 3-35% slower -- tools/gram_bench.py: 256^2 x 2M 18.4 vs 24.8, 940^2 x 349k 25.4 vs 29.1 TFLOP/s)
   if constexpr (TA != TB) {
-    if (v16 && !no_tma && launch_tma<TA, TB>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym)) return;
+    if (v16 && !no_tma && !sym && launch_tma<TA, TB>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym)) return;
   }
   if (v16) launch<TA, TB, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym);
   else launch<TA, TB, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sym);

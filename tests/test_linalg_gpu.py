@@ -66,7 +66,7 @@ def test_gemm_tma_path(ta, tb, M, N, K, tma, monkeypatch):
 
 @pytest.mark.parametrize("ta", [0, 1])
 def test_gram_sym_tma(ta):
-    """Symmetric (Gram) mode through the TMA kernel: lower tiles computed and mirrored."""
+    """Symmetric (Gram) mode: lower tiles computed and mirrored (exactly symmetric result)."""
     from paper_2011_04235_b200 import _lib
     from paper_2011_04235_b200._device import d2h
     rng = np.random.default_rng(5)

@@ -18,6 +18,9 @@ SHAPES = [  # (name, ta, tb, M, N, K)
     ("YtU_c5", 1, 0, 2000, 1000, 2000000),
     ("U_eq_Y_X_c5", 0, 0, 2000000, 1000, 2000),
     ("Gram_NT_c4", 0, 1, 1000, 1000, 200000),
+    ("HH_TN_c5", 1, 0, 256, 256, 2000000),
+    ("H11_TN_c5", 1, 0, 939, 939, 349000),
+    ("H21h_TN_c5", 1, 0, 256, 939, 349000),
     ("Z_L_NT_c4", 0, 1, 10684, 1000, 1000),
 ]
 

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_linalg_gpu.py tests/test_pipeline_gpu.py -q -x > gpurun_out/gpu_tests29.log 2>&1; echo tests_exit=$? >> gpurun_out/gpu_tests29.log
+timeout 600 python bench.py --no-cpu-baseline --no-e2e --no-c5 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
+timeout 900 python bench.py --workload c5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+echo done
