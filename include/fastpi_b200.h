@@ -175,6 +175,8 @@ typedef struct {
   int32_t rank_clamped;           /* s < ceil(alpha n1): the pinv.py:324-328 warning */
   int32_t all_filtered;           /* every sigma below the cutoff: the pinv.py:222-224 warning */
   double tolerance_used;
+  int64_t n_gcc;                  /* len(gcc_sizes) (ReorderResult.gcc_sizes) */
+  int64_t edges_visited, nodes_visited; /* fpi_reorder_info's work counters */
 } fpi_fastpi_info;
 /* check_csr + reorder + partition + block SVD + row/column updates + pinv assembly on a CSR A (m >= n;
  * for m < n factor A^T and swap the factors, pinv.py:291-303) with FastpiConfig's fields; seed is the
@@ -189,6 +191,25 @@ int fpi_fastpi(fpi_handle h, int64_t m, int64_t n, int64_t nnz, const int64_t* d
 int fpi_fastpi_get(fpi_handle h, const double** d_U, const double** d_sigma, const double** d_Vt,
                    const double** d_sigma_dagger, const int64_t** d_row_fwd, const int64_t** d_col_fwd);
 int fpi_fastpi_release(fpi_handle h);
+/* fpi_fastpi with flags: FPI_FASTPI_CANONICAL = the CSR is canonical already (sorted, no duplicates,
+ * no explicit zeros -- what fpi_csr_canonicalize returns), so the check_csr copy is skipped. */
+#define FPI_FASTPI_CANONICAL 1
+int fpi_fastpi_ex(fpi_handle h, int64_t m, int64_t n, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
+                  const double* d_values, double alpha, double k, int64_t seed, double low_rank_threshold,
+                  double pinv_cutoff, int32_t flags, fpi_fastpi_info* h_info);
+/* Ownership transfer of the last fpi_fastpi result: the caller receives the device buffers below
+ * (stream-ordered allocations of the handle's device pool; free each with fpi_device_free) plus,
+ * optionally, the GCC sizes (h_gcc, capacity gcc_cap >= info.n_gcc) and the device time of the five
+ * stages reorder, block_svd, row_update, column_update, pinv_assembly in ms (h_stage_ms[5], pinv.py:95-98;
+ * waits for the solve to finish).  The handle no longer holds a result afterwards. */
+typedef struct {
+  double *U, *sigma, *Vt, *sigma_dagger; /* m x r, r, r x n, r */
+  int64_t *row_fwd, *col_fwd;            /* m, n */
+  int64_t* spans;                        /* n_spans x 4 (BlockSpan rows) */
+} fpi_fastpi_buffers;
+int fpi_fastpi_take(fpi_handle h, fpi_fastpi_buffers* out, int64_t* h_gcc, int64_t gcc_cap, float* h_stage_ms);
+/* Stream-ordered free (on the handle stream) of a buffer handed out by fpi_fastpi_take. */
+int fpi_device_free(fpi_handle h, void* d_ptr);
 
 /* ---- dataset text format (datasets.py:81-167), host-side native parser ---------------------- */
 enum fpi_dataset_error {

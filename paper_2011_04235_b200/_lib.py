@@ -51,7 +51,16 @@ class DatasetInfo(C.Structure):
 class FastpiInfo(C.Structure):
     _fields_ = [("m", i64), ("n", i64), ("rank", i64), ("m1", i64), ("n1", i64), ("m2", i64), ("n2", i64),
                 ("n_iterations", i64), ("n_spans", i64), ("rank11", i64), ("s", i64), ("row_engine", i32),
-                ("col_engine", i32), ("rank_clamped", i32), ("all_filtered", i32), ("tolerance_used", f64)]
+                ("col_engine", i32), ("rank_clamped", i32), ("all_filtered", i32), ("tolerance_used", f64),
+                ("n_gcc", i64), ("edges_visited", i64), ("nodes_visited", i64)]
+
+
+FASTPI_CANONICAL = 1  # fpi_fastpi_ex flag: the CSR is canonical already
+
+
+class FastpiBuffers(C.Structure):
+    _fields_ = [("U", vp), ("sigma", vp), ("Vt", vp), ("sigma_dagger", vp), ("row_fwd", vp), ("col_fwd", vp),
+                ("spans", vp)]
 
 
 class SvdDiag(C.Structure):
@@ -114,6 +123,10 @@ SIGNATURES = {
     "fpi_fastpi": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, f64, f64, i64, f64, f64, C.POINTER(FastpiInfo)]),
     "fpi_fastpi_get": (C.c_int, [vp] + [C.POINTER(vp)] * 6),
     "fpi_fastpi_release": (C.c_int, [vp]),
+    "fpi_fastpi_ex": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, f64, f64, i64, f64, f64, i32,
+                                C.POINTER(FastpiInfo)]),
+    "fpi_fastpi_take": (C.c_int, [vp, C.POINTER(FastpiBuffers), C.POINTER(i64), i64, C.POINTER(C.c_float)]),
+    "fpi_device_free": (C.c_int, [vp, vp]),
     "fpi_timing_enable": (C.c_int, [vp, C.c_int]),
     "fpi_timing_report": (C.c_int, [vp, C.c_char_p, i64, C.c_int]),
     "fpi_dmma_peak": (C.c_int, [vp, C.POINTER(f64)]),

@@ -16,6 +16,7 @@
 // Used for: U.Sigma x X1 and Q^T inner (svd.py:133,135 dense parts), the
 // Gram matrices of CholeskyQR and of the small SVD, the lifts
 // (pinv.py:169,206) and V (Sigma+ U^T Y) (pinv.py:81).
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 
@@ -618,10 +619,29 @@ void gemm(fpi_context* h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
   }
   KTimer kt(h, "gemm_f64_dmma", (sy ? 1.0 : 2.0) * (double)M * (double)N * (double)K,
             8.0 * ((double)M * K + (double)K * N + (beta == 0.0 ? 1.0 : 2.0) * (double)M * N));
+  // FPI_GEMM_LOG=1: shape and device time of every product on stderr (serialising; diagnostics only)
+  static const bool log = getenv("FPI_GEMM_LOG") != nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (log) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, h->stream);
+  }
   if (!ta && !tb) launch_any<false, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
   else if (!ta && tb) launch_any<false, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sy);
   else if (ta && !tb) launch_any<true, false>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, sy);
   else launch_any<true, true>(h, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, 0);
+  if (log) {
+    cudaEventRecord(e1, h->stream);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    fprintf(stderr, "[gemm] %c%c sym=%d M=%lld N=%lld K=%lld %.3f ms %.1f TFLOP/s\n", ta ? 'T' : 'N', tb ? 'T' : 'N',
+            sy, (long long)M, (long long)N, (long long)K, ms,
+            (sy ? 1.0 : 2.0) * (double)M * (double)N * (double)K / (ms * 1e9));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
 }
 
 }  // namespace fpi

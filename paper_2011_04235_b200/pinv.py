@@ -386,8 +386,88 @@ def _trace_mark(label, tm):
     print(f"[fastpi] {label} done at {(time.perf_counter() - tm.t0) * 1e3:.2f} ms", file=sys.stderr)
 
 
-def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = None) -> FastpiResult:
-    """Algorithm 1 on a canonical device CSR (m >= n); everything stays in HBM."""
+class _Owned:
+    """A device buffer handed over by fpi_fastpi_take, viewed by torch through the CUDA array
+    interface (the tensor keeps this object alive); freed stream-ordered (fpi_device_free) with the
+    last tensor that views it."""
+
+    def __init__(self, ptr, shape, typestr, device):
+        self.ptr, self.device = ptr, device
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": typestr,
+                                         "data": (int(ptr or 0), False), "version": 2}
+
+    def __del__(self):
+        if self.ptr:
+            try:
+                with torch().cuda.device(self.device):
+                    _lib.call("fpi_device_free", C.c_void_p(self.ptr))
+            except Exception:  # interpreter shutdown: the process exit releases the pool
+                pass
+
+
+def _adopt(ptr, shape, dtype, device):
+    t = torch()
+    if ptr is None or math.prod(shape) == 0:
+        if ptr:
+            _Owned(ptr, (0,), "<f8", device)  # freed at once
+        return t.empty(shape, dtype=dtype, device=t.device("cuda", device))
+    typestr = "<f8" if dtype == t.float64 else "<i8"
+    return t.as_tensor(_Owned(ptr, shape, typestr, device), device=t.device("cuda", device))
+
+
+def _fastpi_one_call(dev: DeviceCSR, cfg: FastpiConfig) -> FastpiResult:
+    """Algorithm 1 behind one C call (fpi_fastpi_ex, csrc/fastpi_capi.cu): the same stage entry points
+    as the stage-by-stage mirror below, in the same order with the same ranks and seeds (identical
+    bits, tests/test_pipeline_gpu.py), without a Python round trip and its allocations between the
+    stages; the factors are adopted as torch tensors (fpi_fastpi_take)."""
+    m, n = dev.shape
+    t = torch()
+    device = t.cuda.current_device()
+    info = _lib.FastpiInfo()
+    _lib.call("fpi_fastpi_ex", m, n, dev.nnz, _lib.ptr(dev.indptr), _lib.ptr(dev.indices), _lib.ptr(dev.values),
+              float(cfg.alpha), float(cfg.k), int(cfg.seed), float(cfg.low_rank_threshold),
+              float(cfg.pinv_cutoff_factor), _lib.FASTPI_CANONICAL, C.byref(info))
+    if info.rank_clamped:
+        warnings.warn(f"row-update target rank clamped from {math.ceil(cfg.alpha * info.n1)} to {info.s} "
+                      "(block stage produced less derivable rank)")
+    bufs = _lib.FastpiBuffers()
+    gcc = (C.c_int64 * max(info.n_gcc, 1))()
+    ms = (C.c_float * len(STAGES))()
+    _lib.call("fpi_fastpi_take", C.byref(bufs), gcc, max(info.n_gcc, 1), ms)
+    r = int(info.rank)
+    f64, i64 = t.float64, t.int64
+    U = _adopt(bufs.U, (m, r), f64, device)
+    sigma = _adopt(bufs.sigma, (r,), f64, device)
+    Vt = _adopt(bufs.Vt, (r, n), f64, device)
+    sdag = _adopt(bufs.sigma_dagger, (r,), f64, device)
+    row_fwd = _adopt(bufs.row_fwd, (m,), i64, device)
+    col_fwd = _adopt(bufs.col_fwd, (n,), i64, device)
+    spans = _adopt(bufs.spans, (4 * int(info.n_spans),), i64, device)
+    ordering = ReorderResult(Permutation(row_fwd), Permutation(col_fwd), info.m1, info.n1, info.m2, info.n2, None,
+                             info.n_iterations, [gcc[i] for i in range(info.n_gcc)], spans_device=spans)
+    ordering.edges_visited, ordering.nodes_visited = int(info.edges_visited), int(info.nodes_visited)
+    if info.all_filtered:
+        warnings.warn("all singular values filtered; returning the zero pseudoinverse")
+    pv = Pseudoinverse(tolerance_used=info.tolerance_used, all_filtered=bool(info.all_filtered),
+                       _dev=_DevPinv(U, sdag, Vt, row_fwd, col_fwd))
+    factors = SvdFactors(_dev=_Dense(U, sigma, Vt), is_sorted=True, _shape=(m, n))
+    ranks = (0, int(info.rank11), int(info.s), r, pv.retained_rank)
+    timings = [StageTime(name, ms[i] * 1e-3, ranks[i]) for i, name in enumerate(STAGES)]
+    return FastpiResult(pv, factors, ordering, timings)
+
+
+_STAGEWISE = bool(__import__("os").environ.get("FPI_STAGEWISE"))
+
+
+def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = None,
+                  stagewise: bool = False) -> FastpiResult:
+    """Algorithm 1 on a canonical device CSR (m >= n); everything stays in HBM.
+
+    By default the whole solve is one C call (``_fastpi_one_call``); ``stats`` (per-stage
+    intermediates for tests and the bench's structure record), ``stagewise=True`` or FPI_STAGEWISE=1
+    run the stage-by-stage mirror of pinv.py:278-347 below instead -- same kernels, same bits."""
+    if stats is None and not stagewise and not _STAGEWISE and not _TRACE:
+        return _fastpi_one_call(dev, cfg)
     m, n = dev.shape
     clock = _StageClock()
     ordering = reorder_device(dev, cfg.k)

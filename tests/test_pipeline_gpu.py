@@ -202,18 +202,20 @@ def test_apply_to_host_matches_device_apply():
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_c_abi_fastpi_matches_python_pipeline(name):
-    """fpi_fastpi (Algorithm 1 in one C call) runs the same stages as the Python mirror: identical
-    sigma, sigma+, factors and permutations."""
+    """fpi_fastpi (Algorithm 1 in one C call) runs the same stages as the stage-by-stage Python mirror:
+    identical sigma, sigma+, factors and permutations -- through the handle-owned result
+    (fpi_fastpi_get) and through the default fastpi() path (fpi_fastpi_ex + fpi_fastpi_take)."""
     import ctypes as C
     import torch
     import paper_2011_04235_b200 as fp
     from paper_2011_04235_b200 import _lib
     from paper_2011_04235_b200._device import DeviceCSR, d2h
+    from paper_2011_04235_b200.pinv import fastpi_device
     p = problem(name)
     w = p.workload
     cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
-    res = fp.fastpi(p.A, cfg)
-    A = DeviceCSR.from_host(p.A)
+    res = fastpi_device(DeviceCSR.from_host(p.A), cfg, stagewise=True)
+    A = DeviceCSR.from_host(p.A, canonicalize=False)  # fpi_fastpi runs check_csr itself
     info = _lib.FastpiInfo()
     _lib.call("fpi_fastpi", A.shape[0], A.shape[1], A.nnz, _lib.ptr(A.indptr), _lib.ptr(A.indices),
               _lib.ptr(A.values), float(w.alpha), float(w.k), int(w.seed), float(cfg.low_rank_threshold),
@@ -222,9 +224,10 @@ def test_c_abi_fastpi_matches_python_pipeline(name):
     _lib.call("fpi_fastpi_get", *[C.byref(x) for x in ptrs])
     m, n, r = info.m, info.n, info.rank
     assert r == res.factors.rank
-    assert (info.m1, info.n1, info.m2, info.n2, info.n_iterations) == (
+    assert (info.m1, info.n1, info.m2, info.n2, info.n_iterations, info.n_gcc) == (
         res.reordering.n_spoke_rows, res.reordering.n_spoke_cols, res.reordering.n_hub_rows,
-        res.reordering.n_hub_cols, res.reordering.n_iterations)
+        res.reordering.n_hub_cols, res.reordering.n_iterations, len(res.reordering.gcc_sizes))
+    assert (info.edges_visited, info.nodes_visited) == (res.reordering.edges_visited, res.reordering.nodes_visited)
 
     from cuda.bindings import runtime as rt
     d = res.pseudoinverse._device()
@@ -238,6 +241,22 @@ def test_c_abi_fastpi_matches_python_pipeline(name):
         assert int(err) == 0
         np.testing.assert_array_equal(d2h(out), d2h(ref.reshape(-1)))
     _lib.call("fpi_fastpi_release")
+
+    # default public path: one C call, buffers adopted by torch
+    one = fp.fastpi(p.A, cfg)
+    d1, f1 = one.pseudoinverse._device(), one.factors.device()
+    for a, b in ((f1.sigma, fd.sigma), (d1.sdag, d.sdag), (f1.U, fd.U), (f1.Vt, fd.Vt), (d1.row_fwd, d.row_fwd),
+                 (d1.col_fwd, d.col_fwd), (one.reordering.spans_device(), res.reordering.spans_device())):
+        np.testing.assert_array_equal(d2h(a), d2h(b))
+    assert one.reordering.gcc_sizes == res.reordering.gcc_sizes
+    assert one.reordering.n_iterations == res.reordering.n_iterations
+    assert one.pseudoinverse.tolerance_used == res.pseudoinverse.tolerance_used
+    assert [(t.stage, t.rank) for t in one.timings] == [(t.stage, t.rank) for t in res.timings]
+    assert all(t.seconds > 0 for t in one.timings)
+    del one, d1, f1
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()  # the adopted buffers were returned through fpi_device_free
 
 
 def test_wide_input_transpose_branch():

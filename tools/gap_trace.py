@@ -1,7 +1,7 @@
 """GPU idle gaps inside one c4 solve + apply (torch.profiler / CUPTI kernel timeline): where the
 device waits on the host (stream syncs for data-dependent sizes, Python between stages).
 
-    python tools/gap_trace.py [c4] [min_gap_us]
+    python tools/gap_trace.py [c4] [min_gap_us] [capi|stagewise]
 """
 import sys
 from pathlib import Path
@@ -25,6 +25,7 @@ def main():
     cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
     A, Y = DeviceCSR.from_host(p.A), DeviceCSR.from_host(p.Y)
     use_c = len(sys.argv) > 3 and sys.argv[3] == "capi"
+    stagewise = len(sys.argv) > 3 and sys.argv[3] == "stagewise"
     import ctypes as C
     from paper_2011_04235_b200 import _lib
 
@@ -35,7 +36,7 @@ def main():
                       _lib.ptr(A.values), float(cfg.alpha), float(cfg.k), int(cfg.seed),
                       float(cfg.low_rank_threshold), float(cfg.pinv_cutoff_factor), C.byref(info))
             return
-        res = fastpi_device(A, cfg)
+        res = fastpi_device(A, cfg, stagewise=stagewise)
         res.pseudoinverse.apply_device(Y)
 
     for _ in range(3):

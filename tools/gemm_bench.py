@@ -22,6 +22,10 @@ SHAPES = [  # (name, ta, tb, M, N, K)
     ("H11_TN_c5", 1, 0, 939, 939, 349000),
     ("H21h_TN_c5", 1, 0, 256, 939, 349000),
     ("Z_L_NT_c4", 0, 1, 10684, 1000, 1000),
+    ("XtZ_c4_odd", 1, 0, 399, 1000, 8497),   # lda = 399: the s-wide operands of c4's row update
+    ("XtZ_c4_even", 1, 0, 400, 1000, 8497),
+    ("WZ_c4_odd", 0, 0, 6491, 399, 798),
+    ("G_c4_odd", 1, 0, 798, 798, 6491),
 ]
 
 
