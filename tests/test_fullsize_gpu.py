@@ -9,9 +9,12 @@ permute + partition ~5 s, block SVD ~8 s, row update ~2-3 min):
   * P3 row update: the oracle's row_update fed the GPU's own f11 (pinv.py:131-171): every sigma
     per value, and the low-rank product U S Vt to 1e-8 (computed on the GPU with torch as the
     checker: the 2M-row factors do not fit a host QR).
-The column update at c5 is not run through the oracle (its CPU peak RSS, ~130 GB for the 2M x 2000
-B / Q panels, is too close to the box's host memory); it is covered by size-independent
-properties:
+  * P3 column update: the reference's column update (pinv.py:174-208, randomized SVD svd.py:120-138
+    with Householder QR) restated on torch tensors in HBM (oracle/torch_oracle.py: its 2M x 2000
+    B / Q panels, 32 GB each, exceed what the host can hold beside the test -- SURVEY 0.8), fed the
+    GPU's own row-update factors: every sigma per value, U S Vt to 1e-8.  The restatement is pinned
+    to the numpy oracle on c1-c3 (CPU) and on c2 / c3@200 here (cuBLAS / cuSOLVER).
+And size-independent properties of the whole solve:
   * sigma positive and sorted, r = min(ceil(alpha n), s + n2, m) (pinv.py:336);
   * U and V have orthonormal columns (1e-9);
   * Z = pinv(A) Y agrees with V diag(sigma+) (U^T (Y x)) on random probes x (1e-10)."""
@@ -105,6 +108,52 @@ def test_c5_row_update_stagewise(c5):
     d = fr.device()
     rel = lowrank_rel_factored_gpu(d.U, d2h_sigma(d.sigma), d.Vt, fo.U, fo.sigma, fo.Vt)
     print(f"c5 row update: low-rank rel diff {rel:.3e} (s={st['s']}, engine {eng})")
+    assert rel <= REC_TOL
+
+
+@pytest.mark.parametrize("name", ["c2", "c3r200"])
+def test_torch_oracle_cuda_pin(name):
+    """oracle/torch_oracle.py on cuBLAS / cuSOLVER against the numpy oracle (c2: randomized engine,
+    c3@200: dense engine): the checker the c5 column-update test runs."""
+    from oracle import torch_oracle
+    from parity import lowrank_rel_factored
+    p = problem(name)
+    w = p.workload
+    out = orc.fastpi(p.A, w.alpha, w.k, w.seed)
+    fr = out["f_rows"]
+    U, sig, Vt, eng = torch_oracle.column_update(orc.dense(fr.U), fr.sigma, orc.dense(fr.Vt), out["T"], out["r"],
+                                                 0.3, w.seed + 2, device="cuda")
+    want = out["factors"]
+    assert eng == out["engines"][1]
+    assert_sigma(sig.cpu().numpy(), want.sigma, tol=1e-12, label=f"{name} torch-oracle (cuda) column update")
+    rel = lowrank_rel_factored(U.cpu().numpy(), sig.cpu().numpy(), Vt.cpu().numpy(), orc.dense(want.U), want.sigma,
+                               orc.dense(want.Vt))
+    assert rel <= 1e-12, rel
+
+
+def test_c5_column_update_stagewise(c5):
+    """P3 at c5 for the column update (pinv.py:174-208): the reference algorithm restated on torch
+    (oracle/torch_oracle.py: sketch from numpy's PCG64 stream, B = inner X, Householder QR, SVD of
+    Y, all in HBM through cuBLAS / cuSPARSE / cuSOLVER -- none of the repo's kernels) fed the GPU's
+    own row-update factors; the GPU's column-update factors against it."""
+    import torch
+    from oracle import torch_oracle
+    from paper_2011_04235_b200._device import d2h
+    p, res, st = c5
+    w = p.workload
+    fr = st["f_rows"].device()
+    T = st["part"].T.to_host()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    U, sig, Vt, eng = torch_oracle.column_update(fr.U, d2h(fr.sigma), fr.Vt, T, st["r"], 0.3, w.seed + 2)
+    assert eng == ("randomized" if st["engines"][1] == 1 else "dense")
+    d = res.factors.device()
+    sig_o = sig.cpu().numpy()
+    assert_sigma(d2h(d.sigma), sig_o, label="c5 column update")
+    rel = lowrank_rel_factored_gpu(d.U, d2h(d.sigma), d.Vt, U, sig_o, Vt)
+    print(f"c5 column update: low-rank rel diff {rel:.3e} (r={st['r']}, engine {eng})")
+    del U, Vt
+    torch.cuda.empty_cache()
     assert rel <= REC_TOL
 
 

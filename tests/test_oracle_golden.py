@@ -60,3 +60,24 @@ def test_reorder_edge_cases_oracle():
     assert sorted(o.col_fwd.tolist()) == list(range(5))
     with pytest.raises(ValueError):
         orc.reorder(4, 5, A.indptr, A.indices, 1.0)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3r50", "c3r200"])
+def test_torch_oracle_column_update_matches_oracle(name):
+    """Pin of oracle/torch_oracle.py (the column-update restatement the c5 GPU test runs in HBM)
+    against the numpy oracle, itself pinned bit-exact to the reference: torch CPU kernels instead of
+    OpenBLAS, so sigma per value and the sign-invariant product U S Vt agree to rounding."""
+    from oracle import torch_oracle
+    from parity import assert_sigma, lowrank_rel_factored
+    p = problem(name)
+    w = p.workload
+    out = orc.fastpi(p.A, w.alpha, w.k, w.seed)
+    fr = out["f_rows"]
+    U, sig, Vt, eng = torch_oracle.column_update(orc.dense(fr.U), fr.sigma, orc.dense(fr.Vt), out["T"], out["r"],
+                                                 0.3, w.seed + 2, device="cpu")
+    want = out["factors"]
+    assert eng == out["engines"][1]
+    assert_sigma(sig.numpy(), want.sigma, tol=1e-12, label=f"{name} torch-oracle column update")
+    rel = lowrank_rel_factored(U.numpy(), sig.numpy(), Vt.numpy(), orc.dense(want.U), want.sigma, orc.dense(want.Vt))
+    print(f"{name}: torch oracle vs numpy oracle column update, low-rank rel {rel:.2e} ({eng})")
+    assert rel <= 1e-12
