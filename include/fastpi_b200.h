@@ -79,6 +79,10 @@ int fpi_set_stream(fpi_handle h, void* cuda_stream);
 const char* fpi_last_error(fpi_handle h);
 int64_t fpi_kernel_launches(fpi_handle h);
 int fpi_get_svd_diag(fpi_handle h, fpi_svd_diag* out);
+/* Dense core of the last column update's sparse block T (csrc/sparse_core.cu): h_out[0..3] =
+ * core rows, core columns, entries moved to the dense panel, entries left to the SpMM; all 0
+ * when the product ran as a plain SpMM (sparse.py:20-39). */
+int fpi_sparse_core_info(fpi_handle h, int64_t* h_out);
 
 /* ---- validation.py:38-55 check_csr: sum duplicates, drop zeros, sort ---- */
 /* Writes at most nnz entries into the out arrays; *h_out_nnz receives the count. */

@@ -80,6 +80,7 @@ SIGNATURES = {
     "fpi_last_error": (C.c_char_p, [vp]),
     "fpi_kernel_launches": (i64, [vp]),
     "fpi_get_svd_diag": (C.c_int, [vp, C.POINTER(SvdDiag)]),
+    "fpi_sparse_core_info": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "fpi_csr_canonicalize": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, P_i64]),
     "fpi_csr_transpose": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp, vp]),
     "fpi_reorder": (C.c_int, [vp, i64, i64, i64, vp, vp, f64, vp, vp, C.POINTER(ReorderInfo)]),
@@ -243,6 +244,13 @@ def svd_diag() -> dict:
     load().fpi_get_svd_diag(handle(), C.byref(d))
     return {"engine": d.engine, "cholqr_passes": d.cholqr_passes, "cond_estimate": d.cond_estimate,
             "eig_sweeps": list(d.eig_sweeps), "null_completed": d.null_completed}
+
+
+def sparse_core_info() -> dict:
+    """Dense core of the last column update's sparse block (csrc/sparse_core.cu); zeros = plain SpMM."""
+    v = (C.c_int64 * 4)()
+    load().fpi_sparse_core_info(handle(), v)
+    return {"rows": int(v[0]), "cols": int(v[1]), "core_nnz": int(v[2]), "rem_nnz": int(v[3])}
 
 
 def timing_enable(on: bool = True):

@@ -64,4 +64,10 @@ int fpi_get_svd_diag(fpi_handle h, fpi_svd_diag* out) {
   return FPI_OK;
 }
 
+int fpi_sparse_core_info(fpi_handle h, int64_t* h_out) {
+  if (!h || !h_out) return FPI_EDOMAIN;
+  for (int i = 0; i < 4; ++i) h_out[i] = h->sparse_core[i];
+  return FPI_OK;
+}
+
 }  // extern "C"

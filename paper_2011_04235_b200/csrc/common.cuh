@@ -79,6 +79,7 @@ struct fpi_context {
   cudaEvent_t copy_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // numerics diagnostics of the last randomized / dense SVD
   fpi_svd_diag diag{};
+  int64_t sparse_core[4] = {0, 0, 0, 0};  // last column update's dense core (fpi_sparse_core_info)
   // cross-rank communicator of a sharded solve (comm.cu), null for one rank
   fpi::Comm* comm = nullptr;
   // counters

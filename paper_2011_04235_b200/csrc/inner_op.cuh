@@ -3,6 +3,7 @@
 #pragma once
 #include "common.cuh"
 #include "gram_route.cuh"
+#include "sparse_core.cuh"
 
 namespace fpi {
 
@@ -23,6 +24,9 @@ struct InnerOp {
   const int32_t* nz_rows = nullptr;
   const double* Dnz = nullptr;
   int64_t s_nnz = 0;  // stored entries of the sparse part (cost model only)
+  // optional: the heavy rows x heavy columns rectangle of the sparse part as a dense panel
+  // (sparse_core.cu); apply / applyT then run the remainder SpMM plus a gathered DMMA product
+  const SparseCore* core = nullptr;
 
   SparseGramIn gram_in() const {
     SparseGramIn g;
@@ -48,13 +52,19 @@ struct InnerOp {
   // flop-equivalent cost of apply() with k columns (a gathered SpMM byte ~ 10 flops on B200)
   double apply_cost(int64_t k) const {
     const double dense_rows = (double)(nzr >= 0 ? nzr : p);
-    return (D && sd > 0 ? 2.0 * dense_rows * (double)sd * (double)k : 0.0) + 10.0 * 8.0 * (double)s_nnz * (double)k;
+    const double gathered = core ? (double)core->rem_nnz : (double)s_nnz;
+    const double cells = core ? (double)core->nR * (double)core->nC : 0.0;
+    return (D && sd > 0 ? 2.0 * dense_rows * (double)sd * (double)k : 0.0) + 10.0 * 8.0 * gathered * (double)k +
+           2.0 * cells * (double)k;
   }
 
   // B (p x k) = inner * X (q x k)
   void apply(fpi_context* h, const double* X, int64_t k, double* B) const;
   // Z (q x k) = inner^T * B (p x k)
   void applyT(fpi_context* h, const double* B, int64_t k, double* Z) const;
+  // sparse part only: B (+)= S * Xs (Xs: (q - sd) x k), Z2 = S^T * B (Z2: (q - sd) x k)
+  void sparse_apply(fpi_context* h, const double* Xs, int64_t k, double beta, double* B) const;
+  void sparse_applyT(fpi_context* h, const double* B, int64_t k, double* Z2) const;
   // dense copy (p x q)
   void densify(fpi_context* h, double* out) const;
 };

@@ -634,12 +634,48 @@ void dense_svd(fpi_context* h, int64_t p, int64_t q, const double* M, int64_t ld
 
 // ---------------------------------------------------------------------------
 // inner-matrix operator (inner_op.cuh): B (p x k) = inner * X (q x k)
+void InnerOp::sparse_apply(fpi_context* h, const double* Xs, int64_t k, double beta, double* B) const {
+  const int64_t q2 = q - sd;
+  if (!core) {
+    spmm(h, p, q2, k, s_ptr, s_idx, s_val, nullptr, 1.0, Xs, k, beta, B, k);
+    return;
+  }
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  spmm(h, p, q2, k, core->r_ptr, core->r_idx, core->r_val, nullptr, 1.0, Xs, k, beta, B, k);
+  // B[rows] += S[rows, cols] Xs[cols]
+  Scratch<double> Xc(core->nC * k, s), tmp(core->nR * k, s);
+  k_gather_rows32<<<grid_for(core->nC * k, 256, G), 256, 0, s>>>(core->nC, k, Xs, k, core->cols, Xc, k);
+  FPI_LAUNCH_CHECK();
+  gemm(h, false, false, core->nR, k, core->nC, 1.0, core->dense, core->nC, Xc, k, 0.0, tmp, k);
+  k_scatter_add_rows32<<<grid_for(core->nR * k, 256, G), 256, 0, s>>>(core->nR, k, tmp, k, core->rows, B, k);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 2);
+}
+void InnerOp::sparse_applyT(fpi_context* h, const double* B, int64_t k, double* Z2) const {
+  const int64_t q2 = q - sd;
+  if (!core) {
+    spmm(h, q2, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z2, k);
+    return;
+  }
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  spmm(h, q2, p, k, core->rt_ptr, core->rt_idx, core->rt_val, nullptr, 1.0, B, k, 0.0, Z2, k);
+  // Z2[cols] += S[rows, cols]^T B[rows]
+  Scratch<double> Bg(core->nR * k, s), tmp(core->nC * k, s);
+  k_gather_rows32<<<grid_for(core->nR * k, 256, G), 256, 0, s>>>(core->nR, k, B, k, core->rows, Bg, k);
+  FPI_LAUNCH_CHECK();
+  gemm(h, true, false, core->nC, k, core->nR, 1.0, core->dense, core->nC, Bg, k, 0.0, tmp, k);
+  k_scatter_add_rows32<<<grid_for(core->nC * k, 256, G), 256, 0, s>>>(core->nC, k, tmp, k, core->cols, Z2, k);
+  FPI_LAUNCH_CHECK();
+  note_launch(h, 2);
+}
 void InnerOp::apply(fpi_context* h, const double* X, int64_t k, double* B) const {
   if (D && sd > 0 && nzr >= 0) {
     cudaStream_t s = h->stream;
     const unsigned G = (unsigned)(h->num_sms * 16);
     if (q > sd)
-      spmm(h, p, q - sd, k, s_ptr, s_idx, s_val, nullptr, 1.0, X + sd * k, k, 0.0, B, k);
+      sparse_apply(h, X + sd * k, k, 0.0, B);
     else
       FPI_CUDA(cudaMemsetAsync(B, 0, sizeof(double) * p * k, s));
     if (nzr > 0) {
@@ -657,9 +693,9 @@ void InnerOp::apply(fpi_context* h, const double* X, int64_t k, double* B) const
     FPI_CUDA(cudaMemcpyAsync(Xs.get(), X, sizeof(double) * sd * k, cudaMemcpyDeviceToDevice, h->stream));
     if (dscale) scale_rows(h, sd, k, Xs, k, dscale);
     gemm(h, false, false, p, k, sd, 1.0, D, ldd, Xs, k, 0.0, B, k);
-    if (q > sd) spmm(h, p, q - sd, k, s_ptr, s_idx, s_val, nullptr, 1.0, X + sd * k, k, 1.0, B, k);
+    if (q > sd) sparse_apply(h, X + sd * k, k, 1.0, B);
   } else {
-    spmm(h, p, q, k, s_ptr, s_idx, s_val, nullptr, 1.0, X, k, 0.0, B, k);
+    sparse_apply(h, X, k, 0.0, B);
   }
 }
 // Z (q x k) = inner^T * B (p x k)
@@ -676,15 +712,15 @@ void InnerOp::applyT(fpi_context* h, const double* B, int64_t k, double* Z) cons
     } else {
       FPI_CUDA(cudaMemsetAsync(Z, 0, sizeof(double) * sd * k, s));
     }
-    if (q > sd) spmm(h, q - sd, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z + sd * k, k);
+    if (q > sd) sparse_applyT(h, B, k, Z + sd * k);
     return;
   }
   if (D && sd > 0) {
     gemm(h, true, false, sd, k, p, 1.0, D, ldd, B, k, 0.0, Z, k);
     if (dscale) scale_rows(h, sd, k, Z, k, dscale);
-    if (q > sd) spmm(h, q - sd, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z + sd * k, k);
+    if (q > sd) sparse_applyT(h, B, k, Z + sd * k);
   } else {
-    spmm(h, q, p, k, st_ptr, st_idx, st_val, nullptr, 1.0, B, k, 0.0, Z, k);
+    sparse_applyT(h, B, k, Z);
   }
 }
 // dense copy (p x q)
@@ -1055,6 +1091,20 @@ void column_update(fpi_context* h, int64_t m, int64_t s_prev, int64_t n1, const 
     }
   }
   trace_point(h, "col: zero-row scan");
+  // the heavy rows x heavy columns rectangle of T on the tensor pipe (sparse_core.cu)
+  SparseCore core;
+  for (int64_t& v : h->sparse_core) v = 0;
+  if (n2 > 0 && (double)r < thr * (double)q && m > 2 * r) {
+    build_sparse_core(h, m, n2, op.s_nnz, t_ptr, t_idx, t_val, tt_ptr, tt_idx, tt_val, core);
+    if (core.use) {
+      op.core = &core;
+      h->sparse_core[0] = core.nR;
+      h->sparse_core[1] = core.nC;
+      h->sparse_core[2] = core.core_nnz;
+      h->sparse_core[3] = core.rem_nnz;
+    }
+    trace_point(h, "col: sparse core");
+  }
   Scratch<double> Vti(r * q, s);
   inner_svd(h, op, r, q, thr, seed, U, sigma, Vti, engine, &h->diag);
   trace_point(h, "col: inner svd");

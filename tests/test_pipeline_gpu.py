@@ -55,6 +55,24 @@ def test_stagewise_parity_gram_route(name, heavy, monkeypatch):
     _check_stagewise(name)
 
 
+@pytest.mark.parametrize("gram", [False, True])
+@pytest.mark.parametrize("name", ["c2", "c3r50", "c3r100"])
+def test_stagewise_parity_sparse_core(name, gram, monkeypatch):
+    """The dense core of T (sparse_core.cu: heavy rows x heavy columns on DMMA, the rest as a
+    gather SpMM) forced on the small randomized-column configs, through the B route and -- with
+    the inner-Gram route forced -- through the lift alone."""
+    from paper_2011_04235_b200 import _lib
+    monkeypatch.setenv("FPI_SPMM_CORE", "force")
+    if gram:
+        monkeypatch.setenv("FPI_GRAM_ROUTE", "1")
+    _check_stagewise(name)
+    info = _lib.sparse_core_info()
+    assert info["rows"] > 0 and info["cols"] > 0 and info["core_nnz"] > 0, info
+    monkeypatch.setenv("FPI_SPMM_CORE", "0")
+    _run(name)
+    assert _lib.sparse_core_info()["core_nnz"] == 0
+
+
 def _check_stagewise(name):
     p, res, st = _run(name)
     g = golden(name)
@@ -184,6 +202,11 @@ def test_stagewise_parity_c4(route, monkeypatch):
     ff = res.factors
     assert_sigma(ff.sigma, fo_full.sigma, label="c4 column update")
     assert _lowrank_rel_factored(ff, fo_full) <= REC_TOL
+    if route == "auto":
+        # c4's T has a dense heavy-row x heavy-column core (Zipf x Zipf): the cost rule takes it
+        from paper_2011_04235_b200 import _lib
+        info = _lib.sparse_core_info()
+        assert info["core_nnz"] > 0.3 * (info["core_nnz"] + info["rem_nnz"]), info
 
 
 def test_apply_to_host_matches_device_apply():
