@@ -20,6 +20,7 @@
 //
 // Every entry is summed in a fixed order (no atomics): H is deterministic.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -236,6 +237,149 @@ __global__ void k_gather_rows_ld(int64_t nr, int64_t k, const double* __restrict
   }
 }
 
+// ---- is D^T D the identity?  Probe columns G (sd x NPROBE, fixed pseudo-random signs-and-magnitudes):
+// E = D^T (D G) - G.  ||E||_F^2 / ||G||_F^2 estimates ||D^T D - I||_F^2 / sd (Hutchinson), two
+// streaming passes over D instead of the sd x sd x nzr Gram.
+constexpr int NPROBE = 8;
+__device__ __forceinline__ double probe_value(int64_t t, int j) {
+  uint64_t z = (uint64_t)(t * NPROBE + j) * 0x9E3779B97F4A7C15ull + 0xD1B54A32D192ED03ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return ((double)(z >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;  // uniform (-1, 1)
+}
+// T1[r][j] = sum_t D[r][t] G[t][j]; one warp per row
+__global__ void k_probe_fill(int64_t sd, double* __restrict__ Gp) {
+  FPI_GRID_STRIDE(i, sd * NPROBE) Gp[i] = probe_value(i % sd, (int)(i / sd));  // probe-major: Gp[j][t]
+}
+__global__ void k_probe_fwd(int64_t nzr, int64_t sd, const double* __restrict__ D, int64_t ldd,
+                            const double* __restrict__ Gp, double* __restrict__ T1) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nzr; r += nw) {
+    double a[NPROBE];
+#pragma unroll
+    for (int j = 0; j < NPROBE; ++j) a[j] = 0.0;
+    for (int64_t t = lane; t < sd; t += 32) {
+      const double d = D[r * ldd + t];
+#pragma unroll
+      for (int j = 0; j < NPROBE; ++j) a[j] = fma(d, __ldg(Gp + j * sd + t), a[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < NPROBE; ++j) {
+      for (int o = 16; o; o >>= 1) a[j] += __shfl_xor_sync(0xffffffffu, a[j], o);
+      if (lane == j) T1[r * NPROBE + j] = a[j];
+    }
+  }
+}
+// P[chunk][j][t] = sum_{r in chunk} D[r][t] T1[r][j]; CTA = one chunk of rows, thread = column t
+constexpr int PROBE_CHUNK = 512;
+__global__ void k_probe_bwd(int64_t nzr, int64_t sd, const double* __restrict__ D, int64_t ldd,
+                            const double* __restrict__ T1, double* __restrict__ P) {
+  __shared__ double t1[PROBE_CHUNK * NPROBE];
+  const int64_t r0 = (int64_t)blockIdx.x * PROBE_CHUNK;
+  const int64_t nr = nzr - r0 < PROBE_CHUNK ? nzr - r0 : PROBE_CHUNK;
+  for (int64_t i = threadIdx.x; i < nr * NPROBE; i += blockDim.x) t1[i] = T1[r0 * NPROBE + i];
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < sd; t += blockDim.x) {
+    double a[NPROBE];
+#pragma unroll
+    for (int j = 0; j < NPROBE; ++j) a[j] = 0.0;
+    for (int64_t r = 0; r < nr; ++r) {
+      const double d = D[(r0 + r) * ldd + t];
+#pragma unroll
+      for (int j = 0; j < NPROBE; ++j) a[j] = fma(d, t1[r * NPROBE + j], a[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < NPROBE; ++j) P[((int64_t)blockIdx.x * NPROBE + j) * sd + t] = a[j];
+  }
+}
+// W[i] = sum_chunks P[chunk][i] (chunks in order)
+__global__ void k_probe_sum(int64_t nchunks, int64_t n, const double* __restrict__ P, double* __restrict__ W) {
+  FPI_GRID_STRIDE(i, n) {
+    double w = 0.0;
+    for (int64_t c = 0; c < nchunks; ++c) w += P[c * n + i];
+    W[i] = w;
+  }
+}
+// out[0] = ||W - G||_F^2, out[1] = ||G||_F^2   (one CTA, fixed order)
+__global__ void k_probe_defect(int64_t n, const double* __restrict__ W, const double* __restrict__ Gp,
+                               double* __restrict__ out) {
+  __shared__ double se[256], sg[256];
+  double e = 0.0, g = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double gv = Gp[i];
+    e += (W[i] - gv) * (W[i] - gv);
+    g += gv * gv;
+  }
+  se[threadIdx.x] = e;
+  sg[threadIdx.x] = g;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      se[threadIdx.x] += se[threadIdx.x + o];
+      sg[threadIdx.x] += sg[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = se[0];
+    out[1] = sg[0];
+  }
+}
+// H11 = diag(ds)^2 when D^T D = I
+__global__ void k_fill_h11_identity(int64_t sd, const double* __restrict__ ds, double* __restrict__ H, int64_t ldh) {
+  FPI_GRID_STRIDE(e, sd * sd) {
+    const int64_t a = e / sd, b = e - a * sd;
+    H[a * ldh + b] = a == b ? (ds ? ds[a] * ds[a] : 1.0) : 0.0;
+  }
+}
+
+// T_L = S restricted to its light columns (hidx[c] < 0): per-row counts, then entries in order
+__global__ void k_light_count(int64_t p, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                              const int32_t* __restrict__ hidx, int64_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < p; i += nw) {
+    int n = 0;
+    for (int64_t e = ptr[i] + lane; e < ptr[i + 1]; e += 32) n += hidx[idx[e]] < 0;
+    for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) cnt[i] = n;
+  }
+}
+__global__ void k_light_fill(int64_t p, const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                             const double* __restrict__ val, const int32_t* __restrict__ hidx,
+                             const int64_t* __restrict__ optr, int32_t* __restrict__ oidx,
+                             double* __restrict__ oval) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < p; i += nw) {
+    int64_t o = optr[i];
+    const int64_t b = ptr[i], e = ptr[i + 1];
+    for (int64_t base = b; base < e; base += 32) {
+      const int64_t my = base + lane;
+      const int32_t c = my < e ? idx[my] : 0;
+      const bool keep = my < e && hidx[c] < 0;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        const int64_t at = o + __popc(m & ((1u << lane) - 1u));
+        oidx[at] = c;
+        oval[at] = val[my];
+      }
+      o += __popc(m);
+    }
+  }
+}
+// H[sd + light[j]][sd + heavy[a]] = LH[j][a]
+__global__ void k_scatter_light_heavy(int64_t nl, int64_t K, const int32_t* __restrict__ light,
+                                      const int32_t* __restrict__ heavy, const double* __restrict__ LH,
+                                      double* __restrict__ H, int64_t ldh, int64_t sd) {
+  FPI_GRID_STRIDE(t, nl * K) {
+    const int64_t j = t / K, a = t - j * K;
+    H[(sd + light[j]) * ldh + sd + heavy[a]] = LH[t];
+  }
+}
+
 double env_double(const char* name, double dflt) {
   const char* e = getenv(name);
   return e ? atof(e) : dflt;
@@ -329,6 +473,34 @@ void inner_gram(fpi_context* h, const SparseGramIn& in, const GramPlan& pl, doub
   }
   // ---- light rows of H22 (they include the light x heavy block)
   if (nl) {
+    // With heavy columns present the light rows split: the light x light block by the shared-
+    // memory kernel walking T_L (S without its heavy columns: each row's walk shrinks to its few
+    // light entries), the light x heavy block as a gather SpMM of the light rows of S^T over the
+    // heavy panel Sh.
+    const bool split = K > 0 && getenv("FPI_GRAM_NO_SPLIT") == nullptr;
+    const int64_t* gs_ptr = in.s_ptr;
+    const int32_t* gs_idx = in.s_idx;
+    const double* gs_val = in.s_val;
+    Scratch<int64_t> tl_cnt, tl_ptr;
+    Scratch<int32_t> tl_idx;
+    Scratch<double> tl_val;
+    if (split) {
+      CubTemp tmp(s);
+      tl_cnt.alloc(p + 1, s);
+      tl_ptr.alloc(p + 1, s);
+      FPI_CUDA(cudaMemsetAsync(tl_cnt.get() + p, 0, sizeof(int64_t), s));
+      k_light_count<<<grid_for(p * 32, 256, G), 256, 0, s>>>(p, in.s_ptr, in.s_idx, hidx, tl_cnt);
+      exclusive_sum(tmp, tl_cnt.get(), tl_ptr.get(), p + 1, s);
+      tl_idx.alloc(pl.light_nnz + 1, s);
+      tl_val.alloc(pl.light_nnz + 1, s);
+      k_light_fill<<<grid_for(p * 32, 256, G), 256, 0, s>>>(p, in.s_ptr, in.s_idx, in.s_val, hidx, tl_ptr, tl_idx,
+                                                            tl_val);
+      FPI_LAUNCH_CHECK();
+      note_launch(h, 3);
+      gs_ptr = tl_ptr;
+      gs_idx = tl_idx;
+      gs_val = tl_val;
+    }
     std::vector<int64_t> ptr(q2 + 1);
     FPI_CUDA(cudaMemcpyAsync(ptr.data(), in.st_ptr, sizeof(int64_t) * (q2 + 1), cudaMemcpyDeviceToHost, s));
     FPI_CUDA(cudaStreamSynchronize(s));
@@ -376,12 +548,32 @@ void inner_gram(fpi_context* h, const SparseGramIn& in, const GramPlan& pl, doub
     int per_sm = 0;
     FPI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gram_rows, GR_WARPS * 32, smem));
     const int64_t grid = std::min<int64_t>(nit * nparts, (int64_t)h->num_sms * std::max(per_sm, 1));
-    k_gram_rows<<<(unsigned)grid, GR_WARPS * 32, smem, s>>>(nit, nparts, d_icol, d_ib, d_ie, d_idst, q2, in.s_ptr,
-                                                           in.s_idx, in.s_val, in.st_idx, in.st_val, P, H, ldh, sd);
+    k_gram_rows<<<(unsigned)grid, GR_WARPS * 32, smem, s>>>(nit, nparts, d_icol, d_ib, d_ie, d_idst, q2, gs_ptr,
+                                                           gs_idx, gs_val, in.st_idx, in.st_val, P, H, ldh, sd);
     FPI_LAUNCH_CHECK();
     note_launch(h);
     if (nm) {
       k_gram_rows_reduce<<<grid_for(nm * q2, 256, G), 256, 0, s>>>(nm, d_mcol, d_mpb, d_mpe, q2, P, H, ldh, sd);
+      FPI_LAUNCH_CHECK();
+      note_launch(h);
+    }
+    if (split) {
+      // light x heavy: LH = (light rows of S^T) Sh, then into H's light rows
+      Scratch<int32_t> ident(p, s);
+      k_iota_pos<<<grid_for(p, 256, G), 256, 0, s>>>(p, ident);
+      Scratch<int64_t> cnt(nl + 1, s), rptr(nl + 1, s);
+      FPI_CUDA(cudaMemsetAsync(cnt.get() + nl, 0, sizeof(int64_t), s));
+      k_restrict_count<<<grid_for(nl * 32, 256, G), 256, 0, s>>>(nl, light, in.st_ptr, in.st_idx, ident, cnt);
+      CubTemp tmp(s);
+      exclusive_sum(tmp, cnt.get(), rptr.get(), nl + 1, s);
+      Scratch<int32_t> ridx(pl.light_nnz + 1, s);
+      Scratch<double> rval(pl.light_nnz + 1, s), LH(nl * K, s);
+      k_restrict_fill<<<grid_for(nl * 32, 256, G), 256, 0, s>>>(nl, light, in.st_ptr, in.st_idx, in.st_val, ident,
+                                                                rptr, ridx, rval);
+      FPI_LAUNCH_CHECK();
+      note_launch(h, 4);
+      spmm(h, nl, p, K, rptr, ridx, rval, nullptr, 1.0, Sh, K, 0.0, LH, K);
+      k_scatter_light_heavy<<<grid_for(nl * K, 256, G), 256, 0, s>>>(nl, K, light, heavy, LH, H, ldh, sd);
       FPI_LAUNCH_CHECK();
       note_launch(h);
     }
@@ -410,12 +602,41 @@ void inner_gram(fpi_context* h, const SparseGramIn& in, const GramPlan& pl, doub
   k_gather_rows_ld<<<grid_for(nzr * sd, 256, G), 256, 0, s>>>(nzr, sd, Dz, ldz, nullptr, Dp, ldp);
   FPI_LAUNCH_CHECK();
   note_launch(h);
-  Scratch<double> G11(sd * sd, s);
-  gemm(h, true, false, sd, sd, nzr, 1.0, Dp, ldp, Dp, ldp, 0.0, G11, sd, /*sym=*/true);
-  k_fill_h11<<<grid_for(sd * sd, 256, G), 256, 0, s>>>(sd, G11, in.dscale, H, ldh);
-  FPI_LAUNCH_CHECK();
-  note_launch(h);
-  G11.release();
+  // H11 = Sigma (D^T D) Sigma.  The column update's D is the row update's U, whose columns are
+  // orthonormal by construction (svd.py:137, U = Q U~), so D^T D = I and H11 = Sigma^2 -- checked
+  // here on NPROBE probe columns (two streaming passes over D) before the sd x sd x nzr Gram is
+  // skipped; a D that fails the check (a caller's own factors) takes the Gram.
+  bool identity = false;
+  if (getenv("FPI_GRAM_H11_GEMM") == nullptr && nzr >= 4 * sd) {
+    const int64_t nch = (nzr + PROBE_CHUNK - 1) / PROBE_CHUNK;
+    Scratch<double> Gp(sd * NPROBE, s), T1(nzr * NPROBE, s), Pp(nch * sd * NPROBE, s), Wp(sd * NPROBE, s), dq(2, s);
+    k_probe_fill<<<grid_for(sd * NPROBE, 256, G), 256, 0, s>>>(sd, Gp);
+    k_probe_fwd<<<grid_for(nzr * 32, 256, G), 256, 0, s>>>(nzr, sd, Dp, ldp, Gp, T1);
+    k_probe_bwd<<<(unsigned)nch, 256, 0, s>>>(nzr, sd, Dp, ldp, T1, Pp);
+    k_probe_sum<<<grid_for(sd * NPROBE, 128, G), 128, 0, s>>>(nch, sd * NPROBE, Pp, Wp);
+    k_probe_defect<<<1, 256, 0, s>>>(sd * NPROBE, Wp, Gp, dq);
+    FPI_LAUNCH_CHECK();
+    note_launch(h, 5);
+    double hq[2];
+    host_read_n(dq.get(), hq, 2, s);
+    // ||D^T D - I||_F ~ sqrt(sd e / g).  CholeskyQR / Jacobi leave ~1e-13 (eps per entry); the shortcut
+    // perturbs H11 by that much relative to Sigma^2, far inside the 1e-9 singular-value budget
+    const double defect = hq[1] > 0.0 ? std::sqrt((double)sd * hq[0] / hq[1]) : INFINITY;
+    identity = defect <= 1e-10;
+    if (getenv("FPI_TRACE")) fprintf(stderr, "[trace] gram route: ||D^T D - I||_F ~ %.3e -> %s\n", defect,
+                                     identity ? "H11 = Sigma^2" : "H11 by the Gram");
+  }
+  if (identity) {
+    k_fill_h11_identity<<<grid_for(sd * sd, 256, G), 256, 0, s>>>(sd, in.dscale, H, ldh);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+  } else {
+    Scratch<double> G11(sd * sd, s);
+    gemm(h, true, false, sd, sd, nzr, 1.0, Dp, ldp, Dp, ldp, 0.0, G11, sd, /*sym=*/true);
+    k_fill_h11<<<grid_for(sd * sd, 256, G), 256, 0, s>>>(sd, G11, in.dscale, H, ldh);
+    FPI_LAUNCH_CHECK();
+    note_launch(h);
+  }
   Scratch<double> Rh(K * sd + 1, s), Rl(nl * sd + 1, s);
   if (K) {
     Scratch<double> Shz(nzr * K, s);

@@ -73,6 +73,29 @@ def test_stagewise_parity_sparse_core(name, gram, monkeypatch):
     assert _lib.sparse_core_info()["core_nnz"] == 0
 
 
+def test_gram_route_h11_shortcut_declined_for_scaled_factor(monkeypatch):
+    """The inner-Gram route takes H11 = Sigma^2 when its probe finds D^T D = I (the row update's U).
+    column_update(2 U, Sigma / 2, Vt) is the same inner matrix [U Sigma | T] with a D that is not
+    orthonormal: the probe must decline the shortcut and the factors must agree with the unscaled
+    call (pinv.py:174-208 computes with the U it is given)."""
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200.pinv import column_update
+    monkeypatch.setenv("FPI_GRAM_ROUTE", "1")
+    p, res, st = _run("c2")
+    fr = st["f_rows"]
+    T = st["part"].T.to_host()
+    w = p.workload
+    U, sig, Vt = np.asarray(fr.U), np.asarray(fr.sigma), np.asarray(fr.Vt)
+    fa = column_update(fp.SvdFactors(U, sig, Vt, True), T, st["r"], seed=w.seed + 2)
+    fb = column_update(fp.SvdFactors(2.0 * U, 0.5 * sig, Vt, True), T, st["r"], seed=w.seed + 2)
+    assert_sigma(fb.sigma, fa.sigma, tol=1e-11, label="scaled-U column update")
+    assert _lowrank_rel(fb, fa) <= 1e-10
+    monkeypatch.setenv("FPI_GRAM_H11_GEMM", "1")
+    fc = column_update(fp.SvdFactors(U, sig, Vt, True), T, st["r"], seed=w.seed + 2)
+    assert_sigma(fc.sigma, fa.sigma, tol=1e-11, label="H11 shortcut vs Gram")
+    assert _lowrank_rel(fc, fa) <= 1e-10
+
+
 def _check_stagewise(name):
     p, res, st = _run(name)
     g = golden(name)
