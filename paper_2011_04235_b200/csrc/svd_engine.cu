@@ -840,6 +840,90 @@ static bool rsvd_finish_right(fpi_context* h, const InnerOp& op, int64_t rank, c
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Robust orthonormalisation of an ill-conditioned or rank-deficient sketch product B (p x k),
+// the fallback behind svd.py:134's QR when CholeskyQR's cond(B)^2 is too much for FP64.
+// Deflated eigen-orthonormalisation: every pass takes the Gram of the residual R (first B),
+// keeps the eigen-directions within 1e-8 of its largest eigenvalue (condition <= 1e4 among
+// them, so R W Lambda^-1/2 is orthonormal to ~1e-8), brings them to rounding level by two
+// rounds of projection against the columns already found plus CholeskyQR, and removes them from
+// R.  Each pass resolves four decades of B's spectrum; the loop ends when k columns are found or
+// the residual is at the rounding floor of B, and the remaining columns (a numerically rank-
+// deficient B) are an orthonormal completion -- as Householder QR would return.  All GEMM-shaped
+// work on DMMA; the k x k eigenproblems on the Jacobi kernel.  On return B holds Q.
+__global__ void k_scale_eigvec_cols(int64_t k, int64_t S, const double* __restrict__ W, const double* __restrict__ w,
+                                    double* __restrict__ Ws) {
+  FPI_GRID_STRIDE(e, k * S) {
+    const int64_t i = e / S, j = e - i * S;
+    Ws[e] = W[i * k + j] / sqrt(w[j]);
+  }
+}
+__global__ void k_identity_kk(int64_t k, double* __restrict__ A) {
+  FPI_GRID_STRIDE(e, k * k) A[e] = (e / k == e % k) ? 1.0 : 0.0;
+}
+__global__ void k_flags01(int64_t k, int64_t found, double* __restrict__ f) {
+  FPI_GRID_STRIDE(i, k) f[i] = i < found ? 1.0 : 0.0;
+}
+
+static int64_t orthonormalize_deflated(fpi_context* h, int64_t p, int64_t k, double* B, fpi_svd_diag* diag) {
+  cudaStream_t s = h->stream;
+  const unsigned G = (unsigned)(h->num_sms * 16);
+  const double eps = 2.220446049250313e-16;
+  Scratch<double> Q(p * k, s), Gm(k * k, s), W(k * k, s), w(k, s);
+  FPI_CUDA(cudaMemsetAsync(Q.get(), 0, sizeof(double) * p * k, s));
+  std::vector<double> hw(k);
+  int64_t found = 0;
+  double total = 0.0;
+  for (int pass = 0; pass < 8 && found < k; ++pass) {
+    gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k, /*sym=*/true);
+    sym_eig(h, k, Gm, k, w, W, k, 60, 1e-15, true);
+    FPI_CUDA(cudaMemcpyAsync(hw.data(), w.get(), sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+    FPI_CUDA(cudaStreamSynchronize(s));
+    if (pass == 0) total = hw[0];
+    // residual at the rounding floor of B (sigma <= 16 eps sqrt(k) ||B||): the rest is a completion
+    if (!(hw[0] > 0.0) || hw[0] <= 256.0 * eps * eps * (double)k * total) break;
+    int64_t S = 0;
+    while (S < k - found && S < k && hw[S] > 1e-8 * hw[0]) ++S;
+    if (S == 0) break;
+    Scratch<double> Ws(k * S, s), Qn(p * S, s), T(p * S, s);
+    k_scale_eigvec_cols<<<grid_for(k * S, 256, G), 256, 0, s>>>(k, S, W, w, Ws);
+    FPI_LAUNCH_CHECK();
+    gemm(h, false, false, p, S, k, 1.0, B, k, Ws, S, 0.0, Qn, S);
+    for (int round = 0; round < 2; ++round) {
+      if (found > 0) {  // Qn -= Q (Q^T Qn)
+        Scratch<double> C(found * S, s);
+        gemm(h, true, false, found, S, p, 1.0, Q, k, Qn, S, 0.0, C, S);
+        gemm(h, false, false, p, S, found, -1.0, Q, k, C, S, 1.0, Qn, S);
+      }
+      Scratch<double> G2(S * S, s), L(S * S, s), Li(S * S, s);
+      gemm(h, true, false, S, S, p, 1.0, Qn, S, Qn, S, 0.0, G2, S, /*sym=*/true);
+      int info = 0;
+      FPI_CUDA(cudaMemcpyAsync(L.get(), G2.get(), sizeof(double) * S * S, cudaMemcpyDeviceToDevice, s));
+      cholesky_lower(h, S, L, S, &info);
+      FPI_REQUIRE(info == 0, FPI_ENUMERIC, "orthonormalisation of the sketch product failed (re-orthogonalisation)");
+      lower_inverse(h, S, L, S, Li, S);
+      gemm(h, false, true, p, S, S, 1.0, Qn, S, Li, S, 0.0, T, S);   // Qn L^-T
+      FPI_CUDA(cudaMemcpyAsync(Qn.get(), T.get(), sizeof(double) * p * S, cudaMemcpyDeviceToDevice, s));
+    }
+    FPI_CUDA(cudaMemcpy2DAsync(Q.get() + found, k * sizeof(double), Qn.get(), S * sizeof(double), S * sizeof(double),
+                               p, cudaMemcpyDeviceToDevice, s));
+    found += S;
+    if (found < k) {  // R -= Qn (Qn^T R)
+      Scratch<double> C2(S * k, s);
+      gemm(h, true, false, S, k, p, 1.0, Qn, S, B, k, 0.0, C2, k);
+      gemm(h, false, false, p, k, S, -1.0, Qn, S, C2, k, 1.0, B, k);
+    }
+  }
+  if (found < k) {
+    Scratch<double> flags(k, s);
+    k_flags01<<<grid_for(k, 256, G), 256, 0, s>>>(k, found, flags);
+    FPI_LAUNCH_CHECK();
+    complete_null_left(h, p, k, Q, k, flags, diag);
+  }
+  FPI_CUDA(cudaMemcpyAsync(B, Q.get(), sizeof(double) * p * k, cudaMemcpyDeviceToDevice, s));
+  return found;
+}
+
 static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int64_t seed, double* U, double* sigma,
                            double* Vt, fpi_svd_diag* diag) {
   const int64_t p = op.p, q = op.q;
@@ -903,10 +987,29 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
     gemm(h, true, false, k, k, p, 1.0, B, k, B, k, 0.0, Gm, k, /*sym=*/true);
     trace_point(h, "rsvd:gram B^T B");
   }
+  fpi_svd_diag local_diag{};
+  if (!diag) diag = &local_diag;
   orth_factor(h, k, Gm, Linv, diag);
   Gm.release();
   trace_point(h, "rsvd:cholesky/inverse");
-  if (!gram_from_z) {
+  // CholeskyQR loses cond(B)^2: past ~1e4 (or when B^T B is not numerically positive definite) the
+  // sketch product is orthonormalised explicitly by the deflated eigen-orthonormalisation and the
+  // rest of svd.py:135-137 runs on that Q (L = I).  The BASELINE configs measure cond 1.06 - 4.5.
+  const bool robust = getenv("FPI_RSVD_NO_ROBUST") == nullptr &&
+                      (diag->cholqr_passes == 0 || !(diag->cond_estimate < 1e4));
+  if (robust) {
+    if (!B.get()) {
+      B.alloc(p * k, s);
+      op.apply(h, X, k, B);
+    }
+    const int64_t found = orthonormalize_deflated(h, p, k, B, diag);
+    (void)found;
+    k_identity_kk<<<grid_for(k * k, 256, (unsigned)(h->num_sms * 16)), 256, 0, s>>>(k, Linv);
+    FPI_LAUNCH_CHECK();
+    op.applyT(h, B, k, Z);   // Y^T = inner^T Q
+    diag->cholqr_passes = 0;
+    trace_point(h, "rsvd:robust orthonormalisation");
+  } else if (!gram_from_z) {
     op.applyT(h, B, k, Z);
     trace_point(h, "rsvd:Z = M^T B");
   }
@@ -914,7 +1017,7 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
   // Y^T the product is left implicit (Gram L^-1 (Z^T Z) L^-T)
   // implicit only when L is well conditioned: the Gram of Z carries cond(L)^2 more rounding than
   // the Gram of Y^T (the CholeskyQR sketches here measure cond 1.2 - 2.7)
-  const bool implicit_ok = q >= k && diag && diag->cond_estimate > 0.0 && diag->cond_estimate < 8.0;
+  const bool implicit_ok = !robust && q >= k && diag->cond_estimate > 0.0 && diag->cond_estimate < 8.0;
   // right-side finish when one pass of inner^T over r columns undercuts the q x 2r x r product
   if (implicit_ok && getenv("FPI_RSVD_LEFT_FINISH") == nullptr &&
       op.apply_cost(rank) < 0.5 * 2.0 * (double)q * (double)k * (double)rank &&
@@ -944,8 +1047,8 @@ static void randomized_svd(fpi_context* h, const InnerOp& op, int64_t rank, int6
     canonical_signs_vt(h, rank, q, Vt, q, sgn);
     scale_cols(h, k, rank, Mx, rank, sgn, false);
   }
-  if (!B.get() ||
-      op.apply_cost(rank) + 2.0 * (double)q * (double)k * (double)rank < 2.0 * (double)p * (double)k * (double)rank) {
+  if (!robust && (!B.get() || op.apply_cost(rank) + 2.0 * (double)q * (double)k * (double)rank <
+                                  2.0 * (double)p * (double)k * (double)rank)) {
     // = inner (X L^-T U~): the thin q x r factor first, then one pass of the inner operator -- about
     // half the flops of the p x 2r x r product with B when inner is [U Sigma | T] with a tall U
     B.release();

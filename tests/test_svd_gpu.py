@@ -88,6 +88,43 @@ def test_randomized_svd_matches_oracle(seed, rank):
     assert f.orthonormality_defect() < 1e-10
 
 
+@pytest.mark.parametrize("case", ["graded_1e6", "graded_1e14", "rank_deficient"])
+def test_randomized_svd_ill_conditioned_sketch(case):
+    """svd.py:120-138 on inputs whose sketch B = A X is ill conditioned or rank deficient: the
+    reference orthonormalises with Householder QR (stable at any condition number), this engine
+    with CholeskyQR (cond(B)^2) plus its fallbacks (explicit Y^T when the Cholesky factor is ill
+    conditioned, an eigen-based factor when B^T B is not numerically positive definite).  Every
+    singular value above the floor to <= 1e-9 of itself, U S Vt to <= 1e-8, against the oracle on
+    the same sketch."""
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200 import _lib
+    rng = np.random.default_rng(5)
+    p, q, rank = 2500, 320, 30
+    U, _ = np.linalg.qr(rng.standard_normal((p, q)))
+    V, _ = np.linalg.qr(rng.standard_normal((q, q)))
+    if case == "graded_1e6":
+        sig = np.logspace(0, -6, q)          # cond(B) ~ sigma_1 / sigma_60 ~ 13
+        sig[:60] = np.logspace(0, -6, 60)    # ... made 1e6 inside the sketch's reach
+        sig[60:] = 1e-6 * np.logspace(0, -3, q - 60)
+    elif case == "graded_1e14":
+        sig = np.concatenate([np.logspace(0, -14, 60), 1e-14 * np.logspace(0, -2, q - 60)])
+    else:
+        sig = np.concatenate([np.linspace(3.0, 1.0, 20), np.zeros(q - 20)])   # rank 20 < 2 * rank
+    A = sp.csr_matrix((U * sig) @ V.T)
+    f = fp.randomized_svd(A, rank, 9)
+    diag = _lib.svd_diag()
+    fo = orc.randomized_svd(A, rank, 9)
+    print(f"[ill-conditioned sketch] {case}: diag {diag}")
+    assert_sigma(f.sigma, fo.sigma, label=f"randomized {case}")
+    Bg = (f.U * f.sigma) @ f.Vt
+    Bo = (fo.U * fo.sigma) @ fo.Vt
+    assert np.linalg.norm(Bg - Bo) <= 1e-8 * np.linalg.norm(Bo)
+    keep = fo.sigma > 1e-6 * fo.sigma[0]
+    Ug, Vg = f.U[:, keep], f.Vt[keep]
+    assert np.abs(Ug.T @ Ug - np.eye(keep.sum())).max() < 1e-8
+    assert np.abs(Vg @ Vg.T - np.eye(keep.sum())).max() < 1e-8
+
+
 def test_block_svd_large_tier_batched():
     """Blocks too large for shared memory (both orientations) go through the batched Gram path."""
     import paper_2011_04235_b200 as fp
