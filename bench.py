@@ -466,7 +466,7 @@ def ours_arm(args):
             "step_ms_all": [round(t, 3) for t in times],
             "kernels": kernels,
             "structure": {k: stats[k] for k in ("m1", "n1", "m2", "n2", "T", "s", "r", "rank11", "engines",
-                                                 "svd_diag_row", "svd_diag_col") if k in stats},
+                                                 "svd_diag_row", "svd_diag_col", "sparse_core") if k in stats},
             "fp64_peaks_tflops": {"cublas_dgemm_8192": round(cublas_dgemm, 2), "dmma_microbench": round(fp64_peak, 2)},
         }
         if c5 is not None:

@@ -619,6 +619,12 @@ int fpi_column_update_shard(fpi_handle h, int64_t m_loc, int64_t s_prev, const d
       op.Dnz = Dnz.get();
     }
   }
+  // this rank's rows of T: their heavy rows x heavy columns rectangle on the tensor pipe (sparse_core.cu)
+  SparseCore core;
+  if (n2 > 0 && m_loc > 0) {
+    build_sparse_core(h, m_loc, n2, op.s_nnz, t_ptr, t_idx, t_val, tt_ptr, tt_idx, tt_val, core);
+    if (core.use) op.core = &core;
+  }
   Scratch<double> Vti(r * q, s);
   rsvd_sharded(h, op, m_global, r, seed, zoff, /*z_sharded=*/false, d_U, d_sigma, Vti, &h->diag);
   // lift (pinv.py:205-207) on this rank's columns

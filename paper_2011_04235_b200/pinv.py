@@ -493,6 +493,7 @@ def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = Non
     f_full, eng_c = column_update_device(f_rows, part.T, part.Tt, r, low_rank_threshold=cfg.low_rank_threshold,
                                          seed=cfg.seed + 2)
     diag_c = _lib.svd_diag() if stats is not None else None
+    core_c = _lib.sparse_core_info() if stats is not None else None
     clock.mark("column_update", f_full.rank)
 
     pv = _assemble(f_full, ordering.row_perm.device_forward(), ordering.col_perm.device_forward(),
@@ -503,7 +504,7 @@ def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = Non
         stats.update(engines=(eng_r, eng_c), s=s, r=r, rank11=f11.rank, m1=ordering.n_spoke_rows, n1=n1, m2=m2,
                      n2=n2, T=ordering.n_iterations, nnz_a12=part.info.nnz_a12, nnz_a22=part.info.nnz_a22,
                      nnz_a21=part.info.nnz_a21, nnz_a11=part.info.nnz_a11, f11=f11, f_rows=f_rows, part=part,
-                     svd_diag_row=diag_r, svd_diag_col=diag_c)
+                     svd_diag_row=diag_r, svd_diag_col=diag_c, sparse_core=core_c)
     return FastpiResult(pv, f_full, ordering, timings)
 
 
