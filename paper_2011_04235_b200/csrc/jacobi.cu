@@ -44,7 +44,12 @@ constexpr int JT = 256;     // threads per CTA
 constexpr int LDS_ = 36;    // smem stride (doubles): conflict-free DMMA fragment loads
 
 __device__ __forceinline__ int rr_block(int pos, int round, int nb) {
-  return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (nb - 1));
+  // (pos - 1 + round) mod (nb - 1) without the integer division: both terms are below nb - 1
+  const int m = nb - 1;
+  int x = pos - 1 + round;
+  if (x >= m) x -= m;
+  if (x >= m) x %= m;  // not taken for round < nb - 1
+  return pos == 0 ? 0 : 1 + x;
 }
 __device__ __forceinline__ int sub_to_global(int l, int bi, int bj) { return l < JB ? bi * JB + l : bj * JB + (l - JB); }
 
@@ -365,28 +370,35 @@ constexpr int JMAXP = 8;  // batches up to this size keep their descriptors in s
 #define JACOBI_CTAS_PER_SM 2
 #endif
 
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // dst <- M[rows, cols]: local row a -> global row r0 + a (r0 >= 0) or block pair (bi, bj); local
 // cols map to the block pair (ci, cj).  16 B chunks never straddle a 16-wide block.
+__device__ __forceinline__ void cp16s(unsigned smem_addr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr), "l"(gmem));
+}
+// (the shared address is converted once per tile, the column offset is common to a thread's two chunks)
 __device__ __forceinline__ void tile_async(double* dst, const double* M, int64_t ld, int64_t r0, int bi, int bj,
                                            int ci, int cj) {
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(dst);
+  const int c = (threadIdx.x & 15) * 2;
+  const double* Mc = M + sub_to_global(c, ci, cj);
+#pragma unroll
   for (int e = threadIdx.x; e < JS * 16; e += JT) {
-    const int a = e >> 4, c = (e & 15) * 2;
+    const int a = e >> 4;
     const int64_t row = r0 >= 0 ? r0 + a : (int64_t)sub_to_global(a, bi, bj);
-    cp16(dst + a * LDS_ + c, M + row * ld + sub_to_global(c, ci, cj));
+    cp16s(sbase + (unsigned)(a * LDS_ + c) * 8u, Mc + row * ld);
   }
 }
 __device__ __forceinline__ void j_async(double* dst, const double* J) {
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(dst);
+  const int c = (threadIdx.x & 15) * 2;
+#pragma unroll
   for (int e = threadIdx.x; e < JS * 16; e += JT) {
-    const int a = e >> 4, c = (e & 15) * 2;
-    cp16(dst + a * LDS_ + c, J + a * JS + c);
+    const int a = e >> 4;
+    cp16s(sbase + (unsigned)(a * LDS_ + c) * 8u, J + a * JS + c);
   }
 }
 
@@ -487,14 +499,21 @@ __host__ __device__ __forceinline__ int64_t g_runs_before(int64_t P, int64_t c) 
   const int64_t q = P / c, r = P % c;
   return P + c * q * (q - 1) / 2 + r * q;
 }
+// the same count in 32-bit unsigned arithmetic (device: the 64-bit divisions of the host version
+// cost ~100 instructions each, per thread, per step of the search below)
+__device__ __forceinline__ unsigned g_runs_before32(unsigned P, unsigned c) {
+  const unsigned q = P / c, r = P - q * c;
+  return P + ((c * q * (q - 1u)) >> 1) + r * q;
+}
 __device__ __forceinline__ void g_run(int64_t j, int np, int c, int& pb, int& chunk) {
+  const unsigned ju = (unsigned)j, cu = (unsigned)c;
   int lo = 0, hi = np - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (g_runs_before(mid, c) <= j) lo = mid; else hi = mid - 1;
+    if (g_runs_before32((unsigned)mid, cu) <= ju) lo = mid; else hi = mid - 1;
   }
   pb = lo;
-  chunk = (int)(j - g_runs_before(lo, c));
+  chunk = (int)(ju - g_runs_before32((unsigned)lo, cu));
 }
 
 // V[:, P'] <- V[:, P'] R_P' for the pending round of problem pr_: row tiles [r0, r1) of column pb.
@@ -570,7 +589,10 @@ __device__ void g_run_exec(const EigProb& pr_, int q, int pb, int a0, int a1, do
 __device__ __forceinline__ int rr_pos(int x, int rho, int nb) {
   if (x == 0) return 0;
   const int m = nb - 1;
-  return 1 + (((x - 1 - rho) % m) + m) % m;
+  int y = x - 1 - rho;  // in (-m, m) for rho < m: one conditional add instead of two divisions
+  if (y < 0) y += m;
+  if (y < 0 || y >= m) y = ((y % m) + m) % m;
+  return 1 + y;
 }
 
 // C (M x N) = op(A) (M x 32) B (32 x N), all in shared memory with explicit strides; M, N multiples
@@ -709,8 +731,8 @@ __device__ void section(EigProb* P, int nprob, int64_t total_pairs, int64_t tota
       if (!pr_.pend[q]) return;
       const int np = pr_.nb / 2;
       const int per = (np + vchunk - 1) / vchunk;
-      const int64_t j = vi - pr_.vitem_off;
-      const int pb = (int)(j / per), c = (int)(j % per);
+      const unsigned j = (unsigned)(vi - pr_.vitem_off);
+      const int pb = (int)(j / (unsigned)per), c = (int)(j - (unsigned)pb * (unsigned)per);
       const int r0 = c * vchunk, r1 = r0 + vchunk < np ? r0 + vchunk : np;
       v_run(pr_, q, pb, r0, r1, sm, warp, lane);
     }
