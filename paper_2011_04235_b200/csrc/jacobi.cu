@@ -47,8 +47,7 @@ __device__ __forceinline__ int rr_block(int pos, int round, int nb) {
   // (pos - 1 + round) mod (nb - 1) without the integer division: both terms are below nb - 1
   const int m = nb - 1;
   int x = pos - 1 + round;
-  if (x >= m) x -= m;
-  if (x >= m) x %= m;  // not taken for round < nb - 1
+  while (x >= m) x -= m;  // at most once for round < nb - 1
   return pos == 0 ? 0 : 1 + x;
 }
 __device__ __forceinline__ int sub_to_global(int l, int bi, int bj) { return l < JB ? bi * JB + l : bj * JB + (l - JB); }
@@ -499,21 +498,21 @@ __host__ __device__ __forceinline__ int64_t g_runs_before(int64_t P, int64_t c) 
   const int64_t q = P / c, r = P % c;
   return P + c * q * (q - 1) / 2 + r * q;
 }
-// the same count in 32-bit unsigned arithmetic (device: the 64-bit divisions of the host version
-// cost ~100 instructions each, per thread, per step of the search below)
-__device__ __forceinline__ unsigned g_runs_before32(unsigned P, unsigned c) {
-  const unsigned q = P / c, r = P - q * c;
-  return P + ((c * q * (q - 1u)) >> 1) + r * q;
-}
+// Run j of the G queue -> (block column pb, chunk).  Columns q c .. q c + c - 1 hold q + 1 runs each
+// (column P has floor(P / c) + 1), so the groups are walked by subtraction and one small division
+// finds the column inside the group -- the search over the closed form above cost a dozen integer
+// divisions per item and thread.
 __device__ __forceinline__ void g_run(int64_t j, int np, int c, int& pb, int& chunk) {
-  const unsigned ju = (unsigned)j, cu = (unsigned)c;
-  int lo = 0, hi = np - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (g_runs_before32((unsigned)mid, cu) <= ju) lo = mid; else hi = mid - 1;
+  unsigned jj = (unsigned)j, q = 0, step = (unsigned)c;  // step = c (q + 1) runs in group q
+  while (jj >= step) {
+    jj -= step;
+    step += (unsigned)c;
+    ++q;
   }
-  pb = lo;
-  chunk = (int)(ju - g_runs_before32((unsigned)lo, cu));
+  const unsigned col = jj / (q + 1u);
+  pb = (int)(q * (unsigned)c + col);
+  chunk = (int)(jj - col * (q + 1u));
+  (void)np;
 }
 
 // V[:, P'] <- V[:, P'] R_P' for the pending round of problem pr_: row tiles [r0, r1) of column pb.
@@ -590,8 +589,8 @@ __device__ __forceinline__ int rr_pos(int x, int rho, int nb) {
   if (x == 0) return 0;
   const int m = nb - 1;
   int y = x - 1 - rho;  // in (-m, m) for rho < m: one conditional add instead of two divisions
-  if (y < 0) y += m;
-  if (y < 0 || y >= m) y = ((y % m) + m) % m;
+  while (y < 0) y += m;
+  while (y >= m) y -= m;
   return 1 + y;
 }
 

@@ -1,4 +1,4 @@
-"""Time the c4 solve under eigensolver environment settings (one process; env read per call).
+"""Time the c4 (or --workload=c5) solve under eigensolver environment settings (one process; env read per call).
 
 usage: python tools/jacobi_tune.py "FPI_JACOBI_JOIN=1" "FPI_JACOBI_CHUNKS=4,3 FPI_JACOBI_SPREAD=4" ...
 An empty string is the default configuration."""
@@ -16,7 +16,10 @@ import paper_2011_04235_b200 as fp  # noqa: E402
 from paper_2011_04235_b200._device import DeviceCSR  # noqa: E402
 from paper_2011_04235_b200.pinv import fastpi_device  # noqa: E402
 
-p = bench.load_problem("c4")
+WORKLOAD = "c4"
+if len(sys.argv) > 1 and sys.argv[1].startswith("--workload="):
+    WORKLOAD = sys.argv.pop(1).split("=", 1)[1]
+p = bench.load_problem(WORKLOAD)
 w = p.workload
 cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
 A = DeviceCSR.from_host(p.A)
