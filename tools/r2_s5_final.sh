@@ -1,14 +1,11 @@
-# Round-2 evidence: full GPU tests, smoke, default bench (c4 + c5 record + CPU baseline), reference
-# arm, launch list, ncu captures of the top GEMM and the column-update eigensolve, Amdahl bounds.
+# Session-5 evidence at HEAD: full GPU tests, smoke, default bench, reference arm, launch list, Amdahl
 mkdir -p gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q -rf --durations=15 > gpurun_out/s5final_gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/s5final_gpu_tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s5final_smoke.log 2>&1; echo smoke_exit=$? >> gpurun_out/s5final_smoke.log
-timeout 1500 python bench.py > gpurun_out/s5final_bench.json 2> gpurun_out/s5final_bench.err
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/s5final_bench_ref.json 2> gpurun_out/s5final_bench_ref.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s5final_launches_c4.csv \
-  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-c5 > gpurun_out/s5final_ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm --launch-skip 53 -c 1 \
-  -o gpurun_out/s5final_gemm_full -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-c5 > gpurun_out/s5final_ncu_gemm.log 2>&1
-timeout 900 python tools/shard_amdahl.py c4 3 > gpurun_out/s5final_amdahl_c4.json 2> /dev/null
-timeout 1200 python tools/shard_amdahl.py c5 2 > gpurun_out/s5final_amdahl_c5.json 2> /dev/null
+timeout 2400 python -m pytest tests -m gpu -q -rf --durations=10 > gpurun_out/s5f2_gpu_tests.log 2>&1; echo tests_exit=$? >> gpurun_out/s5f2_gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s5f2_smoke.log 2>&1; echo smoke_exit=$? >> gpurun_out/s5f2_smoke.log
+timeout 1500 python bench.py > gpurun_out/s5f2_bench.json 2> gpurun_out/s5f2_bench.err
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/s5f2_bench_ref.json 2> gpurun_out/s5f2_bench_ref.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s5f2_launches_c4.csv \
+  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-c5 > gpurun_out/s5f2_ncu_launch.log 2>&1
+timeout 900 python tools/shard_amdahl.py c4 3 > gpurun_out/s5f2_amdahl_c4.json 2> /dev/null
+timeout 1200 python tools/shard_amdahl.py c5 2 > gpurun_out/s5f2_amdahl_c5.json 2> /dev/null
 echo done
