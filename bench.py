@@ -397,8 +397,9 @@ def ours_arm(args):
             largest = {"kernel": big_name, "share_of_step": round(big["ms"] / ms, 4), "launches": big["launches"],
                        "bound": "latency",
                        "note": "two-sided block Jacobi: sequential rotation chains + one grid barrier per round; "
-                               "ncu (c4 n = 1000 launch): DMMA sub-pipe 24% active, 4.9 barrier stalls per issue "
-                               "(profiles/r02_ncu_jacobi_final.json)"}
+                               "ncu: DMMA sub-pipe 27% active on the c4 n = 1000 launch (29% of the stall samples "
+                               "wait at the grid barrier for the pair CTAs' sub-solves), 40% on the c5 n = 2000 "
+                               "launch (profiles/r02_s5_ncu_jacobi_c5.json, r02_s5_ncu_jacobi_c5_source_after.txt)"}
         if roofline is not None:
             roofline["largest_kernel"] = largest
 
