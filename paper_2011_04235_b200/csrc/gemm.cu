@@ -587,9 +587,49 @@ bool launch_tma(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, c
   return true;
 }
 
+// An operand with an odd leading dimension (or an 8-byte aligned base) would put the whole product on
+// the 8-byte copies (18-24 instead of 26-30 TFLOP/s); the row update's rank s is such a dimension
+// (399 at c4, 939 at c5).  When the product is large enough to pay for one pass over the operand,
+// it is repacked into an even-stride scratch buffer first and the 16-byte / TMA tiles take it.
+__global__ void k_repack(int64_t rows, int64_t cols, const double* __restrict__ src, int64_t lds,
+                         double* __restrict__ dst, int64_t ldd) {
+  FPI_GRID_STRIDE(e, rows * cols) {
+    const int64_t r = e / cols, c = e - r * cols;
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+
 template <bool TA, bool TB>
 void launch_any(fpi_context* h, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
                 const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int sym) {
+  static const bool no_repack = getenv("FPI_GEMM_NO_REPACK") != nullptr;
+  const bool a_ok = (uintptr_t)A % 16 == 0 && lda % 2 == 0, b_ok = (uintptr_t)B % 16 == 0 && ldb % 2 == 0;
+  Scratch<double> Ar, Br;
+  if (!(a_ok && b_ok) && !no_repack && (double)M * (double)N * (double)K >= 2.5e8 && (a_ok || N >= 256) &&
+      (b_ok || M >= 256)) {
+    cudaStream_t s = h->stream;
+    const bool same = A == B && lda == ldb && TA != TB && M == N;  // the Gram products pass one operand twice
+    auto repack = [&](const double* src, int64_t rows, int64_t cols, int64_t ld, Scratch<double>& dst) {
+      const int64_t ldd = cols + (cols & 1);
+      dst.alloc(rows * ldd, s);
+      k_repack<<<grid_for(rows * cols, 256, (int64_t)h->num_sms * 16), 256, 0, s>>>(rows, cols, src, ld, dst.get(), ldd);
+      FPI_LAUNCH_CHECK();
+      note_launch(h);
+      return ldd;
+    };
+    if (!a_ok) {
+      lda = repack(A, TA ? K : M, TA ? M : K, lda, Ar);
+      if (same) {
+        B = Ar;
+        ldb = lda;
+      }
+      A = Ar;
+    }
+    if (!b_ok && B != A) {
+      ldb = repack(B, TB ? N : K, TB ? K : N, ldb, Br);
+      B = Br;
+    }
+  }
   const bool v16 = ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0) && lda % 2 == 0 && ldb % 2 == 0 &&
                    !getenv("FPI_GEMM_NO_V16");
   // TMA needs 16-byte aligned bases and row strides (the v16 condition)

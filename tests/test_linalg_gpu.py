@@ -64,6 +64,34 @@ def test_gemm_tma_path(ta, tb, M, N, K, tma, monkeypatch):
             assert np.abs(got - np.load(other)).max() <= 1e-14 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
 
 
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K,odd", [(399, 1000, 2001, "a"), (700, 399, 1999, "b"), (511, 513, 1001, "ab"),
+                                       (300, 100, 9001, "a")])
+def test_gemm_odd_stride_repack(ta, tb, M, N, K, odd):
+    """Operands with an odd leading dimension (the row update's rank: 399 at c4, 939 at c5) are
+    repacked into an even-stride scratch buffer when the product is large enough, so the 16-byte /
+    TMA tiles take them; the result equals numpy's, with a sub-matrix view as the operand (stride
+    larger than the width, 8-byte aligned base) as well.  (300, 100, 9001) stays on the 8-byte
+    copies (N < 256)."""
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import d2h
+    rng = np.random.default_rng(M + N + K)
+    sa = (K, M) if ta else (M, K)
+    sb = (N, K) if tb else (K, N)
+    pad_a = 1 if ("a" in odd and sa[1] % 2 == 0) else (0 if "a" in odd else sa[1] % 2)
+    pad_b = 1 if ("b" in odd and sb[1] % 2 == 0) else (0 if "b" in odd else sb[1] % 2)
+    Af = rng.standard_normal((sa[0], sa[1] + pad_a + 2))
+    Bf = rng.standard_normal((sb[0], sb[1] + pad_b + 2))
+    A, B = Af[:, 1:1 + sa[1]], Bf[:, :sb[1]]   # A starts one element into its row
+    ref = (A.T if ta else A) @ (B.T if tb else B)
+    dA, dB = _t(Af), _t(Bf)
+    dC = _t(np.zeros((M, N)))
+    _lib.call("fpi_gemm", ta, tb, M, N, K, 1.0, C.c_void_p(dA.data_ptr() + 8), Af.shape[1], _lib.ptr(dB), Bf.shape[1], 0.0,
+              _lib.ptr(dC), N)
+    got = d2h(dC)
+    assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
+
+
 @pytest.mark.parametrize("ta", [0, 1])
 def test_gram_sym_tma(ta):
     """Symmetric (Gram) mode: lower tiles computed and mirrored (exactly symmetric result)."""
