@@ -65,6 +65,7 @@ struct Params {
   double k;
   int levels;  // hub-degree radix-select levels (11 bits each)
   int hk;      // edges in flight per thread when hooking
+  int hshort;  // skip an edge whose endpoints already share a parent
   int ne0;
   uint64_t* e0;
   uint64_t* e1;
@@ -389,6 +390,7 @@ __device__ __forceinline__ void hook_edges(const Params& P, const uint64_t* E, i
 #pragma unroll
     for (int j = 0; j < HK; ++j) {
       if (!ok[j]) continue;
+      if (P.hshort && pu[j] == pv[j]) continue;  // a common parent: already one component
       int32_t ru = find_root_from(u[j], pu[j], P.parent), rv = find_root_from(v[j], pv[j], P.parent);
       while (ru != rv) {
         if (ru < rv) {
@@ -1014,6 +1016,8 @@ bool run_reorder_persistent(fpi_context* h, int64_t m, int64_t n, int64_t nnz, c
   {
     const char* e = getenv("FPI_REORDER_HK");
     P.hk = e ? atoi(e) : 1;
+    const char* e2 = getenv("FPI_REORDER_SHORT");
+    P.hshort = e2 ? atoi(e2) : 1;
   }
   P.e0 = e0;
   P.e1 = e1;
