@@ -17,7 +17,7 @@
  *    return sizes or flags to the host synchronise that stream.
  *  - Return value: FPI_OK or an error code; fpi_last_error(h) has the message.
  *    FPI_EDOMAIN -> ValueError, FPI_ECAPACITY -> CapacityError,
- *    FPI_ESTRUCT -> StructuralViolationError, FPI_ECUDA / FPI_ENUMERIC ->
+ *    FPI_ESTRUCT -> StructuralViolationError, FPI_ERETRY -> (internal) retry, FPI_ECUDA / FPI_ENUMERIC ->
  *    RuntimeError (reference validation.py:22-35).
  *  - Handles are not thread-safe; use one per host thread.
  */
@@ -38,6 +38,7 @@ extern "C" {
 #define FPI_ESTRUCT 3
 #define FPI_ECUDA 4
 #define FPI_ENUMERIC 5
+#define FPI_ERETRY 6 /* a speculative fast path did not apply: repeat the call without it */
 
 typedef struct fpi_context* fpi_handle;
 
@@ -201,6 +202,19 @@ int fpi_fastpi_release(fpi_handle h);
 int fpi_fastpi_ex(fpi_handle h, int64_t m, int64_t n, int64_t nnz, const int64_t* d_indptr, const int32_t* d_indices,
                   const double* d_values, double alpha, double k, int64_t seed, double low_rank_threshold,
                   double pinv_cutoff, int32_t flags, fpi_fastpi_info* h_info);
+/* FPI_FASTPI_DEFERRED_VALUES (with FPI_FASTPI_CANONICAL): d_values is still being uploaded when the
+ * call starts.  Algorithm 2 (reorder.py:158-287) reads only the sparsity pattern, so a host caller can
+ * copy the values (2/3 of a CSR's bytes) to the device on another stream meanwhile.  The solve checks
+ * the pattern half of check_csr (validation.py:38-55: sorted, no duplicates) first, runs the reorder,
+ * then calls the hook registered with fpi_fastpi_values_hook: it blocks until the upload has been
+ * ENQUEUED and returns 0 with the cudaEvent_t recorded behind it in *event_out (the solve's stream
+ * waits for that event), and the value half of the check (no explicit zeros) runs before the
+ * partition (reorder.py:310-337).  A CSR that fails either half returns FPI_ERETRY before any result
+ * exists: canonicalize it (fpi_csr_canonicalize) and call again without the flag.  The hook is
+ * cleared by every fpi_fastpi_ex call. */
+#define FPI_FASTPI_DEFERRED_VALUES 2
+typedef int (*fpi_values_hook)(void* ctx, void** event_out);
+int fpi_fastpi_values_hook(fpi_handle h, fpi_values_hook hook, void* ctx);
 /* Ownership transfer of the last fpi_fastpi result: the caller receives the device buffers below
  * (stream-ordered allocations of the handle's device pool; free each with fpi_device_free) plus,
  * optionally, the GCC sizes (h_gcc, capacity gcc_cap >= info.n_gcc) and the device time of the five

@@ -16,7 +16,12 @@ from .validation import CapacityError, StructuralViolationError
 
 LIB_PATH = Path(__file__).resolve().with_name("libfastpi_b200.so")
 
-FPI_OK, FPI_EDOMAIN, FPI_ECAPACITY, FPI_ESTRUCT, FPI_ECUDA, FPI_ENUMERIC = range(6)
+FPI_OK, FPI_EDOMAIN, FPI_ECAPACITY, FPI_ESTRUCT, FPI_ECUDA, FPI_ENUMERIC, FPI_ERETRY = range(7)
+
+
+class RetryError(RuntimeError):
+    """FPI_ERETRY: a speculative fast path did not apply; the caller repeats the call without it."""
+
 
 i64 = C.c_int64
 i32 = C.c_int32
@@ -56,6 +61,8 @@ class FastpiInfo(C.Structure):
 
 
 FASTPI_CANONICAL = 1  # fpi_fastpi_ex flag: the CSR is canonical already
+FASTPI_DEFERRED_VALUES = 2  # fpi_fastpi_ex flag: d_values is still uploading (fpi_fastpi_values_hook)
+VALUES_HOOK = C.CFUNCTYPE(C.c_int, vp, C.POINTER(vp))
 
 
 class FastpiBuffers(C.Structure):
@@ -126,6 +133,7 @@ SIGNATURES = {
     "fpi_fastpi_release": (C.c_int, [vp]),
     "fpi_fastpi_ex": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, f64, f64, i64, f64, f64, i32,
                                 C.POINTER(FastpiInfo)]),
+    "fpi_fastpi_values_hook": (C.c_int, [vp, VALUES_HOOK, vp]),
     "fpi_fastpi_take": (C.c_int, [vp, C.POINTER(FastpiBuffers), C.POINTER(i64), i64, C.POINTER(C.c_float)]),
     "fpi_device_free": (C.c_int, [vp, vp]),
     "fpi_timing_enable": (C.c_int, [vp, C.c_int]),
@@ -217,6 +225,8 @@ def raise_for_status(rc: int, msg: str, name: str = "") -> None:
         raise CapacityError(msg)
     if rc == FPI_ESTRUCT:
         raise StructuralViolationError(msg)
+    if rc == FPI_ERETRY:
+        raise RetryError(msg)
     raise RuntimeError(f"{name}: {msg}" if name else msg)
 
 

@@ -80,6 +80,9 @@ struct fpi_context {
   // numerics diagnostics of the last randomized / dense SVD
   fpi_svd_diag diag{};
   int64_t sparse_core[4] = {0, 0, 0, 0};  // last column update's dense core (fpi_sparse_core_info)
+  // fpi_fastpi_values_hook: the caller's "values are on their way" callback of a deferred upload
+  int (*values_hook)(void*, void**) = nullptr;
+  void* values_hook_ctx = nullptr;
   // cross-rank communicator of a sharded solve (comm.cu), null for one rank
   fpi::Comm* comm = nullptr;
   // counters

@@ -67,6 +67,35 @@ void fastpi_free(fpi_context* h) {
 
 }  // namespace fpi
 
+namespace fpi {
+namespace {
+// the two halves of the canonical-form check (sparse.cu k_check_canonical) for a deferred upload
+__global__ void k_check_pattern(int64_t m, const int64_t* __restrict__ indptr, const int32_t* __restrict__ idx,
+                                int* __restrict__ bad) {
+  FPI_GRID_STRIDE(r, m) {
+    const int64_t b = indptr[r], e = indptr[r + 1];
+    for (int64_t p = b + 1; p < e; ++p)
+      if (idx[p] <= idx[p - 1]) {
+        *bad = 1;
+        break;
+      }
+  }
+}
+__global__ void k_check_values(int64_t nnz, const double* __restrict__ val, int* __restrict__ bad) {
+  bool z = false;
+  FPI_GRID_STRIDE(i, nnz) z |= val[i] == 0.0;
+  if (z) *bad = 1;
+}
+}  // namespace
+}  // namespace fpi
+
+extern "C" int fpi_fastpi_values_hook(fpi_handle h, fpi_values_hook hook, void* ctx) {
+  FPI_API_BEGIN(h)
+  h->values_hook = hook;
+  h->values_hook_ctx = ctx;
+  FPI_API_END(h)
+}
+
 extern "C" int fpi_fastpi_ex(fpi_handle h, int64_t m, int64_t n, int64_t nnz, const int64_t* d_indptr,
                              const int32_t* d_indices, const double* d_values, double alpha, double k, int64_t seed,
                              double low_rank_threshold, double pinv_cutoff, int32_t flags, fpi_fastpi_info* h_info) {
@@ -76,8 +105,23 @@ extern "C" int fpi_fastpi_ex(fpi_handle h, int64_t m, int64_t n, int64_t nnz, co
   FPI_REQUIRE(m >= n, FPI_EDOMAIN, "fpi_fastpi expects m >= n (factor A^T and swap the factors otherwise)");
   FPI_REQUIRE(alpha > 0.0 && alpha <= 1.0, FPI_EDOMAIN, "target rank ratio alpha must be in (0, 1]");
   cudaStream_t s = h->stream;
+  const fpi_values_hook values_hook = h->values_hook;
+  void* const values_ctx = h->values_hook_ctx;
+  h->values_hook = nullptr;
+  h->values_hook_ctx = nullptr;
+  const bool deferred = (flags & FPI_FASTPI_DEFERRED_VALUES) != 0;
+  FPI_REQUIRE(!deferred || ((flags & FPI_FASTPI_CANONICAL) != 0 && values_hook != nullptr), FPI_EDOMAIN,
+              "FPI_FASTPI_DEFERRED_VALUES needs FPI_FASTPI_CANONICAL and a hook (fpi_fastpi_values_hook)");
   delete h->fastpi;
   h->fastpi = nullptr;
+  if (deferred) {  // pattern half of check_csr before anything is speculated on it
+    Scratch<int> bad(1, s);
+    FPI_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    fpi::k_check_pattern<<<fpi::grid_for(m, 256, (int64_t)h->num_sms * 16), 256, 0, s>>>(m, d_indptr, d_indices, bad);
+    FPI_LAUNCH_CHECK();
+    fpi::note_launch(h);
+    if (fpi::host_read(bad.get(), s)) throw fpi::Error(FPI_ERETRY, "deferred upload: the CSR pattern is not canonical");
+  }
   auto* res = new fpi::FastpiResult();
   h->fastpi = res;
   fpi_fastpi_info& info = res->info;
@@ -127,6 +171,25 @@ extern "C" int fpi_fastpi_ex(fpi_handle h, int64_t m, int64_t n, int64_t nnz, co
   fpi_partition_info pi{};
   fpi::ok(h, fpi_partition_count(h, m, n, cnnz, cp, ci, row_fwd, col_fwd, m1, n1, ri.n_spans, spans, &pi));
   const int64_t nT = pi.nnz_a12 + pi.nnz_a22;
+  if (deferred) {
+    // the values were uploading on the caller's stream while the reorder ran: wait for them, then the
+    // value half of check_csr (no explicit zeros)
+    void* ev = nullptr;
+    if (values_hook(values_ctx, &ev) != 0 || ev == nullptr) {
+      fpi::fastpi_free(h);
+      throw fpi::Error(FPI_ECUDA, "deferred upload: the values hook failed");
+    }
+    FPI_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev), 0));
+    Scratch<int> bad(1, s);
+    FPI_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    fpi::k_check_values<<<fpi::grid_for(cnnz, 256, (int64_t)h->num_sms * 16), 256, 0, s>>>(cnnz, cv, bad);
+    FPI_LAUNCH_CHECK();
+    fpi::note_launch(h);
+    if (fpi::host_read(bad.get(), s)) {
+      fpi::fastpi_free(h);
+      throw fpi::Error(FPI_ERETRY, "deferred upload: the CSR holds explicit zeros");
+    }
+  }
   Scratch<int64_t> a11p(m1 + 1, s), tp(m + 1, s), ttp(n2 + 1, s), a21p(m2 + 1, s), a21tp(n1 + 1, s);
   Scratch<int32_t> a11i(pi.nnz_a11, s), ti(nT, s), tti(nT, s), a21i(pi.nnz_a21, s), a21ti(pi.nnz_a21, s);
   Scratch<double> a11v(pi.nnz_a11, s), tv(nT, s), ttv(nT, s), a21v(pi.nnz_a21, s), a21tv(pi.nnz_a21, s);

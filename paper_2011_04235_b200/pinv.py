@@ -22,7 +22,7 @@ from . import _lib
 from ._device import DeviceCSR, d2h, empty, h2d, torch
 from .reorder import Permutation, ReorderResult, partition_original, reorder_device
 from .svd import SvdFactors, _Dense, _to_dense, block_diagonal_svd_device, dense_svd, truncate
-from .validation import DENSE_CAPACITY, CapacityError
+from .validation import DENSE_CAPACITY, CapacityError, as_csr
 
 EPS = float(np.finfo(np.float64).eps)
 
@@ -415,7 +415,7 @@ def _adopt(ptr, shape, dtype, device):
     return t.as_tensor(_Owned(ptr, shape, typestr, device), device=t.device("cuda", device))
 
 
-def _fastpi_one_call(dev: DeviceCSR, cfg: FastpiConfig) -> FastpiResult:
+def _fastpi_one_call(dev: DeviceCSR, cfg: FastpiConfig, flags: int = _lib.FASTPI_CANONICAL) -> FastpiResult:
     """Algorithm 1 behind one C call (fpi_fastpi_ex, csrc/fastpi_capi.cu): the same stage entry points
     as the stage-by-stage mirror below, in the same order with the same ranks and seeds (identical
     bits, tests/test_pipeline_gpu.py), without a Python round trip and its allocations between the
@@ -426,7 +426,7 @@ def _fastpi_one_call(dev: DeviceCSR, cfg: FastpiConfig) -> FastpiResult:
     info = _lib.FastpiInfo()
     _lib.call("fpi_fastpi_ex", m, n, dev.nnz, _lib.ptr(dev.indptr), _lib.ptr(dev.indices), _lib.ptr(dev.values),
               float(cfg.alpha), float(cfg.k), int(cfg.seed), float(cfg.low_rank_threshold),
-              float(cfg.pinv_cutoff_factor), _lib.FASTPI_CANONICAL, C.byref(info))
+              float(cfg.pinv_cutoff_factor), flags, C.byref(info))
     if info.rank_clamped:
         warnings.warn(f"row-update target rank clamped from {math.ceil(cfg.alpha * info.n1)} to {info.s} "
                       "(block stage produced less derivable rank)")
@@ -457,6 +457,7 @@ def _fastpi_one_call(dev: DeviceCSR, cfg: FastpiConfig) -> FastpiResult:
 
 
 _STAGEWISE = bool(__import__("os").environ.get("FPI_STAGEWISE"))
+_NO_DEFER = bool(__import__("os").environ.get("FPI_NO_DEFERRED_UPLOAD"))
 
 
 def fastpi_device(dev: DeviceCSR, cfg: FastpiConfig, *, stats: dict | None = None,
@@ -523,9 +524,116 @@ def _swap(res: FastpiResult) -> FastpiResult:
     return FastpiResult(swapped, factors, res.reordering, res.timings)
 
 
+_DEFER_MIN_NNZ = 1 << 20
+_DEFER_TRACE = bool(__import__("os").environ.get("FPI_DEFER_TRACE"))
+_UPLOADER = None
+
+
+def _uploader():
+    """One long-lived worker thread for the deferred uploads (its CUDA context binding and torch's
+    per-thread state are set up once, not per solve)."""
+    global _UPLOADER
+    if _UPLOADER is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _UPLOADER = ThreadPoolExecutor(max_workers=1, thread_name_prefix="fastpi-values-upload")
+    return _UPLOADER
+
+
+def _fastpi_host_overlapped(A, cfg: FastpiConfig):
+    """fastpi(A) for a host CSR with the upload of A's values hidden behind the reorder.
+
+    Algorithm 2 (reorder.py:158-287) reads only the sparsity pattern, and the values are 2/3 of a
+    CSR's bytes: the pattern is uploaded first, a worker thread stages the values into page-locked
+    memory and copies them on a side stream while the solve's C call (FPI_FASTPI_DEFERRED_VALUES)
+    runs the reorder; the call waits for the copy's event before the partition.  check_csr's
+    canonical-form test (validation.py:38-55) runs in its two halves (pattern before the reorder,
+    values before the partition); an input that is not canonical already makes the call return
+    FPI_ERETRY, and None is returned for the plain path (canonicalize, then solve).  Same bits."""
+    import threading
+    t = torch()
+    trace = [] if _DEFER_TRACE else None
+    t_0 = time.perf_counter()
+    m, n = A.shape
+    nnz = int(A.nnz)
+    device = t.cuda.current_device()
+    main = t.cuda.current_stream()
+    indptr = h2d(A.indptr, np.int64)
+    indices = h2d(A.indices, np.int32)
+    values = t.empty(nnz, dtype=t.float64, device=t.device("cuda", device))
+    ready = t.cuda.Event()
+    ready.record(main)          # the side stream must not write the block before main could have freed it
+    copied = t.cuda.Event()
+    side = t.cuda.Stream(device=device)
+    enqueued = threading.Event()
+    failure: list = []
+    data = np.ascontiguousarray(A.data, dtype=np.float64)
+
+    def upload():
+        try:
+            if trace is not None:
+                trace.append(("worker starts", time.perf_counter() - t_0))
+            t.cuda.set_device(device)
+            with t.cuda.stream(side):
+                side.wait_event(ready)
+                staged = t.empty(nnz, dtype=t.float64, pin_memory=True)
+                if trace is not None:
+                    trace.append(("pinned block", time.perf_counter() - t_0))
+                staged.copy_(t.from_numpy(data))
+                if trace is not None:
+                    trace.append(("staged", time.perf_counter() - t_0))
+                values.copy_(staged, non_blocking=True)
+                copied.record(side)
+            if trace is not None:
+                trace.append(("enqueued", time.perf_counter() - t_0))
+        except BaseException as e:  # surfaced through the hook's return code
+            failure.append(e)
+        finally:
+            enqueued.set()
+
+    @_lib.VALUES_HOOK
+    def hook(_ctx, event_out):
+        if trace is not None:
+            trace.append(("hook called", time.perf_counter() - t_0))
+        enqueued.wait()
+        if failure:
+            return 1
+        event_out[0] = copied.cuda_event
+        return 0
+
+    worker = _uploader().submit(upload)
+    if trace is not None:
+        trace.append(("pattern uploaded, worker submitted", time.perf_counter() - t_0))
+    dev = DeviceCSR((m, n), indptr, indices, values)
+    try:
+        _lib.call("fpi_fastpi_values_hook", hook, None)
+        res = _fastpi_one_call(dev, cfg, _lib.FASTPI_CANONICAL | _lib.FASTPI_DEFERRED_VALUES)
+    except _lib.RetryError:
+        res = None
+    finally:
+        worker.result()
+        if not failure:
+            main.wait_event(copied)  # later work on the main stream (and the block's reuse) follows the copy
+    if trace is not None:
+        trace.append(("call returned", time.perf_counter() - t_0))
+        print("[deferred upload] " + "  ".join(f"{k} {1e3 * v:.2f}" for k, v in sorted(trace, key=lambda x: x[1])),
+              file=__import__("sys").stderr, flush=True)
+    if failure:
+        raise failure[0]
+    if res is None:
+        return None, dev
+    return res, dev
+
+
 def fastpi(A, config: FastpiConfig | None = None) -> FastpiResult:
     """pinv.py:278-347: reorder, block SVD, two incremental updates, assembly."""
     cfg = config or FastpiConfig()
+    if (not isinstance(A, DeviceCSR) and not _STAGEWISE and not _TRACE and not _NO_DEFER):
+        A = as_csr(A)
+        if A.shape[0] >= A.shape[1] > 0 and A.nnz >= _DEFER_MIN_NNZ:
+            res, raw = _fastpi_host_overlapped(A, cfg)
+            if res is not None:
+                return res
+            A = raw.canonical()  # not canonical: check_csr's copy, then the plain path below
     dev = A if isinstance(A, DeviceCSR) else DeviceCSR.from_host(A)
     m, n = dev.shape
     if m == 0 or n == 0:

@@ -373,3 +373,94 @@ def test_block_sigma_c4_against_lapack():
     from paper_2011_04235_b200.svd import block_diagonal_svd_device
     f1 = block_diagonal_svd_device(part.a11, res.reordering.spans_device(), 1.0)
     assert_block_sigma(f1.sigma, fo1.sigma, spans, 1.0, label="c4 f11 alpha=1")
+
+
+def _result_arrays(res):
+    from paper_2011_04235_b200._device import d2h
+    d = res.pseudoinverse._device()
+    fd = res.factors.device()
+    return [d2h(x) for x in (fd.U, fd.sigma, fd.Vt, d.sdag, d.row_fwd, d.col_fwd)]
+
+
+@pytest.mark.parametrize("name", ["c2", "c3r100"])
+def test_deferred_values_upload_same_bits(name, monkeypatch):
+    """fastpi(host CSR) hides the upload of A's values behind the reorder (fpi_fastpi_ex with
+    FPI_FASTPI_DEFERRED_VALUES + fpi_fastpi_values_hook): the factors, sigma+, and permutations are
+    bit-identical to the plain upload-then-solve path, and so is apply()."""
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200 import pinv as pinv_mod
+    p = problem(name)
+    w = p.workload
+    cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
+    monkeypatch.setattr(pinv_mod, "_NO_DEFER", True)
+    plain = fp.fastpi(p.A, cfg)
+    ref = _result_arrays(plain)
+    Zp = plain.pseudoinverse.apply(p.Y)
+    monkeypatch.setattr(pinv_mod, "_NO_DEFER", False)
+    monkeypatch.setattr(pinv_mod, "_DEFER_MIN_NNZ", 0)
+    calls = []
+    orig = pinv_mod._fastpi_host_overlapped
+    monkeypatch.setattr(pinv_mod, "_fastpi_host_overlapped", lambda A, c: calls.append(1) or orig(A, c))
+    for _ in range(3):  # repeated: the side-stream copy and the worker thread must not race the solve
+        got = fp.fastpi(p.A, cfg)
+        for a, b in zip(_result_arrays(got), ref):
+            np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(got.pseudoinverse.apply(p.Y), Zp)
+    assert len(calls) == 3
+
+
+@pytest.mark.parametrize("defect", ["unsorted", "duplicates", "explicit_zero"])
+def test_deferred_values_upload_falls_back_on_non_canonical_input(defect, monkeypatch):
+    """A CSR that check_csr (validation.py:38-55) would rewrite -- unsorted indices, duplicate entries
+    or explicit zeros -- fails one half of the deferred path's canonical-form test (FPI_ERETRY) and
+    takes the plain path: same bits as with the deferred upload disabled."""
+    import scipy.sparse as sp
+    import paper_2011_04235_b200 as fp
+    from paper_2011_04235_b200 import _lib, pinv as pinv_mod
+    p = problem("c2")
+    w = p.workload
+    cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
+    A = p.A.copy()
+    ip, ix, dv = A.indptr.copy(), A.indices.copy(), A.data.copy()
+    r = int(np.argmax(np.diff(ip) >= 3))
+    b = ip[r]
+    if defect == "unsorted":
+        ix[b], ix[b + 1] = ix[b + 1], ix[b]
+        dv[b], dv[b + 1] = dv[b + 1], dv[b]
+    elif defect == "duplicates":
+        ix[b + 1] = ix[b]
+    else:
+        dv[b + 2] = 0.0
+    B = sp.csr_matrix((dv, ix, ip), shape=A.shape)
+    B.has_sorted_indices = True  # keep scipy from repairing it
+    monkeypatch.setattr(pinv_mod, "_NO_DEFER", True)
+    ref = _result_arrays(fp.fastpi(B, cfg))
+    monkeypatch.setattr(pinv_mod, "_NO_DEFER", False)
+    monkeypatch.setattr(pinv_mod, "_DEFER_MIN_NNZ", 0)
+    seen = []
+    orig = pinv_mod._fastpi_host_overlapped
+
+    def spy(M, c):
+        out = orig(M, c)
+        seen.append(out[0] is None)
+        return out
+    monkeypatch.setattr(pinv_mod, "_fastpi_host_overlapped", spy)
+    got = _result_arrays(fp.fastpi(B, cfg))
+    assert seen == [True]
+    for a, b_ in zip(got, ref):
+        np.testing.assert_array_equal(a, b_)
+
+
+def test_deferred_values_flag_needs_hook():
+    """FPI_FASTPI_DEFERRED_VALUES without a registered hook (or without FPI_FASTPI_CANONICAL) is a
+    domain error, not a solve on half-uploaded values."""
+    import ctypes as C
+    from paper_2011_04235_b200 import _lib
+    from paper_2011_04235_b200._device import DeviceCSR
+    p = problem("c1")
+    A = DeviceCSR.from_host(p.A)
+    info = _lib.FastpiInfo()
+    for flags in (_lib.FASTPI_DEFERRED_VALUES, _lib.FASTPI_DEFERRED_VALUES | _lib.FASTPI_CANONICAL):
+        with pytest.raises(ValueError):
+            _lib.call("fpi_fastpi_ex", A.shape[0], A.shape[1], A.nnz, _lib.ptr(A.indptr), _lib.ptr(A.indices),
+                      _lib.ptr(A.values), 0.5, 0.01, 0, 0.3, 1.0, flags, C.byref(info))
