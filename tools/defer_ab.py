@@ -16,7 +16,8 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 15
 p = bench.load_problem(name)
 w = p.workload
 cfg = fp.FastpiConfig(alpha=w.alpha, k=w.k, seed=w.seed)
-times = {True: [], False: [], "upload": [], "solve": []}
+times = {True: [], False: [], "upload": [], "solve": [], "e2e deferred": [], "e2e plain": [],
+         "apply after deferred": [], "apply after plain": []}
 for i in range(3 + reps):
     for defer in (False, True):
         pinv_mod._NO_DEFER = not defer
@@ -28,6 +29,19 @@ for i in range(3 + reps):
         if i >= 3:
             times[defer].append(dt)
         del res
+    for defer in (False, True):  # the bench's e2e step: fastpi + apply -> numpy Z, no sync between
+        pinv_mod._NO_DEFER = not defer
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = fp.fastpi(p.A, cfg)
+        t1 = time.perf_counter()
+        Z = res.pseudoinverse.apply(p.Y)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        if i >= 3:
+            times["e2e deferred" if defer else "e2e plain"].append(t2 - t0)
+            times["apply after deferred" if defer else "apply after plain"].append(t2 - t1)
+        del res, Z
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     A = DeviceCSR.from_host(p.A)
