@@ -434,7 +434,8 @@ def ours_arm(args):
             del res, Zh
         e2e = {"value": max_over_ranks(statistics.mean(e2e_t), world), "unit": "s",
                "h2d_bytes_per_step": int(h2d_bytes), "d2h_bytes_per_step": int(d2h_bytes),
-               "note": "fastpi(A scipy) + pseudoinverse.apply(Y scipy) -> numpy Z; pinned staging inside"}
+               "note": "fastpi(A scipy) + pseudoinverse.apply(Y scipy) -> numpy Z; pinned staging inside, the upload of "
+                       "A's values overlaps the reorder (FPI_NO_DEFERRED_UPLOAD=1 disables it)"}
 
     # ---- CPU baseline (rank 0, N=1)
     cpu = None
