@@ -252,9 +252,29 @@ def _ncu_traffic():
             "ncu_duration": g.get("duration")}
 
 
+def arm_watchdog(world, rank, seconds):
+    """Multi-rank runs only: a collective that one rank never joins (a crashed peer, a communicator
+    that failed to form) would hang the job.  After `seconds` the rank reports where it stands on
+    stderr and exits non-zero, so torchrun tears the job down instead of waiting out its own limit."""
+    if world <= 1 or seconds <= 0:
+        return None
+    import threading
+
+    def fire():
+        log(f"[bench] rank {rank}/{world}: no result after {seconds:.0f}s -- a collective is stuck; aborting")
+        import faulthandler
+        faulthandler.dump_traceback(file=sys.stderr)
+        os._exit(3)
+    t = threading.Timer(seconds, fire)
+    t.daemon = True
+    t.start()
+    return t
+
+
 def ours_arm(args):
     import torch
     world, rank, local = dist_setup()
+    arm_watchdog(world, rank, args.dist_timeout)
     import paper_2011_04235_b200 as fp
     from paper_2011_04235_b200 import _lib
     from paper_2011_04235_b200._device import DeviceCSR
@@ -539,6 +559,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=240.0, help="seconds of reference steps before stopping")
     ap.add_argument("--no-c5", action="store_true", help="skip the configs[4] (c5) record of the c4 run")
     ap.add_argument("--c5-timeout", type=float, default=600.0)
+    ap.add_argument("--dist-timeout", type=float, default=1800.0,
+                    help="multi-rank runs: abort a rank that has no result after this many seconds")
     ap.add_argument("--cpu-partial", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
