@@ -242,10 +242,16 @@ def workload_config(p, world=1):
 def _ncu_traffic():
     """DRAM bytes of one representative launch of the dominant kernel, from the committed
     `ncu --set full` capture summary (profiles/); None when absent."""
-    f = Path(__file__).resolve().parent / "profiles" / "r02_ncu_full_summary.json"
-    try:
-        g = json.loads(f.read_text())["r02_gemm_c4_apply_lift"]
-    except (OSError, KeyError, ValueError):
+    g = None
+    for name, key in (("r02_s6_ncu_summary.json", "gemm_c4_apply_lift"),
+                      ("r02_ncu_full_summary.json", "r02_gemm_c4_apply_lift")):
+        f = Path(__file__).resolve().parent / "profiles" / name
+        try:
+            g = json.loads(f.read_text())[key]
+            break
+        except (OSError, KeyError, ValueError):
+            continue
+    if g is None:
         return None
     return {"source": f"profiles/{f.name}", "launch": g.get("launch"), "traffic_bytes": g.get("traffic_bytes"),
             "algorithmic_bytes": g.get("algorithmic_bytes"), "dmma_pipe_active": g.get("dmma_pipe_active_pct"),
