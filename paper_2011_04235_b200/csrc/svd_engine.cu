@@ -1370,14 +1370,18 @@ void pinv_apply_csr_host(fpi_context* h, int64_t m, int64_t n, int64_t r, const 
   // ~64 MB chunks, at least 256 rows, double-buffered on the device
   int64_t rows = (int64_t)((64ll << 20) / (8 * L));
   if (rows < 256) rows = 256;
+  rows &= ~(int64_t)1;  // even chunk offsets keep Vg + a 16-byte aligned (the GEMM's 16-byte / TMA tiles)
   if (rows > n) rows = n;
   Scratch<double> buf(2 * rows * L, s);
   cudaStream_t cs = h->copy_stream;
   cudaEvent_t* ready = h->copy_ev;      // [0], [1]: chunk computed
   cudaEvent_t* drained = h->copy_ev + 2;  // [2], [3]: buffer copied out
   int64_t c = 0;
-  for (int64_t a = 0; a < n; a += rows, ++c) {
-    const int64_t nr = (n - a < rows) ? n - a : rows;
+  // the copies are the longer pole (PCIe), so the first one should start early: the chunks grow
+  // 1/8, 1/4, 1/2, 1, 1, ... of the buffer size
+  int64_t step = rows / 8 >= 256 ? (rows / 8) & ~(int64_t)1 : rows;
+  for (int64_t a = 0; a < n; a += step, step = (2 * step < rows ? 2 * step : rows), ++c) {
+    const int64_t nr = (n - a < step) ? n - a : step;
     const int sl = (int)(c & 1);
     double* d = buf.get() + sl * rows * L;
     if (c >= 2) FPI_CUDA(cudaStreamWaitEvent(s, drained[sl], 0));
