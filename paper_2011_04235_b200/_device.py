@@ -25,6 +25,9 @@ def device():
     return t.device("cuda", t.cuda.current_device())
 
 
+_H2D_CHUNK = 16 << 20
+
+
 def h2d(arr: np.ndarray, dtype=None):
     """Host numpy -> device tensor (through pinned memory, async on the current stream).  Large
     arrays are staged into a page-locked block from torch's caching host allocator by a parallel
@@ -32,6 +35,18 @@ def h2d(arr: np.ndarray, dtype=None):
     t = torch()
     a = np.ascontiguousarray(arr if dtype is None else arr.astype(dtype, copy=False))
     host = t.from_numpy(a)
+    if a.nbytes >= 2 * _H2D_CHUNK:
+        # chunked: the staging copy of chunk k runs while the DMA of chunk k - 1 is in flight, so the
+        # upload costs the staging pass plus one chunk's transfer instead of staging + the whole transfer
+        dev = t.empty(host.shape, dtype=host.dtype, device=device())
+        fh, fd = host.reshape(-1), dev.view(-1)
+        step = max(1, _H2D_CHUNK // a.itemsize)
+        for off in range(0, fh.numel(), step):
+            n = min(step, fh.numel() - off)
+            staged = t.empty(n, dtype=host.dtype, pin_memory=True)
+            staged.copy_(fh[off:off + n])
+            fd[off:off + n].copy_(staged, non_blocking=True)
+        return dev
     if a.nbytes >= (1 << 20):
         staged = t.empty(host.shape, dtype=host.dtype, pin_memory=True)
         staged.copy_(host)

@@ -575,13 +575,15 @@ def _fastpi_host_overlapped(A, cfg: FastpiConfig):
             t.cuda.set_device(device)
             with t.cuda.stream(side):
                 side.wait_event(ready)
-                staged = t.empty(nnz, dtype=t.float64, pin_memory=True)
-                if trace is not None:
-                    trace.append(("pinned block", time.perf_counter() - t_0))
-                staged.copy_(t.from_numpy(data))
+                src = t.from_numpy(data)
+                step = max(1, (16 << 20) // 8)  # 16 MB chunks: staging of chunk k overlaps the DMA of k - 1
+                for off in range(0, nnz, step):
+                    cnt = min(step, nnz - off)
+                    staged = t.empty(cnt, dtype=t.float64, pin_memory=True)
+                    staged.copy_(src[off:off + cnt])
+                    values[off:off + cnt].copy_(staged, non_blocking=True)
                 if trace is not None:
                     trace.append(("staged", time.perf_counter() - t_0))
-                values.copy_(staged, non_blocking=True)
                 copied.record(side)
             if trace is not None:
                 trace.append(("enqueued", time.perf_counter() - t_0))
